@@ -1,0 +1,197 @@
+/* vlasim_cuda.h — C-ABI of the B200 (sm_100a) packing + varlen-attention path.
+ *
+ * This is the drop-in boundary between the reference's `vlasim` C++ entry points
+ * (reconstructed in include/vlasim/packing/*.hpp) and the
+ * hand-written CUDA kernels.  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions:
+ *  - Ownership: the caller owns every device buffer and the workspace; hot calls
+ *    never allocate.  All calls are stream-ordered on `stream`.
+ *  - Status: 0 ok; 2 bad input (the reference's ConfigError, errors.hpp:8-12);
+ *    3 runtime/CUDA error (SimError family, errors.hpp:14-18); 4 violated
+ *    invariant (InternalError, errors.hpp:35-39).  The message of the last
+ *    failure on the calling thread is returned by vlasim_last_error_message().
+ *  - Reentrant; no global mutable state on the data path ("pure functions; safe
+ *    for parallel invocation on disjoint inputs").
+ *
+ * Each entry point names the reference operation it replaces.
+ */
+#ifndef VLASIM_CUDA_H_
+#define VLASIM_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VLASIM_ABI_VERSION 1
+
+enum {
+  VLASIM_OK = 0,
+  VLASIM_ECONFIG = 2,
+  VLASIM_ERUNTIME = 3,
+  VLASIM_EINTERNAL = 4
+};
+
+/* cudaStream_t-compatible opaque stream handle (NULL = legacy default stream). */
+typedef struct CUstream_st* vlasim_stream_t;
+
+const char* vlasim_last_error_message(void);
+int vlasim_version(void);
+
+/* ------------------------------------------------------------------ packing
+ * Replaces vlasim::pack_ffd(lengths, capacity) together with
+ * vlasim::cu_seqlens(pack) and the packed-stream layout the
+ * reference's packed_attention consumes ("concatenated tensors consistent with
+ * cu_seqlens").
+ *
+ * Ordering contract (pinned): items are placed in order of
+ * (length descending, id ascending); each goes to the lowest-index open bin it
+ * fits in, else a new bin is appended.  Inside a bin members keep insertion
+ * order.  The packed stream is bins in index order, members in order.
+ *
+ * All arrays are device pointers sized for the worst case (n bins).
+ */
+typedef struct vlasim_pack_out {
+  int32_t* bin_of;          /* [n]   bin index of sample id                               */
+  int32_t* slot;            /* [n]   member index of sample id inside its bin             */
+  int32_t* tok_off;         /* [n]   token offset of sample id inside its bin              */
+  int32_t* bin_count;       /* [n]   members per bin            (first num_bins valid)    */
+  int32_t* bin_fill;        /* [n]   tokens per bin             (first num_bins valid)    */
+  int32_t* bin_member_off;  /* [n+1] exclusive scan of bin_count (CSR over members)       */
+  int32_t* bin_token_off;   /* [n+1] exclusive scan of bin_fill (bin start in the stream)  */
+  int32_t* member_ids;      /* [n]   sample id at packed member position m                 */
+  int32_t* cu_seqlens;      /* [n+1] global segment offsets over the packed stream          */
+  int32_t* cu_seqlens_bins; /* [2n]  per-bin cu_seqlens; bin b at bin_member_off[b] + b     */
+  int32_t* src_off;         /* [n]   exclusive scan of lengths in id order (source layout)  */
+  int32_t* num_bins;        /* [1]                                                           */
+  int64_t* total_tokens;    /* [1]                                                           */
+  int32_t* status;          /* [2]   {error code, offending sample id} written on device     */
+} vlasim_pack_out;
+
+/* Maximum capacity accepted by the GPU packer (larger → VLASIM_ECONFIG). */
+#define VLASIM_PACK_MAX_CAPACITY 16384
+
+size_t vlasim_pack_workspace_size(int64_t n, int32_t capacity);
+
+/* flags */
+#define VLASIM_PACK_SYNC_CHECK 1u /* synchronise `stream` and return the device status
+                                     (oversize / non-positive length → VLASIM_ECONFIG
+                                     naming the id)                         */
+
+int vlasim_pack_ffd_cuda(const int32_t* d_len, int64_t n, int32_t capacity, const vlasim_pack_out* out,
+                         void* d_workspace, size_t workspace_bytes, uint32_t flags, vlasim_stream_t stream);
+
+/* Streaming first-fit in arrival order (SPEC.md:519 greedy variant). Same outputs. */
+int vlasim_pack_greedy_cuda(const int32_t* d_len, int64_t n, int32_t capacity, const vlasim_pack_out* out,
+                            void* d_workspace, size_t workspace_bytes, uint32_t flags, vlasim_stream_t stream);
+
+/* Per packed token: position inside its sample, global segment index (packed member
+ * position) and gather index (row of the sample-major source layout).  Any output
+ * may be NULL.  total_tokens = Σ lengths. */
+int vlasim_pack_token_ids_cuda(const int32_t* d_len, const vlasim_pack_out* out, int64_t n, int64_t total_tokens,
+                               int32_t* d_pos_ids, int32_t* d_seg_ids, int32_t* d_gather_idx,
+                               vlasim_stream_t stream);
+
+/* Token-row gather / scatter between the sample-major source layout (sample id i
+ * occupies rows [src_off[i], src_off[i]+len[i])) and the packed stream (segment m
+ * occupies rows [cu_seqlens[m], cu_seqlens[m+1]) and holds sample member_ids[m]).
+ * row_bytes must be a multiple of 16 and both bases 16-byte aligned (uint4 copies). */
+int vlasim_gather_rows_cuda(const void* d_src, void* d_dst, int64_t row_bytes, const int32_t* d_len,
+                            const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream);
+int vlasim_scatter_rows_cuda(const void* d_packed, void* d_dst, int64_t row_bytes, const int32_t* d_len,
+                             const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream);
+
+/* ------------------------------------------------------------------ attention
+ * Replaces vlasim::packed_attention(q, k, v, cu_seqlens),
+ * multi-head as the reference's looped single-head op.
+ *
+ * Layout: q/o [T, H, d] bf16, k/v [T, Hkv, d] bf16 (row-major, token-major),
+ * lse [H, T] fp32 (natural-log units), cu_seqlens [num_seqs+1] int32 over the
+ * packed stream.  Block-diagonal: token t attends only to keys of its own
+ * segment.  GQA/MQA: kv_head = q_head / (H / Hkv).
+ *
+ * mask_mode: 0 bidirectional, 1 causal, 2 prefix — key j of
+ * segment [s, e) is visible to query t iff j < s + prefix_len[seg] or j <= t.
+ * head_dim ∈ {64, 128, 256}.
+ */
+enum { VLASIM_MASK_BIDIR = 0, VLASIM_MASK_CAUSAL = 1, VLASIM_MASK_PREFIX = 2 };
+
+typedef struct vlasim_attn_args {
+  const void* q;              /* [T, H, d]   bf16 (or e4m3 codes for the fp8 entry)  */
+  const void* k;              /* [T, Hkv, d] bf16 (or e4m3 codes)                    */
+  const void* v;              /* [T, Hkv, d] bf16                                    */
+  void* o;                    /* [T, H, d]   bf16                                    */
+  float* lse;                 /* [H, T]      fp32                                    */
+  const int32_t* cu_seqlens;  /* [num_seqs + 1]                                      */
+  const int32_t* prefix_len;  /* [num_seqs]  (mask_mode == PREFIX only)              */
+  int32_t num_seqs;
+  int64_t total_tokens;       /* T                                                   */
+  int32_t num_heads;          /* H                                                   */
+  int32_t num_kv_heads;       /* Hkv (divides H)                                     */
+  int32_t head_dim;           /* d                                                   */
+  int32_t mask_mode;
+  float softmax_scale;        /* usually 1/sqrt(d)                                   */
+  /* fp8 Q/K only: per-block scales, [H, ceil(T/128), ceil(d/128)] for q and
+     [Hkv, ceil(T/128), ceil(d/128)] for k                       */
+  const float* q_scale;
+  const float* k_scale;
+} vlasim_attn_args;
+
+typedef struct vlasim_attn_grads {
+  const void* dout;  /* [T, H, d]   bf16 */
+  void* dq;          /* [T, H, d]   bf16 */
+  void* dk;          /* [T, Hkv, d] bf16 */
+  void* dv;          /* [T, Hkv, d] bf16 */
+} vlasim_attn_grads;
+
+size_t vlasim_varlen_attn_workspace_size(const vlasim_attn_args* a, int backward);
+
+int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void* d_workspace, size_t workspace_bytes,
+                                vlasim_stream_t stream);
+int vlasim_varlen_attn_bwd_cuda(const vlasim_attn_args* a, const vlasim_attn_grads* g, void* d_workspace,
+                                size_t workspace_bytes, vlasim_stream_t stream);
+/* FP8 Q/K forward: q/k are e4m3 codes with per-(head,128-token,128-d) block scales. */
+int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args* a, void* d_workspace, size_t workspace_bytes,
+                                      vlasim_stream_t stream);
+
+/* ------------------------------------------------------------------ fp8
+ * Replaces vlasim::quantize(t, PerBlock(128,128), E4M3) applied
+ * per head to x [T, heads, d] bf16: scale = amax/448 (1 if the block is all zero),
+ * codes = RNE(x / scale) saturated to ±448.  scales [heads, ceil(T/128), ceil(d/128)].
+ */
+int vlasim_fp8_quant_block_cuda(const void* d_x, int64_t T, int32_t heads, int32_t d, uint8_t* d_codes,
+                                float* d_scales, vlasim_stream_t stream);
+int vlasim_fp8_dequant_block_cuda(const uint8_t* d_codes, const float* d_scales, int64_t T, int32_t heads, int32_t d,
+                                  float* d_out, vlasim_stream_t stream);
+
+/* ------------------------------------------------------------------ synthetic inputs
+ * Counter-based values shared with the CPU oracle:
+ * x[i] = (top8(splitmix64(seed ^ i)) - 128) / 128, exactly representable in bf16. */
+int vlasim_fill_synthetic_bf16(void* d_x, int64_t count, uint64_t seed, vlasim_stream_t stream);
+
+/* Host-side sample-length generator on the reference's seeding API (rng.hpp:28-49):
+ * rng = make_rng(root_seed, label, 0); dist 0 uniform_int(p1, p2); 1 truncated
+ * geometric(p = p1, max = p2) by inverse CDF on uniform01; 2 GR00T-like
+ * 64·uniform_int(1,2) + uniform_int(16,64); 3 π0.5 512 + uniform_int(p1, p2) + p3
+ * (prefix = length − p3).  h_out is a HOST buffer of n int32. */
+int vlasim_gen_lengths(uint64_t root_seed, const char* label, int dist, int64_t n, double p1, double p2, double p3,
+                       int32_t* h_out);
+
+/* ------------------------------------------------------------------ self-test
+ * Single-CTA tcgen05 GEMM used to validate the UMMA/TMA descriptor layouts the
+ * attention kernels rely on.  a, b bf16 row-major, c fp32 [128, N].
+ *  mode 0: C = A[128,K] · B[N,K]ᵀ   (A, B K-major)
+ *  mode 1: C = A[128,K] · B[K,N]    (B MN-major)
+ *  mode 2: C = A[128,K] · B[K,N]    (A staged in TMEM via tcgen05.st, B MN-major)
+ *  mode 3: C = A[K,128]ᵀ · B[K,N]   (A MN-major, B MN-major)
+ */
+int vlasim_selftest_umma(int mode, const void* d_a, const void* d_b, float* d_c, int32_t N, int32_t K,
+                         vlasim_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLASIM_CUDA_H_ */

@@ -1,0 +1,110 @@
+"""Varlen attention API — mirror of the reference's `vlasim::packed_attention(q, k, v, cu_seqlens)`
+(multi-head = the reference's looped single-head op) on the
+hand-written sm_100a kernels.  Every call goes through the C-ABI; no CPU fallback.
+
+Layout: q/o [T, H, d] bf16, k/v [T, Hkv, d] bf16, lse [H, T] fp32, cu_seqlens [nseq+1] int32.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _lib
+from .errors import ConfigError
+
+MASK_BIDIR, MASK_CAUSAL, MASK_PREFIX = 0, 1, 2
+
+
+def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale=None, k_scale=None):
+    if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
+        raise ConfigError("q, k, v must be [T, heads, d]")
+    T, H, d = q.shape
+    if k.shape[0] != T or v.shape != k.shape or k.shape[2] != d:
+        raise ConfigError("k/v shape mismatch with q")
+    if cu_seqlens.dtype != torch.int32:
+        raise ConfigError("cu_seqlens must be int32")
+    for t in (q, k, v, o, cu_seqlens):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ConfigError("tensors must be contiguous CUDA tensors")
+    if mask_mode == MASK_PREFIX and prefix_len is None:
+        raise ConfigError("prefix mask needs prefix_len")
+    scale = float(softmax_scale) if softmax_scale is not None else 1.0 / math.sqrt(d)
+    a = _lib.AttnArgs(
+        _lib.ptr(q).value, _lib.ptr(k).value, _lib.ptr(v).value, _lib.ptr(o).value, _lib.ptr(lse, _lib.f32p),
+        _lib.ptr(cu_seqlens, _lib.i32p), _lib.ptr(prefix_len, _lib.i32p) if prefix_len is not None else None,
+        cu_seqlens.numel() - 1, T, H, k.shape[1], d, int(mask_mode), scale,
+        _lib.ptr(q_scale, _lib.f32p) if q_scale is not None else None,
+        _lib.ptr(k_scale, _lib.f32p) if k_scale is not None else None)
+    return a
+
+
+def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None, softmax_scale=None, out=None,
+                    lse=None, stream=None):
+    """Block-diagonal attention forward. Returns (o [T,H,d] bf16, lse [H,T] fp32 natural-log)."""
+    T, H, d = q.shape
+    o = out if out is not None else torch.empty_like(q)
+    lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=q.device)
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
+    _lib.check(_lib.lib().vlasim_varlen_attn_fwd_cuda(C.byref(a), None, 0, _lib.stream_ptr(stream)),
+               "varlen_attn_fwd")
+    return o, lse
+
+
+class BwdWorkspace:
+    """Reusable fp32 dQ accumulator + LSE/D scratch for the backward kernel."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes, device):
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws = BwdWorkspace()
+
+
+def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None,
+                    softmax_scale=None, dq=None, dk=None, dv=None, workspace: BwdWorkspace | None = None,
+                    stream=None):
+    """Backward of varlen_attn_fwd. Returns (dq, dk, dv) bf16."""
+    dq = dq if dq is not None else torch.empty_like(q)
+    dk = dk if dk is not None else torch.empty_like(k)
+    dv = dv if dv is not None else torch.empty_like(v)
+    if not dout.is_contiguous() or dout.shape != q.shape:
+        raise ConfigError("dout must be contiguous with q's shape")
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
+    g = _lib.AttnGrads(_lib.ptr(dout).value, _lib.ptr(dq).value, _lib.ptr(dk).value, _lib.ptr(dv).value)
+    L = _lib.lib()
+    nbytes = L.vlasim_varlen_attn_workspace_size(C.byref(a), 1)
+    ws = (workspace or _default_ws).get(nbytes, q.device)
+    _lib.check(L.vlasim_varlen_attn_bwd_cuda(C.byref(a), C.byref(g), _lib.ptr(ws), ws.numel(),
+                                             _lib.stream_ptr(stream)), "varlen_attn_bwd")
+    return dq, dk, dv
+
+
+def packed_attention(q, k, v, cu_seqlens, **kw):
+    """Reference name: per-segment attention over the packed stream; returns o."""
+    return varlen_attn_fwd(q, k, v, cu_seqlens, **kw)[0]
+
+
+class VarlenAttention(torch.autograd.Function):
+    """autograd wrapper: o = packed_attention(q, k, v, cu_seqlens) with the hand-written backward."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, cu_seqlens, mask_mode=MASK_BIDIR, prefix_len=None, softmax_scale=None):
+        o, lse = varlen_attn_fwd(q, k, v, cu_seqlens, mask_mode=mask_mode, prefix_len=prefix_len,
+                                 softmax_scale=softmax_scale)
+        ctx.save_for_backward(q, k, v, o, lse, cu_seqlens, prefix_len)
+        ctx.mask_mode, ctx.softmax_scale = mask_mode, softmax_scale
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse, cu, prefix = ctx.saved_tensors
+        dq, dk, dv = varlen_attn_bwd(do.contiguous(), q, k, v, o, lse, cu, mask_mode=ctx.mask_mode,
+                                     prefix_len=prefix, softmax_scale=ctx.softmax_scale)
+        return dq, dk, dv, None, None, None, None

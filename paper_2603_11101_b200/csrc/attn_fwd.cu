@@ -1,0 +1,339 @@
+// attn_fwd.cu — block-diagonal varlen attention forward for sm_100a (bf16 in, fp32 accum).
+//
+// Replaces vlasim::packed_attention (multi-head = looped single head,
+// SPEC.md:521) on the packed stream produced by the GPU packer.
+//
+// One CTA = one 128-row Q tile of the packed stream × one head (tiles on the global
+// 128-row grid, so a tile may span several segments).  The tile's key range is the union
+// of its rows' visible intervals; K/V tiles of BN rows are streamed from there, so no key
+// block outside [first segment start, last visible key) is ever loaded or multiplied
+// (tile skipping at sequence boundaries).  Inside a tile the block-diagonal / causal /
+// prefix mask is a per-row interval test.
+//
+// Warp roles (192 threads):
+//   warps 0-3  softmax + epilogue; thread i owns Q row i == TMEM lane i (32x32b loads)
+//   warp 4     TMA producer: Q once, K/V ring of STAGES stages (SWIZZLE_128B boxes)
+//   warp 5     TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 cols): S double buffer [0, 2·BN), O [2·BN, 2·BN+HD), P (bf16) double buffer
+// after O.  Schedule per K tile j: S_j = Q·K_jᵀ (SS) is issued before PV_{j-1}, so the
+// tensor core computes S_j while the softmax warps turn S_{j-1} into P_{j-1}.
+// O rescaling is lazy: only when a row max grows by more than 2^8 (log2 domain).
+#include <cfloat>
+#include <climits>
+
+#include "attn_common.cuh"
+#include "common.hpp"
+#include "sm100.cuh"
+
+using namespace vlasim_dev;
+
+namespace {
+
+struct FwdParams {
+  __nv_bfloat16* o;
+  float* lse;
+  const int32_t* cu;
+  const int32_t* prefix;
+  int nseq, T, H, Hkv, mask;
+  float scale_log2;
+};
+
+template <int HD, int BN, int STAGES>
+struct FwdCfg {
+  static constexpr int BM = 128;
+  static constexpr int Q_BYTES = BM * HD * 2;
+  static constexpr int KV_BYTES = BN * HD * 2;  // one of K or V
+  static constexpr int SMEM = Q_BYTES + STAGES * 2 * KV_BYTES + 1024;
+  static constexpr uint32_t S_COL = 0;
+  static constexpr uint32_t O_COL = 2 * BN;
+  static constexpr uint32_t P_COL = 2 * BN + HD;
+  static_assert(P_COL + BN <= 512, "TMEM budget");
+  static_assert(SMEM <= 232448, "smem budget");
+  static_assert(HD % 64 == 0 && BN % 32 == 0, "tile shape");
+};
+
+constexpr float kLazyRescale = 8.0f;  // log2-domain growth tolerated before rescaling O
+
+template <int HD, int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdParams p) {
+  using Cfg = FwdCfg<HD, BN, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + Cfg::Q_BYTES;  // stage s: K at s*2*KV_BYTES, V right after
+
+  __shared__ uint64_t bar_q, bar_kv_full[STAGES], bar_kv_empty[STAGES], bar_s_full[2], bar_p_full[2], bar_o_ready;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int s_kv_lo, s_kv_hi;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = blockIdx.x % p.H;
+  const int qt = blockIdx.x / p.H;
+  const int kh = h / (p.H / p.Hkv);
+  const int q0 = qt * Cfg::BM;
+
+  if (tid == 0) {
+    mbar_init(&bar_q, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&bar_kv_full[s], 1);
+      mbar_init(&bar_kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_s_full[b], 1);
+      mbar_init(&bar_p_full[b], 128);
+    }
+    mbar_init(&bar_o_ready, 1);
+    s_kv_lo = INT_MAX;
+    s_kv_hi = INT_MIN;
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(&tmem_base_s);
+  __syncthreads();
+
+  RowSpan rs{0, 0, -1};
+  if (tid < 128) {
+    rs = row_span(p.cu, p.prefix, p.nseq, p.mask, q0 + tid, p.T);
+    if (rs.lo < rs.hi) {
+      atomicMin(&s_kv_lo, rs.lo);
+      atomicMax(&s_kv_hi, rs.hi);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int kv_lo = s_kv_lo;
+  const int nkv = (s_kv_hi - kv_lo + BN - 1) / BN;
+
+  if (warp == 4) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0 && nkv > 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      mbar_expect_tx(&bar_q, Cfg::Q_BYTES);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) tma_load_2d(sQ + c * Cfg::BM * 128, &tmQ, h * HD + c * 64, q0, &bar_q);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % STAGES;
+        if (j >= STAGES) mbar_wait(&bar_kv_empty[st], ((j / STAGES) - 1) & 1);
+        uint8_t* sk = sKV + st * 2 * Cfg::KV_BYTES;
+        uint8_t* sv = sk + Cfg::KV_BYTES;
+        const int kv0 = kv_lo + j * BN;
+        mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::KV_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sk + c * BN * 128, &tmK, kh * HD + c * 64, kv0, &bar_kv_full[st]);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, kh * HD + c * 64, kv0, &bar_kv_full[st]);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0 && nkv > 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait(&bar_q, 0);
+      for (int j = 0; j <= nkv; ++j) {
+        if (j < nkv) {
+          const int st = j % STAGES;
+          mbar_wait(&bar_kv_full[st], (j / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES);
+          const uint32_t d_s = tmem + Cfg::S_COL + (j & 1) * BN;
+#pragma unroll
+          for (int s = 0; s < HD / 16; ++s) {
+            const uint64_t a = make_sdesc_sw128(q_addr + (s / 4) * Cfg::BM * 128 + (s % 4) * 32, 16, 1024);
+            const uint64_t b = make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024);
+            umma_f16_ss(d_s, a, b, idesc_s, s > 0);
+          }
+          umma_commit(&bar_s_full[j & 1]);
+        }
+        if (j > 0) {
+          const int jj = j - 1, st = jj % STAGES;
+          mbar_wait(&bar_p_full[jj & 1], (jj >> 1) & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+          const uint32_t a_tm = tmem + Cfg::P_COL + (jj & 1) * (BN / 2);
+#pragma unroll
+          for (int s = 0; s < BN / 16; ++s) {
+            const uint64_t b = make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024);
+            umma_f16_ts(tmem + Cfg::O_COL, a_tm + s * 8, b, idesc_o, (jj > 0 || s > 0) ? 1u : 0u);
+          }
+          umma_commit(&bar_kv_empty[st]);
+          umma_commit(&bar_o_ready);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax (warps 0-3)
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&bar_s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[BN];
+#pragma unroll
+      for (int c = 0; c < BN; c += 32) tmem_ld32(tmem + lane_off + Cfg::S_COL + sb * BN + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+      tmem_wait_ld();
+      const int kv0 = kv_lo + j * BN;
+      const int c_lo = rs.lo - kv0, c_hi = rs.hi - kv0;
+      float mt = -INFINITY;
+      if (c_lo <= 0 && c_hi >= BN) {
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const float x = __uint_as_float(r[c]) * sl2;
+          r[c] = __float_as_uint(x);
+          mt = fmaxf(mt, x);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const float x = (c >= c_lo && c < c_hi) ? __uint_as_float(r[c]) * sl2 : -INFINITY;
+          r[c] = __float_as_uint(x);
+          mt = fmaxf(mt, x);
+        }
+      }
+      const bool grow = mt > m_run + kLazyRescale;
+      const float alpha = grow ? exp2f(m_run - mt) : 1.f;  // m_run = -inf → 0
+      if (__any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY)) {
+        mbar_wait(&bar_o_ready, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_off + Cfg::O_COL + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tmem + lane_off + Cfg::O_COL + c, o);
+        }
+      }
+      if (grow) {
+        l_run *= alpha;
+        m_run = mt;
+      }
+      const float msub = (m_run == -INFINITY) ? 0.f : m_run;
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2_approx(__uint_as_float(r[c + 2 * i]) - msub);
+          const float p1 = ex2_approx(__uint_as_float(r[c + 2 * i + 1]) - msub);
+          ls += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(tmem + lane_off + Cfg::P_COL + sb * (BN / 2) + c / 2, pk);
+      }
+      l_run += ls;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bar_p_full[sb]);
+    }
+    // ------------------------------------------------ epilogue: O / l → bf16, LSE
+    if (nkv > 0) {
+      mbar_wait(&bar_o_ready, (nkv - 1) & 1);
+      tc_fence_after();
+    }
+    const int row = q0 + tid;
+    const bool valid = row < p.T && rs.lo < rs.hi;
+    const float inv_l = (valid && l_run > 0.f) ? 1.f / l_run : 0.f;
+    __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + h) * HD;
+#pragma unroll
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_off + Cfg::O_COL + c, o);
+      tmem_wait_ld();
+      if (valid) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
+        uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+    if (valid) p.lse[static_cast<int64_t>(h) * p.T + row] = (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+template <int HD, int BN, int STAGES>
+int launch_fwd(const vlasim_attn_args* a, cudaStream_t st) {
+  using namespace vlasim_host;
+  using Cfg = FwdCfg<HD, BN, STAGES>;
+  CUtensorMap tq, tk, tv;
+  const uint64_t T = a->total_tokens;
+  if (int rc = encode_tmap_2d(&tq, a->q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, uint64_t(a->num_heads) * HD,
+                              uint64_t(a->num_heads) * HD * 2, 128, 64, true))
+    return rc;
+  if (int rc = encode_tmap_2d(&tk, a->k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, uint64_t(a->num_kv_heads) * HD,
+                              uint64_t(a->num_kv_heads) * HD * 2, BN, 64, true))
+    return rc;
+  if (int rc = encode_tmap_2d(&tv, a->v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, uint64_t(a->num_kv_heads) * HD,
+                              uint64_t(a->num_kv_heads) * HD * 2, BN, 64, true))
+    return rc;
+  FwdParams p;
+  p.o = static_cast<__nv_bfloat16*>(a->o);
+  p.lse = a->lse;
+  p.cu = a->cu_seqlens;
+  p.prefix = a->prefix_len;
+  p.nseq = a->num_seqs;
+  p.T = static_cast<int>(T);
+  p.H = a->num_heads;
+  p.Hkv = a->num_kv_heads;
+  p.mask = a->mask_mode;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  auto kern = attn_fwd_kernel<HD, BN, STAGES>;
+  VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int64_t qtiles = (int64_t(T) + 127) / 128;
+  kern<<<qtiles * a->num_heads, 192, Cfg::SMEM, st>>>(tq, tk, tv, p);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
+}  // namespace
+
+namespace vlasim_host {
+int validate_attn_args(const vlasim_attn_args* a, bool fp8) {
+  if (!a) return set_error(VLASIM_ECONFIG, "attention: null args");
+  if (!a->q || !a->k || !a->v || !a->o || !a->lse || !a->cu_seqlens)
+    return set_error(VLASIM_ECONFIG, "attention: q, k, v, o, lse, cu_seqlens are required");
+  if (a->total_tokens < 1 || a->total_tokens >= INT_MAX)
+    return set_error(VLASIM_ECONFIG, "attention: total_tokens=%lld out of range", (long long)a->total_tokens);
+  if (a->num_seqs < 1) return set_error(VLASIM_ECONFIG, "attention: num_seqs must be >= 1");
+  if (a->num_heads < 1 || a->num_kv_heads < 1 || a->num_heads % a->num_kv_heads)
+    return set_error(VLASIM_ECONFIG, "attention: num_kv_heads (%d) must divide num_heads (%d)", a->num_kv_heads,
+                     a->num_heads);
+  if (a->head_dim != 64 && a->head_dim != 128 && a->head_dim != 256)
+    return set_error(VLASIM_ECONFIG, "attention: head_dim %d unsupported (64, 128, 256)", a->head_dim);
+  if (a->mask_mode < 0 || a->mask_mode > 2) return set_error(VLASIM_ECONFIG, "attention: bad mask_mode");
+  if (a->mask_mode == VLASIM_MASK_PREFIX && !a->prefix_len)
+    return set_error(VLASIM_ECONFIG, "attention: prefix mask needs prefix_len");
+  if (fp8 && (!a->q_scale || !a->k_scale)) return set_error(VLASIM_ECONFIG, "attention: fp8 path needs scales");
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a->q) | reinterpret_cast<uintptr_t>(a->k) |
+                       reinterpret_cast<uintptr_t>(a->v) | reinterpret_cast<uintptr_t>(a->o);
+  if (al & 15) return set_error(VLASIM_ECONFIG, "attention: q/k/v/o must be 16-byte aligned");
+  return VLASIM_OK;
+}
+}  // namespace vlasim_host
+
+extern "C" int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void*, size_t, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = validate_attn_args(a, false)) return rc;
+  cudaStream_t st = as_stream(stream);
+  switch (a->head_dim) {
+    case 64: return launch_fwd<64, 128, 4>(a, st);
+    case 128: return launch_fwd<128, 128, 3>(a, st);
+    default: return launch_fwd<256, 64, 2>(a, st);
+  }
+}

@@ -1,0 +1,48 @@
+// common.hpp — host-side plumbing shared by the C-ABI entry points:
+// thread-local error state (SURVEY §8(b) status convention), CUDA checks,
+// and TMA tensor-map encoding through the driver entry point (no -lcuda).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/vlasim_cuda.h"
+
+namespace vlasim_host {
+
+// Status codes mirror the reference's exception taxonomy (errors.hpp:8-39):
+// 2 = ConfigError (bad user input), 3 = runtime (SimError family), 4 = InternalError.
+std::string& last_error();
+int set_error(int code, const char* fmt, ...);
+
+#define VLASIM_CUDA_TRY(expr)                                                                          \
+  do {                                                                                                 \
+    cudaError_t _e = (expr);                                                                           \
+    if (_e != cudaSuccess)                                                                             \
+      return ::vlasim_host::set_error(VLASIM_ERUNTIME, "%s failed: %s (%s:%d)", #expr,                  \
+                                      cudaGetErrorString(_e), __FILE__, __LINE__);                     \
+  } while (0)
+
+#define VLASIM_LAUNCH_CHECK()                                                                          \
+  do {                                                                                                 \
+    cudaError_t _e = cudaGetLastError();                                                               \
+    if (_e != cudaSuccess)                                                                             \
+      return ::vlasim_host::set_error(VLASIM_ERUNTIME, "kernel launch failed: %s (%s:%d)",             \
+                                      cudaGetErrorString(_e), __FILE__, __LINE__);                     \
+  } while (0)
+
+// Encodes a 2-D tiled TMA map over a row-major matrix [rows, cols] of elem_bytes-wide
+// elements with row pitch `row_stride_bytes`; box = [box_rows, box_cols] (box_cols*elem
+// must be 128 B for SWIZZLE_128B).  Returns 0 or a status code.
+int encode_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint64_t rows, uint64_t cols,
+                   uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+inline cudaStream_t as_stream(vlasim_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms();
+
+}  // namespace vlasim_host

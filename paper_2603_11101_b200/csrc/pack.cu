@@ -1,0 +1,538 @@
+// pack.cu — GPU packer: length histogram → stable class ranks → class-wise first-fit-
+// decreasing → packed-stream layout (cu_seqlens, member order, token ids) → token-row
+// gather/scatter.  Bit-exact with the reference's sequential FFD under
+// the pinned order (length desc, id asc) — see DESIGN.md §2 for the equivalence proof:
+//
+//   All items of one length L are placed in id order; each lands in the lowest-index bin
+//   with rem >= L, and after it lands every lower-index bin has rem < L.  Hence class L
+//   fills open bins in index order, bin b taking min(floor(rem_b / L), remaining) items,
+//   and the leftover opens new bins of floor(cap / L) items each.  FFD = a sequence of
+//   per-class exclusive scans over the open bins, driven by the length histogram.
+//
+// Kernels (one launch each, all stream-ordered, no host sync unless SYNC_CHECK):
+//   k_init        status / per-bin counters
+//   k_hist        validate 1 <= len <= cap, per-chunk histogram in smem
+//   k_class_scan  per-class exclusive base across chunks (stable rank offsets) + counts
+//   k_ffd         single CTA: class-wise FFD over the open-bin list (smem), emits "runs"
+//   k_assign      stable rank inside class → run → (bin, slot, token offset)
+//   k_scan_*      exclusive scans: bin member/token offsets, source offsets
+//   k_layout      member order, global + per-bin cu_seqlens
+#include <climits>
+
+#include "common.hpp"
+#include "scan.cuh"
+
+using namespace vlasim_dev;
+
+namespace {
+
+constexpr int kChunk = 4096;         // items per histogram / rank chunk
+constexpr int kRankThreads = 1024;   // k_assign block (4 rounds of 1024 items)
+constexpr int kScanItems = 4096;     // items per scan block (1024 threads × 4)
+constexpr int kMaxActiveBins = 16384;  // open bins kept in k_ffd shared memory
+
+struct PackWs {
+  int32_t* chunk_hist;       // [C][cap+1]   → exclusive per-class base after k_class_scan
+  int32_t* class_count;      // [cap+1]
+  int32_t* class_run_start;  // [cap+1]
+  int32_t* class_nruns;      // [cap+1]
+  int32_t* run_bin;          // [n]
+  int32_t* run_cum;          // [n]  items of the class placed before this run
+  int32_t* run_tok;          // [n]  bin fill (tokens) before this run
+  int32_t* run_mem;          // [n]  bin member count before this run
+  int64_t* scan_part;        // [3][num_scan_blocks + 1]
+};
+
+inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline int64_t num_chunks(int64_t n) { return (n + kChunk - 1) / kChunk; }
+inline int64_t num_scan_blocks(int64_t n) { return (n + 1 + kScanItems - 1) / kScanItems; }
+
+size_t carve(PackWs* w, void* base, int64_t n, int cap) {
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* r = p ? p + off : nullptr;
+    off += align_up(bytes);
+    return r;
+  };
+  const size_t nc = size_t(cap) + 1;
+  w->chunk_hist = reinterpret_cast<int32_t*>(take(size_t(num_chunks(n)) * nc * 4));
+  w->class_count = reinterpret_cast<int32_t*>(take(nc * 4));
+  w->class_run_start = reinterpret_cast<int32_t*>(take(nc * 4));
+  w->class_nruns = reinterpret_cast<int32_t*>(take(nc * 4));
+  w->run_bin = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+  w->run_cum = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+  w->run_tok = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+  w->run_mem = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+  w->scan_part = reinterpret_cast<int64_t*>(take(size_t(3) * (num_scan_blocks(n) + 1) * 8));
+  return off;
+}
+
+// ------------------------------------------------------------------ init / validate
+__global__ void k_init(vlasim_pack_out out, int64_t n) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i == 0) {
+    out.status[0] = 0;
+    out.status[1] = INT_MAX;
+    *out.num_bins = 0;
+  }
+  if (i < n) {
+    out.bin_count[i] = 0;
+    out.bin_fill[i] = 0;
+  }
+}
+
+__global__ void k_hist(const int32_t* __restrict__ len, int64_t n, int cap, int32_t* __restrict__ chunk_hist,
+                       int32_t* status) {
+  extern __shared__ int32_t sh[];
+  for (int i = threadIdx.x; i <= cap; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t base = int64_t(blockIdx.x) * kChunk;
+  for (int j = threadIdx.x; j < kChunk; j += blockDim.x) {
+    const int64_t i = base + j;
+    if (i >= n) break;
+    const int L = len[i];
+    if (L < 1 || L > cap) {
+      atomicMin(&status[1], int(i));
+      status[0] = VLASIM_ECONFIG;
+      continue;
+    }
+    atomicAdd(&sh[L], 1);
+  }
+  __syncthreads();
+  int32_t* o = chunk_hist + size_t(blockIdx.x) * (cap + 1);
+  for (int i = threadIdx.x; i <= cap; i += blockDim.x) o[i] = sh[i];
+}
+
+// One thread per length class: exclusive base over chunks (in chunk order = id order).
+__global__ void k_class_scan(int32_t* __restrict__ chunk_hist, int64_t nchunks, int cap,
+                             int32_t* __restrict__ class_count) {
+  const int L = blockIdx.x * blockDim.x + threadIdx.x;
+  if (L > cap) return;
+  int32_t run = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    int32_t* p = chunk_hist + size_t(c) * (cap + 1) + L;
+    const int32_t v = *p;
+    *p = run;
+    run += v;
+  }
+  class_count[L] = run;
+}
+
+// ------------------------------------------------------------------ class-wise FFD
+// Single CTA.  Open ("active") bins are kept in shared memory sorted by bin id:
+// act_id / act_rem / act_cnt.  A bin whose remaining room is below the smallest length
+// still to come can never receive an item again; it is retired (final count/fill written)
+// during compaction, which preserves the id order of the survivors.
+__global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack_out out) {
+  extern __shared__ int32_t sm[];
+  int32_t* act_id = sm;
+  int32_t* act_rem = sm + kMaxActiveBins;
+  int32_t* act_cnt = sm + 2 * kMaxActiveBins;
+  int32_t* cls = sm + 3 * kMaxActiveBins;  // [1024] compacted class list of the current L-chunk
+  __shared__ int32_t scratch[33];
+  __shared__ int32_t s_ncls, s_lmin;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  if (out.status[0] != 0) return;  // validation failed upstream
+
+  // smallest present length (retirement threshold)
+  int lmin_local = INT_MAX;
+  for (int L = 1 + tid; L <= cap; L += nt)
+    if (ws.class_count[L] > 0) lmin_local = min(lmin_local, L);
+  for (int o = 16; o > 0; o >>= 1) lmin_local = min(lmin_local, __shfl_xor_sync(0xffffffffu, lmin_local, o));
+  if (tid == 0) s_lmin = INT_MAX;
+  __syncthreads();
+  if ((tid & 31) == 0) atomicMin(&s_lmin, lmin_local);
+  __syncthreads();
+  const int lmin = s_lmin;
+
+  int nact = 0, nb = 0, nruns = 0;  // uniform across the block
+  int32_t tot;
+
+  for (int hi = cap; hi >= 1; hi -= 1024) {
+    // ---- compact the non-empty classes of L ∈ (hi-1024, hi] in descending order
+    const int span = min(1024, hi);
+    const int per_c = (span + nt - 1) / nt;
+    int mine = 0;
+    for (int j = tid * per_c; j < min(span, (tid + 1) * per_c); ++j) mine += ws.class_count[hi - j] > 0;
+    int pos = block_exclusive_scan<int32_t>(mine, scratch, &tot);
+    for (int j = tid * per_c; j < min(span, (tid + 1) * per_c); ++j)
+      if (ws.class_count[hi - j] > 0) cls[pos++] = hi - j;
+    if (tid == 0) s_ncls = tot;
+    __syncthreads();
+    const int ncls = s_ncls;
+
+    for (int ci = 0; ci < ncls; ++ci) {
+      const int L = cls[ci];
+      const int c = ws.class_count[L];
+      const int runs_before = nruns;
+
+      // ---- phase A: existing open bins, in id order
+      const int per = (nact + nt - 1) / nt;
+      const int b0 = min(nact, tid * per), b1 = min(nact, b0 + per);
+      int sumq = 0;
+      for (int b = b0; b < b1; ++b) sumq += act_rem[b] / L;
+      int32_t totq;
+      const int exq = block_exclusive_scan<int32_t>(sumq, scratch, &totq);
+      int running = exq, nr = 0;
+      for (int b = b0; b < b1 && running < c; ++b) {
+        const int q = act_rem[b] / L;
+        if (q > 0) ++nr;
+        running += q;
+      }
+      int32_t nr_tot;
+      int ridx = nruns + block_exclusive_scan<int32_t>(nr, scratch, &nr_tot);
+      running = exq;
+      for (int b = b0; b < b1 && running < c; ++b) {
+        const int rem = act_rem[b];
+        const int q = rem / L;
+        if (q > 0) {
+          const int take = min(q, c - running);
+          ws.run_bin[ridx] = act_id[b];
+          ws.run_cum[ridx] = running;
+          ws.run_tok[ridx] = cap - rem;
+          ws.run_mem[ridx] = act_cnt[b];
+          ++ridx;
+          act_rem[b] = rem - take * L;
+          act_cnt[b] += take;
+        }
+        running += q;
+      }
+      nruns += nr_tot;
+      const int placed = min(c, totq);
+      const int r = c - placed;
+
+      // ---- phase B: new bins of floor(cap / L) items each
+      if (r > 0) {
+        const int k = cap / L;
+        const int nnew = (r + k - 1) / k;
+        if (nact + nnew > kMaxActiveBins) {
+          // retire bins that can never be used again, then re-check
+          __syncthreads();
+          int keep = 0;
+          for (int b = b0; b < b1; ++b) keep += act_rem[b] >= lmin;
+          int32_t kept;
+          int kpos = block_exclusive_scan<int32_t>(keep, scratch, &kept);
+          int32_t tid_buf[32], rem_buf[32], cnt_buf[32];  // per <= kMaxActiveBins / 1024 = 16
+          int nk = 0;
+          for (int b = b0; b < b1; ++b) {
+            if (act_rem[b] >= lmin) {
+              tid_buf[nk] = act_id[b];
+              rem_buf[nk] = act_rem[b];
+              cnt_buf[nk] = act_cnt[b];
+              ++nk;
+            } else {
+              out.bin_count[act_id[b]] = act_cnt[b];
+              out.bin_fill[act_id[b]] = cap - act_rem[b];
+            }
+          }
+          __syncthreads();
+          for (int j = 0; j < nk; ++j) {
+            act_id[kpos + j] = tid_buf[j];
+            act_rem[kpos + j] = rem_buf[j];
+            act_cnt[kpos + j] = cnt_buf[j];
+          }
+          nact = kept;
+          __syncthreads();
+          if (nact + nnew > kMaxActiveBins) {
+            if (tid == 0) {
+              out.status[0] = VLASIM_ECONFIG;
+              out.status[1] = -2;  // open-bin limit
+            }
+            return;
+          }
+        }
+        for (int j = tid; j < nnew; j += nt) {
+          const int take = min(k, r - j * k);
+          ws.run_bin[nruns + j] = nb + j;
+          ws.run_cum[nruns + j] = placed + j * k;
+          ws.run_tok[nruns + j] = 0;
+          ws.run_mem[nruns + j] = 0;
+          act_id[nact + j] = nb + j;
+          act_rem[nact + j] = cap - take * L;
+          act_cnt[nact + j] = take;
+        }
+        nb += nnew;
+        nact += nnew;
+        nruns += nnew;
+      }
+      if (tid == 0) {
+        ws.class_run_start[L] = runs_before;
+        ws.class_nruns[L] = nruns - runs_before;
+      }
+      __syncthreads();
+    }
+  }
+  // final state of the still-open bins
+  for (int b = tid; b < nact; b += nt) {
+    out.bin_count[act_id[b]] = act_cnt[b];
+    out.bin_fill[act_id[b]] = cap - act_rem[b];
+  }
+  if (tid == 0) *out.num_bins = nb;
+}
+
+// ------------------------------------------------------------------ stable ranks → bins
+__global__ void __launch_bounds__(kRankThreads) k_assign(const int32_t* __restrict__ len, int64_t n, int cap,
+                                                          PackWs ws, vlasim_pack_out out) {
+  extern __shared__ int32_t cnt[];  // [cap+1] running per-class rank inside this chunk
+  if (out.status[0] != 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t* base = ws.chunk_hist + size_t(blockIdx.x) * (cap + 1);
+  for (int i = tid; i <= cap; i += blockDim.x) cnt[i] = base[i];
+  __syncthreads();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int round = 0; round < kChunk / kRankThreads; ++round) {
+    const int64_t i = int64_t(blockIdx.x) * kChunk + round * kRankThreads + tid;
+    const bool valid = i < n;
+    const int L = valid ? len[i] : -1 - lane;  // invalid lanes never match anyone
+    const unsigned peers = __match_any_sync(0xffffffffu, L);
+    const int leader = __ffs(peers) - 1;
+    const int before = __popc(peers & lt_mask);
+    int rank0 = 0;
+    for (int w = 0; w < kRankThreads / 32; ++w) {
+      if (w == warp && valid && lane == leader) {
+        rank0 = cnt[L];
+        cnt[L] = rank0 + __popc(peers);
+      }
+      __syncthreads();
+    }
+    rank0 = __shfl_sync(0xffffffffu, rank0, leader);
+    if (!valid) continue;
+    const int rank = rank0 + before;
+    // binary search the run of class L containing `rank`
+    int lo = ws.class_run_start[L], hi = lo + ws.class_nruns[L] - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ws.run_cum[mid] <= rank) lo = mid; else hi = mid - 1;
+    }
+    const int within = rank - ws.run_cum[lo];
+    out.bin_of[i] = ws.run_bin[lo];
+    out.slot[i] = ws.run_mem[lo] + within;
+    out.tok_off[i] = ws.run_tok[lo] + within * L;
+  }
+}
+
+// ------------------------------------------------------------------ device-wide scans
+// Exclusive scan of int32 in[0..n) (+ total at out[n]) in three passes; partial sums int64.
+__global__ void k_scan_reduce(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ part) {
+  __shared__ int64_t scratch[33];
+  int64_t s = 0;
+  const int64_t b = int64_t(blockIdx.x) * kScanItems;
+  for (int j = threadIdx.x; j < kScanItems; j += blockDim.x) {
+    const int64_t i = b + j;
+    if (i < n) s += in[i];
+  }
+  int64_t tot;
+  block_exclusive_scan<int64_t>(s, scratch, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+__global__ void k_scan_parts(int64_t* part, int64_t nparts, int64_t* total_out) {
+  __shared__ int64_t scratch[33];
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < nparts; b0 += blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;
+    const int64_t v = i < nparts ? part[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_exclusive_scan<int64_t>(v, scratch, &tot);
+    if (i < nparts) part[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry;
+}
+template <typename OutT>
+__global__ void k_scan_apply(const int32_t* __restrict__ in, int64_t n, const int64_t* __restrict__ part,
+                             OutT* __restrict__ out, int32_t* status) {
+  __shared__ int64_t scratch[33];
+  const int64_t b = int64_t(blockIdx.x) * kScanItems;
+  const int64_t i0 = b + threadIdx.x * 4;
+  int64_t v[4], s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[j] = (i0 + j < n) ? in[i0 + j] : 0;
+    s += v[j];
+  }
+  int64_t tot;
+  int64_t run = part[blockIdx.x] + block_exclusive_scan<int64_t>(s, scratch, &tot);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t i = i0 + j;
+    if (i <= n) {
+      if (run > INT_MAX && status) {
+        status[0] = VLASIM_ECONFIG;
+        status[1] = -3;  // token count overflows int32 cu_seqlens
+      }
+      out[i] = OutT(run);
+    }
+    run += v[j];
+  }
+}
+
+// ------------------------------------------------------------------ layout
+__global__ void k_layout(const int32_t* __restrict__ len, int64_t n, vlasim_pack_out out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (out.status[0] != 0) return;
+  if (i >= n) return;
+  const int b = out.bin_of[i], s = out.slot[i], t = out.tok_off[i];
+  const int mo = out.bin_member_off[b];
+  const int m = mo + s;
+  out.member_ids[m] = int32_t(i);
+  out.cu_seqlens[m] = out.bin_token_off[b] + t;
+  int32_t* cb = out.cu_seqlens_bins + mo + b;
+  cb[s + 1] = t + len[i];
+  if (s == 0) cb[0] = 0;
+  if (i == 0) out.cu_seqlens[n] = out.bin_token_off[n];
+}
+
+__global__ void k_token_ids(const int32_t* __restrict__ len, vlasim_pack_out out, int64_t n, int32_t* pos_ids,
+                            int32_t* seg_ids, int32_t* gather_idx) {
+  // one warp per segment (grid-stride)
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  for (int64_t m = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32; m < n; m += warps) {
+    const int id = out.member_ids[m];
+    const int start = out.cu_seqlens[m];
+    const int L = len[id];
+    const int src = out.src_off[id];
+    for (int p = lane; p < L; p += 32) {
+      if (pos_ids) pos_ids[start + p] = p;
+      if (seg_ids) seg_ids[start + p] = int32_t(m);
+      if (gather_idx) gather_idx[start + p] = src + p;
+    }
+  }
+}
+
+// One CTA per segment: contiguous copy of len × row_bytes with 16-byte vectors, 4 in flight.
+template <bool kGather>
+__global__ void __launch_bounds__(256) k_copy_rows(const uint4* __restrict__ a, uint4* __restrict__ b,
+                                                   int64_t row_vecs, const int32_t* __restrict__ len,
+                                                   vlasim_pack_out out) {
+  const int64_t m = blockIdx.x;
+  const int id = out.member_ids[m];
+  const int64_t nvec = int64_t(len[id]) * row_vecs;
+  const int64_t packed = int64_t(out.cu_seqlens[m]) * row_vecs;
+  const int64_t source = int64_t(out.src_off[id]) * row_vecs;
+  const uint4* src = a + (kGather ? source : packed);
+  uint4* dst = b + (kGather ? packed : source);
+  const int64_t stride = 4 * blockDim.x;
+  int64_t j = threadIdx.x;
+  for (; j + 3 * blockDim.x < nvec; j += stride) {
+    uint4 v0 = __ldcs(src + j), v1 = __ldcs(src + j + blockDim.x), v2 = __ldcs(src + j + 2 * blockDim.x),
+          v3 = __ldcs(src + j + 3 * blockDim.x);
+    __stcs(dst + j, v0);
+    __stcs(dst + j + blockDim.x, v1);
+    __stcs(dst + j + 2 * blockDim.x, v2);
+    __stcs(dst + j + 3 * blockDim.x, v3);
+  }
+  for (; j < nvec; j += blockDim.x) __stcs(dst + j, __ldcs(src + j));
+}
+
+int run_scan(const int32_t* in, int64_t n, int32_t* out, int64_t* part, int64_t* total, int32_t* status,
+             cudaStream_t st) {
+  const int64_t nb = num_scan_blocks(n);
+  k_scan_reduce<<<nb, 1024, 0, st>>>(in, n, part);
+  k_scan_parts<<<1, 1024, 0, st>>>(part, nb, total);
+  k_scan_apply<int32_t><<<nb, 1024, 0, st>>>(in, n, part, out, status);
+  return 0;
+}
+
+int check_out(const vlasim_pack_out* o) {
+  if (!o || !o->bin_of || !o->slot || !o->tok_off || !o->bin_count || !o->bin_fill || !o->bin_member_off ||
+      !o->bin_token_off || !o->member_ids || !o->cu_seqlens || !o->cu_seqlens_bins || !o->src_off || !o->num_bins ||
+      !o->total_tokens || !o->status)
+    return vlasim_host::set_error(VLASIM_ECONFIG, "vlasim_pack_out: every output pointer must be set");
+  return 0;
+}
+
+int finish(const vlasim_pack_out* out, int64_t n, uint32_t flags, cudaStream_t st) {
+  using namespace vlasim_host;
+  if (!(flags & VLASIM_PACK_SYNC_CHECK)) return VLASIM_OK;
+  int32_t h[2];
+  VLASIM_CUDA_TRY(cudaMemcpyAsync(h, out->status, sizeof(h), cudaMemcpyDeviceToHost, st));
+  VLASIM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h[0] == 0) return VLASIM_OK;
+  if (h[1] == -2) return set_error(VLASIM_ECONFIG, "GPU packer: more than %d simultaneously open bins", kMaxActiveBins);
+  if (h[1] == -3) return set_error(VLASIM_ECONFIG, "GPU packer: total tokens exceed int32 cu_seqlens range");
+  return set_error(VLASIM_ECONFIG, "oversize or empty sample: id %d (length must be in [1, capacity])", h[1]);
+}
+
+}  // namespace
+
+extern "C" size_t vlasim_pack_workspace_size(int64_t n, int32_t capacity) {
+  PackWs w;
+  return carve(&w, nullptr, n < 1 ? 1 : n, capacity < 1 ? 1 : capacity);
+}
+
+extern "C" int vlasim_pack_ffd_cuda(const int32_t* d_len, int64_t n, int32_t cap, const vlasim_pack_out* out,
+                                    void* d_ws, size_t ws_bytes, uint32_t flags, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = check_out(out)) return rc;
+  if (n < 1) return set_error(VLASIM_ECONFIG, "pack_ffd: need at least one sample (n=%lld)", (long long)n);
+  if (n >= INT_MAX) return set_error(VLASIM_ECONFIG, "pack_ffd: n=%lld exceeds int32 ids", (long long)n);
+  if (cap < 1 || cap > VLASIM_PACK_MAX_CAPACITY)
+    return set_error(VLASIM_ECONFIG, "pack_ffd: capacity %d outside [1, %d]", cap, VLASIM_PACK_MAX_CAPACITY);
+  PackWs w;
+  const size_t need = carve(&w, nullptr, n, cap);
+  if (!d_ws || ws_bytes < need)
+    return set_error(VLASIM_ECONFIG, "pack_ffd: workspace too small (%zu < %zu)", ws_bytes, need);
+  carve(&w, d_ws, n, cap);
+  cudaStream_t st = as_stream(stream);
+  const int64_t nchunks = num_chunks(n);
+
+  k_init<<<(n + 255) / 256, 256, 0, st>>>(*out, n);
+  k_hist<<<nchunks, 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);
+  k_class_scan<<<(cap + 1 + 255) / 256, 256, 0, st>>>(w.chunk_hist, nchunks, cap, w.class_count);
+  const int ffd_threads = n <= 8192 ? 32 : 1024;
+  const size_t ffd_smem = (3 * kMaxActiveBins + 1024) * 4;
+  VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffd_smem));
+  k_ffd<<<1, ffd_threads, ffd_smem, st>>>(cap, w, *out);
+  const size_t as_smem = (cap + 1) * 4;
+  if (as_smem > 48 * 1024)
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as_smem));
+  k_assign<<<nchunks, kRankThreads, as_smem, st>>>(d_len, n, cap, w, *out);
+  const int64_t nsb = num_scan_blocks(n) + 1;
+  run_scan(out->bin_count, n, out->bin_member_off, w.scan_part, nullptr, nullptr, st);
+  run_scan(out->bin_fill, n, out->bin_token_off, w.scan_part + nsb, nullptr, out->status, st);
+  run_scan(d_len, n, out->src_off, w.scan_part + 2 * nsb, out->total_tokens, out->status, st);
+  k_layout<<<(n + 255) / 256, 256, 0, st>>>(d_len, n, *out);
+  VLASIM_LAUNCH_CHECK();
+  return finish(out, n, flags, st);
+}
+
+extern "C" int vlasim_pack_token_ids_cuda(const int32_t* d_len, const vlasim_pack_out* out, int64_t n,
+                                          int64_t total_tokens, int32_t* d_pos, int32_t* d_seg, int32_t* d_gather,
+                                          vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = check_out(out)) return rc;
+  if (n < 1 || total_tokens < 1) return set_error(VLASIM_ECONFIG, "token_ids: empty input");
+  const int64_t warps_needed = n;
+  const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, int64_t(num_sms()) * 16);
+  k_token_ids<<<blocks, 256, 0, as_stream(stream)>>>(d_len, *out, n, d_pos, d_seg, d_gather);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
+static int copy_rows(bool gather, const void* a, void* b, int64_t row_bytes, const int32_t* d_len,
+                     const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = check_out(out)) return rc;
+  if (row_bytes <= 0 || row_bytes % 16) return set_error(VLASIM_ECONFIG, "row_bytes must be a positive multiple of 16");
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)
+    return set_error(VLASIM_ECONFIG, "gather/scatter buffers must be 16-byte aligned");
+  if (n < 1) return VLASIM_OK;
+  auto kern = gather ? k_copy_rows<true> : k_copy_rows<false>;
+  kern<<<n, 256, 0, as_stream(stream)>>>(static_cast<const uint4*>(a), static_cast<uint4*>(b), row_bytes / 16, d_len,
+                                        *out);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
+extern "C" int vlasim_gather_rows_cuda(const void* d_src, void* d_dst, int64_t row_bytes, const int32_t* d_len,
+                                       const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream) {
+  return copy_rows(true, d_src, d_dst, row_bytes, d_len, out, n, stream);
+}
+extern "C" int vlasim_scatter_rows_cuda(const void* d_packed, void* d_dst, int64_t row_bytes, const int32_t* d_len,
+                                        const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream) {
+  return copy_rows(false, d_packed, d_dst, row_bytes, d_len, out, n, stream);
+}

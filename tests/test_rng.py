@@ -1,0 +1,48 @@
+"""Seeding API pinned against the reference's own rng.hpp (SPEC.md:390 determinism; rng.hpp:9-49)."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLD = json.loads((ROOT / "tests/golden/rng_kat.json").read_text())
+
+
+def _run(binary):
+    return json.loads(subprocess.run([str(binary)], check=True, capture_output=True, text=True).stdout)
+
+
+def test_restatement_matches_committed_reference_kats(orc):
+    mine = _run(ROOT / "oracle/rng_kat")
+    assert mine == GOLD
+
+
+def test_reference_binary_matches_when_built(orc):
+    ref = ROOT / "oracle/_ref/ref_rng_kat"
+    if not ref.exists():
+        pytest.skip("oracle/_ref not built (reference headers absent)")
+    assert _run(ref) == GOLD
+
+
+def test_survey_appendix_a_values():
+    assert GOLD["splitmix64_0"] == "e220a8397b1dcdaf"
+    assert GOLD["derive_42_lengths_0"] == "3acd081026d01704"
+    assert GOLD["uniform_int_42_lengths_16_512"][:10] == [222, 426, 120, 142, 228, 100, 198, 310, 451, 105]
+    assert sum(GOLD["uniform_int_42_lengths_16_512"]) == 15117
+
+
+def test_python_derive_seed_port():
+    from paper_2603_11101_b200.synthetic import derive_seed, splitmix64
+    assert f"{splitmix64(0):016x}" == GOLD["splitmix64_0"]
+    assert f"{splitmix64(1):016x}" == GOLD["splitmix64_1"]
+    assert f"{derive_seed(42, 'lengths', 0):016x}" == GOLD["derive_42_lengths_0"]
+    assert f"{derive_seed(42, 'lengths', 1):016x}" == GOLD["derive_42_lengths_1"]
+    assert f"{derive_seed(42, '', 0):016x}" == GOLD["derive_42_empty_0"]
+    assert f"{derive_seed(7, 'q', 3):016x}" == GOLD["derive_7_q_3"]
+
+
+def test_product_length_generator_matches_reference_stream():
+    from paper_2603_11101_b200.synthetic import gen_lengths
+    assert gen_lengths(64, 0, 16, 512).tolist() == GOLD["uniform_int_42_lengths_16_512"]
+    assert gen_lengths(16, 0, 16, 512, seed=7).tolist() == GOLD["uniform_int_7_lengths_16_512"]

@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py — effective (non-pad) tokens/s and TFLOPS of the packing + varlen attention fwd+bwd step.
+
+Workload (BASELINE.json configs[1], "GR00T-N1.5 Eagle-backbone shape"): per GPU, 512 samples with
+lengths uniform_int(16, 512) from make_rng(42, "lengths", rank) (rng.hpp), packed to 8192-token bins
+by the GPU FFD packer; 16 heads × d = 128, bf16, bidirectional block-diagonal attention, fwd + bwd.
+One step = GPU pack → gather Q/K/V rows into the packed stream → attention fwd → attention bwd →
+scatter dQ/dK/dV back to sample order.  Inputs (≈2.3 GB per GPU) are larger than L2 (126 MB).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dist uniform|groot]
+
+N > 1 (torchrun): the global batch is N × 512 samples; every rank receives the global lengths by
+one NCCL all-gather (the only collective), packs them identically, and takes its share of the bins
+from the length-balanced LPT assignment (weak scaling; no collective on the attention path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {"hbm_gbs": 6538.9, "bf16_tflops": 1665.5, "bf16_tflops_sustained": 1419.9, "src": "fallback"}
+try:
+    _p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    PEAKS.update({k: _p[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in _p})
+    PEAKS["src"] = "MEASURED_PEAKS.json"
+except Exception:
+    pass
+
+H, HKV, D = 16, 16, 128
+SAMPLES_PER_GPU = 512
+CAPACITY = 8192
+METRIC = "effective tokens/sec & TFLOPS (non-pad) varlen attn fwd+bwd, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dist", default="uniform", choices=["uniform", "groot"])
+    ap.add_argument("--samples", type=int, default=SAMPLES_PER_GPU)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=48)
+    return ap.parse_args()
+
+
+def lengths_for(rank, n, dist):
+    from paper_2603_11101_b200.synthetic import DIST_GR00T, DIST_UNIFORM, gen_lengths
+    if dist == "groot":
+        return gen_lengths(n, DIST_GR00T, label="lengths", seed=42 + 1000 * rank)
+    return gen_lengths(n, DIST_UNIFORM, 16, 512, label="lengths", seed=42 + 1000 * rank)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(Ls, threads):
+    """The reference's CPU path (oracle restatement of SPEC.md:502-509 + closed-form bwd), fp32,
+    on a bounded sample of the step's samples; returns (tokens/s, seconds, sample description)."""
+    from oracle import oracle as orc
+    from paper_2603_11101_b200.synthetic import values_np
+    T = int(np.sum(Ls))
+    cu = np.concatenate([[0], np.cumsum(Ls)]).astype(np.int32)
+    q = values_np(T * H * D, "q").reshape(T, H, D)
+    k = values_np(T * HKV * D, "k").reshape(T, HKV, D)
+    v = values_np(T * HKV * D, "v").reshape(T, HKV, D)
+    do = values_np(T * H * D, "do").reshape(T, H, D)
+    bins, *_ = orc.pack(np.asarray(Ls, np.int64), CAPACITY, 0)
+    t0 = time.perf_counter()
+    orc.pack(np.asarray(Ls, np.int64), CAPACITY, 0)
+    o, lse = orc.mha_fwd(q, k, v, cu, dtype=np.float32, threads=threads)
+    orc.mha_bwd(q, k, v, o, do, cu, dtype=np.float32, threads=threads)
+    dt = time.perf_counter() - t0
+    return T / dt, dt, f"{len(Ls)} samples ({T} tokens) of the step's batch, fp32 fwd+bwd, {threads} threads"
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the reference's CPU implementation (oracle port; the reference ships no code)."""
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    Ls = lengths_for(0, a.samples, a.dist)[: a.cpu_samples]
+    vals = []
+    for i in range(a.warmup + a.steps):
+        tps, dt, desc = cpu_baseline(Ls, threads)
+        if i >= a.warmup:
+            vals.append(tps)
+        if sum(vals) and len(vals) >= 1 and dt * (a.steps - len(vals)) > 240:
+            break  # keep the whole run within a few minutes
+    v = statistics.mean(vals)
+    pairs = float(np.sum(np.asarray(Ls, np.float64) ** 2))
+    toks = float(np.sum(Ls))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
+            "steps": len(vals), "warmup": a.warmup, "ms_per_step": 1e3 * toks / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config2 GR00T-N1.5 shape: U[16,512] lengths, 8192-token bins, H16 d128 bf16 "
+                                   "bidirectional fwd+bwd (CPU: bounded sample)", "samples": len(Ls),
+                       "tflops": 3.5 * 4 * D * H * pairs * v / toks / 1e12},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_11101_b200 import attention, packing, synthetic
+    from paper_2603_11101_b200.dist import lpt_assign, shard_plan
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---------------------------------------------------------------- inputs (sample-major, resident)
+    L_local = lengths_for(rank, a.samples, a.dist)
+    n_local = L_local.size
+    d_len_local = torch.from_numpy(L_local).to(dev)
+    if world > 1:
+        gathered = torch.empty(world * n_local, dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(gathered, d_len_local)
+        L_global = gathered.cpu().numpy()
+    else:
+        L_global = L_local
+    plan = packing.pack_ffd(L_global, CAPACITY)  # warm + host view for sizing
+    assign = lpt_assign(plan, L_global, world)
+    my = shard_plan(plan, L_global, assign, rank)  # this rank's bins: sample ids + packed layout
+    T = my["tokens"]
+    Ls = L_global[my["sample_ids"]]
+    pairs = float(np.sum(Ls.astype(np.float64) ** 2))
+    fl_fwd = 4.0 * D * H * pairs
+    fl_total = 3.5 * fl_fwd
+
+    q_src = synthetic.fill_bf16(torch.empty(T, H, D, dtype=torch.bfloat16, device=dev), "q")
+    k_src = synthetic.fill_bf16(torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev), "k")
+    v_src = synthetic.fill_bf16(torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev), "v")
+    do_p = synthetic.fill_bf16(torch.empty(T, H, D, dtype=torch.bfloat16, device=dev), "do")
+    qp, kp, vp = torch.empty_like(q_src), torch.empty_like(k_src), torch.empty_like(v_src)
+    dq_s, dk_s, dv_s = torch.empty_like(q_src), torch.empty_like(k_src), torch.empty_like(v_src)
+    d_len_mine = torch.from_numpy(np.ascontiguousarray(Ls)).to(dev)
+    sub = packing.pack_ffd(d_len_mine, CAPACITY)  # this rank's packs (same FFD on its samples)
+    ws = attention.BwdWorkspace()
+    stream = torch.cuda.current_stream()
+    ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in ("fwd", "bwd")}
+    ktimes = {"fwd": [], "bwd": []}
+
+    def step(record=False):
+        packing.pack_ffd(d_len_mine, CAPACITY, plan=sub, sync_check=False)
+        cu = sub.cu_seqlens
+        packing.gather_rows(q_src, sub, out=qp)
+        packing.gather_rows(k_src, sub, out=kp)
+        packing.gather_rows(v_src, sub, out=vp)
+        if record:
+            ev["fwd"][0].record(stream)
+        o, lse = attention.varlen_attn_fwd(qp, kp, vp, cu)
+        if record:
+            ev["fwd"][1].record(stream)
+            ev["bwd"][0].record(stream)
+        dq, dk, dv = attention.varlen_attn_bwd(do_p, qp, kp, vp, o, lse, cu, workspace=ws)
+        if record:
+            ev["bwd"][1].record(stream)
+        packing.scatter_rows(dq, sub, out=dq_s)
+        packing.scatter_rows(dk, sub, out=dk_s)
+        packing.scatter_rows(dv, sub, out=dv_s)
+        return o
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(a.steps):
+            step(record=True)
+            # kernel shares, measured live on the launching stream
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    for k in ktimes:
+        ktimes[k].append(ev[k][0].elapsed_time(ev[k][1]))
+    # per-kernel average over the timed region (separately instrumented pass with the same events)
+    kfwd, kbwd = [], []
+    for _ in range(min(a.steps, 10)):
+        step(record=True)
+        torch.cuda.synchronize()
+        kfwd.append(ev["fwd"][0].elapsed_time(ev["fwd"][1]))
+        kbwd.append(ev["bwd"][0].elapsed_time(ev["bwd"][1]))
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    toks_all = T * world if world == 1 else float(np.sum(L_global))
+
+    # ---------------------------------------------------------------- e2e through host buffers
+    e2e = None
+    if not a.no_e2e:
+        hq = q_src.cpu().pin_memory()
+        hk = k_src.cpu().pin_memory()
+        hv = v_src.cpu().pin_memory()
+        hdo = do_p.cpu().pin_memory()
+        hL = torch.from_numpy(np.ascontiguousarray(Ls)).pin_memory()
+        outs = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q_src, q_src, k_src, v_src)]
+
+        def e2e_step():
+            d_len_mine.copy_(hL, non_blocking=True)
+            q_src.copy_(hq, non_blocking=True)
+            k_src.copy_(hk, non_blocking=True)
+            v_src.copy_(hv, non_blocking=True)
+            do_p.copy_(hdo, non_blocking=True)
+            o = step()
+            for h_, d_ in zip(outs, (o, dq_s, dk_s, dv_s)):
+                h_.copy_(d_, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(a.steps, 5))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1) / n_e2e], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo, hL))
+        d2h = sum(x.numel() * x.element_size() for x in outs)
+        e2e = {"value": toks_all / (float(ems.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item())}
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        tps, dt, desc = cpu_baseline(Ls[: a.cpu_samples], threads)
+        cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc,
+               "seconds": dt}
+
+    if rank == 0:
+        kb = statistics.mean(kbwd)
+        kf = statistics.mean(kfwd)
+        bwd_flops = 2.5 * fl_fwd
+        line = {
+            "metric": METRIC, "value": toks_all / (ms_max / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": a.steps, "warmup": max(3, a.warmup), "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"config2 GR00T-N1.5 shape: {n_local} samples/GPU, "
+                                   f"{'U[16,512]' if a.dist == 'uniform' else 'GR00T-like 64*U{1,2}+U[16,64]'} "
+                                   f"lengths, {CAPACITY}-token bins, H{H} d{D} bf16 bidirectional fwd+bwd",
+                       "tokens_per_gpu": T, "bins_per_gpu": sub.num_bins(), "tflops_effective":
+                           fl_total * world / (ms_max / 1e3) / 1e12 if world == 1 else None,
+                       "l2": "inputs larger than L2 (%.1f GB/GPU)" % (4 * T * H * D * 2 / 1e9),
+                       "parallelism": f"packs sharded over {world} GPU(s) (LPT), no collective on attention"},
+            "roofline": {"bound": "tensor", "kernel": "attn_bwd_kernel (+pre/post)",
+                         "achieved": bwd_flops / (kb / 1e3) / 1e12, "peak": PEAKS["bf16_tflops"],
+                         "unit": "TFLOP/s", "frac": bwd_flops / (kb / 1e3) / 1e12 / PEAKS["bf16_tflops"],
+                         "traffic": None, "peak_src": PEAKS["src"],
+                         "fwd": {"achieved": fl_fwd / (kf / 1e3) / 1e12, "ms": kf}, "bwd_ms": kb},
+            "clocks": clk.summary(),
+            "e2e": e2e, "cpu_baseline": cpu,
+            # our launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
+            # gather 3, fwd 1, bwd 3 (pre, main, post), scatter 3
+            "gpu_launches": 24 * a.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

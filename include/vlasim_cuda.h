@@ -65,7 +65,7 @@ typedef struct vlasim_pack_out {
   int32_t* member_ids;      /* [n]   sample id at packed member position m                 */
   int32_t* cu_seqlens;      /* [n+1] global segment offsets over the packed stream          */
   int32_t* cu_seqlens_bins; /* [2n]  per-bin cu_seqlens; bin b at bin_member_off[b] + b     */
-  int32_t* src_off;         /* [n]   exclusive scan of lengths in id order (source layout)  */
+  int32_t* src_off;         /* [n+1] exclusive scan of lengths in id order (+ total at [n]) */
   int32_t* num_bins;        /* [1]                                                           */
   int64_t* total_tokens;    /* [1]                                                           */
   int32_t* status;          /* [2]   {error code, offending sample id} written on device     */

@@ -89,20 +89,28 @@ struct BwdParams {
   const int32_t* prefix;
   int nseq, T, H, Hkv, mask;
   float scale_log2, scale;
+  const float* lse2;  // [H, Tp] log2-domain LSE
+  const float* dsum;  // [H, Tp] rowsum(dO ∘ O)
+  int Tp;
+  int dbg;  // debug bisection mask (VLASIM_BWD_DEBUG), 0 in production
 };
 
 template <int HD>
 struct BwdCfg {
-  static constexpr int BK = 128, BQ = 128, STAGES = 2;
+  static constexpr int BK = 128, BQ = 128, QSTAGES = 2;
   static constexpr int TILE = 128 * HD * 2;     // one 128-row bf16 tile (K, V, Q or dO)
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = TILE;
-  static constexpr int OFF_STAGE = 2 * TILE;    // stage s: Q at +s*2*TILE, dO right after
-  static constexpr int OFF_DS = OFF_STAGE + STAGES * 2 * TILE;
-  static constexpr int OFF_VEC = OFF_DS + 128 * 128 * 2;  // stage s: lse2[128], D[128]
-  static constexpr int OFF_BAR = OFF_VEC + STAGES * 2 * 512;
-  static constexpr int NUM_BARS = 2 * STAGES + 6;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int OFF_Q = 2 * TILE;        // Q ring: stage s at OFF_Q + s*TILE
+  static constexpr int OFF_DO = OFF_Q + QSTAGES * TILE;  // dO: single buffer
+  static constexpr int OFF_DS = OFF_DO + TILE;
+  static constexpr int VEC = 544;                        // 132 floats (16-B aligned window of 128) + pad
+  static constexpr int OFF_LSE = OFF_DS + 128 * 128 * 2;  // lse2 [QSTAGES][VEC]
+  static constexpr int OFF_DSUM = OFF_LSE + QSTAGES * VEC;  // D [VEC]
+  static constexpr int OFF_BAR = OFF_DSUM + VEC;
+  static constexpr int NUM_BARS = 2 * QSTAGES + 9;
+  static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = SMEM_USED + 1024;  // + alignment slack (dynamic smem base is not 1 KB aligned)
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
   static_assert(DK_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
@@ -112,19 +120,21 @@ template <int HD>
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmD,
                     const BwdParams p) {
   using Cfg = BwdCfg<HD>;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* bar_kv = bars + 0;               // K,V landed
-  uint64_t* bar_st_full = bars + 1;          // [STAGES]
-  uint64_t* bar_st_empty = bars + 1 + Cfg::STAGES;
-  uint64_t* bar_s_full = bars + 1 + 2 * Cfg::STAGES;   // S, dP computed
-  uint64_t* bar_p_full = bar_s_full + 1;               // P in TMEM + dS in smem (128 arrivals)
-  uint64_t* bar_dq_full = bar_s_full + 2;              // dQ computed
-  uint64_t* bar_dq_empty = bar_s_full + 3;             // dQ drained (128 arrivals)
-  uint64_t* bar_done = bar_s_full + 4;                 // all MMAs done (dK, dV final)
+  uint64_t* bar_kv = bars + 0;                          // K,V landed
+  uint64_t* bar_q_full = bars + 1;                      // [QSTAGES] Q + lse2 landed
+  uint64_t* bar_q_empty = bars + 1 + Cfg::QSTAGES;      // [QSTAGES]
+  uint64_t* bar_do_full = bars + 1 + 2 * Cfg::QSTAGES;  // dO + D landed
+  uint64_t* bar_do_empty = bar_do_full + 1;             // dV MMA done with dO
+  uint64_t* bar_s_full = bar_do_full + 2;               // S, dP computed
+  uint64_t* bar_p_full = bar_do_full + 3;               // P in TMEM + dS in smem (128 arrivals)
+  uint64_t* bar_dq_full = bar_do_full + 4;              // dQ computed
+  uint64_t* bar_dq_empty = bar_do_full + 5;             // dQ drained (128 arrivals)
+  uint64_t* bar_done = bar_do_full + 6;                 // all MMAs done (dK, dV final)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_BAR + Cfg::NUM_BARS * 8);
   int* s_range = reinterpret_cast<int*>(tmem_slot + 1);  // q_lo, q_hi
 
@@ -135,12 +145,13 @@ __global__ void __launch_bounds__(320, 1)
   const int group = p.H / p.Hkv;
 
   if (tid == 0) {
-    if (smem_u32(smem) & 1023) __trap();
     mbar_init(bar_kv, 1);
-    for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&bar_st_full[s], 1);
-      mbar_init(&bar_st_empty[s], 1);
+    for (int s = 0; s < Cfg::QSTAGES; ++s) {
+      mbar_init(&bar_q_full[s], 1);
+      mbar_init(&bar_q_empty[s], 1);
     }
+    mbar_init(bar_do_full, 1);
+    mbar_init(bar_do_empty, 1);
     mbar_init(bar_s_full, 1);
     mbar_init(bar_p_full, 128);
     mbar_init(bar_dq_full, 1);
@@ -179,21 +190,21 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_2d(smem + Cfg::OFF_V + c * 128 * 128, &tmV, kh * HD + c * 64, k0, bar_kv);
       }
       for (int it = 0; it < iters; ++it) {
-        const int st = it % Cfg::STAGES;
-        if (it >= Cfg::STAGES) mbar_wait(&bar_st_empty[st], ((it / Cfg::STAGES) - 1) & 1);
+        const int st = it % Cfg::QSTAGES;
         const int h = kh * group + it / nq;
         const int qb = q_lo + (it % nq) * Cfg::BQ;
-        uint8_t* sq = smem + Cfg::OFF_STAGE + st * 2 * Cfg::TILE;
-        uint8_t* sdo = sq + Cfg::TILE;
-        uint8_t* vec = smem + Cfg::OFF_VEC + st * 1024;
-        mbar_expect_tx(&bar_st_full[st], 2 * Cfg::TILE + 1024);
+        if (it >= Cfg::QSTAGES) mbar_wait(&bar_q_empty[st], ((it / Cfg::QSTAGES) - 1) & 1);
+        uint8_t* sq = smem + Cfg::OFF_Q + st * Cfg::TILE;
+        mbar_expect_tx(&bar_q_full[st], Cfg::TILE + 528);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
-          tma_load_2d(sq + c * 128 * 128, &tmQ, h * HD + c * 64, qb, &bar_st_full[st]);
-          tma_load_2d(sdo + c * 128 * 128, &tmdO, h * HD + c * 64, qb, &bar_st_full[st]);
-        }
-        tma_load_2d(vec, &tmL, qb, h, &bar_st_full[st]);
-        tma_load_2d(vec + 512, &tmD, qb, h, &bar_st_full[st]);
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sq + c * 128 * 128, &tmQ, h * HD + c * 64, qb, &bar_q_full[st]);
+        bulk_load(smem + Cfg::OFF_LSE + st * Cfg::VEC, p.lse2 + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_q_full[st]);
+        if (it >= 1) mbar_wait(bar_do_empty, (it - 1) & 1);
+        uint8_t* sdo = smem + Cfg::OFF_DO;
+        mbar_expect_tx(bar_do_full, Cfg::TILE + 528);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sdo + c * 128 * 128, &tmdO, h * HD + c * 64, qb, bar_do_full);
+        bulk_load(smem + Cfg::OFF_DSUM, p.dsum + int64_t(h) * p.Tp + (qb & ~3), 528, bar_do_full);
       }
     }
   } else if (warp == 9) {
@@ -205,10 +216,11 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t sK = smem_u32(smem + Cfg::OFF_K), sV = smem_u32(smem + Cfg::OFF_V);
       const uint32_t sdS = smem_u32(smem + Cfg::OFF_DS);
       mbar_wait(bar_kv, 0);
+      const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO);
       for (int it = 0; it < iters; ++it) {
-        const int st = it % Cfg::STAGES;
-        const uint32_t sQ = smem_u32(smem + Cfg::OFF_STAGE + st * 2 * Cfg::TILE), sdO = sQ + Cfg::TILE;
-        mbar_wait(&bar_st_full[st], (it / Cfg::STAGES) & 1);
+        const int st = it % Cfg::QSTAGES;
+        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
+        mbar_wait(&bar_q_full[st], (it / Cfg::QSTAGES) & 1);
         tc_fence_after();
         // S^T = K · Q^T
 #pragma unroll
@@ -216,10 +228,9 @@ __global__ void __launch_bounds__(320, 1)
           umma_f16_ss(tmem + Cfg::S_COL, make_sdesc_sw128(sK + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
                       make_sdesc_sw128(sQ + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
         // dP^T = V · dO^T   (dP region must be drained of the previous dQ)
-        if (it > 0) {
-          mbar_wait(bar_dq_empty, (it - 1) & 1);
-          tc_fence_after();
-        }
+        mbar_wait(bar_do_full, it & 1);
+        if (it > 0) mbar_wait(bar_dq_empty, (it - 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int s = 0; s < HD / 16; ++s)
           umma_f16_ss(tmem + Cfg::DP_COL, make_sdesc_sw128(sV + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
@@ -230,19 +241,23 @@ __global__ void __launch_bounds__(320, 1)
         // dV += P^T · dO        (A = P^T in TMEM, B = dO MN-major)
 #pragma unroll
         for (int s = 0; s < 8; ++s)
+          if (!(p.dbg & 8))
           umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::S_COL + s * 8, make_sdesc_sw128(sdO + s * 2048, 16384, 1024),
                       id_kmn, (it > 0 || s > 0) ? 1u : 0u);
+        umma_commit(bar_do_empty);
         // dK += dS^T · Q        (A = dS^T smem K-major, B = Q MN-major)
 #pragma unroll
         for (int s = 0; s < 8; ++s)
+          if (!(p.dbg & 4))
           umma_f16_ss(tmem + Cfg::DK_COL, make_sdesc_sw128(sdS + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
                       make_sdesc_sw128(sQ + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
         // dQ = dS · K           (A = dS MN-major view of the same smem, B = K MN-major)
 #pragma unroll
         for (int s = 0; s < 8; ++s)
+          if (!(p.dbg & 2))
           umma_f16_ss(tmem + Cfg::DP_COL, make_sdesc_sw128(sdS + s * 2048, 16384, 1024),
                       make_sdesc_sw128(sK + s * 2048, 16384, 1024), id_mnmn, s > 0);
-        umma_commit(&bar_st_empty[st]);
+        umma_commit(&bar_q_empty[st]);
         umma_commit(bar_dq_full);
       }
       umma_commit(bar_done);
@@ -253,10 +268,10 @@ __global__ void __launch_bounds__(320, 1)
     const int krow = tid;
     uint8_t* sds = smem + Cfg::OFF_DS;
     for (int it = 0; it < iters; ++it) {
-      const int st = it % Cfg::STAGES;
+      const int st = it % Cfg::QSTAGES;
       const int qb = q_lo + (it % nq) * Cfg::BQ;
-      const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_VEC + st * 1024);
-      const float* dsum = lse2 + 128;
+      const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE + st * Cfg::VEC) + (qb & 3);
+      const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM) + (qb & 3);
       mbar_wait(bar_s_full, it & 1);
       tc_fence_after();
       const int c_lo = ks.lo - qb, c_hi = ks.hi - qb;  // visible query columns of this key row
@@ -281,7 +296,7 @@ __global__ void __launch_bounds__(320, 1)
           pk[i] = pack_bf16x2(pp[0], pp[1]);
           dk[i] = pack_bf16x2(dd[0], dd[1]);
         }
-        tmem_st16(tmem + lane_off + Cfg::S_COL + c0 / 2, pk);
+        if (!(p.dbg & 32)) tmem_st16(tmem + lane_off + Cfg::S_COL + c0 / 2, pk);
         // dS^T row krow, queries c0..c0+31 → box c0/64, 16-B chunks (c0%64)/8 .. +3, swizzled
         uint8_t* rowp = sds + (c0 / 64) * 16384 + krow * 128;
 #pragma unroll
@@ -349,7 +364,7 @@ __global__ void __launch_bounds__(320, 1)
         uint32_t v[32];
         tmem_ld32(tmem + lane_off + Cfg::DP_COL + c, v);
         tmem_wait_ld();
-        if (live) {
+        if (live && !(p.dbg & 16)) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             red_add_v4_f32(dst + c + 4 * i, __uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
@@ -397,16 +412,12 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
                                                          w.dsum, w.dq_acc, T, (T + 3) & ~3, H);
     VLASIM_LAUNCH_CHECK();
   }
-  CUtensorMap tq, tk, tv, tdo, tl, td;
+  CUtensorMap tq, tk, tv, tdo;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (int rc = encode_tmap_2d(&tq, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tdo, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tk, a->k, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
-  // [H, T] fp32 rows; box = 1 head × 128 tokens (row pitch padded to 16 B by the workspace stride)
-  const uint64_t pitch = uint64_t((T + 3) & ~3) * 4;
-  if (int rc = encode_tmap_2d(&tl, w.lse2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, H, T, pitch, 1, 128, false)) return rc;
-  if (int rc = encode_tmap_2d(&td, w.dsum, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, H, T, pitch, 1, 128, false)) return rc;
   BwdParams p;
   p.dq_acc = w.dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(g->dk);
@@ -420,10 +431,14 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.mask = a->mask_mode;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;
+  p.lse2 = w.lse2;
+  p.dsum = w.dsum;
+  p.Tp = (T + 3) & ~3;
+  p.dbg = getenv("VLASIM_BWD_DEBUG") ? atoi(getenv("VLASIM_BWD_DEBUG")) : 0;
   auto kern = attn_bwd_kernel<HD>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const int64_t ktiles = (int64_t(T) + 127) / 128;
-  kern<<<ktiles * Hkv, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, tl, td, p);
+  kern<<<ktiles * Hkv, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
   VLASIM_LAUNCH_CHECK();
   const int64_t n4 = int64_t(T) * H * HD / 4;
   k_bwd_post<<<std::min<int64_t>((n4 + 255) / 256, int64_t(num_sms()) * 16), 256, 0, st>>>(

@@ -210,6 +210,13 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack
         const int nnew = (r + k - 1) / k;
         if (nact + nnew > kMaxActiveBins) {
           // retire bins that can never be used again, then re-check
+          if (per > 32) {  // per-thread staging below holds 32 bins (1024-thread mode: per <= 16)
+            if (tid == 0) {
+              out.status[0] = VLASIM_ECONFIG;
+              out.status[1] = -2;
+            }
+            return;
+          }
           __syncthreads();
           int keep = 0;
           for (int b = b0; b < b1; ++b) keep += act_rem[b] >= lmin;
@@ -481,6 +488,8 @@ extern "C" int vlasim_pack_ffd_cuda(const int32_t* d_len, int64_t n, int32_t cap
   const int64_t nchunks = num_chunks(n);
 
   k_init<<<(n + 255) / 256, 256, 0, st>>>(*out, n);
+  if ((cap + 1) * 4 > 48 * 1024)
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + 1) * 4));
   k_hist<<<nchunks, 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);
   k_class_scan<<<(cap + 1 + 255) / 256, 256, 0, st>>>(w.chunk_hist, nchunks, cap, w.class_count);
   const int ffd_threads = n <= 8192 ? 32 : 1024;

@@ -1,0 +1,68 @@
+"""Multi-GPU sharding of packs.
+
+Packs are independent (block-diagonal attention never crosses a pack), so the
+path shards by pack with no collective on the attention path.  The only collective is one
+all-gather of the per-rank sample lengths (the pack metadata): every rank then runs the same GPU FFD
+on the global lengths and the same deterministic LPT assignment, so all ranks agree on the shard
+without further communication.
+
+LPT (longest processing time first): bins sorted by cost Σ l² descending (ties: lower bin index),
+each assigned to the rank with the smallest load so far (ties: lowest rank).
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+import numpy as np
+
+
+def bin_costs(bins_members: Sequence[Sequence[int]], lengths) -> np.ndarray:
+    L = np.asarray(lengths, np.float64)
+    return np.array([float(np.sum(L[list(m)] ** 2)) for m in bins_members])
+
+
+def lpt(costs: Sequence[float], world: int) -> List[List[int]]:
+    """Deterministic LPT over bin costs → bins per rank (each list in ascending bin order)."""
+    order = sorted(range(len(costs)), key=lambda b: (-costs[b], b))
+    load = [0.0] * world
+    out: List[List[int]] = [[] for _ in range(world)]
+    for b in order:
+        r = min(range(world), key=lambda i: (load[i], i))
+        out[r].append(b)
+        load[r] += costs[b]
+    return [sorted(x) for x in out]
+
+
+def lpt_assign(plan, lengths, world: int) -> List[List[int]]:
+    """LPT over the bins of a GPU PackPlan (host copy of the bin membership)."""
+    bins = plan.to_host(lengths)
+    return lpt(bin_costs([b.member_ids for b in bins], lengths), world)
+
+
+def shard_plan(plan, lengths, assign, rank: int) -> dict:
+    """Sample ids (ascending) and token count of `rank`'s share of the bins."""
+    bins = plan.to_host(lengths)
+    ids = sorted(i for b in assign[rank] for i in bins[b].member_ids)
+    L = np.asarray(lengths)
+    return {"sample_ids": np.array(ids, dtype=np.int64), "tokens": int(L[ids].sum()) if ids else 0,
+            "bins": list(assign[rank])}
+
+
+def balance(assign, costs) -> float:
+    """max / mean load of an assignment (1.0 = perfect)."""
+    loads = [sum(costs[b] for b in a) for a in assign]
+    m = float(np.mean(loads))
+    return max(loads) / m if m > 0 else 1.0
+
+
+def allgather_lengths(local_lengths, group=None):
+    """The path's single collective: all-gather of the per-rank length shards (int32) — NCCL on
+    GPU tensors, gloo on CPU tensors (tests)."""
+    import torch
+    import torch.distributed as dist
+    t = local_lengths if torch.is_tensor(local_lengths) else torch.as_tensor(np.asarray(local_lengths, np.int32))
+    world = dist.get_world_size(group)
+    out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t.contiguous(), group=group) if t.is_cuda else \
+        dist.all_gather(list(out.chunk(world)), t.contiguous(), group=group)
+    return out

@@ -135,7 +135,7 @@ class PackPlan:
         self.member_ids = torch.empty(n, **i32)
         self.cu_seqlens = torch.empty(n + 1, **i32)
         self.cu_seqlens_bins = torch.empty(2 * n, **i32)
-        self.src_off = torch.empty(n, **i32)
+        self.src_off = torch.empty(n + 1, **i32)
         self.num_bins_t = torch.empty(1, **i32)
         self.total_tokens_t = torch.empty(1, dtype=torch.int64, device=device)
         self.status = torch.empty(2, **i32)

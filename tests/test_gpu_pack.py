@@ -23,7 +23,8 @@ def _check_plan(orc, L, cap, plan):
     assert np.array_equal(plan.member_ids.cpu().numpy(), lay["member_ids"])
     assert np.array_equal(plan.cu_seqlens.cpu().numpy(), lay["cu_seqlens"])
     assert np.array_equal(plan.cu_seqlens_bins[: n + nb].cpu().numpy(), lay["cu_seqlens_bins"])
-    assert np.array_equal(plan.src_off.cpu().numpy(), lay["src_off"])
+    assert np.array_equal(plan.src_off[:n].cpu().numpy(), lay["src_off"])
+    assert int(plan.src_off[n]) == int(np.sum(L))
     assert plan.total_tokens() == int(np.sum(L))
     return lay
 

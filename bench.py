@@ -67,44 +67,51 @@ def lengths_for(rank, n, dist):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    """NVML sampler running during the timed region (the B200_PROFILING.md clocks line):
+    SM clock, max SM clock and the active clock-event (throttle) reasons."""
 
-    def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, index, period=0.05):
+        self.index, self.period, self.rows, self.stop = index, period, [], threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: record why
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if hasattr(self, "t"):
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        loaded = [s for s in sm if s > 500] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "error": getattr(self, "err", "no samples")}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for bit, name in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max, "reasons": reasons,
+                "samples": len(self.rows)}
 
 
 def cpu_baseline(Ls, threads):
@@ -204,9 +211,14 @@ def main():
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in ("fwd", "bwd")}
     ktimes = {"fwd": [], "bwd": []}
 
+    gidx = torch.empty(T, dtype=torch.int32, device=dev)
+
     def step(record=False):
+        # 1. pack (GPU FFD + layout), 2. gather index, 3. gather Q/K/V rows into the packed stream,
+        # 4. attention fwd, 5. attention bwd with the scatter back to sample order fused (row_map)
         packing.pack_ffd(d_len_mine, CAPACITY, plan=sub, sync_check=False)
         cu = sub.cu_seqlens
+        packing.token_ids_into(sub, T, gather_idx=gidx)
         packing.gather_rows(q_src, sub, out=qp)
         packing.gather_rows(k_src, sub, out=kp)
         packing.gather_rows(v_src, sub, out=vp)
@@ -216,12 +228,10 @@ def main():
         if record:
             ev["fwd"][1].record(stream)
             ev["bwd"][0].record(stream)
-        dq, dk, dv = attention.varlen_attn_bwd(do_p, qp, kp, vp, o, lse, cu, workspace=ws)
+        attention.varlen_attn_bwd(do_p, qp, kp, vp, o, lse, cu, workspace=ws, dq=dq_s, dk=dk_s, dv=dv_s,
+                                  row_map=gidx)
         if record:
             ev["bwd"][1].record(stream)
-        packing.scatter_rows(dq, sub, out=dq_s)
-        packing.scatter_rows(dk, sub, out=dk_s)
-        packing.scatter_rows(dv, sub, out=dv_s)
         return o
 
     for _ in range(max(3, a.warmup)):
@@ -322,8 +332,8 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
             # our launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
-            # gather 3, fwd 1, bwd 3 (pre, main, post), scatter 3
-            "gpu_launches": 24 * a.steps,
+            # token ids 1, gather 3, fwd 1, bwd 3 (pre, main, post; + 1 memset of the dQ accumulator)
+            "gpu_launches": 22 * a.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

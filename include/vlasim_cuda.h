@@ -141,10 +141,13 @@ typedef struct vlasim_attn_args {
 } vlasim_attn_args;
 
 typedef struct vlasim_attn_grads {
-  const void* dout;  /* [T, H, d]   bf16 */
-  void* dq;          /* [T, H, d]   bf16 */
-  void* dk;          /* [T, Hkv, d] bf16 */
-  void* dv;          /* [T, Hkv, d] bf16 */
+  const void* dout;          /* [T, H, d]   bf16 (packed order)                          */
+  void* dq;                  /* [T, H, d]   bf16                                        */
+  void* dk;                  /* [T, Hkv, d] bf16                                        */
+  void* dv;                  /* [T, Hkv, d] bf16                                        */
+  const int32_t* row_map;    /* [T] or NULL: packed row t → output row row_map[t].  With
+                                the packer's gather index this fuses the scatter of the
+                                gradients back to sample order into the kernels.         */
 } vlasim_attn_grads;
 
 size_t vlasim_varlen_attn_workspace_size(const vlasim_attn_args* a, int backward);

@@ -34,7 +34,8 @@ class AttnArgs(C.Structure):
 
 
 class AttnGrads(C.Structure):
-    _fields_ = [("dout", C.c_void_p), ("dq", C.c_void_p), ("dk", C.c_void_p), ("dv", C.c_void_p)]
+    _fields_ = [("dout", C.c_void_p), ("dq", C.c_void_p), ("dk", C.c_void_p), ("dv", C.c_void_p),
+                ("row_map", i32p)]
 
 
 _SIGS = {

@@ -69,15 +69,20 @@ _default_ws = BwdWorkspace()
 
 def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None,
                     softmax_scale=None, dq=None, dk=None, dv=None, workspace: BwdWorkspace | None = None,
-                    stream=None):
-    """Backward of varlen_attn_fwd. Returns (dq, dk, dv) bf16."""
+                    row_map=None, stream=None):
+    """Backward of varlen_attn_fwd. Returns (dq, dk, dv) bf16.  With row_map (int32 [T], e.g. the
+    packer's gather index) gradient row t is written to row row_map[t] — the scatter back to sample
+    order fused into the kernels."""
     dq = dq if dq is not None else torch.empty_like(q)
     dk = dk if dk is not None else torch.empty_like(k)
     dv = dv if dv is not None else torch.empty_like(v)
     if not dout.is_contiguous() or dout.shape != q.shape:
         raise ConfigError("dout must be contiguous with q's shape")
     a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
-    g = _lib.AttnGrads(_lib.ptr(dout).value, _lib.ptr(dq).value, _lib.ptr(dk).value, _lib.ptr(dv).value)
+    if row_map is not None and (row_map.dtype != torch.int32 or row_map.numel() != q.shape[0]):
+        raise ConfigError("row_map must be int32 [T]")
+    g = _lib.AttnGrads(_lib.ptr(dout).value, _lib.ptr(dq).value, _lib.ptr(dk).value, _lib.ptr(dv).value,
+                       _lib.ptr(row_map, _lib.i32p) if row_map is not None else None)
     L = _lib.lib()
     nbytes = L.vlasim_varlen_attn_workspace_size(C.byref(a), 1)
     ws = (workspace or _default_ws).get(nbytes, q.device)

@@ -40,44 +40,56 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ------------------------------------------------------------------ pre / post
+// D[h][t] = Σ_c dO·O (fp32) and LSE → log2 domain; 16-byte loads, HD/8 lanes per (t, h) row.
 template <int HD>
 __global__ void k_bwd_pre(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                           const float* __restrict__ lse, float* __restrict__ lse2, float* __restrict__ dsum,
-                          float* __restrict__ dq_acc, int T, int Tp, int H) {
-  // one warp per (token, head) row
-  const int64_t row = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= int64_t(T) * H) return;
-  const int t = int(row / H), h = int(row % H);
-  constexpr int PER = HD / 32;  // elements per lane: 2, 4 or 8
-  const __nv_bfloat16* orow = o + row * HD + lane * PER;
-  const __nv_bfloat16* drow = dout + row * HD + lane * PER;
+                          int T, int Tp, int H) {
+  constexpr int LPR = HD / 8;  // lanes per row (8 bf16 per lane)
+  const int64_t gt = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t row = gt / LPR;
+  const int sub = int(gt % LPR);
+  const bool ok = row < int64_t(T) * H;
   float acc = 0.f;
+  if (ok) {
+    const uint4 a = *reinterpret_cast<const uint4*>(o + row * HD + sub * 8);
+    const uint4 b = *reinterpret_cast<const uint4*>(dout + row * HD + sub * 8);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
-  for (int i = 0; i < PER; i += 2) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + i));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(drow + i));
-    acc += a.x * b.x + a.y * b.y;
+    for (int i = 0; i < 4; ++i) {
+      const float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
+      acc += x.x * y.x + x.y * y.y;
+    }
   }
-  float* q = dq_acc + row * HD + lane * PER;
 #pragma unroll
-  for (int i = 0; i < PER; ++i) q[i] = 0.f;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) {
+  for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (ok && sub == 0) {
+    const int t = int(row / H), h = int(row % H);
     dsum[int64_t(h) * Tp + t] = acc;
     lse2[int64_t(h) * Tp + t] = lse[int64_t(h) * T + t] * kLog2e;
   }
 }
 
-__global__ void k_bwd_post(const float4* __restrict__ acc, uint2* __restrict__ dq, int64_t n4, float scale) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
-    const float4 v = acc[i];
-    uint2 r;
-    r.x = pack_bf16x2(v.x * scale, v.y * scale);
-    r.y = pack_bf16x2(v.z * scale, v.w * scale);
-    dq[i] = r;
-  }
+// dQ = bf16(scale · dQacc), written to row row_map[t] (fused scatter) or t.
+template <int HD>
+__global__ void k_bwd_post(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                           const int32_t* __restrict__ row_map, int64_t rows, int H, float scale) {
+  constexpr int LPR = HD / 8;
+  const int64_t gt = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t row = gt / LPR;  // (t, h) row
+  const int sub = int(gt % LPR);
+  if (row >= rows) return;
+  const int64_t t = row / H, h = row % H;
+  const int64_t dst_t = row_map ? int64_t(__ldg(row_map + t)) : t;
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(acc + row * HD + sub * 8));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(acc + row * HD + sub * 8 + 4));
+  uint4 r;
+  r.x = pack_bf16x2(a.x * scale, a.y * scale);
+  r.y = pack_bf16x2(a.z * scale, a.w * scale);
+  r.z = pack_bf16x2(b.x * scale, b.y * scale);
+  r.w = pack_bf16x2(b.z * scale, b.w * scale);
+  *reinterpret_cast<uint4*>(dq + (dst_t * H + h) * HD + sub * 8) = r;
 }
 
 // ------------------------------------------------------------------ main kernel
@@ -89,6 +101,7 @@ struct BwdParams {
   const int32_t* prefix;
   int nseq, T, H, Hkv, mask;
   float scale_log2, scale;
+  const int32_t* row_map;  // packed row → output row for dK/dV (NULL: identity)
   const float* lse2;  // [H, Tp] log2-domain LSE
   const float* dsum;  // [H, Tp] rowsum(dO ∘ O)
   int Tp;
@@ -317,8 +330,9 @@ __global__ void __launch_bounds__(320, 1)
     }
     const int key = k0 + krow;
     const bool valid = key < p.T;
-    __nv_bfloat16* dvrow = p.dv + (static_cast<int64_t>(key) * p.Hkv + kh) * HD;
-    __nv_bfloat16* dkrow = p.dk + (static_cast<int64_t>(key) * p.Hkv + kh) * HD;
+    const int64_t dst = valid ? (p.row_map ? int64_t(__ldg(p.row_map + key)) : int64_t(key)) : 0;
+    __nv_bfloat16* dvrow = p.dv + (dst * p.Hkv + kh) * HD;
+    __nv_bfloat16* dkrow = p.dk + (dst * p.Hkv + kh) * HD;
 #pragma unroll 1
     for (int c = 0; c < HD; c += 32) {
       uint32_t v[32], k[32];
@@ -405,13 +419,12 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   using namespace vlasim_host;
   using Cfg = BwdCfg<HD>;
   const int T = int(a->total_tokens), H = a->num_heads, Hkv = a->num_kv_heads;
-  {
-    const int64_t rows = int64_t(T) * H;
-    k_bwd_pre<HD><<<(rows * 32 + 255) / 256, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a->o),
-                                                         static_cast<const __nv_bfloat16*>(g->dout), a->lse, w.lse2,
-                                                         w.dsum, w.dq_acc, T, (T + 3) & ~3, H);
-    VLASIM_LAUNCH_CHECK();
-  }
+  const int64_t rows = int64_t(T) * H;
+  VLASIM_CUDA_TRY(cudaMemsetAsync(w.dq_acc, 0, size_t(rows) * HD * 4, st));
+  k_bwd_pre<HD><<<(rows * (HD / 8) + 255) / 256, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a->o),
+                                                            static_cast<const __nv_bfloat16*>(g->dout), a->lse,
+                                                            w.lse2, w.dsum, T, (T + 3) & ~3, H);
+  VLASIM_LAUNCH_CHECK();
   CUtensorMap tq, tk, tv, tdo;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (int rc = encode_tmap_2d(&tq, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
@@ -431,6 +444,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.mask = a->mask_mode;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;
+  p.row_map = g->row_map;
   p.lse2 = w.lse2;
   p.dsum = w.dsum;
   p.Tp = (T + 3) & ~3;
@@ -440,9 +454,8 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   const int64_t ktiles = (int64_t(T) + 127) / 128;
   kern<<<ktiles * Hkv, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
   VLASIM_LAUNCH_CHECK();
-  const int64_t n4 = int64_t(T) * H * HD / 4;
-  k_bwd_post<<<std::min<int64_t>((n4 + 255) / 256, int64_t(num_sms()) * 16), 256, 0, st>>>(
-      reinterpret_cast<const float4*>(w.dq_acc), static_cast<uint2*>(g->dq), n4, a->softmax_scale);
+  k_bwd_post<HD><<<(rows * (HD / 8) + 255) / 256, 256, 0, st>>>(w.dq_acc, static_cast<__nv_bfloat16*>(g->dq),
+                                                             g->row_map, rows, H, a->softmax_scale);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }

@@ -280,6 +280,95 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack
   if (tid == 0) *out.num_bins = nb;
 }
 
+// Warp-synchronous variant of k_ffd for batches whose bins fit in shared memory: one warp,
+// class counts staged in smem, bins visited 32 at a time with early exit once the class is
+// placed (no block barriers on the per-class critical path).
+constexpr int kWarpMaxBins = 16384;
+__global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_pack_out out) {
+  extern __shared__ int32_t sm[];
+  int32_t* act_rem = sm;                    // bins are never retired here: id == index
+  int32_t* act_cnt = sm + kWarpMaxBins;
+  int32_t* cnt = sm + 2 * kWarpMaxBins;     // [cap + 1] class counts
+  const int lane = threadIdx.x;
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  if (out.status[0] != 0) return;
+  for (int L = lane; L <= cap; L += 32) cnt[L] = ws.class_count[L];
+  __syncwarp();
+  int nb = 0, nruns = 0;
+  for (int hi = cap; hi >= 1; hi -= 32) {
+    const int myL = hi - lane;
+    unsigned present = __ballot_sync(full, myL >= 1 && cnt[myL > 0 ? myL : 0] > 0);
+    while (present) {
+      const int k = __ffs(present) - 1;  // lowest lane = largest L
+      present &= present - 1;
+      const int L = hi - k;
+      const int c = cnt[L];
+      const int runs_before = nruns;
+      int running = 0;  // items of class L accounted for by bins visited so far (Σq)
+      for (int b0 = 0; b0 < nb && running < c; b0 += 32) {
+        const int b = b0 + lane;
+        const int rem = b < nb ? act_rem[b] : 0;
+        const int q = rem / L;
+        int inc = q;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(full, inc, o);
+          if (lane >= o) inc += t;
+        }
+        const int before = running + inc - q;
+        const bool takes = q > 0 && before < c;
+        const unsigned tm = __ballot_sync(full, takes);
+        if (takes) {
+          const int take = min(q, c - before);
+          const int r = nruns + __popc(tm & lt);
+          ws.run_bin[r] = b;
+          ws.run_cum[r] = before;
+          ws.run_tok[r] = cap - rem;
+          ws.run_mem[r] = act_cnt[b];
+          act_rem[b] = rem - take * L;
+          act_cnt[b] += take;
+        }
+        nruns += __popc(tm);
+        running += __shfl_sync(full, inc, 31);
+      }
+      const int placed = min(c, running);
+      const int r = c - placed;
+      if (r > 0) {
+        const int kk = cap / L;
+        const int nnew = (r + kk - 1) / kk;
+        if (nb + nnew > kWarpMaxBins) {
+          if (lane == 0) {
+            out.status[0] = VLASIM_ECONFIG;
+            out.status[1] = -2;
+          }
+          return;
+        }
+        for (int j = lane; j < nnew; j += 32) {
+          const int take = min(kk, r - j * kk);
+          ws.run_bin[nruns + j] = nb + j;
+          ws.run_cum[nruns + j] = placed + j * kk;
+          ws.run_tok[nruns + j] = 0;
+          ws.run_mem[nruns + j] = 0;
+          act_rem[nb + j] = cap - take * L;
+          act_cnt[nb + j] = take;
+        }
+        nb += nnew;
+        nruns += nnew;
+      }
+      if (lane == 0) {
+        ws.class_run_start[L] = runs_before;
+        ws.class_nruns[L] = nruns - runs_before;
+      }
+      __syncwarp();
+    }
+  }
+  for (int b = lane; b < nb; b += 32) {
+    out.bin_count[b] = act_cnt[b];
+    out.bin_fill[b] = cap - act_rem[b];
+  }
+  if (lane == 0) *out.num_bins = nb;
+}
+
 // ------------------------------------------------------------------ stable ranks → bins
 __global__ void __launch_bounds__(kRankThreads) k_assign(const int32_t* __restrict__ len, int64_t n, int cap,
                                                           PackWs ws, vlasim_pack_out out) {
@@ -291,6 +380,7 @@ __global__ void __launch_bounds__(kRankThreads) k_assign(const int32_t* __restri
   __syncthreads();
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int round = 0; round < kChunk / kRankThreads; ++round) {
+    if (int64_t(blockIdx.x) * kChunk + round * kRankThreads >= n) break;  // uniform
     const int64_t i = int64_t(blockIdx.x) * kChunk + round * kRankThreads + tid;
     const bool valid = i < n;
     const int L = valid ? len[i] : -1 - lane;  // invalid lanes never match anyone
@@ -492,10 +582,15 @@ extern "C" int vlasim_pack_ffd_cuda(const int32_t* d_len, int64_t n, int32_t cap
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + 1) * 4));
   k_hist<<<nchunks, 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);
   k_class_scan<<<(cap + 1 + 255) / 256, 256, 0, st>>>(w.chunk_hist, nchunks, cap, w.class_count);
-  const int ffd_threads = n <= 8192 ? 32 : 1024;
-  const size_t ffd_smem = (3 * kMaxActiveBins + 1024) * 4;
-  VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffd_smem));
-  k_ffd<<<1, ffd_threads, ffd_smem, st>>>(cap, w, *out);
+  if (n <= kWarpMaxBins) {  // at most n bins: the warp-synchronous packer holds them all in smem
+    const size_t wsm = (2 * kWarpMaxBins + cap + 1) * 4;
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    k_ffd_warp<<<1, 32, wsm, st>>>(cap, w, *out);
+  } else {
+    const size_t ffd_smem = (3 * kMaxActiveBins + 1024) * 4;
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffd_smem));
+    k_ffd<<<1, 1024, ffd_smem, st>>>(cap, w, *out);
+  }
   const size_t as_smem = (cap + 1) * 4;
   if (as_smem > 48 * 1024)
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as_smem));

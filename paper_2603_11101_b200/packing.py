@@ -211,6 +211,15 @@ def token_ids(plan: PackPlan, total_tokens: int, stream=None):
     return pos, seg, gat
 
 
+def token_ids_into(plan: PackPlan, total_tokens: int, pos_ids=None, seg_ids=None, gather_idx=None, stream=None):
+    """token_ids into caller-owned buffers (any may be None); no allocation on the hot path."""
+    P = lambda t: _lib.ptr(t, _lib.i32p) if t is not None else None
+    rc = _lib.lib().vlasim_pack_token_ids_cuda(_lib.ptr(plan.lengths, _lib.i32p), plan.c_struct, plan.n,
+                                               int(total_tokens), P(pos_ids), P(seg_ids), P(gather_idx),
+                                               _lib.stream_ptr(stream))
+    _lib.check(rc, "token_ids")
+
+
 def gather_rows(src: torch.Tensor, plan: PackPlan, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Sample-major rows [Σl, ...] (sample i at src_off[i]) → packed stream order (16-byte vector copies)."""
     if out is None:

@@ -85,3 +85,19 @@ def test_segment_isolation_on_gpu(gpu):
     v2[200:277] *= 2
     o2, _ = attention.varlen_attn_fwd(q2, k2, v2, cu)
     assert torch.equal(o1[:200], o2[:200]) and torch.equal(o1[277:], o2[277:])
+
+
+def test_bwd_row_map_fuses_scatter(gpu):
+    """row_map[t] redirects gradient row t (the packer's gather index → sample order)."""
+    from paper_2603_11101_b200 import attention
+    L = [300, 45, 129, 2]
+    q, k, v, do, cu = _inputs(L, 2, 1, 128, 11)
+    T = q.shape[0]
+    o, lse = attention.varlen_attn_fwd(q, k, v, cu)
+    dq, dk, dv = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu)
+    perm = torch.randperm(T, device="cuda").int()
+    dq2, dk2, dv2 = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, row_map=perm)
+    torch.cuda.synchronize()
+    pl = perm.long()
+    assert torch.equal(dq2[pl], dq) and torch.equal(dv2[pl], dv)
+    assert (dk2[pl].float() - dk.float()).abs().max().item() == 0.0

@@ -99,5 +99,6 @@ def test_bwd_row_map_fuses_scatter(gpu):
     dq2, dk2, dv2 = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, row_map=perm)
     torch.cuda.synchronize()
     pl = perm.long()
-    assert torch.equal(dq2[pl], dq) and torch.equal(dv2[pl], dv)
-    assert (dk2[pl].float() - dk.float()).abs().max().item() == 0.0
+    # dK/dV rows are produced by exactly one CTA (deterministic); dQ accumulates with fp32 atomics
+    assert torch.equal(dv2[pl], dv) and torch.equal(dk2[pl], dk)
+    assert (dq2[pl].float() - dq.float()).abs().max().item() <= 1e-2 * max(1.0, dq.float().abs().max().item())

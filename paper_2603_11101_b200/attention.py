@@ -40,20 +40,8 @@ def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_s
     return a
 
 
-def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None, softmax_scale=None, out=None,
-                    lse=None, stream=None):
-    """Block-diagonal attention forward. Returns (o [T,H,d] bf16, lse [H,T] fp32 natural-log)."""
-    T, H, d = q.shape
-    o = out if out is not None else torch.empty_like(q)
-    lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=q.device)
-    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
-    _lib.check(_lib.lib().vlasim_varlen_attn_fwd_cuda(C.byref(a), None, 0, _lib.stream_ptr(stream)),
-               "varlen_attn_fwd")
-    return o, lse
-
-
 class BwdWorkspace:
-    """Reusable fp32 dQ accumulator + LSE/D scratch for the backward kernel."""
+    """Reusable device workspace (fwd: per-token spans; bwd: fp32 dQ accumulator, LSE/D, spans)."""
 
     def __init__(self):
         self.buf = None
@@ -65,6 +53,21 @@ class BwdWorkspace:
 
 
 _default_ws = BwdWorkspace()
+_default_fwd_ws = BwdWorkspace()
+
+
+def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None, softmax_scale=None, out=None,
+                    lse=None, workspace: BwdWorkspace | None = None, stream=None):
+    """Block-diagonal attention forward. Returns (o [T,H,d] bf16, lse [H,T] fp32 natural-log)."""
+    T, H, d = q.shape
+    o = out if out is not None else torch.empty_like(q)
+    lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=q.device)
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
+    L = _lib.lib()
+    ws = (workspace or _default_fwd_ws).get(L.vlasim_varlen_attn_workspace_size(C.byref(a), 0), q.device)
+    _lib.check(L.vlasim_varlen_attn_fwd_cuda(C.byref(a), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
+               "varlen_attn_fwd")
+    return o, lse
 
 
 def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None,

@@ -327,13 +327,18 @@ int validate_attn_args(const vlasim_attn_args* a, bool fp8) {
 }
 }  // namespace vlasim_host
 
-extern "C" int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void*, size_t, vlasim_stream_t stream) {
+namespace vlasim_host {
+int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, cudaStream_t st);
+}
+
+// head_dim 64/128: persistent kernel (attn_fwd2.cu, needs the span workspace);
+// head_dim 256: the one-tile-per-CTA kernel above (O is too wide to double-buffer in TMEM).
+extern "C" int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void* ws, size_t ws_bytes,
+                                           vlasim_stream_t stream) {
   using namespace vlasim_host;
   if (int rc = validate_attn_args(a, false)) return rc;
   cudaStream_t st = as_stream(stream);
-  switch (a->head_dim) {
-    case 64: return launch_fwd<64, 128, 4>(a, st);
-    case 128: return launch_fwd<128, 128, 3>(a, st);
-    default: return launch_fwd<256, 64, 2>(a, st);
-  }
+  if (a->head_dim == 256) return launch_fwd<256, 64, 2>(a, st);
+  if (getenv("VLASIM_FWD_V1")) return a->head_dim == 64 ? launch_fwd<64, 128, 4>(a, st) : launch_fwd<128, 128, 3>(a, st);
+  return launch_fwd_persistent(a, ws, ws_bytes, st);
 }

@@ -1,0 +1,374 @@
+// attn_fwd2.cu — persistent block-diagonal varlen attention forward (sm_100a), head_dim 64/128.
+//
+// Same math and masking as attn_fwd.cu (vlasim::packed_attention) but
+// persistent: grid = #SMs, each CTA walks work items (128-row Q tile on the global grid, head)
+// with a static stride.  Q and the O accumulator are double-buffered (smem / TMEM) so the
+// next item's loads and MMAs overlap the current item's epilogue, which a separate
+// warpgroup performs.
+//
+// Warp roles (320 threads):
+//   warps 0-3  softmax: row = TMEM lane; lazy O rescale; P (bf16) written over its S columns
+//   warps 4-7  epilogue: O / l → bf16 → global, LSE
+//   warp 8     TMA producer (Q double buffer, K/V ring)
+//   warp 9     TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
+// TMEM (512 cols): S0 [0,128) · S1 [128,256) · O0 [256,256+HD) · O1 after O0.
+// Visible-key spans per token come from k_fwd_spans (one binary search per token).
+#include <cfloat>
+#include <climits>
+
+#include "attn_common.cuh"
+#include "common.hpp"
+#include "sm100.cuh"
+
+using namespace vlasim_dev;
+
+namespace vlasim_host {
+int validate_attn_args(const vlasim_attn_args* a, bool fp8);
+}
+
+namespace {
+
+constexpr float kLazyRescale = 8.0f;  // log2-domain row-max growth tolerated before rescaling O
+
+__global__ void k_fwd_spans(const int32_t* __restrict__ cu, const int32_t* __restrict__ prefix, int nseq, int mask,
+                            int T, int2* __restrict__ rows_span) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const RowSpan r = row_span(cu, prefix, nseq, mask, t, T);
+  rows_span[t] = make_int2(r.lo, r.hi);
+}
+
+struct Fwd2Params {
+  __nv_bfloat16* o;
+  float* lse;
+  const int2* rows_span;
+  int T, H, Hkv, num_items;
+  float scale_log2;
+};
+
+template <int HD, int STAGES>
+struct Fwd2Cfg {
+  static constexpr int BM = 128, BN = 128;
+  static constexpr int Q_BYTES = BM * HD * 2;
+  static constexpr int KV_BYTES = BN * HD * 2;  // one of K or V
+  static constexpr int OFF_Q = 0;                // [2]
+  static constexpr int OFF_KV = 2 * Q_BYTES;     // stage s: K at +s*2*KV_BYTES, V right after
+  static constexpr int OFF_STATS = OFF_KV + STAGES * 2 * KV_BYTES;  // float2 [2][128]
+  static constexpr int OFF_BAR = OFF_STATS + 2 * 128 * 8;
+  static constexpr int NUM_BARS = 4 + 2 * STAGES + 4 + 4 + 1 + 4;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr uint32_t S_COL = 0, O_COL = 256;
+  static_assert(O_COL + 2 * HD <= 512, "TMEM budget");
+  static_assert(SMEM <= 232448, "smem budget");
+};
+
+struct FwdItem {
+  int q0, h, kh, kv_lo, nkv;
+};
+__device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) {
+  FwdItem it;
+  it.h = i % p.H;
+  it.q0 = (i / p.H) * 128;
+  it.kh = it.h / (p.H / p.Hkv);
+  const int2 a = __ldg(p.rows_span + it.q0);
+  const int2 b = __ldg(p.rows_span + min(it.q0 + 127, p.T - 1));
+  it.kv_lo = a.x;
+  it.nkv = max(0, (b.y - a.x + BN - 1) / BN);
+  return it;
+}
+
+template <int HD, int STAGES>
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const Fwd2Params p) {
+  using Cfg = Fwd2Cfg<HD, STAGES>;
+  constexpr int BN = Cfg::BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* bar_q_full = bars;                       // [2]
+  uint64_t* bar_q_empty = bars + 2;                  // [2]
+  uint64_t* bar_kv_full = bars + 4;                  // [STAGES]
+  uint64_t* bar_kv_empty = bars + 4 + STAGES;        // [STAGES]
+  uint64_t* bar_s_full = bars + 4 + 2 * STAGES;      // [2]
+  uint64_t* bar_p_full = bar_s_full + 2;             // [2] 128 arrivals
+  uint64_t* bar_o_full = bar_s_full + 4;             // [2]
+  uint64_t* bar_o_empty = bar_s_full + 6;            // [2] 128 arrivals
+  uint64_t* bar_o_ready = bar_s_full + 8;            // one completion per PV
+  uint64_t* bar_st_full = bar_s_full + 9;            // [2] 128 arrivals
+  uint64_t* bar_st_empty = bar_s_full + 11;          // [2] 128 arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  float2* stats = reinterpret_cast<float2*>(smem + Cfg::OFF_STATS);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_q_full[s], 1);
+      mbar_init(&bar_q_empty[s], 1);
+      mbar_init(&bar_s_full[s], 1);
+      mbar_init(&bar_p_full[s], 128);
+      mbar_init(&bar_o_full[s], 1);
+      mbar_init(&bar_o_empty[s], 128);
+      mbar_init(&bar_st_full[s], 128);
+      mbar_init(&bar_st_empty[s], 128);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&bar_kv_full[s], 1);
+      mbar_init(&bar_kv_empty[s], 1);
+    }
+    mbar_init(bar_o_ready, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ================================================ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      int g = 0, k = 0;
+      for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+        const FwdItem itm = fwd_item(p, i, BN);
+        const int qs = k & 1;
+        if (k >= 2) mbar_wait(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
+        uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
+        mbar_expect_tx(&bar_q_full[qs], Cfg::Q_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * 64, itm.q0, &bar_q_full[qs]);
+        for (int j = 0; j < itm.nkv; ++j, ++g) {
+          const int st = g % STAGES;
+          if (g >= STAGES) mbar_wait(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
+          uint8_t* sk = smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES;
+          uint8_t* sv = sk + Cfg::KV_BYTES;
+          const int kv0 = itm.kv_lo + j * BN;
+          mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::KV_BYTES);
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sk + c * BN * 128, &tmK, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
+      int g = 0, k = 0;
+      // pending PV (issued one tile late so S_{g} overlaps softmax of g-1)
+      int pk = -1, pj = 0, pg = 0;
+      bool plast = false;
+      auto do_pv = [&]() {
+        mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
+        if (pj == 0 && pk >= 2) mbar_wait(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
+        tc_fence_after();
+        const int st = pg % STAGES;
+        const uint32_t v_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+        const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
+        const uint32_t d_o = tmem + Cfg::O_COL + (pk & 1) * HD;
+#pragma unroll
+        for (int s = 0; s < BN / 16; ++s)
+          umma_f16_ts(d_o, a_tm + s * 8, make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024), idesc_o,
+                      (pj > 0 || s > 0) ? 1u : 0u);
+        umma_commit(&bar_kv_empty[st]);
+        umma_commit(bar_o_ready);
+        if (plast) umma_commit(&bar_o_full[pk & 1]);
+      };
+      for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+        const FwdItem itm = fwd_item(p, i, BN);
+        const int qs = k & 1;
+        const uint32_t q_addr = smem_u32(smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES);
+        mbar_wait(&bar_q_full[qs], (k >> 1) & 1);
+        for (int j = 0; j < itm.nkv; ++j, ++g) {
+          const int st = g % STAGES;
+          mbar_wait(&bar_kv_full[st], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES);
+          const uint32_t d_s = tmem + Cfg::S_COL + (g & 1) * 128;
+#pragma unroll
+          for (int s = 0; s < HD / 16; ++s)
+            umma_f16_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
+                        make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_s, s > 0);
+          umma_commit(&bar_s_full[g & 1]);
+          if (j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);
+          if (pk >= 0) do_pv();
+          pk = k;
+          pj = j;
+          pg = g;
+          plast = (j == itm.nkv - 1);
+        }
+      }
+      if (pk >= 0) do_pv();
+    }
+  } else if (warp < 4) {
+    // ================================================ softmax warps
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const int r = warp * 32 + lane;
+    const float sl2 = p.scale_log2;
+    int g = 0, k = 0;
+    for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+      const FwdItem itm = fwd_item(p, i, BN);
+      const int row = itm.q0 + r;
+      const int2 rs = row < p.T ? __ldg(p.rows_span + row) : make_int2(0, 0);
+      float m_run = -INFINITY, l_run = 0.f;
+      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD;
+      for (int j = 0; j < itm.nkv; ++j, ++g) {
+        const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128;
+        mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        const int kv0 = itm.kv_lo + j * BN;
+        const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
+        const bool full_tile = c_lo <= 0 && c_hi >= BN;
+        // pass 1: masked row max (S stays in TMEM; two passes keep the register footprint small)
+        float mt = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t t32[32];
+          tmem_ld32(s_tm + c, t32);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (full_tile || (c + t >= c_lo && c + t < c_hi)) mt = fmaxf(mt, __uint_as_float(t32[t]));
+        }
+        mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
+        const bool grow = mt > m_run + kLazyRescale;
+        const float alpha = grow ? exp2f(m_run - mt) : 1.f;
+        if (__any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY)) {
+          mbar_wait(bar_o_ready, (g - 1) & 1);  // PV_{g-1} has landed in O
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(o_tm + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tmem_st32(o_tm + c, o);
+          }
+        }
+        if (grow) {
+          l_run *= alpha;
+          m_run = mt;
+        }
+        const float msub = (m_run == -INFINITY) ? 0.f : m_run;
+        float ls = 0.f;
+        // pass 2: P = exp2(S·scale − m) → bf16 over the S columns already read
+#pragma unroll
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t t32[32];
+          tmem_ld32(s_tm + c, t32);
+          tmem_wait_ld();
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int c0 = c + 2 * t;
+            const bool v0 = full_tile || (c0 >= c_lo && c0 < c_hi);
+            const bool v1 = full_tile || (c0 + 1 >= c_lo && c0 + 1 < c_hi);
+            const float p0 = v0 ? ex2_approx(fmaf(__uint_as_float(t32[2 * t]), sl2, -msub)) : 0.f;
+            const float p1 = v1 ? ex2_approx(fmaf(__uint_as_float(t32[2 * t + 1]), sl2, -msub)) : 0.f;
+            ls += p0 + p1;
+            pk[t] = pack_bf16x2(p0, p1);
+          }
+          tmem_st16(s_tm + c / 2, pk);
+        }
+        l_run += ls;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bar_p_full[g & 1]);
+      }
+      // hand the row statistics to the epilogue warpgroup
+      if (k >= 2) mbar_wait(&bar_st_empty[k & 1], ((k >> 1) - 1) & 1);
+      stats[(k & 1) * 128 + r] = make_float2(m_run, l_run);
+      mbar_arrive(&bar_st_full[k & 1]);
+    }
+  } else {
+    // ================================================ epilogue warps 4-7
+    const int quad = warp & 3;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int r = quad * 32 + lane;
+    int k = 0;
+    for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+      const FwdItem itm = fwd_item(p, i, BN);
+      const int row = itm.q0 + r;
+      mbar_wait(&bar_st_full[k & 1], (k >> 1) & 1);
+      const float2 ml = stats[(k & 1) * 128 + r];
+      mbar_arrive(&bar_st_empty[k & 1]);
+      const bool valid = row < p.T && itm.nkv > 0;
+      if (itm.nkv > 0) {
+        mbar_wait(&bar_o_full[k & 1], (k >> 1) & 1);
+        tc_fence_after();
+      }
+      const float inv_l = (valid && ml.y > 0.f) ? 1.f / ml.y : 0.f;
+      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + itm.h) * HD;
+      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD;
+#pragma unroll
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(o_tm + c, o);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_o_empty[k & 1]);
+      if (valid) p.lse[static_cast<int64_t>(itm.h) * p.T + row] = (ml.x + __log2f(ml.y)) * 0.69314718055994530942f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+template <int HD, int STAGES>
+int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
+  using namespace vlasim_host;
+  using Cfg = Fwd2Cfg<HD, STAGES>;
+  const int T = int(a->total_tokens);
+  k_fwd_spans<<<(T + 255) / 256, 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, rows_span);
+  VLASIM_LAUNCH_CHECK();
+  CUtensorMap tq, tk, tv;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const uint64_t H = a->num_heads, Hkv = a->num_kv_heads;
+  if (int rc = encode_tmap_2d(&tq, a->q, BF, T, H * HD, H * HD * 2, 128, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&tk, a->k, BF, T, Hkv * HD, Hkv * HD * 2, Cfg::BN, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&tv, a->v, BF, T, Hkv * HD, Hkv * HD * 2, Cfg::BN, 64, true)) return rc;
+  Fwd2Params p;
+  p.o = static_cast<__nv_bfloat16*>(a->o);
+  p.lse = a->lse;
+  p.rows_span = rows_span;
+  p.T = T;
+  p.H = a->num_heads;
+  p.Hkv = a->num_kv_heads;
+  p.num_items = int((int64_t(T) + 127) / 128) * a->num_heads;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  auto kern = attn_fwd2_kernel<HD, STAGES>;
+  VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  kern<<<std::min(p.num_items, num_sms()), 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
+}  // namespace
+
+namespace vlasim_host {
+// Forward for head_dim 64 / 128; the workspace holds the per-token spans (T int2).
+int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const size_t need = size_t(a->total_tokens) * sizeof(int2);
+  if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
+  int2* spans = static_cast<int2*>(ws);
+  if (a->head_dim == 64) return launch_fwd2<64, 4>(a, spans, st);
+  return launch_fwd2<128, 2>(a, spans, st);
+}
+}  // namespace vlasim_host

@@ -78,14 +78,17 @@ def build_host(force=False, verbose=False) -> Path | None:
     deps = HOST_SOURCES + sorted(INCLUDE.rglob("*.hpp")) + [INCLUDE / "vlasim_cuda.h", LIB / "libvlasim_cuda.so"]
     lib_sources = [s for s in HOST_SOURCES if not s.name.startswith("cli_")]
     cuda_inc = Path(NVCC).resolve().parent.parent / "include"
+    cuda_lib = Path(NVCC).resolve().parent.parent / "lib64"
     if force or _stale(so, deps):
         _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, "-I", cuda_inc, "-o", so] + lib_sources +
-             ["-L", LIB, "-lvlasim_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
+             ["-L", LIB, "-lvlasim_cuda", "-Wl,-rpath,$ORIGIN", "-L", cuda_lib, "-lcudart",
+              "-Wl,-rpath," + str(cuda_lib)], verbose)
     for cli in [s for s in HOST_SOURCES if s.name.startswith("cli_")]:
         exe = LIB / cli.stem.replace("cli_", "vlasim_")
         if force or _stale(exe, deps + [so]):
             _run([CXX, "-std=c++20", "-O2", "-I", INCLUDE, "-I", cuda_inc, "-o", exe, cli, "-L", LIB, "-lvlasim",
-                  "-lvlasim_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
+                  "-lvlasim_cuda", "-Wl,-rpath,$ORIGIN", "-L", cuda_lib, "-lcudart", "-Wl,-rpath," + str(cuda_lib)],
+                 verbose)
     return so
 
 

@@ -1,17 +1,18 @@
 // attn_fwd2.cu — persistent block-diagonal varlen attention forward (sm_100a), head_dim 64/128.
 //
-// Same math and masking as attn_fwd.cu (vlasim::packed_attention) but
+// Same math and masking as attn_fwd.cu (vlasim::packed_attention), but
 // persistent: grid = #SMs, each CTA walks work items (128-row Q tile on the global grid, head)
-// with a static stride.  Q and the O accumulator are double-buffered (smem / TMEM) so the
-// next item's loads and MMAs overlap the current item's epilogue, which a separate
-// warpgroup performs.
+// with a static stride; Q is double-buffered so the next item's loads and first S MMAs
+// overlap the current item's epilogue.
 //
 // Warp roles (320 threads):
-//   warps 0-3  softmax: row = TMEM lane; lazy O rescale; P (bf16) written over its S columns
-//   warps 4-7  epilogue: O / l → bf16 → global, LSE
+//   warps 0-7  softmax + epilogue: warp w owns rows 32·(w%4).. (TMEM lane quadrant w%4) and
+//              S columns [64·(w/4), +64); the two halves of a row exchange their partial row
+//              max through smem (named barrier per quadrant), P (bf16) is written over the S
+//              columns each half read, and each half stores its half of the O row.
 //   warp 8     TMA producer (Q double buffer, K/V ring)
 //   warp 9     TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
-// TMEM (512 cols): S0 [0,128) · S1 [128,256) · O0 [256,256+HD) · O1 after O0.
+// TMEM (512 cols): S0 [0,128) · S1 [128,256) · O [256, 256+HD).
 // Visible-key spans per token come from k_fwd_spans (one binary search per token).
 #include <cfloat>
 #include <climits>
@@ -53,12 +54,12 @@ struct Fwd2Cfg {
   static constexpr int KV_BYTES = BN * HD * 2;  // one of K or V
   static constexpr int OFF_Q = 0;                // [2]
   static constexpr int OFF_KV = 2 * Q_BYTES;     // stage s: K at +s*2*KV_BYTES, V right after
-  static constexpr int OFF_STATS = OFF_KV + STAGES * 2 * KV_BYTES;  // float2 [2][128]
-  static constexpr int OFF_BAR = OFF_STATS + 2 * 128 * 8;
-  static constexpr int NUM_BARS = 4 + 2 * STAGES + 4 + 4 + 1 + 4;
+  static constexpr int OFF_XCH = OFF_KV + STAGES * 2 * KV_BYTES;  // float [2 parity][2 half][128]
+  static constexpr int OFF_BAR = OFF_XCH + 2 * 2 * 128 * 4;
+  static constexpr int NUM_BARS = 4 + 2 * STAGES + 4 + 2;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
-  static_assert(O_COL + 2 * HD <= 512, "TMEM budget");
+  static_assert(O_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
 
@@ -86,19 +87,16 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* bar_q_full = bars;                       // [2]
-  uint64_t* bar_q_empty = bars + 2;                  // [2]
-  uint64_t* bar_kv_full = bars + 4;                  // [STAGES]
-  uint64_t* bar_kv_empty = bars + 4 + STAGES;        // [STAGES]
-  uint64_t* bar_s_full = bars + 4 + 2 * STAGES;      // [2]
-  uint64_t* bar_p_full = bar_s_full + 2;             // [2] 128 arrivals
-  uint64_t* bar_o_full = bar_s_full + 4;             // [2]
-  uint64_t* bar_o_empty = bar_s_full + 6;            // [2] 128 arrivals
-  uint64_t* bar_o_ready = bar_s_full + 8;            // one completion per PV
-  uint64_t* bar_st_full = bar_s_full + 9;            // [2] 128 arrivals
-  uint64_t* bar_st_empty = bar_s_full + 11;          // [2] 128 arrivals
+  uint64_t* bar_q_full = bars;                   // [2]
+  uint64_t* bar_q_empty = bars + 2;              // [2]
+  uint64_t* bar_kv_full = bars + 4;              // [STAGES]
+  uint64_t* bar_kv_empty = bars + 4 + STAGES;    // [STAGES]
+  uint64_t* bar_s_full = bars + 4 + 2 * STAGES;  // [2]
+  uint64_t* bar_p_full = bar_s_full + 2;         // [2] 256 arrivals
+  uint64_t* bar_o_full = bar_s_full + 4;         // one completion per item (last PV landed)
+  uint64_t* bar_o_ready = bar_s_full + 5;        // one completion per PV
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
-  float2* stats = reinterpret_cast<float2*>(smem + Cfg::OFF_STATS);
+  float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -106,16 +104,13 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&bar_q_full[s], 1);
       mbar_init(&bar_q_empty[s], 1);
       mbar_init(&bar_s_full[s], 1);
-      mbar_init(&bar_p_full[s], 128);
-      mbar_init(&bar_o_full[s], 1);
-      mbar_init(&bar_o_empty[s], 128);
-      mbar_init(&bar_st_full[s], 128);
-      mbar_init(&bar_st_empty[s], 128);
+      mbar_init(&bar_p_full[s], 256);
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bar_kv_full[s], 1);
       mbar_init(&bar_kv_empty[s], 1);
     }
+    mbar_init(bar_o_full, 1);
     mbar_init(bar_o_ready, 1);
     fence_barrier_init();
   }
@@ -160,24 +155,21 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
       int g = 0, k = 0;
-      // pending PV (issued one tile late so S_{g} overlaps softmax of g-1)
-      int pk = -1, pj = 0, pg = 0;
+      int pj = -1, pg = 0;  // pending PV (issued one tile late so S_g overlaps softmax of g-1)
       bool plast = false;
       auto do_pv = [&]() {
         mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
-        if (pj == 0 && pk >= 2) mbar_wait(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
         tc_fence_after();
         const int st = pg % STAGES;
         const uint32_t v_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
         const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
-        const uint32_t d_o = tmem + Cfg::O_COL + (pk & 1) * HD;
 #pragma unroll
-        for (int s = 0; s < BN / 16; ++s)
-          umma_f16_ts(d_o, a_tm + s * 8, make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024), idesc_o,
-                      (pj > 0 || s > 0) ? 1u : 0u);
+        for (int s = 0; s < BN / 16; ++s)  // P: columns 0-63 at +0..31, 64-127 at +64..95
+          umma_f16_ts(tmem + Cfg::O_COL, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+                      make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024), idesc_o, (pj > 0 || s > 0) ? 1u : 0u);
         umma_commit(&bar_kv_empty[st]);
         umma_commit(bar_o_ready);
-        if (plast) umma_commit(&bar_o_full[pk & 1]);
+        if (plast) umma_commit(bar_o_full);
       };
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
         const FwdItem itm = fwd_item(p, i, BN);
@@ -196,19 +188,20 @@ __global__ void __launch_bounds__(320, 1)
                         make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_s, s > 0);
           umma_commit(&bar_s_full[g & 1]);
           if (j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);
-          if (pk >= 0) do_pv();
-          pk = k;
+          if (pj >= 0) do_pv();
           pj = j;
           pg = g;
           plast = (j == itm.nkv - 1);
         }
       }
-      if (pk >= 0) do_pv();
+      if (pj >= 0) do_pv();
     }
-  } else if (warp < 4) {
-    // ================================================ softmax warps
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    const int r = warp * 32 + lane;
+  } else {
+    // ================================================ softmax + epilogue warps 0-7
+    const int quad = warp & 3, half = warp >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int r = quad * 32 + lane;
+    const int c0 = half * 64;
     const float sl2 = p.scale_log2;
     int g = 0, k = 0;
     for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
@@ -216,25 +209,41 @@ __global__ void __launch_bounds__(320, 1)
       const int row = itm.q0 + r;
       const int2 rs = row < p.T ? __ldg(p.rows_span + row) : make_int2(0, 0);
       float m_run = -INFINITY, l_run = 0.f;
-      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
-        const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128;
+        const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
         mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
-        const int kv0 = itm.kv_lo + j * BN;
-        const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        const bool full_tile = c_lo <= 0 && c_hi >= BN;
-        // pass 1: masked row max (S stays in TMEM; two passes keep the register footprint small)
-        float mt = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t t32[32];
-          tmem_ld32(s_tm + c, t32);
+        uint32_t x[64];
+        {
+          uint32_t a[32], b[32];
+          tmem_ld32(s_tm, a);
+          tmem_ld32(s_tm + 32, b);
           tmem_wait_ld();
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (full_tile || (c + t >= c_lo && c + t < c_hi)) mt = fmaxf(mt, __uint_as_float(t32[t]));
+          for (int t = 0; t < 32; ++t) {
+            x[t] = a[t];
+            x[32 + t] = b[t];
+          }
         }
+        const int kv0 = itm.kv_lo + j * BN + c0;
+        const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
+        float mt = -INFINITY;
+        if (c_lo <= 0 && c_hi >= 64) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) mt = fmaxf(mt, __uint_as_float(x[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            const bool v = c >= c_lo && c < c_hi;
+            if (!v) x[c] = __float_as_uint(-INFINITY);
+            mt = fmaxf(mt, __uint_as_float(x[c]));
+          }
+        }
+        // combine the two column halves of this row
+        float* xs = xch + (g & 1) * 256;
+        xs[half * 128 + r] = mt;
+        named_bar_sync(1 + quad, 64);
+        mt = fmaxf(mt, xs[(1 - half) * 128 + r]);
         mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
         const bool grow = mt > m_run + kLazyRescale;
         const float alpha = grow ? exp2f(m_run - mt) : 1.f;
@@ -242,13 +251,13 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(bar_o_ready, (g - 1) & 1);  // PV_{g-1} has landed in O
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < HD; c += 32) {
+          for (int c = 0; c < HD / 2; c += 32) {
             uint32_t o[32];
-            tmem_ld32(o_tm + c, o);
+            tmem_ld32(tmem + lane_off + Cfg::O_COL + half * (HD / 2) + c, o);
             tmem_wait_ld();
 #pragma unroll
             for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-            tmem_st32(o_tm + c, o);
+            tmem_st32(tmem + lane_off + Cfg::O_COL + half * (HD / 2) + c, o);
           }
         }
         if (grow) {
@@ -257,20 +266,13 @@ __global__ void __launch_bounds__(320, 1)
         }
         const float msub = (m_run == -INFINITY) ? 0.f : m_run;
         float ls = 0.f;
-        // pass 2: P = exp2(S·scale − m) → bf16 over the S columns already read
 #pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t t32[32];
-          tmem_ld32(s_tm + c, t32);
-          tmem_wait_ld();
+        for (int c = 0; c < 64; c += 32) {
           uint32_t pk[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            const int c0 = c + 2 * t;
-            const bool v0 = full_tile || (c0 >= c_lo && c0 < c_hi);
-            const bool v1 = full_tile || (c0 + 1 >= c_lo && c0 + 1 < c_hi);
-            const float p0 = v0 ? ex2_approx(fmaf(__uint_as_float(t32[2 * t]), sl2, -msub)) : 0.f;
-            const float p1 = v1 ? ex2_approx(fmaf(__uint_as_float(t32[2 * t + 1]), sl2, -msub)) : 0.f;
+            const float p0 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t]), sl2, -msub));
+            const float p1 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t + 1]), sl2, -msub));
             ls += p0 + p1;
             pk[t] = pack_bf16x2(p0, p1);
           }
@@ -281,35 +283,22 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_before();
         mbar_arrive(&bar_p_full[g & 1]);
       }
-      // hand the row statistics to the epilogue warpgroup
-      if (k >= 2) mbar_wait(&bar_st_empty[k & 1], ((k >> 1) - 1) & 1);
-      stats[(k & 1) * 128 + r] = make_float2(m_run, l_run);
-      mbar_arrive(&bar_st_full[k & 1]);
-    }
-  } else {
-    // ================================================ epilogue warps 4-7
-    const int quad = warp & 3;
-    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int r = quad * 32 + lane;
-    int k = 0;
-    for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-      const FwdItem itm = fwd_item(p, i, BN);
-      const int row = itm.q0 + r;
-      mbar_wait(&bar_st_full[k & 1], (k >> 1) & 1);
-      const float2 ml = stats[(k & 1) * 128 + r];
-      mbar_arrive(&bar_st_empty[k & 1]);
+      // ---- epilogue: combine the halves' row sums, O / l → bf16, LSE
+      float* xs = xch + (g & 1) * 256;  // parity not used by any in-flight tile
+      xs[half * 128 + r] = l_run;
+      named_bar_sync(1 + quad, 64);
+      const float l_tot = l_run + xs[(1 - half) * 128 + r];
       const bool valid = row < p.T && itm.nkv > 0;
       if (itm.nkv > 0) {
-        mbar_wait(&bar_o_full[k & 1], (k >> 1) & 1);
+        mbar_wait(bar_o_full, k & 1);
         tc_fence_after();
       }
-      const float inv_l = (valid && ml.y > 0.f) ? 1.f / ml.y : 0.f;
-      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + itm.h) * HD;
-      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD;
+      const float inv_l = (valid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
+      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + itm.h) * HD + half * (HD / 2);
 #pragma unroll
-      for (int c = 0; c < HD; c += 32) {
+      for (int c = 0; c < HD / 2; c += 32) {
         uint32_t o[32];
-        tmem_ld32(o_tm + c, o);
+        tmem_ld32(tmem + lane_off + Cfg::O_COL + half * (HD / 2) + c, o);
         tmem_wait_ld();
         if (valid) {
           uint32_t pk[16];
@@ -321,9 +310,11 @@ __global__ void __launch_bounds__(320, 1)
           for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
         }
       }
-      tc_fence_before();
-      mbar_arrive(&bar_o_empty[k & 1]);
-      if (valid) p.lse[static_cast<int64_t>(itm.h) * p.T + row] = (ml.x + __log2f(ml.y)) * 0.69314718055994530942f;
+      if (valid && half == 0)
+        p.lse[static_cast<int64_t>(itm.h) * p.T + row] = (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
+      // O is overwritten by the next item's first PV only after p_full of that item, which this
+      // warp arrives on after these tcgen05.ld have completed.
+      named_bar_sync(1 + quad, 64);
     }
   }
   tc_fence_before();

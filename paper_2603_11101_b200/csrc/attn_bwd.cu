@@ -5,27 +5,20 @@
 //   P = exp(S·scale − LSE), dV = Pᵀ dO, dP = dO Vᵀ, dS = P ∘ (dP − D), D = rowsum(dO ∘ O),
 //   dQ = scale · dS K, dK = scale · dSᵀ Q.
 //
-// Launches:
-//   memset      zero the fp32 dQ accumulator
+// Launches (no atomics, no fp32 dQ accumulator in HBM — dQ is deterministic):
 //   k_bwd_pre   D = rowsum(dO∘O), LSE → log2 domain, per-token visible spans    [HBM-bound]
-//   k_bwd_main  persistent: each CTA loops over work items = (128-key tile on the global grid,
-//               KV head).  Per item, K and V stay in smem; the q heads of the group × the
-//               128-row Q tiles of the tile's visible query range stream through a TMA ring
+//   k_bwd_dkdv  persistent, KV-stationary: items = (128-key tile, kv head); loops over the q
+//               heads of the group × the 128-row Q tiles of the tile's visible query range
 //               (tile skipping: queries outside [q_lo, q_hi) are never loaded or multiplied).
-//   k_bwd_post  dQ = bf16(scale · dQacc), optionally scattered through row_map
-//
-// k_bwd_main warp roles (448 threads):
-//   warps 0-7   "softmax": warp w owns key rows 32·(w%4).. (TMEM lane quadrant w%4) and query
-//               columns [64·(w/4), +64).  Phase A: S → Pᵀ (bf16, written back into the S
-//               columns it read).  Phase B: dP → dSᵀ (bf16, SWIZZLE_128B smem, read back as the
-//               K-major A of dK and the MN-major A of dQ).  Item end: dK/dV epilogue.
-//   warps 8-11  dQ drain: TMEM dQ rows → red.global.add.v4.f32 into the fp32 accumulator.
-//   warp 12     TMA producer.   warp 13  TMEM allocator + tcgen05.mma issuer.
-// TMEM (512 columns): S/P [0,128) · dP/dQ [128,256) · dV [256,256+HD) · dK after dV.
-// Issue order per iteration (FA4-style): dV, dK, S(next), dQ, dP(next) — the next S is
-// computed while the drain warps empty dQ and the softmax warps run phase A of the next
-// iteration.  The P→S and dP→dQ column aliasing relies on tcgen05.mma executing in issue
-// order.
+//               4 GEMMs per (key tile, Q tile): Sᵀ, dPᵀ, dV, dK.
+//   k_bwd_dq    persistent, Q-stationary: items = (128-row Q tile, head); loops over the key
+//               tiles of the visible key range.  3 GEMMs per tile: S, dP, dQ (recomputing S and
+//               dP costs 2 GEMMs but removes the dQ reduction across key tiles).
+// Both kernels: warps 0-7 softmax (warp w: TMEM lane quadrant w%4, column half w/4), warp 8 TMA
+// producer, warp 9 TMEM allocator + tcgen05.mma issuer.  P / dS are written as bf16 over the
+// TMEM columns they were computed from and fed back as the A operand (A-from-TMEM MMAs); the
+// column aliasing relies on tcgen05.mma executing in issue order.  dQ/dK/dV rows are written
+// through the optional row_map (scatter back to sample order fused into the epilogues).
 #include <cfloat>
 #include <climits>
 
@@ -84,69 +77,50 @@ __global__ void k_bwd_pre(const __nv_bfloat16* __restrict__ o, const __nv_bfloat
   }
 }
 
-// dQ = bf16(scale · dQacc), written to row row_map[t] (fused scatter) or t.
-template <int HD>
-__global__ void k_bwd_post(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                           const int32_t* __restrict__ row_map, int64_t rows, int H, float scale) {
-  constexpr int LPR = HD / 8;
-  const int64_t gt = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int64_t row = gt / LPR;  // (t, h) row
-  const int sub = int(gt % LPR);
-  if (row >= rows) return;
-  const int64_t t = row / H, h = row % H;
-  const int64_t dst_t = row_map ? int64_t(__ldg(row_map + t)) : t;
-  const float4 a = __ldcs(reinterpret_cast<const float4*>(acc + row * HD + sub * 8));
-  const float4 b = __ldcs(reinterpret_cast<const float4*>(acc + row * HD + sub * 8 + 4));
-  uint4 r;
-  r.x = pack_bf16x2(a.x * scale, a.y * scale);
-  r.y = pack_bf16x2(a.z * scale, a.w * scale);
-  r.z = pack_bf16x2(b.x * scale, b.y * scale);
-  r.w = pack_bf16x2(b.z * scale, b.w * scale);
-  *reinterpret_cast<uint4*>(dq + (dst_t * H + h) * HD + sub * 8) = r;
-}
-
-// ------------------------------------------------------------------ main kernel
+// ------------------------------------------------------------------ main kernels
 struct BwdParams {
-  float* dq_acc;
+  __nv_bfloat16* dq;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
-  const int32_t* row_map;  // packed row → output row for dK/dV (NULL: identity)
+  const int32_t* row_map;  // packed row → output row for dQ/dK/dV (NULL: identity)
   const float* lse2;       // [H, Tp] log2-domain LSE
   const float* dsum;       // [H, Tp] rowsum(dO ∘ O)
   const int2* rows_span;   // [T] visible keys of query t
   const int2* cols_span;   // [T] queries that see key t
-  int T, Tp, H, Hkv, num_items;
+  int T, Tp, H, Hkv, kv_items, q_items;
   float scale_log2, scale;
 };
 
+// ================================================================== dK / dV (KV-stationary)
+// One CTA loops over items = (128-key tile, kv head).  Per iteration (q head of the group,
+// 128-row Q tile of the visible query range):
+//   Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ                                  (SS, K-major operands)
+//   softmax warps: Pᵀ = exp2(Sᵀ·scale·log2e − lse2) → bf16 over the S columns,
+//                  dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
+//   dV += Pᵀ·dO, dK += dSᵀ·Q                                  (A from TMEM, B MN-major)
+// TMEM: S/P [0,128) · dP/dS [128,256) · dV [256,256+HD) · dK after.  Q and dO double-buffered.
 template <int HD>
-struct BwdCfg {
-  static constexpr int BK = 128, BQ = 128;
-  static constexpr int TILE = 128 * HD * 2;  // one 128-row bf16 tile (K, V, Q or dO)
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = TILE;
-  static constexpr int OFF_Q = 2 * TILE;                 // Q ring: stage s at OFF_Q + s*TILE
-  static constexpr int OFF_DO = OFF_Q + 2 * TILE;        // dO: single buffer
-  static constexpr int OFF_DS = OFF_DO + TILE;           // dSᵀ [128 keys × 128 q] bf16
-  static constexpr int VEC = 544;                        // 132 floats (16-B aligned window) + pad
-  static constexpr int OFF_LSE = OFF_DS + 128 * 128 * 2;  // lse2 [2][VEC]
-  static constexpr int OFF_DSUM = OFF_LSE + 2 * VEC;      // D [VEC]
-  static constexpr int OFF_BAR = OFF_DSUM + VEC;
+struct DkvCfg {
+  static constexpr int TILE = 128 * HD * 2;
+  static constexpr int OFF_K = 0, OFF_V = TILE;
+  static constexpr int OFF_Q = 2 * TILE;        // [2]
+  static constexpr int OFF_DO = 4 * TILE;       // [2]
+  static constexpr int VEC = 544;               // 132 floats (16-B aligned window of 128) + pad
+  static constexpr int OFF_LSE = 6 * TILE;      // [2][VEC]
+  static constexpr int OFF_DSUM = OFF_LSE + 2 * VEC;  // [2][VEC]
+  static constexpr int OFF_BAR = OFF_DSUM + 2 * VEC;
   static constexpr int NUM_BARS = 16;
-  static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int SMEM = SMEM_USED + 1024;  // + alignment slack for the 1 KB swizzle atoms
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
-  static constexpr int THREADS = 448;
   static_assert(DK_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
 
-// Work item i → (key tile, kv head); the q range comes from the precomputed key spans.
-struct BwdItem {
+struct KvItem {
   int k0, kh, q_lo, nq, iters;
 };
-__device__ __forceinline__ BwdItem bwd_item(const BwdParams& p, int i) {
-  BwdItem it;
+__device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
+  KvItem it;
   it.kh = i % p.Hkv;
   it.k0 = (i / p.Hkv) * 128;
   const int2 first = __ldg(p.cols_span + it.k0);
@@ -158,73 +132,67 @@ __device__ __forceinline__ BwdItem bwd_item(const BwdParams& p, int i) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(448, 1)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const BwdParams p) {
-  using Cfg = BwdCfg<HD>;
+__global__ void __launch_bounds__(320, 1)
+    k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
+  using Cfg = DkvCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_kv_full = bars + 0;
   uint64_t* bar_kv_empty = bars + 1;
-  uint64_t* bar_q_full = bars + 2;   // [2]
-  uint64_t* bar_q_empty = bars + 4;  // [2]
-  uint64_t* bar_do_full = bars + 6;
-  uint64_t* bar_do_empty = bars + 7;
-  uint64_t* bar_s_full = bars + 8;
-  uint64_t* bar_dp_full = bars + 9;
-  uint64_t* bar_p_full = bars + 10;    // 256 arrivals
-  uint64_t* bar_dq_full = bars + 11;
-  uint64_t* bar_dq_empty = bars + 12;  // 128 arrivals
+  uint64_t* bar_q_full = bars + 2;    // [2]
+  uint64_t* bar_q_empty = bars + 4;   // [2]
+  uint64_t* bar_do_full = bars + 6;   // [2]
+  uint64_t* bar_do_empty = bars + 8;  // [2]
+  uint64_t* bar_s_full = bars + 10;
+  uint64_t* bar_dp_full = bars + 11;
+  uint64_t* bar_p_full = bars + 12;     // 256 arrivals
   uint64_t* bar_dkv_full = bars + 13;
   uint64_t* bar_dkv_empty = bars + 14;  // 256 arrivals
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int group = p.H / p.Hkv;
-
   if (tid == 0) {
     mbar_init(bar_kv_full, 1);
     mbar_init(bar_kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_q_full[s], 1);
       mbar_init(&bar_q_empty[s], 1);
+      mbar_init(&bar_do_full[s], 1);
+      mbar_init(&bar_do_empty[s], 1);
     }
-    mbar_init(bar_do_full, 1);
-    mbar_init(bar_do_empty, 1);
     mbar_init(bar_s_full, 1);
     mbar_init(bar_dp_full, 1);
     mbar_init(bar_p_full, 256);
-    mbar_init(bar_dq_full, 1);
-    mbar_init(bar_dq_empty, 128);
     mbar_init(bar_dkv_full, 1);
     mbar_init(bar_dkv_empty, 256);
     fence_barrier_init();
   }
-  if (warp == 13) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 12) {
+  if (warp == 8) {
     // ================================================ TMA producer
     if (lane == 0) {
       int G = 0, k = 0;
-      for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
-        const BwdItem itm = bwd_item(p, i);
+      for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
+        const KvItem itm = kv_item(p, i);
         if (itm.iters == 0) continue;
         for (int it = 0; it < itm.iters; ++it, ++G) {
           const int h = itm.kh * group + it / itm.nq;
-          const int qb = itm.q_lo + (it % itm.nq) * Cfg::BQ;
-          const int qs = G & 1;
-          if (G >= 2) mbar_wait(&bar_q_empty[qs], ((G >> 1) - 1) & 1);
-          uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::TILE;
-          mbar_expect_tx(&bar_q_full[qs], Cfg::TILE + 528);
+          const int qb = itm.q_lo + (it % itm.nq) * 128;
+          const int b = G & 1;
+          if (G >= 2) mbar_wait(&bar_q_empty[b], ((G >> 1) - 1) & 1);
+          mbar_expect_tx(&bar_q_full[b], Cfg::TILE + 528);
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sq + c * 16384, &tmQ, h * HD + c * 64, qb, &bar_q_full[qs]);
-          bulk_load(smem + Cfg::OFF_LSE + qs * Cfg::VEC, p.lse2 + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_q_full[qs]);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_2d(smem + Cfg::OFF_Q + b * Cfg::TILE + c * 16384, &tmQ, h * HD + c * 64, qb, &bar_q_full[b]);
+          bulk_load(smem + Cfg::OFF_LSE + b * Cfg::VEC, p.lse2 + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_q_full[b]);
           if (it == 0) {
             if (k > 0) mbar_wait(bar_kv_empty, (k - 1) & 1);
             mbar_expect_tx(bar_kv_full, 2 * Cfg::TILE);
@@ -234,24 +202,22 @@ __global__ void __launch_bounds__(448, 1)
               tma_load_2d(smem + Cfg::OFF_V + c * 16384, &tmV, itm.kh * HD + c * 64, itm.k0, bar_kv_full);
             }
           }
-          if (G >= 1) mbar_wait(bar_do_empty, (G - 1) & 1);
-          mbar_expect_tx(bar_do_full, Cfg::TILE + 528);
+          if (G >= 2) mbar_wait(&bar_do_empty[b], ((G >> 1) - 1) & 1);
+          mbar_expect_tx(&bar_do_full[b], Cfg::TILE + 528);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
-            tma_load_2d(smem + Cfg::OFF_DO + c * 16384, &tmdO, h * HD + c * 64, qb, bar_do_full);
-          bulk_load(smem + Cfg::OFF_DSUM, p.dsum + int64_t(h) * p.Tp + (qb & ~3), 528, bar_do_full);
+            tma_load_2d(smem + Cfg::OFF_DO + b * Cfg::TILE + c * 16384, &tmdO, h * HD + c * 64, qb, &bar_do_full[b]);
+          bulk_load(smem + Cfg::OFF_DSUM + b * Cfg::VEC, p.dsum + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_do_full[b]);
         }
         ++k;
       }
     }
-  } else if (warp == 13) {
+  } else if (warp == 9) {
     // ================================================ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // S, dP
+      constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ
       constexpr uint32_t id_kmn = make_idesc_bf16(128, HD, false, true);   // dV, dK
-      constexpr uint32_t id_mnmn = make_idesc_bf16(128, HD, true, true);   // dQ
       const uint32_t sK = smem_u32(smem + Cfg::OFF_K), sV = smem_u32(smem + Cfg::OFF_V);
-      const uint32_t sdS = smem_u32(smem + Cfg::OFF_DS), sdO = smem_u32(smem + Cfg::OFF_DO);
       auto mma_S = [&](int G) {
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
         mbar_wait(&bar_q_full[G & 1], (G >> 1) & 1);
@@ -263,8 +229,8 @@ __global__ void __launch_bounds__(448, 1)
         umma_commit(bar_s_full);
       };
       auto mma_dP = [&](int G) {
-        mbar_wait(bar_do_full, G & 1);
-        if (G > 0) mbar_wait(bar_dq_empty, (G - 1) & 1);
+        const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
+        mbar_wait(&bar_do_full[G & 1], (G >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < HD / 16; ++s)
@@ -273,8 +239,8 @@ __global__ void __launch_bounds__(448, 1)
         umma_commit(bar_dp_full);
       };
       int G = 0, k = 0;
-      for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
-        const BwdItem itm = bwd_item(p, i);
+      for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
+        const KvItem itm = kv_item(p, i);
         if (itm.iters == 0) continue;
         mbar_wait(bar_kv_full, k & 1);
         tc_fence_after();
@@ -282,58 +248,51 @@ __global__ void __launch_bounds__(448, 1)
         mma_dP(G);
         for (int it = 0; it < itm.iters; ++it, ++G) {
           const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
+          const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
           mbar_wait(bar_p_full, G & 1);
           if (it == 0 && k > 0) mbar_wait(bar_dkv_empty, (k - 1) & 1);
           tc_fence_after();
-          // dV += Pᵀ·dO  (A = Pᵀ in TMEM: queries 0-63 at S cols 0-31, 64-127 at cols 64-95)
+          // dV += Pᵀ·dO and dK += dSᵀ·Q; A from TMEM: queries 0-63 at +0..31, 64-127 at +64..95
 #pragma unroll
           for (int s = 0; s < 8; ++s)
             umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::S_COL + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
                         make_sdesc_sw128(sdO + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
-          umma_commit(bar_do_empty);
-          // dK += dSᵀ·Q  (A = dSᵀ smem K-major, B = Q MN-major)
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_f16_ss(tmem + Cfg::DK_COL, make_sdesc_sw128(sdS + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
+            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::DP_COL + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
                         make_sdesc_sw128(sQ + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
-          const bool more = it + 1 < itm.iters;
-          if (more) mma_S(G + 1);  // next S into the S/P columns (after dV read P: issue order)
-          // dQ = dS·K  (A = dS MN-major view of the same smem, B = K MN-major) → dP columns
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            umma_f16_ss(tmem + Cfg::DP_COL, make_sdesc_sw128(sdS + s * 2048, 16384, 1024),
-                        make_sdesc_sw128(sK + s * 2048, 16384, 1024), id_mnmn, s > 0);
+          umma_commit(&bar_do_empty[G & 1]);
           umma_commit(&bar_q_empty[G & 1]);
-          umma_commit(bar_dq_full);
-          if (!more) {
+          if (it + 1 < itm.iters) {
+            mma_S(G + 1);   // over P/S columns after dV read them (issue order)
+            mma_dP(G + 1);  // over dS/dP columns after dK read them
+          } else {
             umma_commit(bar_kv_empty);
             umma_commit(bar_dkv_full);
-          } else {
-            mma_dP(G + 1);
           }
         }
         ++k;
       }
     }
-  } else if (warp < 8) {
-    // ================================================ softmax warps
+  } else {
+    // ================================================ softmax warps 0-7 (key row, query-column half)
     const int quad = warp & 3, half = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int krow = quad * 32 + lane;
-    uint8_t* sds = smem + Cfg::OFF_DS + half * 16384 + krow * 128;  // this thread's 128-B dSᵀ row chunk
+    const int c0 = half * 64;
     int G = 0, k = 0;
-    for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
-      const BwdItem itm = bwd_item(p, i);
+    for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
+      const KvItem itm = kv_item(p, i);
       if (itm.iters == 0) continue;
       const int key = itm.k0 + krow;
       const int2 ks = key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0);
       for (int it = 0; it < itm.iters; ++it, ++G) {
-        const int qb = itm.q_lo + (it % itm.nq) * Cfg::BQ;
-        const int c0 = half * 64;
+        const int qb = itm.q_lo + (it % itm.nq) * 128;
         const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
+        const bool full = c_lo <= 0 && c_hi >= 64;
         const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
-        const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM) + (qb & 3) + c0;
-        // ---- phase A: S → P (kept in fp32 registers, written to TMEM as bf16)
+        const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
+        // ---- phase A: Sᵀ → Pᵀ (fp32 in registers, bf16 over the S columns)
         mbar_wait(bar_s_full, G & 1);
         tc_fence_after();
         float pr[64];
@@ -346,13 +305,14 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int c = cc + j;
-            pr[c] = (c >= c_lo && c < c_hi) ? ex2_approx(__uint_as_float(sr[j]) * p.scale_log2 - lse2[c]) : 0.f;
+            const float e = ex2_approx(fmaf(__uint_as_float(sr[j]), p.scale_log2, -lse2[c]));
+            pr[c] = (full || (c >= c_lo && c < c_hi)) ? e : 0.f;
           }
 #pragma unroll
           for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pr[cc + 2 * j], pr[cc + 2 * j + 1]);
           tmem_st16(tmem + lane_off + Cfg::S_COL + c0 + cc / 2, pk);
         }
-        // ---- phase B: dP → dS = P ∘ (dP − D) → smem (dSᵀ row, swizzled)
+        // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
         mbar_wait(bar_dp_full, G & 1);
         tc_fence_after();
 #pragma unroll
@@ -367,18 +327,13 @@ __global__ void __launch_bounds__(448, 1)
             dk[j] = pack_bf16x2(pr[c] * (__uint_as_float(dr[2 * j]) - dsum[c]),
                                 pr[c + 1] * (__uint_as_float(dr[2 * j + 1]) - dsum[c + 1]));
           }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int chunk = (cc / 8 + j) ^ (krow & 7);
-            *reinterpret_cast<uint4*>(sds + chunk * 16) = make_uint4(dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
-          }
+          tmem_st16(tmem + lane_off + Cfg::DP_COL + c0 + cc / 2, dk);
         }
         tmem_wait_st();
-        fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(bar_p_full);
       }
-      // ---- item end: dK / dV epilogue (this thread: key row krow, head-dim half `half`)
+      // ---- item end: dK / dV epilogue (key row krow, head-dim half `half`)
       mbar_wait(bar_dkv_full, k & 1);
       tc_fence_after();
       const bool valid = key < p.T;
@@ -409,49 +364,260 @@ __global__ void __launch_bounds__(448, 1)
       mbar_arrive(bar_dkv_empty);
       ++k;
     }
-  } else if (warp < 12) {
-    // ================================================ dQ drain: query row (warp-8)*32 + lane
-    const int quad = warp & 3;
-    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int r = quad * 32 + lane;
-    int G = 0;
-    for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
-      const BwdItem itm = bwd_item(p, i);
-      for (int it = 0; it < itm.iters; ++it, ++G) {
-        const int h = itm.kh * group + it / itm.nq;
-        const int q = itm.q_lo + (it % itm.nq) * Cfg::BQ + r;
-        bool live = false;
-        if (q < p.T) {
-          const int2 rs = __ldg(p.rows_span + q);
-          live = rs.x < itm.k0 + Cfg::BK && rs.y > itm.k0;
-        }
-        float* dst = p.dq_acc + (static_cast<int64_t>(q) * p.H + h) * HD;
-        mbar_wait(bar_dq_full, G & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c, v);
-          tmem_wait_ld();
-          if (live) {
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================== dQ (Q-stationary)
+// One CTA loops over items = (128-row Q tile, head).  Per key tile of the visible key range:
+//   S = Q·Kᵀ (→ S buffer g%2), dP = dO·Vᵀ                    (SS, K-major operands)
+//   softmax warps: P = exp2(S·scale·log2e − lse2_row) (registers), dS = P ∘ (dP − D_row) → bf16
+//                  over the S columns
+//   dQ += dS·K                                                (A from TMEM, B = K MN-major)
+// and writes dQ = scale · dQacc once per item in bf16 (through row_map).  Deterministic: no atomics.
+// TMEM: S0 [0,128) · dP [128,256) · dQ [256,256+HD) · S1 [384,512).
+template <int HD, int STAGES>
+struct DqCfg {
+  static constexpr int TILE = 128 * HD * 2;
+  static constexpr int OFF_Q = 0, OFF_DO = TILE;
+  static constexpr int OFF_KV = 2 * TILE;  // stage s: K at +s*2*TILE, V right after
+  static constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
+  static constexpr int NUM_BARS = 2 + 2 * STAGES + 2 + 2 + 2 + 2;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr uint32_t DP_COL = 128, DQ_COL = 256;
+  __host__ __device__ static constexpr uint32_t s_col(int g) { return (g & 1) ? 384u : 0u; }
+  static_assert(DQ_COL + HD <= 384, "TMEM budget");
+  static_assert(SMEM <= 232448, "smem budget");
+};
+
+struct QItem {
+  int q0, h, kh, kv_lo, nkv;
+};
+__device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {
+  QItem it;
+  it.h = i % p.H;
+  it.q0 = (i / p.H) * 128;
+  it.kh = it.h / (p.H / p.Hkv);
+  const int2 a = __ldg(p.rows_span + it.q0);
+  const int2 b = __ldg(p.rows_span + min(it.q0 + 127, p.T - 1));
+  it.kv_lo = a.x;
+  it.nkv = max(0, (b.y - a.x + 127) / 128);
+  return it;
+}
+
+template <int HD, int STAGES>
+__global__ void __launch_bounds__(320, 1)
+    k_bwd_dq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
+  using Cfg = DqCfg<HD, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* bar_qdo_full = bars + 0;
+  uint64_t* bar_qdo_empty = bars + 1;
+  uint64_t* bar_kv_full = bars + 2;                // [STAGES]
+  uint64_t* bar_kv_empty = bars + 2 + STAGES;      // [STAGES]
+  uint64_t* bar_s_full = bars + 2 + 2 * STAGES;    // [2]
+  uint64_t* bar_dp_full = bar_s_full + 2;          // one per tile
+  uint64_t* bar_p_full = bar_s_full + 3;           // [2] 256 arrivals (dS written over S buffer g%2)
+  uint64_t* bar_dq_full = bar_s_full + 5;          // one per item
+  uint64_t* bar_dq_empty = bar_s_full + 6;         // 256 arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(bar_qdo_full, 1);
+    mbar_init(bar_qdo_empty, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&bar_kv_full[s], 1);
+      mbar_init(&bar_kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_s_full[s], 1);
+      mbar_init(&bar_p_full[s], 256);
+    }
+    mbar_init(bar_dp_full, 1);
+    mbar_init(bar_dq_full, 1);
+    mbar_init(bar_dq_empty, 256);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ================================================ TMA producer
+    if (lane == 0) {
+      int g = 0, k = 0;
+      for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
+        const QItem itm = q_item(p, i);
+        if (itm.nkv == 0) continue;
+        if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
+        mbar_expect_tx(bar_qdo_full, 2 * Cfg::TILE);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              red_add_v4_f32(dst + c + 4 * j, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_load_2d(smem + Cfg::OFF_Q + c * 16384, &tmQ, itm.h * HD + c * 64, itm.q0, bar_qdo_full);
+          tma_load_2d(smem + Cfg::OFF_DO + c * 16384, &tmdO, itm.h * HD + c * 64, itm.q0, bar_qdo_full);
+        }
+        for (int j = 0; j < itm.nkv; ++j, ++g) {
+          const int st = g % STAGES;
+          if (g >= STAGES) mbar_wait(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
+          uint8_t* sk = smem + Cfg::OFF_KV + st * 2 * Cfg::TILE;
+          const int kv0 = itm.kv_lo + j * 128;
+          mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::TILE);
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            tma_load_2d(sk + c * 16384, &tmK, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
+            tma_load_2d(sk + Cfg::TILE + c * 16384, &tmV, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
           }
         }
-        tc_fence_before();
-        mbar_arrive(bar_dq_empty);
+        ++k;
       }
+    }
+  } else if (warp == 9) {
+    // ================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // S, dP
+      constexpr uint32_t id_dq = make_idesc_bf16(128, HD, false, true);    // dQ (A from TMEM, B MN-major)
+      const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q), sdO = smem_u32(smem + Cfg::OFF_DO);
+      int g = 0, k = 0;
+      int pj = -1, pg = 0;  // pending dQ MMA of tile pg (local index pj)
+      bool plast = false;
+      auto do_dq = [&]() {
+        mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + Cfg::OFF_KV + (pg % STAGES) * 2 * Cfg::TILE);
+        const uint32_t a = tmem + Cfg::s_col(pg);
+#pragma unroll
+        for (int s = 0; s < 8; ++s)  // dS: keys 0-63 at +0..31, 64-127 at +64..95
+          umma_f16_ts(tmem + Cfg::DQ_COL, a + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+                      make_sdesc_sw128(sK + s * 2048, 16384, 1024), id_dq, (pj > 0 || s > 0) ? 1u : 0u);
+        umma_commit(&bar_kv_empty[pg % STAGES]);
+        if (plast) umma_commit(bar_dq_full);
+      };
+      for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
+        const QItem itm = q_item(p, i);
+        if (itm.nkv == 0) continue;
+        mbar_wait(bar_qdo_full, k & 1);
+        for (int j = 0; j < itm.nkv; ++j, ++g) {
+          const int st = g % STAGES;
+          mbar_wait(&bar_kv_full[st], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sK = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::TILE);
+          const uint32_t sV = sK + Cfg::TILE;
+          // S_g = Q·K_gᵀ into S buffer g%2 (its previous dS was consumed by dQ_{g-2}: issue order)
+#pragma unroll
+          for (int s = 0; s < HD / 16; ++s)
+            umma_f16_ss(tmem + Cfg::s_col(g), make_sdesc_sw128(sQ + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
+                        make_sdesc_sw128(sK + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
+          umma_commit(&bar_s_full[g & 1]);
+          // dQ of the previous tile (needs its dS), then dP_g over the dP columns it freed
+          if (pj >= 0) do_dq();
+          if (j == 0 && k > 0) mbar_wait(bar_dq_empty, (k - 1) & 1);  // previous item's dQ drained
+#pragma unroll
+          for (int s = 0; s < HD / 16; ++s)
+            umma_f16_ss(tmem + Cfg::DP_COL, make_sdesc_sw128(sdO + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
+                        make_sdesc_sw128(sV + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
+          umma_commit(bar_dp_full);
+          if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
+          pj = j;
+          pg = g;
+          plast = (j == itm.nkv - 1);
+        }
+        ++k;
+      }
+      if (pj >= 0) do_dq();
+    }
+  } else {
+    // ================================================ softmax + epilogue warps 0-7 (query row, key-column half)
+    const int quad = warp & 3, half = warp >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int r = quad * 32 + lane;
+    const int c0 = half * 64;
+    int g = 0, k = 0;
+    for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
+      const QItem itm = q_item(p, i);
+      if (itm.nkv == 0) continue;
+      const int row = itm.q0 + r;
+      const bool valid = row < p.T;
+      const int2 rs = valid ? __ldg(p.rows_span + row) : make_int2(0, 0);
+      const float lse2 = valid ? __ldg(p.lse2 + int64_t(itm.h) * p.Tp + row) : 0.f;
+      const float dsum = valid ? __ldg(p.dsum + int64_t(itm.h) * p.Tp + row) : 0.f;
+      for (int j = 0; j < itm.nkv; ++j, ++g) {
+        const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
+        const int kv0 = itm.kv_lo + j * 128 + c0;
+        const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
+        const bool full = c_lo <= 0 && c_hi >= 64;
+        mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        float pr[64];
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+          uint32_t sr[32];
+          tmem_ld32(s_tm + cc, sr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int c = cc + t;
+            const float e = ex2_approx(fmaf(__uint_as_float(sr[t]), p.scale_log2, -lse2));
+            pr[c] = (full || (c >= c_lo && c < c_hi)) ? e : 0.f;
+          }
+        }
+        mbar_wait(bar_dp_full, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+          uint32_t dr[32];
+          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0 + cc, dr);
+          tmem_wait_ld();
+          uint32_t dk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int c = cc + 2 * t;
+            dk[t] = pack_bf16x2(pr[c] * (__uint_as_float(dr[2 * t]) - dsum),
+                                pr[c + 1] * (__uint_as_float(dr[2 * t + 1]) - dsum));
+          }
+          tmem_st16(s_tm + cc / 2, dk);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bar_p_full[g & 1]);
+      }
+      // ---- item end: dQ = scale · acc → bf16 (half of the head dim per warp)
+      mbar_wait(bar_dq_full, k & 1);
+      tc_fence_after();
+      const int64_t dst = valid ? (p.row_map ? int64_t(__ldg(p.row_map + row)) : int64_t(row)) : 0;
+      __nv_bfloat16* dqrow = p.dq + (dst * p.H + itm.h) * HD + half * (HD / 2);
+#pragma unroll 1
+      for (int c = 0; c < HD / 2; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + Cfg::DQ_COL + half * (HD / 2) + c, v);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            pk[t] = pack_bf16x2(__uint_as_float(v[2 * t]) * p.scale, __uint_as_float(v[2 * t + 1]) * p.scale);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            reinterpret_cast<uint4*>(dqrow + c)[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar_dq_empty);
+      ++k;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 13) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 struct BwdWs {
-  float* dq_acc;
   float* lse2;
   float* dsum;
   int2* rows_span;
@@ -469,7 +635,7 @@ size_t bwd_ws(BwdWs* w, void* base, const vlasim_attn_args* a) {
     off += up(bytes);
     return r;
   };
-  w->dq_acc = reinterpret_cast<float*>(take(T * H * d * 4));
+  (void)d;
   w->lse2 = reinterpret_cast<float*>(take(Tp * H * 4 + 512 * 4));
   w->dsum = reinterpret_cast<float*>(take(Tp * H * 4 + 512 * 4));
   w->rows_span = reinterpret_cast<int2*>(take(T * 8));
@@ -480,11 +646,9 @@ size_t bwd_ws(BwdWs* w, void* base, const vlasim_attn_args* a) {
 template <int HD>
 int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdWs& w, cudaStream_t st) {
   using namespace vlasim_host;
-  using Cfg = BwdCfg<HD>;
   const int T = int(a->total_tokens), H = a->num_heads, Hkv = a->num_kv_heads;
   const int Tp = (T + 3) & ~3;
   const int64_t rows = int64_t(T) * H;
-  VLASIM_CUDA_TRY(cudaMemsetAsync(w.dq_acc, 0, size_t(rows) * HD * 4, st));
   k_bwd_pre<HD><<<(rows * (HD / 8) + 255) / 256, 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(a->o), static_cast<const __nv_bfloat16*>(g->dout), a->lse, w.lse2, w.dsum,
       w.rows_span, w.cols_span, a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, Tp, H);
@@ -496,7 +660,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   if (int rc = encode_tmap_2d(&tk, a->k, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
   BwdParams p;
-  p.dq_acc = w.dq_acc;
+  p.dq = static_cast<__nv_bfloat16*>(g->dq);
   p.dk = static_cast<__nv_bfloat16*>(g->dk);
   p.dv = static_cast<__nv_bfloat16*>(g->dv);
   p.row_map = g->row_map;
@@ -508,17 +672,25 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.Tp = Tp;
   p.H = H;
   p.Hkv = Hkv;
-  p.num_items = int((int64_t(T) + 127) / 128) * Hkv;
+  p.kv_items = int((int64_t(T) + 127) / 128) * Hkv;
+  p.q_items = int((int64_t(T) + 127) / 128) * H;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;
-  auto kern = attn_bwd_kernel<HD>;
-  VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const int grid = std::min(p.num_items, num_sms());
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
-  VLASIM_LAUNCH_CHECK();
-  k_bwd_post<HD><<<(rows * (HD / 8) + 255) / 256, 256, 0, st>>>(w.dq_acc, static_cast<__nv_bfloat16*>(g->dq),
-                                                             g->row_map, rows, H, a->softmax_scale);
-  VLASIM_LAUNCH_CHECK();
+  {
+    using Cfg = DkvCfg<HD>;
+    auto kern = k_bwd_dkdv<HD>;
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    kern<<<std::min(p.kv_items, num_sms()), 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    VLASIM_LAUNCH_CHECK();
+  }
+  {
+    constexpr int ST = HD == 64 ? 4 : 2;
+    using Cfg = DqCfg<HD, ST>;
+    auto kern = k_bwd_dq<HD, ST>;
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    kern<<<std::min(p.q_items, num_sms()), 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    VLASIM_LAUNCH_CHECK();
+  }
   return VLASIM_OK;
 }
 

@@ -12,7 +12,8 @@
 //              columns each half read, and each half stores its half of the O row.
 //   warp 8     TMA producer (Q double buffer, K/V ring)
 //   warp 9     TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
-// TMEM (512 cols): S0 [0,128) · S1 [128,256) · O [256, 256+HD).
+// TMEM (512 cols): S0 [0,128) · S1 [128,256) · O0 [256, 256+HD) · O1 after O0 (double-buffered so an
+// item's epilogue can be deferred past the next item's first tile).
 // Visible-key spans per token come from k_fwd_spans (one binary search per token).
 #include <cfloat>
 #include <climits>
@@ -56,10 +57,10 @@ struct Fwd2Cfg {
   static constexpr int OFF_KV = 2 * Q_BYTES;     // stage s: K at +s*2*KV_BYTES, V right after
   static constexpr int OFF_XCH = OFF_KV + STAGES * 2 * KV_BYTES;  // float [2 parity][2 half][128]
   static constexpr int OFF_BAR = OFF_XCH + 2 * 2 * 128 * 4;
-  static constexpr int NUM_BARS = 4 + 2 * STAGES + 4 + 2;
+  static constexpr int NUM_BARS = 4 + 2 * STAGES + 4 + 5;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
-  static_assert(O_COL + HD <= 512, "TMEM budget");
+  static_assert(O_COL + 2 * HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
 
@@ -93,8 +94,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar_kv_empty = bars + 4 + STAGES;    // [STAGES]
   uint64_t* bar_s_full = bars + 4 + 2 * STAGES;  // [2]
   uint64_t* bar_p_full = bar_s_full + 2;         // [2] 256 arrivals
-  uint64_t* bar_o_full = bar_s_full + 4;         // one completion per item (last PV landed)
-  uint64_t* bar_o_ready = bar_s_full + 5;        // one completion per PV
+  uint64_t* bar_o_full = bar_s_full + 4;         // [2] per item: last PV landed in O[k%2]
+  uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 256 arrivals: epilogue drained O[k%2]
+  uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
   float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
@@ -110,7 +112,10 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&bar_kv_full[s], 1);
       mbar_init(&bar_kv_empty[s], 1);
     }
-    mbar_init(bar_o_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_o_full[s], 1);
+      mbar_init(&bar_o_empty[s], 256);
+    }
     mbar_init(bar_o_ready, 1);
     fence_barrier_init();
   }
@@ -155,21 +160,22 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
       int g = 0, k = 0;
-      int pj = -1, pg = 0;  // pending PV (issued one tile late so S_g overlaps softmax of g-1)
+      int pj = -1, pg = 0, pk = 0;  // pending PV (issued one tile late so S_g overlaps softmax of g-1)
       bool plast = false;
       auto do_pv = [&]() {
         mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
+        if (pj == 0 && pk >= 2) mbar_wait(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
         tc_fence_after();
         const int st = pg % STAGES;
         const uint32_t v_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
         const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
 #pragma unroll
         for (int s = 0; s < BN / 16; ++s)  // P: columns 0-63 at +0..31, 64-127 at +64..95
-          umma_f16_ts(tmem + Cfg::O_COL, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+          umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
                       make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024), idesc_o, (pj > 0 || s > 0) ? 1u : 0u);
         umma_commit(&bar_kv_empty[st]);
         umma_commit(bar_o_ready);
-        if (plast) umma_commit(bar_o_full);
+        if (plast) umma_commit(&bar_o_full[pk & 1]);
       };
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
         const FwdItem itm = fwd_item(p, i, BN);
@@ -191,6 +197,7 @@ __global__ void __launch_bounds__(320, 1)
           if (pj >= 0) do_pv();
           pj = j;
           pg = g;
+          pk = k;
           plast = (j == itm.nkv - 1);
         }
       }
@@ -203,11 +210,44 @@ __global__ void __launch_bounds__(320, 1)
     const int r = quad * 32 + lane;
     const int c0 = half * 64;
     const float sl2 = p.scale_log2;
+    // Epilogue of item `ek` is deferred until the first tile of the next item has been handed to
+    // the MMA warp, so the tensor core never idles on it (O is double-buffered in TMEM).
+    int ek = -1, e_row = 0, e_h = 0;
+    float e_m = 0.f, e_l = 0.f;
+    auto epilogue = [&]() {
+      mbar_wait(&bar_o_full[ek & 1], (ek >> 1) & 1);
+      tc_fence_after();
+      const bool valid = e_row < p.T;
+      const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
+      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(valid ? e_row : 0) * p.H + e_h) * HD + half * (HD / 2);
+      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + half * (HD / 2);
+#pragma unroll
+      for (int c = 0; c < HD / 2; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(o_tm + c, o);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_o_empty[ek & 1]);
+      if (valid && half == 0)
+        p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
+      ek = -1;
+    };
     int g = 0, k = 0;
     for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
       const FwdItem itm = fwd_item(p, i, BN);
       const int row = itm.q0 + r;
       const int2 rs = row < p.T ? __ldg(p.rows_span + row) : make_int2(0, 0);
+      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + half * (HD / 2);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
@@ -253,11 +293,11 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int c = 0; c < HD / 2; c += 32) {
             uint32_t o[32];
-            tmem_ld32(tmem + lane_off + Cfg::O_COL + half * (HD / 2) + c, o);
+            tmem_ld32(o_tm + c, o);
             tmem_wait_ld();
 #pragma unroll
             for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-            tmem_st32(tmem + lane_off + Cfg::O_COL + half * (HD / 2) + c, o);
+            tmem_st32(o_tm + c, o);
           }
         }
         if (grow) {
@@ -282,40 +322,24 @@ __global__ void __launch_bounds__(320, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bar_p_full[g & 1]);
+        if (j == 0 && ek >= 0) epilogue();  // previous item, now that this tile is in flight
       }
-      // ---- epilogue: combine the halves' row sums, O / l → bf16, LSE
+      // combine the halves' row sums and defer this item's epilogue
       float* xs = xch + (g & 1) * 256;  // parity not used by any in-flight tile
       xs[half * 128 + r] = l_run;
       named_bar_sync(1 + quad, 64);
       const float l_tot = l_run + xs[(1 - half) * 128 + r];
-      const bool valid = row < p.T && itm.nkv > 0;
+      named_bar_sync(1 + quad, 64);  // both halves read before the slot is reused
+      if (ek >= 0) epilogue();       // (only when this item had no tiles)
       if (itm.nkv > 0) {
-        mbar_wait(bar_o_full, k & 1);
-        tc_fence_after();
+        ek = k;
+        e_row = row;
+        e_h = itm.h;
+        e_m = m_run;
+        e_l = l_tot;
       }
-      const float inv_l = (valid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
-      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + itm.h) * HD + half * (HD / 2);
-#pragma unroll
-      for (int c = 0; c < HD / 2; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem + lane_off + Cfg::O_COL + half * (HD / 2) + c, o);
-        tmem_wait_ld();
-        if (valid) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t)
-            pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-        }
-      }
-      if (valid && half == 0)
-        p.lse[static_cast<int64_t>(itm.h) * p.T + row] = (m_run + __log2f(l_tot)) * 0.69314718055994530942f;
-      // O is overwritten by the next item's first PV only after p_full of that item, which this
-      // warp arrives on after these tcgen05.ld have completed.
-      named_bar_sync(1 + quad, 64);
     }
+    if (ek >= 0) epilogue();
   }
   tc_fence_before();
   __syncthreads();

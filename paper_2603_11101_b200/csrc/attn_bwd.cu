@@ -180,8 +180,10 @@ __global__ void __launch_bounds__(320, 1)
     // ================================================ TMA producer
     if (lane == 0) {
       int G = 0, k = 0;
+      KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
-        const KvItem itm = kv_item(p, i);
+        const KvItem itm = nxt;
+        if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);  // prefetch
         if (itm.iters == 0) continue;
         for (int it = 0; it < itm.iters; ++it, ++G) {
           const int h = itm.kh * group + it / itm.nq;
@@ -239,13 +241,16 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(bar_dp_full);
       };
       int G = 0, k = 0;
+      KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
-        const KvItem itm = kv_item(p, i);
+        const KvItem itm = nxt;
+        if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);  // prefetch
         if (itm.iters == 0) continue;
         mbar_wait(bar_kv_full, k & 1);
         tc_fence_after();
         mma_S(G);
         mma_dP(G);
+        if (itm.iters == 1) umma_commit(bar_kv_empty);  // K, V read only by S and dP
         for (int it = 0; it < itm.iters; ++it, ++G) {
           const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
           const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
@@ -266,8 +271,8 @@ __global__ void __launch_bounds__(320, 1)
           if (it + 1 < itm.iters) {
             mma_S(G + 1);   // over P/S columns after dV read them (issue order)
             mma_dP(G + 1);  // over dS/dP columns after dK read them
+            if (it + 2 == itm.iters) umma_commit(bar_kv_empty);  // last reader of K and V issued
           } else {
-            umma_commit(bar_kv_empty);
             umma_commit(bar_dkv_full);
           }
         }
@@ -281,11 +286,17 @@ __global__ void __launch_bounds__(320, 1)
     const int krow = quad * 32 + lane;
     const int c0 = half * 64;
     int G = 0, k = 0;
+    KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
+    int2 ks_nxt = nxt.k0 + krow < p.T ? __ldg(p.cols_span + nxt.k0 + krow) : make_int2(0, 0);
     for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
-      const KvItem itm = kv_item(p, i);
+      const KvItem itm = nxt;
+      const int2 ks = ks_nxt;
+      if (i + int(gridDim.x) < p.kv_items) {  // prefetch the next item's parameters
+        nxt = kv_item(p, i + gridDim.x);
+        ks_nxt = nxt.k0 + krow < p.T ? __ldg(p.cols_span + nxt.k0 + krow) : make_int2(0, 0);
+      }
       if (itm.iters == 0) continue;
       const int key = itm.k0 + krow;
-      const int2 ks = key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0);
       for (int it = 0; it < itm.iters; ++it, ++G) {
         const int qb = itm.q_lo + (it % itm.nq) * 128;
         const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
@@ -453,8 +464,10 @@ __global__ void __launch_bounds__(320, 1)
     // ================================================ TMA producer
     if (lane == 0) {
       int g = 0, k = 0;
+      QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-        const QItem itm = q_item(p, i);
+        const QItem itm = nxt;
+        if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
         mbar_expect_tx(bar_qdo_full, 2 * Cfg::TILE);
@@ -499,8 +512,10 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(&bar_kv_empty[pg % STAGES]);
         if (plast) umma_commit(bar_dq_full);
       };
+      QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-        const QItem itm = q_item(p, i);
+        const QItem itm = nxt;
+        if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         mbar_wait(bar_qdo_full, k & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
@@ -539,14 +554,29 @@ __global__ void __launch_bounds__(320, 1)
     const int r = quad * 32 + lane;
     const int c0 = half * 64;
     int g = 0, k = 0;
+    // row parameters of the next item are prefetched one item ahead
+    auto load_row = [&](const QItem& it, int2& rs_, float& l_, float& d_) {
+      const int rw = it.q0 + r;
+      const bool v = rw < p.T;
+      rs_ = v ? __ldg(p.rows_span + rw) : make_int2(0, 0);
+      l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw) : 0.f;
+      d_ = v ? __ldg(p.dsum + int64_t(it.h) * p.Tp + rw) : 0.f;
+    };
+    QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
+    int2 rs_n;
+    float lse_n, dsum_n;
+    load_row(nxt, rs_n, lse_n, dsum_n);
     for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-      const QItem itm = q_item(p, i);
+      const QItem itm = nxt;
+      const int2 rs = rs_n;
+      const float lse2 = lse_n, dsum = dsum_n;
+      if (i + int(gridDim.x) < p.q_items) {
+        nxt = q_item(p, i + gridDim.x);
+        load_row(nxt, rs_n, lse_n, dsum_n);
+      }
       if (itm.nkv == 0) continue;
       const int row = itm.q0 + r;
       const bool valid = row < p.T;
-      const int2 rs = valid ? __ldg(p.rows_span + row) : make_int2(0, 0);
-      const float lse2 = valid ? __ldg(p.lse2 + int64_t(itm.h) * p.Tp + row) : 0.f;
-      const float dsum = valid ? __ldg(p.dsum + int64_t(itm.h) * p.Tp + row) : 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
         const int kv0 = itm.kv_lo + j * 128 + c0;

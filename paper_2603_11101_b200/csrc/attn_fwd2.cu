@@ -132,8 +132,10 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       int g = 0, k = 0;
+      FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-        const FwdItem itm = fwd_item(p, i, BN);
+        const FwdItem itm = nxt;
+        if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
         if (k >= 2) mbar_wait(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
         uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
@@ -177,8 +179,10 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(bar_o_ready);
         if (plast) umma_commit(&bar_o_full[pk & 1]);
       };
+      FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-        const FwdItem itm = fwd_item(p, i, BN);
+        const FwdItem itm = nxt;
+        if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
         const uint32_t q_addr = smem_u32(smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES);
         mbar_wait(&bar_q_full[qs], (k >> 1) & 1);
@@ -243,10 +247,16 @@ __global__ void __launch_bounds__(320, 1)
       ek = -1;
     };
     int g = 0, k = 0;
+    FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
+    int2 rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
     for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-      const FwdItem itm = fwd_item(p, i, BN);
+      const FwdItem itm = nxt;
+      const int2 rs = rs_n;
+      if (i + int(gridDim.x) < p.num_items) {  // prefetch the next item's parameters
+        nxt = fwd_item(p, i + gridDim.x, BN);
+        rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
+      }
       const int row = itm.q0 + r;
-      const int2 rs = row < p.T ? __ldg(p.rows_span + row) : make_int2(0, 0);
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + half * (HD / 2);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {

@@ -10,7 +10,7 @@ si = h.index("Warp Stall Sampling (All Samples)")
 tot = {r: 0 for r in reasons}
 data = []
 for r in rows[2:]:
-    if len(r) <= si:
+    if len(r) < len(h) or not (r[si] or "0").isdigit():
         continue
     s = int(r[si] or 0)
     rs = {x: int(r[h.index(x)] or 0) for x in reasons}

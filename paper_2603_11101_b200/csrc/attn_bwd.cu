@@ -89,6 +89,7 @@ struct BwdParams {
   const int2* cols_span;   // [T] queries that see key t
   int T, Tp, H, Hkv, kv_items, q_items;
   float scale_log2, scale;
+  unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
 };
 
 // ================================================================== dK / dV (KV-stationary)
@@ -131,7 +132,7 @@ __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   return it;
 }
 
-template <int HD>
+template <int HD, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 8) {
     // ================================================ TMA producer
     if (lane == 0) {
+      WaitProf<PROF> wp;
       int G = 0, k = 0;
       KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
@@ -189,14 +191,14 @@ __global__ void __launch_bounds__(320, 1)
           const int h = itm.kh * group + it / itm.nq;
           const int qb = itm.q_lo + (it % itm.nq) * 128;
           const int b = G & 1;
-          if (G >= 2) mbar_wait(&bar_q_empty[b], ((G >> 1) - 1) & 1);
+          if (G >= 2) wp.template wait<0>(&bar_q_empty[b], ((G >> 1) - 1) & 1);
           mbar_expect_tx(&bar_q_full[b], Cfg::TILE + 528);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
             tma_load_2d(smem + Cfg::OFF_Q + b * Cfg::TILE + c * 16384, &tmQ, h * HD + c * 64, qb, &bar_q_full[b]);
           bulk_load(smem + Cfg::OFF_LSE + b * Cfg::VEC, p.lse2 + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_q_full[b]);
           if (it == 0) {
-            if (k > 0) mbar_wait(bar_kv_empty, (k - 1) & 1);
+            if (k > 0) wp.template wait<1>(bar_kv_empty, (k - 1) & 1);
             mbar_expect_tx(bar_kv_full, 2 * Cfg::TILE);
 #pragma unroll
             for (int c = 0; c < HD / 64; ++c) {
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(320, 1)
               tma_load_2d(smem + Cfg::OFF_V + c * 16384, &tmV, itm.kh * HD + c * 64, itm.k0, bar_kv_full);
             }
           }
-          if (G >= 2) mbar_wait(&bar_do_empty[b], ((G >> 1) - 1) & 1);
+          if (G >= 2) wp.template wait<2>(&bar_do_empty[b], ((G >> 1) - 1) & 1);
           mbar_expect_tx(&bar_do_full[b], Cfg::TILE + 528);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         ++k;
       }
+      wp.flush(p.prof);
     }
   } else if (warp == 9) {
     // ================================================ MMA issuer
@@ -220,9 +223,10 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ
       constexpr uint32_t id_kmn = make_idesc_bf16(128, HD, false, true);   // dV, dK
       const uint32_t sK = smem_u32(smem + Cfg::OFF_K), sV = smem_u32(smem + Cfg::OFF_V);
+      WaitProf<PROF> wp;
       auto mma_S = [&](int G) {
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
-        mbar_wait(&bar_q_full[G & 1], (G >> 1) & 1);
+        wp.template wait<1>(&bar_q_full[G & 1], (G >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < HD / 16; ++s)
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(320, 1)
       };
       auto mma_dP = [&](int G) {
         const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
-        mbar_wait(&bar_do_full[G & 1], (G >> 1) & 1);
+        wp.template wait<2>(&bar_do_full[G & 1], (G >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < HD / 16; ++s)
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(320, 1)
         const KvItem itm = nxt;
         if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);  // prefetch
         if (itm.iters == 0) continue;
-        mbar_wait(bar_kv_full, k & 1);
+        wp.template wait<0>(bar_kv_full, k & 1);
         tc_fence_after();
         mma_S(G);
         mma_dP(G);
@@ -254,8 +258,8 @@ __global__ void __launch_bounds__(320, 1)
         for (int it = 0; it < itm.iters; ++it, ++G) {
           const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
           const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
-          mbar_wait(bar_p_full, G & 1);
-          if (it == 0 && k > 0) mbar_wait(bar_dkv_empty, (k - 1) & 1);
+          wp.template wait<3>(bar_p_full, G & 1);
+          if (it == 0 && k > 0) wp.template wait<4>(bar_dkv_empty, (k - 1) & 1);
           tc_fence_after();
           // dV += Pᵀ·dO and dK += dSᵀ·Q; A from TMEM: queries 0-63 at +0..31, 64-127 at +64..95
 #pragma unroll
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         ++k;
       }
+      wp.flush(p.prof + 8);
     }
   } else {
     // ================================================ softmax warps 0-7 (key row, query-column half)
@@ -285,6 +290,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int krow = quad * 32 + lane;
     const int c0 = half * 64;
+    WaitProf<PROF> wp;
     int G = 0, k = 0;
     KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
     int2 ks_nxt = nxt.k0 + krow < p.T ? __ldg(p.cols_span + nxt.k0 + krow) : make_int2(0, 0);
@@ -304,7 +310,8 @@ __global__ void __launch_bounds__(320, 1)
         const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
         const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
         // ---- phase A: Sᵀ → Pᵀ (fp32 in registers, bf16 over the S columns)
-        mbar_wait(bar_s_full, G & 1);
+        wp.template wait<0>(bar_s_full, G & 1);
+        const long long ta = wp.now();
         tc_fence_after();
         float pr[64];
 #pragma unroll
@@ -324,7 +331,9 @@ __global__ void __launch_bounds__(320, 1)
           tmem_st16(tmem + lane_off + Cfg::S_COL + c0 + cc / 2, pk);
         }
         // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
-        mbar_wait(bar_dp_full, G & 1);
+        wp.template add_since<4>(ta);
+        wp.template wait<1>(bar_dp_full, G & 1);
+        const long long tb = wp.now();
         tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 32) {
@@ -343,9 +352,11 @@ __global__ void __launch_bounds__(320, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bar_p_full);
+        wp.template add_since<5>(tb);
       }
       // ---- item end: dK / dV epilogue (key row krow, head-dim half `half`)
-      mbar_wait(bar_dkv_full, k & 1);
+      const long long te = wp.now();
+      wp.template wait<2>(bar_dkv_full, k & 1);
       tc_fence_after();
       const bool valid = key < p.T;
       const int64_t dst = valid ? (p.row_map ? int64_t(__ldg(p.row_map + key)) : int64_t(key)) : 0;
@@ -373,8 +384,10 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(bar_dkv_empty);
+      wp.template add_since<3>(te);
       ++k;
     }
+    if (warp == 0 && lane == 0) wp.flush(p.prof + 16);
   }
   tc_fence_before();
   __syncthreads();
@@ -708,10 +721,17 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.scale_log2 = a->softmax_scale * kLog2e;
   {
     using Cfg = DkvCfg<HD>;
-    auto kern = k_bwd_dkdv<HD>;
+    const int grid = std::min(p.kv_items, num_sms());
+    p.prof = prof_enabled() ? prof_buffer() : nullptr;
+    auto kern = p.prof ? k_bwd_dkdv<HD, true> : k_bwd_dkdv<HD, false>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<std::min(p.kv_items, num_sms()), 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
     VLASIM_LAUNCH_CHECK();
+    if (p.prof)
+      prof_report("k_bwd_dkdv", grid, st,
+                  {"prod:q_empty", "prod:kv_empty", "prod:do_empty", "", "", "", "", "prod:total", "mma:kv_full",
+                   "mma:q_full", "mma:do_full", "mma:p_full", "mma:dkv_empty", "", "", "mma:total", "smx:s_full",
+                   "smx:dp_full", "smx:dkv_full", "smx:epilogue", "smx:phaseA", "smx:phaseB", "", "smx:total"});
   }
   {
     constexpr int ST = HD == 64 ? 4 : 2;

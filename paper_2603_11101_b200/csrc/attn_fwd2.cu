@@ -46,6 +46,7 @@ struct Fwd2Params {
   const int2* rows_span;
   int T, H, Hkv, num_items;
   float scale_log2;
+  unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
 };
 
 template <int HD, int STAGES>
@@ -79,7 +80,7 @@ __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) 
   return it;
 }
 
-template <int HD, int STAGES>
+template <int HD, int STAGES, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const Fwd2Params p) {
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 8) {
     // ================================================ TMA producer
     if (lane == 0) {
+      WaitProf<PROF> wp;
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
@@ -137,14 +139,14 @@ __global__ void __launch_bounds__(320, 1)
         const FwdItem itm = nxt;
         if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
-        if (k >= 2) mbar_wait(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
+        if (k >= 2) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
         uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
         mbar_expect_tx(&bar_q_full[qs], Cfg::Q_BYTES);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * 64, itm.q0, &bar_q_full[qs]);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           const int st = g % STAGES;
-          if (g >= STAGES) mbar_wait(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
+          if (g >= STAGES) wp.template wait<1>(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
           uint8_t* sk = smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES;
           uint8_t* sv = sk + Cfg::KV_BYTES;
           const int kv0 = itm.kv_lo + j * BN;
@@ -155,18 +157,20 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
         }
       }
+      wp.flush(p.prof);
     }
   } else if (warp == 9) {
     // ================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
+      WaitProf<PROF> wp;
       int g = 0, k = 0;
       int pj = -1, pg = 0, pk = 0;  // pending PV (issued one tile late so S_g overlaps softmax of g-1)
       bool plast = false;
       auto do_pv = [&]() {
-        mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
-        if (pj == 0 && pk >= 2) mbar_wait(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
+        wp.template wait<2>(&bar_p_full[pg & 1], (pg >> 1) & 1);
+        if (pj == 0 && pk >= 2) wp.template wait<3>(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
         tc_fence_after();
         const int st = pg % STAGES;
         const uint32_t v_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
@@ -185,10 +189,10 @@ __global__ void __launch_bounds__(320, 1)
         if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
         const uint32_t q_addr = smem_u32(smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES);
-        mbar_wait(&bar_q_full[qs], (k >> 1) & 1);
+        wp.template wait<0>(&bar_q_full[qs], (k >> 1) & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           const int st = g % STAGES;
-          mbar_wait(&bar_kv_full[st], (g / STAGES) & 1);
+          wp.template wait<1>(&bar_kv_full[st], (g / STAGES) & 1);
           tc_fence_after();
           const uint32_t k_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES);
           const uint32_t d_s = tmem + Cfg::S_COL + (g & 1) * 128;
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
       if (pj >= 0) do_pv();
+      wp.flush(p.prof + 8);
     }
   } else {
     // ================================================ softmax + epilogue warps 0-7
@@ -216,10 +221,12 @@ __global__ void __launch_bounds__(320, 1)
     const float sl2 = p.scale_log2;
     // Epilogue of item `ek` is deferred until the first tile of the next item has been handed to
     // the MMA warp, so the tensor core never idles on it (O is double-buffered in TMEM).
+    WaitProf<PROF> wp;
     int ek = -1, e_row = 0, e_h = 0;
     float e_m = 0.f, e_l = 0.f;
     auto epilogue = [&]() {
-      mbar_wait(&bar_o_full[ek & 1], (ek >> 1) & 1);
+      const long long te = wp.now();
+      wp.template wait<2>(&bar_o_full[ek & 1], (ek >> 1) & 1);
       tc_fence_after();
       const bool valid = e_row < p.T;
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
@@ -245,6 +252,7 @@ __global__ void __launch_bounds__(320, 1)
       if (valid && half == 0)
         p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
       ek = -1;
+      wp.template add_since<4>(te);
     };
     int g = 0, k = 0;
     FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(320, 1)
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
-        mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+        wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
         uint32_t x[64];
         {
@@ -292,13 +300,17 @@ __global__ void __launch_bounds__(320, 1)
         // combine the two column halves of this row
         float* xs = xch + (g & 1) * 256;
         xs[half * 128 + r] = mt;
-        named_bar_sync(1 + quad, 64);
+        {
+          const long long tb = wp.now();
+          named_bar_sync(1 + quad, 64);
+          wp.template add_since<3>(tb);
+        }
         mt = fmaxf(mt, xs[(1 - half) * 128 + r]);
         mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
         const bool grow = mt > m_run + kLazyRescale;
         const float alpha = grow ? exp2f(m_run - mt) : 1.f;
         if (__any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY)) {
-          mbar_wait(bar_o_ready, (g - 1) & 1);  // PV_{g-1} has landed in O
+          wp.template wait<1>(bar_o_ready, (g - 1) & 1);  // PV_{g-1} has landed in O
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD / 2; c += 32) {
@@ -350,6 +362,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     if (ek >= 0) epilogue();
+    if (warp == 0 && lane == 0) wp.flush(p.prof + 16);
   }
   tc_fence_before();
   __syncthreads();
@@ -378,9 +391,22 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   p.Hkv = a->num_kv_heads;
   p.num_items = int((int64_t(T) + 127) / 128) * a->num_heads;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
-  auto kern = attn_fwd2_kernel<HD, STAGES>;
+  const int grid = std::min(p.num_items, num_sms());
+  if (prof_enabled()) {
+    p.prof = prof_buffer();
+    auto kern = attn_fwd2_kernel<HD, STAGES, true>;
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
+    VLASIM_LAUNCH_CHECK();
+    return prof_report("attn_fwd2", grid, st,
+                       {"prod:q_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:q_full", "mma:kv_full",
+                        "mma:p_full", "mma:o_empty", "", "", "", "mma:total", "smx:s_full", "smx:o_ready",
+                        "smx:o_full", "smx:xchg_bar", "smx:epilogue", "", "", "smx:total"});
+  }
+  p.prof = nullptr;
+  auto kern = attn_fwd2_kernel<HD, STAGES, false>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  kern<<<std::min(p.num_items, num_sms()), 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
+  kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }

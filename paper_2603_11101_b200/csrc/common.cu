@@ -64,6 +64,37 @@ int num_sms() {
   return n;
 }
 
+bool prof_enabled() {
+  static const bool on = getenv("VLASIM_PROF") != nullptr;
+  return on;
+}
+
+static unsigned long long* g_prof = nullptr;
+static unsigned long long* prof_buffer_peek() { return g_prof; }
+unsigned long long* prof_buffer() {
+  if (!g_prof) cudaMalloc(&g_prof, 64 * sizeof(unsigned long long));
+  cudaMemset(g_prof, 0, 64 * sizeof(unsigned long long));
+  return g_prof;
+}
+
+int prof_report(const char* kernel, int grid, cudaStream_t st, std::initializer_list<const char*> names) {
+  unsigned long long h[64];
+  VLASIM_CUDA_TRY(cudaStreamSynchronize(st));
+  VLASIM_CUDA_TRY(cudaMemcpy(h, prof_buffer_peek(), sizeof(h), cudaMemcpyDeviceToHost));
+  std::string line = std::string("[vlasim prof] ") + kernel + " avg cycles/CTA:";
+  int i = 0;
+  for (const char* n : names) {
+    if (n && *n) {
+      char b[96];
+      snprintf(b, sizeof(b), " %s=%.0f", n, double(h[i]) / grid);
+      line += b;
+    }
+    ++i;
+  }
+  fprintf(stderr, "%s\n", line.c_str());
+  return VLASIM_OK;
+}
+
 }  // namespace vlasim_host
 
 extern "C" {

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <initializer_list>
 #include <string>
 
 #include "../../include/vlasim_cuda.h"
@@ -44,5 +45,11 @@ int encode_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype
 inline cudaStream_t as_stream(vlasim_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int num_sms();
+
+// VLASIM_PROF=1: kernels with wait-time accounting are launched instead and each launch prints
+// (stderr) the average cycles per CTA spent in every named wait category.
+bool prof_enabled();
+unsigned long long* prof_buffer();  // zeroed device buffer of 64 counters
+int prof_report(const char* kernel, int grid, cudaStream_t st, std::initializer_list<const char*> names);
 
 }  // namespace vlasim_host

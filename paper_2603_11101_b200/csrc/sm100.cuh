@@ -233,4 +233,47 @@ __device__ __forceinline__ void red_add_v4_f32(float* gaddr, float a, float b, f
                : "memory");
 }
 
+// ---------------------------------------------------------------- profiling (VLASIM_PROF)
+// Per-role wait-time accounting, compiled in only for the PROF kernel instantiations:
+// accumulates clock64 cycles spent in each mbarrier wait category and flushes them to a global
+// counter array (one warp-lane per role) at kernel exit.
+template <bool ON, int N = 8>
+struct WaitProf {
+  unsigned long long acc[N];
+  long long t_start;
+  __device__ __forceinline__ WaitProf() {
+    if constexpr (ON) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = 0;
+      t_start = clock64();
+    }
+  }
+  template <int C>
+  __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+    if constexpr (ON) {
+      const long long t0 = clock64();
+      mbar_wait(bar, parity);
+      acc[C] += clock64() - t0;
+    } else {
+      mbar_wait(bar, parity);
+    }
+  }
+  template <int C>
+  __device__ __forceinline__ void add_since(long long t0) {
+    if constexpr (ON) acc[C] += clock64() - t0;
+  }
+  __device__ __forceinline__ long long now() const {
+    if constexpr (ON) return clock64();
+    return 0;
+  }
+  // slot N-1 receives the role's total elapsed cycles
+  __device__ __forceinline__ void flush(unsigned long long* out) {
+    if constexpr (ON) {
+      acc[N - 1] = clock64() - t_start;
+#pragma unroll
+      for (int i = 0; i < N; ++i) atomicAdd(out + i, acc[i]);
+    }
+  }
+};
+
 }  // namespace vlasim_dev

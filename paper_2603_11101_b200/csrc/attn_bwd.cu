@@ -106,16 +106,45 @@ struct DkvCfg {
   static constexpr int OFF_K = 0, OFF_V = TILE;
   static constexpr int OFF_Q = 2 * TILE;        // [2]
   static constexpr int OFF_DO = 4 * TILE;       // [2]
+  static constexpr int OFF_STG = 6 * TILE;      // epilogue staging: 128 rows × HD bf16 (swizzled 16-B chunks)
   static constexpr int VEC = 544;               // 132 floats (16-B aligned window of 128) + pad
-  static constexpr int OFF_LSE = 6 * TILE;      // [2][VEC]
+  static constexpr int OFF_LSE = 7 * TILE;      // [2][VEC]
   static constexpr int OFF_DSUM = OFF_LSE + 2 * VEC;  // [2][VEC]
-  static constexpr int OFF_BAR = OFF_DSUM + 2 * VEC;
+  static constexpr int OFF_ROWS = OFF_DSUM + 2 * VEC;  // int [128] destination rows
+  static constexpr int OFF_BAR = OFF_ROWS + 512;
   static constexpr int NUM_BARS = 16;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
   static_assert(DK_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
+
+// Coalesced epilogue store of a [128 rows × HD] bf16 tile held as packed registers by the 256
+// softmax threads (thread = (row, head-dim half)): registers → swizzled smem staging → 16-B
+// global stores, 16 consecutive threads per 256-B row.  rows[r] < 0 skips row r.
+template <int HD>
+__device__ __forceinline__ void store_tile_coalesced(uint8_t* stg, const int* rows, const uint32_t (&pk)[HD / 4],
+                                                     int krow, int half, int tid, __nv_bfloat16* base,
+                                                     int64_t row_stride_elems, int bar_id) {
+  constexpr int CH = HD / 8;  // 16-B chunks per row
+#pragma unroll
+  for (int j = 0; j < CH / 2; ++j) {
+    const int ch = (half * (CH / 2) + j) ^ (krow & (CH - 1));
+    *reinterpret_cast<uint4*>(stg + krow * (HD * 2) + ch * 16) =
+        make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+  }
+  named_bar_sync(bar_id, 256);
+#pragma unroll
+  for (int idx = tid; idx < 128 * CH; idx += 256) {
+    const int r = idx / CH, ch = idx % CH;
+    const int dst = rows[r];
+    if (dst >= 0) {
+      const uint4 v = *reinterpret_cast<const uint4*>(stg + r * (HD * 2) + ((ch ^ (r & (CH - 1))) * 16));
+      *reinterpret_cast<uint4*>(base + int64_t(dst) * row_stride_elems + ch * 8) = v;
+    }
+  }
+  named_bar_sync(bar_id, 256);
+}
 
 struct KvItem {
   int k0, kh, q_lo, nq, iters;
@@ -138,7 +167,7 @@ __global__ void __launch_bounds__(320, 1)
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
   using Cfg = DkvCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_kv_full = bars + 0;
   uint64_t* bar_kv_empty = bars + 1;
@@ -358,32 +387,28 @@ __global__ void __launch_bounds__(320, 1)
       const long long te = wp.now();
       wp.template wait<2>(bar_dkv_full, k & 1);
       tc_fence_after();
-      const bool valid = key < p.T;
-      const int64_t dst = valid ? (p.row_map ? int64_t(__ldg(p.row_map + key)) : int64_t(key)) : 0;
-      __nv_bfloat16* dvrow = p.dv + (dst * p.Hkv + itm.kh) * HD + half * (HD / 2);
-      __nv_bfloat16* dkrow = p.dk + (dst * p.Hkv + itm.kh) * HD + half * (HD / 2);
-#pragma unroll 1
+      uint32_t pv[HD / 4], pkk[HD / 4];
+#pragma unroll
       for (int c = 0; c < HD / 2; c += 32) {
         uint32_t v[32], kk[32];
         tmem_ld32(tmem + lane_off + Cfg::DV_COL + half * (HD / 2) + c, v);
         tmem_ld32(tmem + lane_off + Cfg::DK_COL + half * (HD / 2) + c, kk);
         tmem_wait_ld();
-        if (valid) {
-          uint32_t pv[16], pk2[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            pv[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-            pk2[j] = pack_bf16x2(__uint_as_float(kk[2 * j]) * p.scale, __uint_as_float(kk[2 * j + 1]) * p.scale);
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            reinterpret_cast<uint4*>(dvrow + c)[j] = make_uint4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
-            reinterpret_cast<uint4*>(dkrow + c)[j] = make_uint4(pk2[4 * j], pk2[4 * j + 1], pk2[4 * j + 2], pk2[4 * j + 3]);
-          }
+        for (int j = 0; j < 16; ++j) {
+          pv[c / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+          pkk[c / 2 + j] = pack_bf16x2(__uint_as_float(kk[2 * j]) * p.scale, __uint_as_float(kk[2 * j + 1]) * p.scale);
         }
       }
       tc_fence_before();
-      mbar_arrive(bar_dkv_empty);
+      mbar_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
+      int* rows = reinterpret_cast<int*>(smem + Cfg::OFF_ROWS);
+      if (half == 0)
+        rows[krow] = key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1;
+      uint8_t* stg = smem + Cfg::OFF_STG;
+      named_bar_sync(5, 256);
+      store_tile_coalesced<HD>(stg, rows, pv, krow, half, tid, p.dv + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
+      store_tile_coalesced<HD>(stg, rows, pkk, krow, half, tid, p.dk + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
       wp.template add_since<3>(te);
       ++k;
     }
@@ -407,9 +432,11 @@ struct DqCfg {
   static constexpr int TILE = 128 * HD * 2;
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
   static constexpr int OFF_KV = 2 * TILE;  // stage s: K at +s*2*TILE, V right after
-  static constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
+  static constexpr int OFF_STG = OFF_KV + STAGES * 2 * TILE;  // epilogue staging (128 × HD bf16)
+  static constexpr int OFF_ROWS = OFF_STG + TILE;             // int [128]
+  static constexpr int OFF_BAR = OFF_ROWS + 512;
   static constexpr int NUM_BARS = 2 + 2 * STAGES + 2 + 2 + 2 + 2;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t DP_COL = 128, DQ_COL = 256;
   __host__ __device__ static constexpr uint32_t s_col(int g) { return (g & 1) ? 384u : 0u; }
   static_assert(DQ_COL + HD <= 384, "TMEM budget");
@@ -437,7 +464,7 @@ __global__ void __launch_bounds__(320, 1)
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
   using Cfg = DqCfg<HD, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_qdo_full = bars + 0;
   uint64_t* bar_qdo_empty = bars + 1;
@@ -630,28 +657,25 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_before();
         mbar_arrive(&bar_p_full[g & 1]);
       }
-      // ---- item end: dQ = scale · acc → bf16 (half of the head dim per warp)
+      // ---- item end: dQ = scale · acc → bf16 (half of the head dim per warp), coalesced store
       mbar_wait(bar_dq_full, k & 1);
       tc_fence_after();
-      const int64_t dst = valid ? (p.row_map ? int64_t(__ldg(p.row_map + row)) : int64_t(row)) : 0;
-      __nv_bfloat16* dqrow = p.dq + (dst * p.H + itm.h) * HD + half * (HD / 2);
-#pragma unroll 1
+      uint32_t pq[HD / 4];
+#pragma unroll
       for (int c = 0; c < HD / 2; c += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + lane_off + Cfg::DQ_COL + half * (HD / 2) + c, v);
         tmem_wait_ld();
-        if (valid) {
-          uint32_t pk[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t)
-            pk[t] = pack_bf16x2(__uint_as_float(v[2 * t]) * p.scale, __uint_as_float(v[2 * t + 1]) * p.scale);
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            reinterpret_cast<uint4*>(dqrow + c)[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-        }
+        for (int t = 0; t < 16; ++t)
+          pq[c / 2 + t] = pack_bf16x2(__uint_as_float(v[2 * t]) * p.scale, __uint_as_float(v[2 * t + 1]) * p.scale);
       }
       tc_fence_before();
-      mbar_arrive(bar_dq_empty);
+      mbar_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
+      int* rows = reinterpret_cast<int*>(smem + Cfg::OFF_ROWS);
+      if (half == 0) rows[r] = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
+      named_bar_sync(5, 256);
+      store_tile_coalesced<HD>(smem + Cfg::OFF_STG, rows, pq, r, half, tid, p.dq + itm.h * HD, int64_t(p.H) * HD, 5);
       ++k;
     }
   }

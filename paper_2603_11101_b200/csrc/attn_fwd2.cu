@@ -49,17 +49,19 @@ struct Fwd2Params {
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
 };
 
-template <int HD, int STAGES>
+template <int HD, int KS, int VS>
 struct Fwd2Cfg {
   static constexpr int BM = 128, BN = 128;
   static constexpr int Q_BYTES = BM * HD * 2;
-  static constexpr int KV_BYTES = BN * HD * 2;  // one of K or V
-  static constexpr int OFF_Q = 0;                // [2]
-  static constexpr int OFF_KV = 2 * Q_BYTES;     // stage s: K at +s*2*KV_BYTES, V right after
-  static constexpr int OFF_XCH = OFF_KV + STAGES * 2 * KV_BYTES;  // float [2 parity][2 half][128]
+  static constexpr int KV_BYTES = BN * HD * 2;          // one K or V tile
+  static constexpr int OFF_Q = 0;                        // [2]
+  static constexpr int OFF_K = 2 * Q_BYTES;              // [KS] K ring
+  static constexpr int OFF_V = OFF_K + KS * KV_BYTES;    // [VS] V ring
+  static constexpr int OFF_XCH = OFF_V + VS * KV_BYTES;  // float [2 parity][2 half][128]
   static constexpr int OFF_BAR = OFF_XCH + 2 * 2 * 128 * 4;
-  static constexpr int NUM_BARS = 4 + 2 * STAGES + 4 + 5;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5;
+  // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
   static_assert(O_COL + 2 * HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
@@ -80,20 +82,22 @@ __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) 
   return it;
 }
 
-template <int HD, int STAGES, bool PROF>
+template <int HD, int KS, int VS, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const Fwd2Params p) {
-  using Cfg = Fwd2Cfg<HD, STAGES>;
+  using Cfg = Fwd2Cfg<HD, KS, VS>;
   constexpr int BN = Cfg::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* bar_q_full = bars;                   // [2]
-  uint64_t* bar_q_empty = bars + 2;              // [2]
-  uint64_t* bar_kv_full = bars + 4;              // [STAGES]
-  uint64_t* bar_kv_empty = bars + 4 + STAGES;    // [STAGES]
-  uint64_t* bar_s_full = bars + 4 + 2 * STAGES;  // [2]
+  uint64_t* bar_q_full = bars;                          // [2]
+  uint64_t* bar_q_empty = bars + 2;                     // [2]
+  uint64_t* bar_k_full = bars + 4;                      // [KS]
+  uint64_t* bar_k_empty = bar_k_full + KS;              // [KS]
+  uint64_t* bar_v_full = bar_k_full + 2 * KS;           // [VS]
+  uint64_t* bar_v_empty = bar_v_full + VS;              // [VS]
+  uint64_t* bar_s_full = bar_v_full + 2 * VS;           // [2]
   uint64_t* bar_p_full = bar_s_full + 2;         // [2] 256 arrivals
   uint64_t* bar_o_full = bar_s_full + 4;         // [2] per item: last PV landed in O[k%2]
   uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 256 arrivals: epilogue drained O[k%2]
@@ -109,9 +113,14 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&bar_s_full[s], 1);
       mbar_init(&bar_p_full[s], 256);
     }
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&bar_kv_full[s], 1);
-      mbar_init(&bar_kv_empty[s], 1);
+    if (smem_u32(smem) & 1023) __trap();  // swizzle atoms need 1 KB alignment
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(&bar_k_full[s], 1);
+      mbar_init(&bar_k_empty[s], 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(&bar_v_full[s], 1);
+      mbar_init(&bar_v_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_o_full[s], 1);
@@ -133,7 +142,18 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
+      // Load order K0, K1, V0, K2, V1, …: K runs one tile ahead of V, so a K stage (freed as soon
+      // as its S MMA completes) is refilled without waiting for the slower-retiring V stages.
       int g = 0, k = 0;
+      int pv_g = -1, pv_kh = 0, pv_kv0 = 0;
+      auto load_v = [&]() {
+        const int vs = pv_g % VS;
+        if (pv_g >= VS) wp.template wait<1>(&bar_v_empty[vs], ((pv_g / VS) - 1) & 1);
+        uint8_t* sv = smem + Cfg::OFF_V + vs * Cfg::KV_BYTES;
+        mbar_expect_tx(&bar_v_full[vs], Cfg::KV_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, pv_kh * HD + c * 64, pv_kv0, &bar_v_full[vs]);
+      };
       FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
         const FwdItem itm = nxt;
@@ -145,18 +165,20 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * 64, itm.q0, &bar_q_full[qs]);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int st = g % STAGES;
-          if (g >= STAGES) wp.template wait<1>(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
-          uint8_t* sk = smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES;
-          uint8_t* sv = sk + Cfg::KV_BYTES;
+          const int ks = g % KS;
+          if (g >= KS) wp.template wait<1>(&bar_k_empty[ks], ((g / KS) - 1) & 1);
+          uint8_t* sk = smem + Cfg::OFF_K + ks * Cfg::KV_BYTES;
           const int kv0 = itm.kv_lo + j * BN;
-          mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::KV_BYTES);
+          mbar_expect_tx(&bar_k_full[ks], Cfg::KV_BYTES);
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sk + c * BN * 128, &tmK, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
-#pragma unroll
-          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
+          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sk + c * BN * 128, &tmK, itm.kh * HD + c * 64, kv0, &bar_k_full[ks]);
+          if (pv_g >= 0) load_v();
+          pv_g = g;
+          pv_kh = itm.kh;
+          pv_kv0 = kv0;
         }
       }
+      if (pv_g >= 0) load_v();
       wp.flush(p.prof);
     }
   } else if (warp == 9) {
@@ -172,14 +194,15 @@ __global__ void __launch_bounds__(320, 1)
         wp.template wait<2>(&bar_p_full[pg & 1], (pg >> 1) & 1);
         if (pj == 0 && pk >= 2) wp.template wait<3>(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
         tc_fence_after();
-        const int st = pg % STAGES;
-        const uint32_t v_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+        const int vs = pg % VS;
+        wp.template wait<1>(&bar_v_full[vs], (pg / VS) & 1);
+        const uint32_t v_addr = smem_u32(smem + Cfg::OFF_V + vs * Cfg::KV_BYTES);
         const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
 #pragma unroll
         for (int s = 0; s < BN / 16; ++s)  // P: columns 0-63 at +0..31, 64-127 at +64..95
           umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
                       make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024), idesc_o, (pj > 0 || s > 0) ? 1u : 0u);
-        umma_commit(&bar_kv_empty[st]);
+        umma_commit(&bar_v_empty[vs]);
         umma_commit(bar_o_ready);
         if (plast) umma_commit(&bar_o_full[pk & 1]);
       };
@@ -191,16 +214,17 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t q_addr = smem_u32(smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES);
         wp.template wait<0>(&bar_q_full[qs], (k >> 1) & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int st = g % STAGES;
-          wp.template wait<1>(&bar_kv_full[st], (g / STAGES) & 1);
+          const int ks = g % KS;
+          wp.template wait<1>(&bar_k_full[ks], (g / KS) & 1);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::KV_BYTES);
+          const uint32_t k_addr = smem_u32(smem + Cfg::OFF_K + ks * Cfg::KV_BYTES);
           const uint32_t d_s = tmem + Cfg::S_COL + (g & 1) * 128;
 #pragma unroll
           for (int s = 0; s < HD / 16; ++s)
             umma_f16_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
                         make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_s, s > 0);
           umma_commit(&bar_s_full[g & 1]);
+          umma_commit(&bar_k_empty[ks]);
           if (j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);
           if (pj >= 0) do_pv();
           pj = j;
@@ -369,10 +393,10 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
-template <int HD, int STAGES>
+template <int HD, int KS, int VS>
 int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   using namespace vlasim_host;
-  using Cfg = Fwd2Cfg<HD, STAGES>;
+  using Cfg = Fwd2Cfg<HD, KS, VS>;
   const int T = int(a->total_tokens);
   k_fwd_spans<<<(T + 255) / 256, 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, rows_span);
   VLASIM_LAUNCH_CHECK();
@@ -394,17 +418,17 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   const int grid = std::min(p.num_items, num_sms());
   if (prof_enabled()) {
     p.prof = prof_buffer();
-    auto kern = attn_fwd2_kernel<HD, STAGES, true>;
+    auto kern = attn_fwd2_kernel<HD, KS, VS, true>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
     VLASIM_LAUNCH_CHECK();
     return prof_report("attn_fwd2", grid, st,
-                       {"prod:q_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:q_full", "mma:kv_full",
+                       {"prod:q_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:q_full", "mma:k/v_full",
                         "mma:p_full", "mma:o_empty", "", "", "", "mma:total", "smx:s_full", "smx:o_ready",
                         "smx:o_full", "smx:xchg_bar", "smx:epilogue", "", "", "smx:total"});
   }
   p.prof = nullptr;
-  auto kern = attn_fwd2_kernel<HD, STAGES, false>;
+  auto kern = attn_fwd2_kernel<HD, KS, VS, false>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
   VLASIM_LAUNCH_CHECK();
@@ -419,7 +443,7 @@ int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, 
   const size_t need = size_t(a->total_tokens) * sizeof(int2);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
   int2* spans = static_cast<int2*>(ws);
-  if (a->head_dim == 64) return launch_fwd2<64, 4>(a, spans, st);
-  return launch_fwd2<128, 2>(a, spans, st);
+  if (a->head_dim == 64) return launch_fwd2<64, 4, 4>(a, spans, st);
+  return launch_fwd2<128, 3, 2>(a, spans, st);
 }
 }  // namespace vlasim_host

@@ -309,18 +309,18 @@ __global__ void __launch_bounds__(320, 1)
         }
         const int kv0 = itm.kv_lo + j * BN + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        float mt = -INFINITY;
-        if (c_lo <= 0 && c_hi >= 64) {
+        if (!(c_lo <= 0 && c_hi >= 64)) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) mt = fmaxf(mt, __uint_as_float(x[c]));
-        } else {
-#pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            const bool v = c >= c_lo && c < c_hi;
-            if (!v) x[c] = __float_as_uint(-INFINITY);
-            mt = fmaxf(mt, __uint_as_float(x[c]));
-          }
+          for (int c = 0; c < 64; ++c)
+            if (!(c >= c_lo && c < c_hi)) x[c] = __float_as_uint(-INFINITY);
         }
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent max chains
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) mq[u] = fmaxf(mq[u], __uint_as_float(x[c + u]));
+        }
+        float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         // combine the two column halves of this row
         float* xs = xch + (g & 1) * 256;
         xs[half * 128 + r] = mt;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(320, 1)
           m_run = mt;
         }
         const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-        float ls = 0.f;
+        float lq[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent sum chains
 #pragma unroll
         for (int c = 0; c < 64; c += 32) {
           uint32_t pk[16];
@@ -359,12 +359,13 @@ __global__ void __launch_bounds__(320, 1)
           for (int t = 0; t < 16; ++t) {
             const float p0 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t]), sl2, -msub));
             const float p1 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t + 1]), sl2, -msub));
-            ls += p0 + p1;
+            lq[(2 * t) & 3] += p0;
+            lq[(2 * t + 1) & 3] += p1;
             pk[t] = pack_bf16x2(p0, p1);
           }
           tmem_st16(s_tm + c / 2, pk);
         }
-        l_run += ls;
+        l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bar_p_full[g & 1]);

@@ -23,6 +23,8 @@ def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_s
     T, H, d = q.shape
     if k.shape[0] != T or v.shape != k.shape or k.shape[2] != d:
         raise ConfigError("k/v shape mismatch with q")
+    if H % k.shape[1]:
+        raise ConfigError("num_kv_heads must divide num_heads")
     if cu_seqlens.dtype != torch.int32:
         raise ConfigError("cu_seqlens must be int32")
     for t in (q, k, v, o, cu_seqlens):

@@ -44,19 +44,24 @@ struct Fwd2Params {
   __nv_bfloat16* o;
   float* lse;
   const int2* rows_span;
-  int T, H, Hkv, num_items;
+  const float* q_scale;  // FP8 only: [H, nbt] per-(head, 128-token block) E4M3 scales (d = 128)
+  const float* k_scale;  // FP8 only: [Hkv, nbt]
+  int T, H, Hkv, num_items, nbt;
   float scale_log2;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
 };
 
-template <int HD, int KS, int VS>
+template <int HD, int KS, int VS, bool FP8>
 struct Fwd2Cfg {
   static constexpr int BM = 128, BN = 128;
-  static constexpr int Q_BYTES = BM * HD * 2;
-  static constexpr int KV_BYTES = BN * HD * 2;          // one K or V tile
+  static constexpr int QK_ELEM = FP8 ? 1 : 2;           // Q/K element bytes (E4M3 codes or bf16)
+  static constexpr int QK_BOX = 128 / QK_ELEM;          // elements per 128-B swizzle row
+  static constexpr int Q_BYTES = BM * HD * QK_ELEM;
+  static constexpr int K_BYTES = BN * HD * QK_ELEM;
+  static constexpr int KV_BYTES = BN * HD * 2;          // one V tile (bf16)
   static constexpr int OFF_Q = 0;                        // [2]
   static constexpr int OFF_K = 2 * Q_BYTES;              // [KS] K ring
-  static constexpr int OFF_V = OFF_K + KS * KV_BYTES;    // [VS] V ring
+  static constexpr int OFF_V = OFF_K + KS * K_BYTES;     // [VS] V ring
   static constexpr int OFF_XCH = OFF_V + VS * KV_BYTES;  // float [2 parity][2 half][128]
   static constexpr int OFF_BAR = OFF_XCH + 2 * 2 * 128 * 4;
   static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5;
@@ -82,11 +87,11 @@ __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) 
   return it;
 }
 
-template <int HD, int KS, int VS, bool PROF>
+template <int HD, int KS, int VS, bool FP8, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const Fwd2Params p) {
-  using Cfg = Fwd2Cfg<HD, KS, VS>;
+  using Cfg = Fwd2Cfg<HD, KS, VS, FP8>;
   constexpr int BN = Cfg::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -163,15 +168,17 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
         mbar_expect_tx(&bar_q_full[qs], Cfg::Q_BYTES);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c) tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * 64, itm.q0, &bar_q_full[qs]);
+        for (int c = 0; c < HD / Cfg::QK_BOX; ++c)
+          tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * Cfg::QK_BOX, itm.q0, &bar_q_full[qs]);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           const int ks = g % KS;
           if (g >= KS) wp.template wait<1>(&bar_k_empty[ks], ((g / KS) - 1) & 1);
-          uint8_t* sk = smem + Cfg::OFF_K + ks * Cfg::KV_BYTES;
+          uint8_t* sk = smem + Cfg::OFF_K + ks * Cfg::K_BYTES;
           const int kv0 = itm.kv_lo + j * BN;
-          mbar_expect_tx(&bar_k_full[ks], Cfg::KV_BYTES);
+          mbar_expect_tx(&bar_k_full[ks], Cfg::K_BYTES);
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c) tma_load_2d(sk + c * BN * 128, &tmK, itm.kh * HD + c * 64, kv0, &bar_k_full[ks]);
+          for (int c = 0; c < HD / Cfg::QK_BOX; ++c)
+            tma_load_2d(sk + c * BN * 128, &tmK, itm.kh * HD + c * Cfg::QK_BOX, kv0, &bar_k_full[ks]);
           if (pv_g >= 0) load_v();
           pv_g = g;
           pv_kh = itm.kh;
@@ -217,12 +224,20 @@ __global__ void __launch_bounds__(320, 1)
           const int ks = g % KS;
           wp.template wait<1>(&bar_k_full[ks], (g / KS) & 1);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(smem + Cfg::OFF_K + ks * Cfg::KV_BYTES);
+          const uint32_t k_addr = smem_u32(smem + Cfg::OFF_K + ks * Cfg::K_BYTES);
           const uint32_t d_s = tmem + Cfg::S_COL + (g & 1) * 128;
+          if constexpr (FP8) {  // kind::f8f6f4: 32 E4M3 elements (32 B) per K step
+            constexpr uint32_t idesc_f8 = make_idesc_e4m3(128, BN);
 #pragma unroll
-          for (int s = 0; s < HD / 16; ++s)
-            umma_f16_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
-                        make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_s, s > 0);
+            for (int s = 0; s < HD / 32; ++s)
+              umma_f8_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
+                         make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_f8, s > 0);
+          } else {
+#pragma unroll
+            for (int s = 0; s < HD / 16; ++s)
+              umma_f16_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
+                          make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_s, s > 0);
+          }
           umma_commit(&bar_s_full[g & 1]);
           umma_commit(&bar_k_empty[ks]);
           if (j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);
@@ -242,7 +257,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int r = quad * 32 + lane;
     const int c0 = half * 64;
-    const float sl2 = p.scale_log2;
+    float sl2 = p.scale_log2;
     // Epilogue of item `ek` is deferred until the first tile of the next item has been handed to
     // the MMA warp, so the tensor core never idles on it (O is double-buffered in TMEM).
     WaitProf<PROF> wp;
@@ -290,6 +305,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       const int row = itm.q0 + r;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + half * (HD / 2);
+      if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + itm.q0 / 128);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
@@ -309,6 +325,14 @@ __global__ void __launch_bounds__(320, 1)
         }
         const int kv0 = itm.kv_lo + j * BN + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
+        if constexpr (FP8) {  // per-column K block scale (a 64-column half spans at most 2 blocks)
+          const int b0 = kv0 / 128;
+          const int cb = (b0 + 1) * 128 - kv0;
+          const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
+          const float k0s = __ldg(ksc + min(b0, p.nbt - 1)), k1s = __ldg(ksc + min(b0 + 1, p.nbt - 1));
+#pragma unroll
+          for (int c = 0; c < 64; ++c) x[c] = __float_as_uint(__uint_as_float(x[c]) * (c < cb ? k0s : k1s));
+        }
         if (!(c_lo <= 0 && c_hi >= 64)) {
 #pragma unroll
           for (int c = 0; c < 64; ++c)
@@ -394,32 +418,36 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
-template <int HD, int KS, int VS>
+template <int HD, int KS, int VS, bool FP8>
 int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   using namespace vlasim_host;
-  using Cfg = Fwd2Cfg<HD, KS, VS>;
+  using Cfg = Fwd2Cfg<HD, KS, VS, FP8>;
   const int T = int(a->total_tokens);
   k_fwd_spans<<<(T + 255) / 256, 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, rows_span);
   VLASIM_LAUNCH_CHECK();
   CUtensorMap tq, tk, tv;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const auto QK = FP8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : BF;
   const uint64_t H = a->num_heads, Hkv = a->num_kv_heads;
-  if (int rc = encode_tmap_2d(&tq, a->q, BF, T, H * HD, H * HD * 2, 128, 64, true)) return rc;
-  if (int rc = encode_tmap_2d(&tk, a->k, BF, T, Hkv * HD, Hkv * HD * 2, Cfg::BN, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&tq, a->q, QK, T, H * HD, H * HD * Cfg::QK_ELEM, 128, Cfg::QK_BOX, true)) return rc;
+  if (int rc = encode_tmap_2d(&tk, a->k, QK, T, Hkv * HD, Hkv * HD * Cfg::QK_ELEM, Cfg::BN, Cfg::QK_BOX, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, Hkv * HD, Hkv * HD * 2, Cfg::BN, 64, true)) return rc;
   Fwd2Params p;
   p.o = static_cast<__nv_bfloat16*>(a->o);
   p.lse = a->lse;
   p.rows_span = rows_span;
+  p.q_scale = a->q_scale;
+  p.k_scale = a->k_scale;
   p.T = T;
   p.H = a->num_heads;
   p.Hkv = a->num_kv_heads;
+  p.nbt = (T + 127) / 128;
   p.num_items = int((int64_t(T) + 127) / 128) * a->num_heads;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
   const int grid = std::min(p.num_items, num_sms());
   if (prof_enabled()) {
     p.prof = prof_buffer();
-    auto kern = attn_fwd2_kernel<HD, KS, VS, true>;
+    auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, true>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
     VLASIM_LAUNCH_CHECK();
@@ -429,7 +457,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
                         "smx:o_full", "smx:xchg_bar", "smx:epilogue", "", "", "smx:total"});
   }
   p.prof = nullptr;
-  auto kern = attn_fwd2_kernel<HD, KS, VS, false>;
+  auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, false>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
   VLASIM_LAUNCH_CHECK();
@@ -444,7 +472,20 @@ int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, 
   const size_t need = size_t(a->total_tokens) * sizeof(int2);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
   int2* spans = static_cast<int2*>(ws);
-  if (a->head_dim == 64) return launch_fwd2<64, 4, 4>(a, spans, st);
-  return launch_fwd2<128, 3, 2>(a, spans, st);
+  if (a->head_dim == 64) return launch_fwd2<64, 4, 4, false>(a, spans, st);
+  return launch_fwd2<128, 3, 2, false>(a, spans, st);
 }
 }  // namespace vlasim_host
+
+// FP8 Q/K forward (config 4): q/k are E4M3 codes with per-(head, 128-token, 128-d) block scales
+// (vlasim_fp8_quant_block_cuda); QKᵀ runs as tcgen05.mma kind::f8f6f4 and the block scales are
+// applied to S in the softmax; P·V stays bf16.  head_dim 128 (one d block per head).
+extern "C" int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args* a, void* ws, size_t ws_bytes,
+                                                 vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = validate_attn_args(a, true)) return rc;
+  if (a->head_dim != 128) return set_error(VLASIM_ECONFIG, "fp8 Q/K attention: head_dim must be 128");
+  const size_t need = size_t(a->total_tokens) * sizeof(int2);
+  if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
+  return launch_fwd2<128, 4, 3, true>(a, static_cast<int2*>(ws), as_stream(stream));
+}

@@ -1,16 +1,122 @@
-// fp8.cu — E4M3 per-block quantisation and the FP8 Q/K forward entry.
+// fp8.cu — E4M3 per-block quantisation for the FP8 Q/K attention path.
+//
+// x [T, heads, d] bf16, quantised per head in 128-token × 128-d blocks (the SPEC's "last two
+// dimensions" blocks, applied per head — DESIGN.md §2):
+//   scale = amax(block) / 448 (1 if the block is all zero)
+//   code  = RNE(x / scale) onto E4M3, saturating to ±448
+// Arithmetic is fp32 (scale = fp32(amax) / 448.f, quotient = correctly rounded fp32 division,
+// then cvt.rn.satfinite.e4m3x2.f32), which the oracle's quotient_fp32 mode restates bit-exactly.
+#include <cuda_bf16.h>
+
 #include "common.hpp"
 
-extern "C" int vlasim_fp8_quant_block_cuda(const void*, int64_t, int32_t, int32_t, uint8_t*, float*, vlasim_stream_t) {
-  return vlasim_host::set_error(VLASIM_ECONFIG, "fp8 quantisation: not implemented in this build");
+namespace {
+
+__device__ __forceinline__ uint16_t cvt_e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
 }
-extern "C" int vlasim_fp8_dequant_block_cuda(const uint8_t*, const float*, int64_t, int32_t, int32_t, float*,
-                                             vlasim_stream_t) {
-  return vlasim_host::set_error(VLASIM_ECONFIG, "fp8 dequantisation: not implemented in this build");
+
+// One CTA (256 threads) per (head, 128-token block, 128-d block).
+__global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __restrict__ x, int T, int heads, int d,
+                                                     uint8_t* __restrict__ codes, float* __restrict__ scales) {
+  const int nbd = (d + 127) / 128, nbt = (T + 127) / 128;
+  const int bd = blockIdx.x % nbd, bt = (blockIdx.x / nbd) % nbt, h = blockIdx.x / (nbd * nbt);
+  const int t0 = bt * 128, c0 = bd * 128;
+  const int rows = min(128, T - t0), cols = min(128, d - c0);
+  __shared__ float red[8];
+  // pass 1: amax (each thread: 2-element chunks of the block)
+  float amax = 0.f;
+  for (int e = threadIdx.x * 2; e < rows * 128; e += 512) {
+    const int r = e / 128, c = e % 128;
+    if (c < cols) {
+      const __nv_bfloat16* p = x + (int64_t(t0 + r) * heads + h) * d + c0 + c;
+      amax = fmaxf(amax, fabsf(__bfloat162float(p[0])));
+      if (c + 1 < cols) amax = fmaxf(amax, fabsf(__bfloat162float(p[1])));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < 8 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  amax = red[0];
+  const float scale = amax == 0.f ? 1.f : __fdiv_rn(amax, 448.f);
+  if (threadIdx.x == 0) scales[(int64_t(h) * nbt + bt) * nbd + bd] = scale;
+  // pass 2: codes
+  for (int e = threadIdx.x * 2; e < rows * 128; e += 512) {
+    const int r = e / 128, c = e % 128;
+    if (c < cols) {
+      const int64_t off = (int64_t(t0 + r) * heads + h) * d + c0 + c;
+      const float a = __fdiv_rn(__bfloat162float(x[off]), scale);
+      if (c + 1 < cols) {
+        const float b = __fdiv_rn(__bfloat162float(x[off + 1]), scale);
+        const uint16_t pr = cvt_e4m3x2(a, b);
+        codes[off] = uint8_t(pr & 0xFF);
+        codes[off + 1] = uint8_t(pr >> 8);
+      } else {
+        codes[off] = uint8_t(cvt_e4m3x2(a, 0.f) & 0xFF);
+      }
+    }
+  }
 }
-extern "C" int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args*, void*, size_t, vlasim_stream_t) {
-  return vlasim_host::set_error(VLASIM_ECONFIG, "fp8 Q/K attention: not implemented in this build");
+
+__device__ __forceinline__ float e4m3_to_float(uint8_t c) {
+  const int e = (c >> 3) & 0xF, m = c & 7;
+  float v;
+  if (e == 0) v = ldexpf(float(m) / 8.f, -6);
+  else if (e == 15 && m == 7) v = __int_as_float(0x7fc00000);
+  else v = ldexpf(1.f + float(m) / 8.f, e - 7);
+  return (c & 0x80) ? -v : v;
 }
+
+__global__ void k_dequant_block(const uint8_t* __restrict__ codes, const float* __restrict__ scales, int64_t T,
+                                int heads, int d, float* __restrict__ out) {
+  const int64_t n = T * heads * d;
+  const int nbd = (d + 127) / 128, nbt = int((T + 127) / 128);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % d);
+    const int64_t th = i / d;
+    const int h = int(th % heads);
+    const int64_t t = th / heads;
+    out[i] = e4m3_to_float(codes[i]) * scales[(int64_t(h) * nbt + t / 128) * nbd + c / 128];
+  }
+}
+
+}  // namespace
+
+extern "C" int vlasim_fp8_quant_block_cuda(const void* d_x, int64_t T, int32_t heads, int32_t d, uint8_t* d_codes,
+                                           float* d_scales, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (!d_x || !d_codes || !d_scales) return set_error(VLASIM_ECONFIG, "fp8_quant_block: null buffer");
+  if (T < 1 || heads < 1 || d < 1 || T >= (int64_t(1) << 31))
+    return set_error(VLASIM_ECONFIG, "fp8_quant_block: bad shape T=%lld heads=%d d=%d", (long long)T, heads, d);
+  const int64_t blocks = int64_t(heads) * ((T + 127) / 128) * ((d + 127) / 128);
+  k_quant_block<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(d_x), int(T), heads, d,
+                                                      d_codes, d_scales);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
+extern "C" int vlasim_fp8_dequant_block_cuda(const uint8_t* d_codes, const float* d_scales, int64_t T, int32_t heads,
+                                             int32_t d, float* d_out, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (!d_codes || !d_scales || !d_out) return set_error(VLASIM_ECONFIG, "fp8_dequant_block: null buffer");
+  if (T < 1 || heads < 1 || d < 1) return set_error(VLASIM_ECONFIG, "fp8_dequant_block: bad shape");
+  const int64_t n = T * heads * d;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 16);
+  k_dequant_block<<<blocks, 256, 0, as_stream(stream)>>>(d_codes, d_scales, T, heads, d, d_out);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
 extern "C" int vlasim_pack_greedy_cuda(const int32_t*, int64_t, int32_t, const vlasim_pack_out*, void*, size_t, uint32_t,
                                        vlasim_stream_t) {
   return vlasim_host::set_error(VLASIM_ECONFIG, "greedy packer: not implemented in this build");

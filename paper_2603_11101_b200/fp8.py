@@ -1,0 +1,52 @@
+"""E4M3 per-block quantisation and the FP8 Q/K attention forward (config 4).
+
+quant_block(x [T, heads, d] bf16) → (codes uint8 [T, heads, d], scales fp32 [heads, ⌈T/128⌉, ⌈d/128⌉]):
+per head, 128-token × 128-d blocks; scale = amax/448 (1 for an all-zero block); codes = RNE(x/scale)
+saturated to ±448.  GPU only (vlasim_fp8_quant_block_cuda).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .attention import _args, _default_fwd_ws
+from .errors import ConfigError
+
+
+def quant_block(x: torch.Tensor, stream=None):
+    if x.dtype != torch.bfloat16 or x.dim() != 3 or not x.is_cuda or not x.is_contiguous():
+        raise ConfigError("quant_block expects a contiguous CUDA bf16 [T, heads, d] tensor")
+    T, Hh, d = x.shape
+    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    scales = torch.empty(Hh, (T + 127) // 128, (d + 127) // 128, dtype=torch.float32, device=x.device)
+    _lib.check(_lib.lib().vlasim_fp8_quant_block_cuda(_lib.ptr(x), T, Hh, d, _lib.ptr(codes),
+                                                      _lib.ptr(scales, _lib.f32p), _lib.stream_ptr(stream)),
+               "fp8_quant_block")
+    return codes, scales
+
+
+def dequant_block(codes: torch.Tensor, scales: torch.Tensor, stream=None) -> torch.Tensor:
+    T, Hh, d = codes.shape
+    out = torch.empty(codes.shape, dtype=torch.float32, device=codes.device)
+    _lib.check(_lib.lib().vlasim_fp8_dequant_block_cuda(_lib.ptr(codes), _lib.ptr(scales, _lib.f32p), T, Hh, d,
+                                                        _lib.ptr(out, _lib.f32p), _lib.stream_ptr(stream)),
+               "fp8_dequant_block")
+    return out
+
+
+def varlen_attn_fwd_fp8qk(q_codes, q_scale, k_codes, k_scale, v, cu_seqlens, *, mask_mode=0, prefix_len=None,
+                          softmax_scale=None, out=None, lse=None, stream=None):
+    """Forward with E4M3 Q/K (tcgen05 kind::f8f6f4 for QKᵀ, block scales applied to S; P·V in bf16)."""
+    T, H, d = q_codes.shape
+    if q_codes.dtype != torch.uint8 or k_codes.dtype != torch.uint8:
+        raise ConfigError("q_codes / k_codes must be uint8 E4M3 codes")
+    o = out if out is not None else torch.empty(T, H, d, dtype=torch.bfloat16, device=v.device)
+    lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=v.device)
+    a = _args(q_codes, k_codes, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale, k_scale)
+    L = _lib.lib()
+    ws = _default_fwd_ws.get(L.vlasim_varlen_attn_workspace_size(C.byref(a), 0), v.device)
+    _lib.check(L.vlasim_varlen_attn_fwd_fp8qk_cuda(C.byref(a), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
+               "varlen_attn_fwd_fp8qk")
+    return o, lse

@@ -93,58 +93,34 @@ struct BwdParams {
 };
 
 // ================================================================== dK / dV (KV-stationary)
-// One CTA loops over items = (128-key tile, kv head).  Per iteration (q head of the group,
+// One CTA loops over items = (128-key tile, kv head).  Per iteration G (q head of the group,
 // 128-row Q tile of the visible query range):
 //   Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ                                  (SS, K-major operands)
-//   softmax warps: Pᵀ = exp2(Sᵀ·scale·log2e − lse2) → bf16 over the S columns,
-//                  dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
-//   dV += Pᵀ·dO, dK += dSᵀ·Q                                  (A from TMEM, B MN-major)
-// TMEM: S/P [0,128) · dP/dS [128,256) · dV [256,256+HD) · dK after.  Q and dO double-buffered.
+//   softmax warps: phase A  Pᵀ = exp2(Sᵀ·scale·log2e − lse2) → bf16 → smem (K-major SW128)
+//                  phase B  dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP TMEM columns
+//   dV += Pᵀ·dO (A = Pᵀ smem), dK += dSᵀ·Q (A = dSᵀ TMEM)     (B = dO / Q, MN-major)
+// Because Pᵀ lives in smem, the S columns are free as soon as phase A has read them, so S(G+1)
+// is issued before dV(G)/dK(G) and phase A(G+1) overlaps them.  The Pᵀ buffer doubles as the
+// epilogue staging buffer (dK/dV rows leave through per-thread async bulk stores).
+// TMEM: S [0,128) · dP/dS [128,256) · dV [256,256+HD) · dK after.  Q and dO double-buffered.
 template <int HD>
 struct DkvCfg {
   static constexpr int TILE = 128 * HD * 2;
   static constexpr int OFF_K = 0, OFF_V = TILE;
   static constexpr int OFF_Q = 2 * TILE;        // [2]
   static constexpr int OFF_DO = 4 * TILE;       // [2]
-  static constexpr int OFF_STG = 6 * TILE;      // epilogue staging: 128 rows × HD bf16 (swizzled 16-B chunks)
+  static constexpr int OFF_PT = 6 * TILE;       // Pᵀ [128 keys × 128 q] bf16 (SW128) / epilogue staging
+  static constexpr int PT_BYTES = 128 * 128 * 2 > TILE ? 128 * 128 * 2 : TILE;
   static constexpr int VEC = 544;               // 132 floats (16-B aligned window of 128) + pad
-  static constexpr int OFF_LSE = 7 * TILE;      // [2][VEC]
+  static constexpr int OFF_LSE = OFF_PT + PT_BYTES;   // [2][VEC]
   static constexpr int OFF_DSUM = OFF_LSE + 2 * VEC;  // [2][VEC]
-  static constexpr int OFF_ROWS = OFF_DSUM + 2 * VEC;  // int [128] destination rows
-  static constexpr int OFF_BAR = OFF_ROWS + 512;
-  static constexpr int NUM_BARS = 16;
+  static constexpr int OFF_BAR = OFF_DSUM + 2 * VEC;
+  static constexpr int NUM_BARS = 18;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
   static_assert(DK_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
-
-// Coalesced epilogue store of a [128 rows × HD] bf16 tile held as packed registers by the 256
-// softmax threads (thread = (row, head-dim half)): registers → swizzled smem staging → 16-B
-// global stores, 16 consecutive threads per 256-B row.  rows[r] < 0 skips row r.
-template <int HD>
-__device__ __forceinline__ void store_tile_coalesced(uint8_t* stg, const int* rows, const uint32_t (&pk)[HD / 4],
-                                                     int krow, int half, int tid, __nv_bfloat16* base,
-                                                     int64_t row_stride_elems, int bar_id) {
-  constexpr int CH = HD / 8;  // 16-B chunks per row
-#pragma unroll
-  for (int j = 0; j < CH / 2; ++j) {
-    const int ch = (half * (CH / 2) + j) ^ (krow & (CH - 1));
-    *reinterpret_cast<uint4*>(stg + krow * (HD * 2) + ch * 16) =
-        make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-  }
-  named_bar_sync(bar_id, 256);
-#pragma unroll
-  for (int idx = tid; idx < 128 * CH; idx += 256) {
-    const int r = idx / CH, ch = idx % CH;
-    const int dst = rows[r];
-    if (dst >= 0) {
-      const uint4 v = *reinterpret_cast<const uint4*>(stg + r * (HD * 2) + ((ch ^ (r & (CH - 1))) * 16));
-      *reinterpret_cast<uint4*>(base + int64_t(dst) * row_stride_elems + ch * 8) = v;
-    }
-  }
-  named_bar_sync(bar_id, 256);
-}
 
 struct KvItem {
   int k0, kh, q_lo, nq, iters;
@@ -177,14 +153,17 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar_do_empty = bars + 8;  // [2]
   uint64_t* bar_s_full = bars + 10;
   uint64_t* bar_dp_full = bars + 11;
-  uint64_t* bar_p_full = bars + 12;     // 256 arrivals
+  uint64_t* bar_p_full = bars + 12;     // 256 arrivals: Pᵀ in smem, dSᵀ in TMEM
   uint64_t* bar_dkv_full = bars + 13;
   uint64_t* bar_dkv_empty = bars + 14;  // 256 arrivals
+  uint64_t* bar_s_free = bars + 15;     // 256 arrivals: S columns read by phase A
+  uint64_t* bar_pv_done = bars + 16;    // dV(G) has read Pᵀ from smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int group = p.H / p.Hkv;
   if (tid == 0) {
+    if (smem_u32(smem) & 1023) __trap();
     mbar_init(bar_kv_full, 1);
     mbar_init(bar_kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
@@ -198,6 +177,8 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(bar_p_full, 256);
     mbar_init(bar_dkv_full, 1);
     mbar_init(bar_dkv_empty, 256);
+    mbar_init(bar_s_free, 256);
+    mbar_init(bar_pv_done, 1);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -252,6 +233,7 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ
       constexpr uint32_t id_kmn = make_idesc_bf16(128, HD, false, true);   // dV, dK
       const uint32_t sK = smem_u32(smem + Cfg::OFF_K), sV = smem_u32(smem + Cfg::OFF_V);
+      const uint32_t sPT = smem_u32(smem + Cfg::OFF_PT);
       WaitProf<PROF> wp;
       auto mma_S = [&](int G) {
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
@@ -281,30 +263,37 @@ __global__ void __launch_bounds__(320, 1)
         if (itm.iters == 0) continue;
         wp.template wait<0>(bar_kv_full, k & 1);
         tc_fence_after();
+        if (G > 0) wp.template wait<5>(bar_s_free, (G - 1) & 1);  // previous item's last S was read
         mma_S(G);
         mma_dP(G);
-        if (itm.iters == 1) umma_commit(bar_kv_empty);  // K, V read only by S and dP
+        if (itm.iters == 1) umma_commit(bar_kv_empty);  // K, V are read only by S and dP
         for (int it = 0; it < itm.iters; ++it, ++G) {
           const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
           const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
+          const bool more = it + 1 < itm.iters;
+          if (more) {  // S(G+1) as soon as phase A(G) has read S(G)
+            wp.template wait<5>(bar_s_free, G & 1);
+            mma_S(G + 1);
+          }
           wp.template wait<3>(bar_p_full, G & 1);
           if (it == 0 && k > 0) wp.template wait<4>(bar_dkv_empty, (k - 1) & 1);
           tc_fence_after();
-          // dV += Pᵀ·dO and dK += dSᵀ·Q; A from TMEM: queries 0-63 at +0..31, 64-127 at +64..95
+          // dV += Pᵀ·dO  (A = Pᵀ smem K-major, B = dO MN-major)
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::S_COL + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+            umma_f16_ss(tmem + Cfg::DV_COL, make_sdesc_sw128(sPT + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
                         make_sdesc_sw128(sdO + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
+          umma_commit(bar_pv_done);
+          umma_commit(&bar_do_empty[G & 1]);
+          // dK += dSᵀ·Q  (A = dSᵀ in TMEM: queries 0-63 at +0..31, 64-127 at +64..95)
 #pragma unroll
           for (int s = 0; s < 8; ++s)
             umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::DP_COL + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
                         make_sdesc_sw128(sQ + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
-          umma_commit(&bar_do_empty[G & 1]);
           umma_commit(&bar_q_empty[G & 1]);
-          if (it + 1 < itm.iters) {
-            mma_S(G + 1);   // over P/S columns after dV read them (issue order)
-            mma_dP(G + 1);  // over dS/dP columns after dK read them
-            if (it + 2 == itm.iters) umma_commit(bar_kv_empty);  // last reader of K and V issued
+          if (more) {
+            mma_dP(G + 1);  // over the dS columns after dK read them (issue order)
+            if (it + 2 == itm.iters) umma_commit(bar_kv_empty);  // last readers of K and V issued
           } else {
             umma_commit(bar_dkv_full);
           }
@@ -319,6 +308,8 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int krow = quad * 32 + lane;
     const int c0 = half * 64;
+    uint8_t* spt_row = smem + Cfg::OFF_PT + half * 16384 + krow * 128;  // Pᵀ row chunk (swizzled)
+    uint8_t* stg_row = smem + Cfg::OFF_PT + krow * (HD * 2) + half * HD;  // epilogue staging (linear)
     WaitProf<PROF> wp;
     int G = 0, k = 0;
     KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
@@ -338,29 +329,41 @@ __global__ void __launch_bounds__(320, 1)
         const bool full = c_lo <= 0 && c_hi >= 64;
         const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
         const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
-        // ---- phase A: Sᵀ → Pᵀ (fp32 in registers, bf16 over the S columns)
+        // ---- phase A: Sᵀ → Pᵀ (fp32 registers; bf16 to smem)
         wp.template wait<0>(bar_s_full, G & 1);
         const long long ta = wp.now();
         tc_fence_after();
         float pr[64];
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
-          uint32_t sr[32];
-          tmem_ld32(tmem + lane_off + Cfg::S_COL + c0 + cc, sr);
+        {
+          uint32_t sa[32], sb[32];
+          tmem_ld32(tmem + lane_off + Cfg::S_COL + c0, sa);
+          tmem_ld32(tmem + lane_off + Cfg::S_COL + c0 + 32, sb);
           tmem_wait_ld();
-          uint32_t pk[16];
+          tc_fence_before();
+          mbar_arrive(bar_s_free);  // the MMA warp may overwrite S now
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const int c = cc + j;
-            const float e = ex2_approx(fmaf(__uint_as_float(sr[j]), p.scale_log2, -lse2[c]));
-            pr[c] = (full || (c >= c_lo && c < c_hi)) ? e : 0.f;
+            const float e0 = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lse2[j]));
+            const float e1 = ex2_approx(fmaf(__uint_as_float(sb[j]), p.scale_log2, -lse2[32 + j]));
+            pr[j] = (full || (j >= c_lo && j < c_hi)) ? e0 : 0.f;
+            pr[32 + j] = (full || (32 + j >= c_lo && 32 + j < c_hi)) ? e1 : 0.f;
           }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(pr[cc + 2 * j], pr[cc + 2 * j + 1]);
-          tmem_st16(tmem + lane_off + Cfg::S_COL + c0 + cc / 2, pk);
         }
-        // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
+        if (G > 0) wp.template wait<2>(bar_pv_done, (G - 1) & 1);  // dV(G-1) has read the Pᵀ buffer
+        if (it == 0 && k > 0) {  // every thread's epilogue bulk stores have read the staging rows
+          bulk_wait_read0();
+          named_bar_sync(6, 256);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w[u] = pack_bf16x2(pr[8 * j + 2 * u], pr[8 * j + 2 * u + 1]);
+          *reinterpret_cast<uint4*>(spt_row + ((j ^ (krow & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();
         wp.template add_since<4>(ta);
+        // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
         wp.template wait<1>(bar_dp_full, G & 1);
         const long long tb = wp.now();
         tc_fence_after();
@@ -383,9 +386,10 @@ __global__ void __launch_bounds__(320, 1)
         mbar_arrive(bar_p_full);
         wp.template add_since<5>(tb);
       }
-      // ---- item end: dK / dV epilogue (key row krow, head-dim half `half`)
+      // ---- item end: dK / dV epilogue — TMEM → registers → release TMEM → per-thread async
+      //      bulk stores of this thread's half row through the (now idle) Pᵀ buffer
       const long long te = wp.now();
-      wp.template wait<2>(bar_dkv_full, k & 1);
+      wp.template wait<3>(bar_dkv_full, k & 1);
       tc_fence_after();
       uint32_t pv[HD / 4], pkk[HD / 4];
 #pragma unroll
@@ -402,16 +406,27 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
-      int* rows = reinterpret_cast<int*>(smem + Cfg::OFF_ROWS);
-      if (half == 0)
-        rows[krow] = key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1;
-      uint8_t* stg = smem + Cfg::OFF_STG;
-      named_bar_sync(5, 256);
-      store_tile_coalesced<HD>(stg, rows, pv, krow, half, tid, p.dv + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
-      store_tile_coalesced<HD>(stg, rows, pkk, krow, half, tid, p.dk + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
-      wp.template add_since<3>(te);
+      if (key < p.T) {
+        const int64_t dst = p.row_map ? int64_t(__ldg(p.row_map + key)) : int64_t(key);
+        const int64_t goff = (dst * p.Hkv + itm.kh) * HD + half * (HD / 2);
+#pragma unroll
+        for (int j = 0; j < HD / 16; ++j)
+          *reinterpret_cast<uint4*>(stg_row + j * 16) = make_uint4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
+        fence_proxy_async_smem();
+        bulk_store(p.dv + goff, stg_row, HD);
+        bulk_commit();
+        bulk_wait_read0();
+#pragma unroll
+        for (int j = 0; j < HD / 16; ++j)
+          *reinterpret_cast<uint4*>(stg_row + j * 16) = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
+        fence_proxy_async_smem();
+        bulk_store(p.dk + goff, stg_row, HD);
+        bulk_commit();
+      }
+      wp.template add_since<6>(te);
       ++k;
     }
+    bulk_wait_all();
     if (warp == 0 && lane == 0) wp.flush(p.prof + 16);
   }
   tc_fence_before();
@@ -672,12 +687,20 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       mbar_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
-      int* rows = reinterpret_cast<int*>(smem + Cfg::OFF_ROWS);
-      if (half == 0) rows[r] = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
-      named_bar_sync(5, 256);
-      store_tile_coalesced<HD>(smem + Cfg::OFF_STG, rows, pq, r, half, tid, p.dq + itm.h * HD, int64_t(p.H) * HD, 5);
+      if (valid) {  // this thread's half row → staging → async bulk store
+        uint8_t* stg_row = smem + Cfg::OFF_STG + r * (HD * 2) + half * HD;
+        const int64_t dst = p.row_map ? int64_t(__ldg(p.row_map + row)) : int64_t(row);
+        bulk_wait_read0();  // previous item's store has finished reading the staging row
+#pragma unroll
+        for (int j = 0; j < HD / 16; ++j)
+          *reinterpret_cast<uint4*>(stg_row + j * 16) = make_uint4(pq[4 * j], pq[4 * j + 1], pq[4 * j + 2], pq[4 * j + 3]);
+        fence_proxy_async_smem();
+        bulk_store(p.dq + (dst * p.H + itm.h) * HD + half * (HD / 2), stg_row, HD);
+        bulk_commit();
+      }
       ++k;
     }
+    bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -754,8 +777,9 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,
                   {"prod:q_empty", "prod:kv_empty", "prod:do_empty", "", "", "", "", "prod:total", "mma:kv_full",
-                   "mma:q_full", "mma:do_full", "mma:p_full", "mma:dkv_empty", "", "", "mma:total", "smx:s_full",
-                   "smx:dp_full", "smx:dkv_full", "smx:epilogue", "smx:phaseA", "smx:phaseB", "", "smx:total"});
+                   "mma:q_full", "mma:do_full", "mma:p_full", "mma:dkv_empty", "mma:s_free", "", "mma:total",
+                   "smx:s_full", "smx:dp_full", "smx:pv_done", "smx:dkv_full", "smx:phaseA", "smx:phaseB",
+                   "smx:epilogue", "smx:total"});
   }
   {
     constexpr int ST = HD == 64 ? 4 : 2;

@@ -116,7 +116,7 @@ struct DkvCfg {
   static constexpr int OFF_DSUM = OFF_LSE + 2 * VEC;  // [2][VEC]
   static constexpr int OFF_BAR = OFF_DSUM + 2 * VEC;
   static constexpr int NUM_BARS = 18;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 512;  // + rows[128]; base is 1 KB aligned
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
   static_assert(DK_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
@@ -137,8 +137,42 @@ __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   return it;
 }
 
+// Coalesced epilogue store of a [128 rows × HD] bf16 tile held by NT softmax threads as packed
+// registers (thread = (row, 1/NP of the head dim)): registers → swizzled smem staging → 16-B
+// global stores, consecutive threads covering consecutive 16-B chunks of a 256-B row.
+// rows[r] < 0 skips row r.  NT = 128·NP threads participate (named barrier bar_id).
+template <int HD, int NP>
+__device__ __forceinline__ void store_tile_coalesced(uint8_t* stg, const int* rows, const uint32_t* pk, int krow,
+                                                     int part, int tid, __nv_bfloat16* base, int64_t row_stride,
+                                                     int bar_id) {
+  constexpr int CH = HD / 8;        // 16-B chunks per row
+  constexpr int CPT = CH / NP;      // chunks per thread
+  constexpr int NT = 128 * NP;
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int ch = (part * CPT + j) ^ (krow & (CH - 1));
+    *reinterpret_cast<uint4*>(stg + krow * (HD * 2) + ch * 16) =
+        make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+  }
+  named_bar_sync(bar_id, NT);
+#pragma unroll
+  for (int idx = tid; idx < 128 * CH; idx += NT) {
+    const int r = idx / CH, ch = idx % CH;
+    const int dst = rows[r];
+    if (dst >= 0) {
+      const uint4 v = *reinterpret_cast<const uint4*>(stg + r * (HD * 2) + ((ch ^ (r & (CH - 1))) * 16));
+      *reinterpret_cast<uint4*>(base + int64_t(dst) * row_stride + ch * 8) = v;
+    }
+  }
+  named_bar_sync(bar_id, NT);
+}
+
+// Warp roles (576 threads): warps 0-15 softmax — warp w owns key rows 32·(w%4).. (TMEM lane
+// quadrant w%4) and query columns [32·(w/4), +32); warp 16 TMA producer; warp 17 MMA issuer.
+constexpr int kDkvThreads = 576;
+
 template <int HD, bool PROF>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kDkvThreads, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
   using Cfg = DkvCfg<HD>;
@@ -153,12 +187,13 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar_do_empty = bars + 8;  // [2]
   uint64_t* bar_s_full = bars + 10;
   uint64_t* bar_dp_full = bars + 11;
-  uint64_t* bar_p_full = bars + 12;     // 256 arrivals: Pᵀ in smem, dSᵀ in TMEM
+  uint64_t* bar_p_full = bars + 12;     // 512 arrivals: Pᵀ in smem, dSᵀ in TMEM
   uint64_t* bar_dkv_full = bars + 13;
-  uint64_t* bar_dkv_empty = bars + 14;  // 256 arrivals
-  uint64_t* bar_s_free = bars + 15;     // 256 arrivals: S columns read by phase A
+  uint64_t* bar_dkv_empty = bars + 14;  // 512 arrivals
+  uint64_t* bar_s_free = bars + 15;     // 512 arrivals: S columns read by phase A
   uint64_t* bar_pv_done = bars + 16;    // dV(G) has read Pᵀ from smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  int* rows = reinterpret_cast<int*>(tmem_slot + 4);  // [128] epilogue destination rows
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int group = p.H / p.Hkv;
@@ -174,20 +209,20 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_init(bar_s_full, 1);
     mbar_init(bar_dp_full, 1);
-    mbar_init(bar_p_full, 256);
+    mbar_init(bar_p_full, 512);
     mbar_init(bar_dkv_full, 1);
-    mbar_init(bar_dkv_empty, 256);
-    mbar_init(bar_s_free, 256);
+    mbar_init(bar_dkv_empty, 512);
+    mbar_init(bar_s_free, 512);
     mbar_init(bar_pv_done, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == 17) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 16) {
     // ================================================ TMA producer
     if (lane == 0) {
       WaitProf<PROF> wp;
@@ -227,7 +262,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       wp.flush(p.prof);
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     // ================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ
@@ -285,10 +320,10 @@ __global__ void __launch_bounds__(320, 1)
                         make_sdesc_sw128(sdO + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
           umma_commit(bar_pv_done);
           umma_commit(&bar_do_empty[G & 1]);
-          // dK += dSᵀ·Q  (A = dSᵀ in TMEM: queries 0-63 at +0..31, 64-127 at +64..95)
+          // dK += dSᵀ·Q  (A = dSᵀ in TMEM: queries 32j..32j+31 packed at dP cols 32j .. 32j+15)
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::DP_COL + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::DP_COL + (s >> 1) * 32 + (s & 1) * 8,
                         make_sdesc_sw128(sQ + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
           umma_commit(&bar_q_empty[G & 1]);
           if (more) {
@@ -303,13 +338,13 @@ __global__ void __launch_bounds__(320, 1)
       wp.flush(p.prof + 8);
     }
   } else {
-    // ================================================ softmax warps 0-7 (key row, query-column half)
-    const int quad = warp & 3, half = warp >> 2;
+    // ================================================ softmax warps 0-15 (key row, 32-query quarter)
+    const int quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int krow = quad * 32 + lane;
-    const int c0 = half * 64;
-    uint8_t* spt_row = smem + Cfg::OFF_PT + half * 16384 + krow * 128;  // Pᵀ row chunk (swizzled)
-    uint8_t* stg_row = smem + Cfg::OFF_PT + krow * (HD * 2) + half * HD;  // epilogue staging (linear)
+    const int c0 = part * 32;
+    // Pᵀ row chunk: box part/2 (queries 64·(part/2)..), 16-B chunks (part%2)*4 .. +3, swizzled
+    uint8_t* spt_row = smem + Cfg::OFF_PT + (part >> 1) * 16384 + krow * 128;
     WaitProf<PROF> wp;
     int G = 0, k = 0;
     KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
@@ -325,41 +360,36 @@ __global__ void __launch_bounds__(320, 1)
       const int key = itm.k0 + krow;
       for (int it = 0; it < itm.iters; ++it, ++G) {
         const int qb = itm.q_lo + (it % itm.nq) * 128;
-        const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
-        const bool full = c_lo <= 0 && c_hi >= 64;
+        const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this quarter
+        const bool full = c_lo <= 0 && c_hi >= 32;
         const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
         const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
         // ---- phase A: Sᵀ → Pᵀ (fp32 registers; bf16 to smem)
         wp.template wait<0>(bar_s_full, G & 1);
         const long long ta = wp.now();
         tc_fence_after();
-        float pr[64];
+        float pr[32];
         {
-          uint32_t sa[32], sb[32];
+          uint32_t sa[32];
           tmem_ld32(tmem + lane_off + Cfg::S_COL + c0, sa);
-          tmem_ld32(tmem + lane_off + Cfg::S_COL + c0 + 32, sb);
           tmem_wait_ld();
           tc_fence_before();
           mbar_arrive(bar_s_free);  // the MMA warp may overwrite S now
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float e0 = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lse2[j]));
-            const float e1 = ex2_approx(fmaf(__uint_as_float(sb[j]), p.scale_log2, -lse2[32 + j]));
-            pr[j] = (full || (j >= c_lo && j < c_hi)) ? e0 : 0.f;
-            pr[32 + j] = (full || (32 + j >= c_lo && 32 + j < c_hi)) ? e1 : 0.f;
+            const float e = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lse2[j]));
+            pr[j] = (full || (j >= c_lo && j < c_hi)) ? e : 0.f;
           }
         }
         if (G > 0) wp.template wait<2>(bar_pv_done, (G - 1) & 1);  // dV(G-1) has read the Pᵀ buffer
-        if (it == 0 && k > 0) {  // every thread's epilogue bulk stores have read the staging rows
-          bulk_wait_read0();
-          named_bar_sync(6, 256);
-        }
+        if (it == 0 && k > 0) named_bar_sync(6, 512);              // epilogue staging reads finished
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4; ++j) {
           uint32_t w[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) w[u] = pack_bf16x2(pr[8 * j + 2 * u], pr[8 * j + 2 * u + 1]);
-          *reinterpret_cast<uint4*>(spt_row + ((j ^ (krow & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(spt_row + ((((part & 1) * 4 + j) ^ (krow & 7)) * 16)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
         }
         fence_proxy_async_smem();
         wp.template add_since<4>(ta);
@@ -367,71 +397,57 @@ __global__ void __launch_bounds__(320, 1)
         wp.template wait<1>(bar_dp_full, G & 1);
         const long long tb = wp.now();
         tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
+        {
           uint32_t dr[32];
-          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0 + cc, dr);
+          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0, dr);
           tmem_wait_ld();
           uint32_t dk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int c = cc + 2 * j;
+            const int c = 2 * j;
             dk[j] = pack_bf16x2(pr[c] * (__uint_as_float(dr[2 * j]) - dsum[c]),
                                 pr[c + 1] * (__uint_as_float(dr[2 * j + 1]) - dsum[c + 1]));
           }
-          tmem_st16(tmem + lane_off + Cfg::DP_COL + c0 + cc / 2, dk);
+          tmem_st16(tmem + lane_off + Cfg::DP_COL + c0, dk);
         }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(bar_p_full);
         wp.template add_since<5>(tb);
       }
-      // ---- item end: dK / dV epilogue — TMEM → registers → release TMEM → per-thread async
-      //      bulk stores of this thread's half row through the (now idle) Pᵀ buffer
+      // ---- item end: dK / dV epilogue — TMEM → registers → release TMEM → coalesced stores
+      //      through the (now idle) Pᵀ buffer
       const long long te = wp.now();
       wp.template wait<3>(bar_dkv_full, k & 1);
       tc_fence_after();
-      uint32_t pv[HD / 4], pkk[HD / 4];
+      uint32_t pv[HD / 8], pkk[HD / 8];
 #pragma unroll
-      for (int c = 0; c < HD / 2; c += 32) {
+      for (int c = 0; c < HD / 4; c += 32 > HD / 4 ? HD / 4 : 32) {
         uint32_t v[32], kk[32];
-        tmem_ld32(tmem + lane_off + Cfg::DV_COL + half * (HD / 2) + c, v);
-        tmem_ld32(tmem + lane_off + Cfg::DK_COL + half * (HD / 2) + c, kk);
+        tmem_ld32(tmem + lane_off + Cfg::DV_COL + part * (HD / 4) + c, v);
+        tmem_ld32(tmem + lane_off + Cfg::DK_COL + part * (HD / 4) + c, kk);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < (HD / 4 < 32 ? HD / 8 : 16); ++j) {
           pv[c / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
           pkk[c / 2 + j] = pack_bf16x2(__uint_as_float(kk[2 * j]) * p.scale, __uint_as_float(kk[2 * j + 1]) * p.scale);
         }
       }
       tc_fence_before();
       mbar_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
-      if (key < p.T) {
-        const int64_t dst = p.row_map ? int64_t(__ldg(p.row_map + key)) : int64_t(key);
-        const int64_t goff = (dst * p.Hkv + itm.kh) * HD + half * (HD / 2);
-#pragma unroll
-        for (int j = 0; j < HD / 16; ++j)
-          *reinterpret_cast<uint4*>(stg_row + j * 16) = make_uint4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
-        fence_proxy_async_smem();
-        bulk_store(p.dv + goff, stg_row, HD);
-        bulk_commit();
-        bulk_wait_read0();
-#pragma unroll
-        for (int j = 0; j < HD / 16; ++j)
-          *reinterpret_cast<uint4*>(stg_row + j * 16) = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
-        fence_proxy_async_smem();
-        bulk_store(p.dk + goff, stg_row, HD);
-        bulk_commit();
-      }
+      if (part == 0) rows[krow] = key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1;
+      named_bar_sync(5, 512);
+      uint8_t* stg = smem + Cfg::OFF_PT;
+      store_tile_coalesced<HD, 4>(stg, rows, pv, krow, part, tid, p.dv + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
+      store_tile_coalesced<HD, 4>(stg, rows, pkk, krow, part, tid, p.dk + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
       wp.template add_since<6>(te);
       ++k;
     }
-    bulk_wait_all();
     if (warp == 0 && lane == 0) wp.flush(p.prof + 16);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == 17) tmem_dealloc<512>(tmem);
 }
 
 // ================================================================== dQ (Q-stationary)
@@ -772,7 +788,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
     auto kern = p.prof ? k_bwd_dkdv<HD, true> : k_bwd_dkdv<HD, false>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,

@@ -66,8 +66,15 @@ __global__ void k_bwd_pre(const __nv_bfloat16* __restrict__ o, const __nv_bfloat
   for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (ok && sub == 0) {
     const int t = int(row / H), h = int(row % H);
-    dsum[int64_t(h) * Tp + t] = acc;
-    lse2[int64_t(h) * Tp + t] = lse[int64_t(h) * T + t] * kLog2e;
+    // 4 copies shifted by s = 0..3 elements: any 128-wide window [qb, qb+128) starts 16-B aligned
+    // in copy (−qb) & 3, so the dK/dV kernel reads it with 128-bit shared loads.
+    const int64_t cp = int64_t(H) * Tp + 512;
+    const float l2 = lse[int64_t(h) * T + t] * kLog2e;
+#pragma unroll
+    for (int sh = 0; sh < 4; ++sh) {
+      dsum[sh * cp + int64_t(h) * Tp + t + sh] = acc;
+      lse2[sh * cp + int64_t(h) * Tp + t + sh] = l2;
+    }
     if (h == 0) {
       const RowSpan r = row_span(cu, prefix, nseq, mask, t, T);
       const RowSpan c = key_span(cu, prefix, nseq, mask, t, T);
@@ -88,6 +95,7 @@ struct BwdParams {
   const int2* rows_span;   // [T] visible keys of query t
   const int2* cols_span;   // [T] queries that see key t
   int T, Tp, H, Hkv, kv_items, q_items;
+  int64_t vec_copy;  // element stride between the 4 shifted copies of lse2 / dsum
   float scale_log2, scale;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
 };
@@ -237,11 +245,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           const int qb = itm.q_lo + (it % itm.nq) * 128;
           const int b = G & 1;
           if (G >= 2) wp.template wait<0>(&bar_q_empty[b], ((G >> 1) - 1) & 1);
-          mbar_expect_tx(&bar_q_full[b], Cfg::TILE + 528);
+          mbar_expect_tx(&bar_q_full[b], Cfg::TILE + 512);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
             tma_load_2d(smem + Cfg::OFF_Q + b * Cfg::TILE + c * 16384, &tmQ, h * HD + c * 64, qb, &bar_q_full[b]);
-          bulk_load(smem + Cfg::OFF_LSE + b * Cfg::VEC, p.lse2 + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_q_full[b]);
+          bulk_load(smem + Cfg::OFF_LSE + b * Cfg::VEC, p.lse2 + ((-qb) & 3) * p.vec_copy + int64_t(h) * p.Tp + qb + ((-qb) & 3), 512, &bar_q_full[b]);
           if (it == 0) {
             if (k > 0) wp.template wait<1>(bar_kv_empty, (k - 1) & 1);
             mbar_expect_tx(bar_kv_full, 2 * Cfg::TILE);
@@ -252,11 +260,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             }
           }
           if (G >= 2) wp.template wait<2>(&bar_do_empty[b], ((G >> 1) - 1) & 1);
-          mbar_expect_tx(&bar_do_full[b], Cfg::TILE + 528);
+          mbar_expect_tx(&bar_do_full[b], Cfg::TILE + 512);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
             tma_load_2d(smem + Cfg::OFF_DO + b * Cfg::TILE + c * 16384, &tmdO, h * HD + c * 64, qb, &bar_do_full[b]);
-          bulk_load(smem + Cfg::OFF_DSUM + b * Cfg::VEC, p.dsum + int64_t(h) * p.Tp + (qb & ~3), 528, &bar_do_full[b]);
+          bulk_load(smem + Cfg::OFF_DSUM + b * Cfg::VEC, p.dsum + ((-qb) & 3) * p.vec_copy + int64_t(h) * p.Tp + qb + ((-qb) & 3), 512, &bar_do_full[b]);
         }
         ++k;
       }
@@ -362,8 +370,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const int qb = itm.q_lo + (it % itm.nq) * 128;
         const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this quarter
         const bool full = c_lo <= 0 && c_hi >= 32;
-        const float* lse2 = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
-        const float* dsum = reinterpret_cast<const float*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + (qb & 3) + c0;
+        const float4* lse4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + c0 / 4;
+        const float4* dsum4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + c0 / 4;
         // ---- phase A: Sᵀ → Pᵀ (fp32 registers; bf16 to smem)
         wp.template wait<0>(bar_s_full, G & 1);
         const long long ta = wp.now();
@@ -376,9 +384,15 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           tc_fence_before();
           mbar_arrive(bar_s_free);  // the MMA warp may overwrite S now
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float e = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lse2[j]));
-            pr[j] = (full || (j >= c_lo && j < c_hi)) ? e : 0.f;
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 l = lse4[j4];  // 128-bit broadcast load
+            const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * j4 + u;
+              const float e = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lv[u]));
+              pr[j] = (full || (j >= c_lo && j < c_hi)) ? e : 0.f;
+            }
           }
         }
         if (G > 0) wp.template wait<2>(bar_pv_done, (G - 1) & 1);  // dV(G-1) has read the Pᵀ buffer
@@ -403,10 +417,12 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           tmem_wait_ld();
           uint32_t dk[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int c = 2 * j;
-            dk[j] = pack_bf16x2(pr[c] * (__uint_as_float(dr[2 * j]) - dsum[c]),
-                                pr[c + 1] * (__uint_as_float(dr[2 * j + 1]) - dsum[c + 1]));
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 dd = dsum4[j4];  // 128-bit broadcast load
+            const int c = 4 * j4;
+            dk[2 * j4] = pack_bf16x2(pr[c] * (__uint_as_float(dr[c]) - dd.x), pr[c + 1] * (__uint_as_float(dr[c + 1]) - dd.y));
+            dk[2 * j4 + 1] =
+                pack_bf16x2(pr[c + 2] * (__uint_as_float(dr[c + 2]) - dd.z), pr[c + 3] * (__uint_as_float(dr[c + 3]) - dd.w));
           }
           tmem_st16(tmem + lane_off + Cfg::DP_COL + c0, dk);
         }
@@ -630,7 +646,7 @@ __global__ void __launch_bounds__(320, 1)
       const int rw = it.q0 + r;
       const bool v = rw < p.T;
       rs_ = v ? __ldg(p.rows_span + rw) : make_int2(0, 0);
-      l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw) : 0.f;
+      l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw) : 0.f;  // copy 0 (unshifted)
       d_ = v ? __ldg(p.dsum + int64_t(it.h) * p.Tp + rw) : 0.f;
     };
     QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
@@ -742,8 +758,8 @@ size_t bwd_ws(BwdWs* w, void* base, const vlasim_attn_args* a) {
     return r;
   };
   (void)d;
-  w->lse2 = reinterpret_cast<float*>(take(Tp * H * 4 + 512 * 4));
-  w->dsum = reinterpret_cast<float*>(take(Tp * H * 4 + 512 * 4));
+  w->lse2 = reinterpret_cast<float*>(take(4 * (Tp * H + 512) * 4));  // 4 shifted copies
+  w->dsum = reinterpret_cast<float*>(take(4 * (Tp * H + 512) * 4));
   w->rows_span = reinterpret_cast<int2*>(take(T * 8));
   w->cols_span = reinterpret_cast<int2*>(take(T * 8));
   return off;
@@ -779,6 +795,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.H = H;
   p.Hkv = Hkv;
   p.kv_items = int((int64_t(T) + 127) / 128) * Hkv;
+  p.vec_copy = int64_t(H) * Tp + 512;
   p.q_items = int((int64_t(T) + 127) / 128) * H;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;

@@ -390,8 +390,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int j = 4 * j4 + u;
-              const float xarg = fmaf(__uint_as_float(sa[j]), p.scale_log2, -lv[u]);
-              const float e = (u & 1) ? ex2_poly(xarg) : ex2_approx(xarg);  // half on MUFU, half on FMA
+              const float e = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lv[u]));
               pr[j] = (full || (j >= c_lo && j < c_hi)) ? e : 0.f;
             }
           }
@@ -681,8 +680,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
             const int c = cc + t;
-            const float xarg = fmaf(__uint_as_float(sr[t]), p.scale_log2, -lse2);
-            const float e = (t & 1) ? ex2_poly(xarg) : ex2_approx(xarg);  // half on MUFU, half on FMA
+            const float e = ex2_approx(fmaf(__uint_as_float(sr[t]), p.scale_log2, -lse2));
             pr[c] = (full || (c >= c_lo && c < c_hi)) ? e : 0.f;
           }
         }

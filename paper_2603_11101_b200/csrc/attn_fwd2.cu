@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             const float p0 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t]), sl2, -msub));
-            const float p1 = ex2_poly(fmaf(__uint_as_float(x[c + 2 * t + 1]), sl2, -msub));  // FMA pipe
+            const float p1 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t + 1]), sl2, -msub));
             lq[(2 * t) & 3] += p0;
             lq[(2 * t + 1) & 3] += p1;
             pk[t] = pack_bf16x2(p0, p1);

@@ -237,19 +237,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA/ALU pipes (offloads MUFU, FA4-style): x = n + f with n = rint(x) obtained by the
-// 1.5·2^23 rounding trick, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max relative error
-// 1.0e-4, far below the bf16 rounding of P), 2^n added to the exponent field.  Inputs below -126
-// (incl. -inf) return 0, like ex2.approx.ftz.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -127.f);
-  const float t = xc + 12582912.f;
-  const float n = t - 12582912.f;
-  const float f = xc - n;
-  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221097f), f, 0.6932829f), f, 1.0f);
-  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-  return x < -126.f ? 0.f : r;
-}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

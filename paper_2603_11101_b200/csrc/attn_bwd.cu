@@ -98,34 +98,42 @@ struct BwdParams {
   int64_t vec_copy;  // element stride between the 4 shifted copies of lse2 / dsum
   float scale_log2, scale;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
+  int dbg;                   // VLASIM_DBG ablations (timing experiments only; results invalid if ≠ 0)
 };
 
 // ================================================================== dK / dV (KV-stationary)
-// One CTA loops over items = (128-key tile, kv head).  Per iteration G (q head of the group,
-// 128-row Q tile of the visible query range):
-//   Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ                                  (SS, K-major operands)
-//   softmax warps: phase A  Pᵀ = exp2(Sᵀ·scale·log2e − lse2) → bf16 → smem (K-major SW128)
-//                  phase B  dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP TMEM columns
-//   dV += Pᵀ·dO (A = Pᵀ smem), dK += dSᵀ·Q (A = dSᵀ TMEM)     (B = dO / Q, MN-major)
-// Because Pᵀ lives in smem, the S columns are free as soon as phase A has read them, so S(G+1)
-// is issued before dV(G)/dK(G) and phase A(G+1) overlaps them.  The Pᵀ buffer doubles as the
-// epilogue staging buffer (dK/dV rows leave through per-thread async bulk stores).
-// TMEM: S [0,128) · dP/dS [128,256) · dV [256,256+HD) · dK after.  Q and dO double-buffered.
+// One CTA loops over items = (128-key tile, kv head).  An item is a run of units u = (q head of
+// the group, 64-row Q tile of the key tile's visible query range); per unit:
+//   Sᵀ = K·Qᵀ → S[u&1], dPᵀ = V·dOᵀ → dP[u&1]                  (SS, K-major operands, N = 64)
+//   softmax group u&1: phase A  Pᵀ = exp2(Sᵀ·scale·log2e − lse2) → bf16 over the S columns
+//                      phase B  dSᵀ = Pᵀ ∘ (dPᵀ − D)        → bf16 over the dP columns
+//   dV += Pᵀ·dO, dK += dSᵀ·Q                                 (A from TMEM, B = dO / Q MN-major)
+// Two softmax groups of 8 warps take alternate units, so while one group exponentiates unit u
+// the tensor cores run the GEMMs of its neighbours: the MMA warp issues S/dP two units ahead
+// (S(u+2) right after dV(u) consumed Pᵀ(u) from S[u&1], dP(u+2) after dK(u) consumed dSᵀ(u));
+// the column aliasing relies on tcgen05.mma executing in issue order.  Q/dO stream through
+// NS = 5 stages (the look-ahead of 2 units plus ~2 units of HBM latency); every role prefetches
+// the next item's descriptor so item boundaries do not expose a global-load round trip.  The
+// item epilogue writes dK/dV straight from TMEM-loaded registers (64-B row segments) through
+// row_map.  TMEM: S0 [0,64) · S1 [64,128) · dP0 [128,192) · dP1 [192,256) · dV · dK.
 template <int HD>
 struct DkvCfg {
-  static constexpr int TILE = 128 * HD * 2;
-  static constexpr int OFF_K = 0, OFF_V = TILE;
-  static constexpr int OFF_Q = 2 * TILE;        // [2]
-  static constexpr int OFF_DO = 4 * TILE;       // [2]
-  static constexpr int OFF_PT = 6 * TILE;       // Pᵀ [128 keys × 128 q] bf16 (SW128) / epilogue staging
-  static constexpr int PT_BYTES = 128 * 128 * 2 > TILE ? 128 * 128 * 2 : TILE;
-  static constexpr int VEC = 544;               // 132 floats (16-B aligned window of 128) + pad
-  static constexpr int OFF_LSE = OFF_PT + PT_BYTES;   // [2][VEC]
-  static constexpr int OFF_DSUM = OFF_LSE + 2 * VEC;  // [2][VEC]
-  static constexpr int OFF_BAR = OFF_DSUM + 2 * VEC;
-  static constexpr int NUM_BARS = 18;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 512;  // + rows[128]; base is 1 KB aligned
-  static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
+  static constexpr int KT = 128 * HD * 2;  // K or V tile (128 keys)
+  static constexpr int QT = 64 * HD * 2;   // Q or dO tile (64 queries)
+  static constexpr int NS = 4;             // Q / dO stages
+  static constexpr int OFF_K = 0, OFF_V = KT;
+  static constexpr int OFF_Q = 2 * KT;              // [NS]
+  static constexpr int OFF_DO = OFF_Q + NS * QT;    // [NS]
+  static constexpr int OFF_STG = OFF_DO + NS * QT;  // epilogue staging: one [128 × HD] bf16 tile (SW128)
+  static constexpr int VEC = 256;                   // 64 floats of lse2 / D (16-B aligned window)
+  static constexpr int OFF_LSE = OFF_STG + KT;      // [NS][VEC]
+  static constexpr int OFF_DSUM = OFF_LSE + NS * VEC;
+  static constexpr int OFF_BAR = OFF_DSUM + NS * VEC;
+  static constexpr int NUM_BARS = 12 + 2 * NS;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
+  static constexpr uint32_t DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
+  __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? 64u : 0u; }
+  __host__ __device__ static constexpr uint32_t dp_col(int b) { return b ? 192u : 128u; }
   static_assert(DK_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
@@ -140,88 +148,91 @@ __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   const int2 first = __ldg(p.cols_span + it.k0);
   const int2 last = __ldg(p.cols_span + min(it.k0 + 127, p.T - 1));
   it.q_lo = first.x;
-  it.nq = max(0, (last.y - first.x + 127) / 128);
+  it.nq = max(0, (last.y - first.x + 63) / 64);
   it.iters = it.nq * (p.H / p.Hkv);
   return it;
 }
 
-// Coalesced epilogue store of a [128 rows × HD] bf16 tile held by NT softmax threads as packed
-// registers (thread = (row, 1/NP of the head dim)): registers → swizzled smem staging → 16-B
-// global stores, consecutive threads covering consecutive 16-B chunks of a 256-B row.
-// rows[r] < 0 skips row r.  NT = 128·NP threads participate (named barrier bar_id).
-template <int HD, int NP>
-__device__ __forceinline__ void store_tile_coalesced(uint8_t* stg, const int* rows, const uint32_t* pk, int krow,
-                                                     int part, int tid, __nv_bfloat16* base, int64_t row_stride,
-                                                     int bar_id) {
-  constexpr int CH = HD / 8;        // 16-B chunks per row
-  constexpr int CPT = CH / NP;      // chunks per thread
-  constexpr int NT = 128 * NP;
-#pragma unroll
-  for (int j = 0; j < CPT; ++j) {
-    const int ch = (part * CPT + j) ^ (krow & (CH - 1));
-    *reinterpret_cast<uint4*>(stg + krow * (HD * 2) + ch * 16) =
-        make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+// Walks this CTA's units in order: item i (blockIdx.x + m·gridDim.x), unit it within the item,
+// k = ordinal of the item, u = ordinal of the unit.  The next item's descriptor is loaded one
+// item ahead (its global loads overlap the current item).  Every key sees itself, so every
+// item has iters ≥ 1.
+struct UnitCursor {
+  int i, it, k, u;
+  KvItem itm, nxt;
+  __device__ __forceinline__ bool start(const BwdParams& p) {
+    i = blockIdx.x;
+    it = k = u = 0;
+    if (i >= p.kv_items) return false;
+    itm = kv_item(p, i);
+    if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
+    return true;
   }
-  named_bar_sync(bar_id, NT);
-#pragma unroll
-  for (int idx = tid; idx < 128 * CH; idx += NT) {
-    const int r = idx / CH, ch = idx % CH;
-    const int dst = rows[r];
-    if (dst >= 0) {
-      const uint4 v = *reinterpret_cast<const uint4*>(stg + r * (HD * 2) + ((ch ^ (r & (CH - 1))) * 16));
-      *reinterpret_cast<uint4*>(base + int64_t(dst) * row_stride + ch * 8) = v;
-    }
+  __device__ __forceinline__ bool next(const BwdParams& p) {
+    ++u;
+    if (++it < itm.iters) return true;
+    it = 0;
+    ++k;
+    i += gridDim.x;
+    if (i >= p.kv_items) return false;
+    itm = nxt;
+    if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
+    return true;
   }
-  named_bar_sync(bar_id, NT);
-}
+  __device__ __forceinline__ bool last() const { return it + 1 == itm.iters; }
+  __device__ __forceinline__ int head(int group) const { return itm.kh * group + it / itm.nq; }
+  __device__ __forceinline__ int qb() const { return itm.q_lo + (it % itm.nq) * 64; }
+};
 
-// Warp roles (576 threads): warps 0-15 softmax — warp w owns key rows 32·(w%4).. (TMEM lane
-// quadrant w%4) and query columns [32·(w/4), +32); warp 16 TMA producer; warp 17 MMA issuer.
+// Warp roles (576 threads): warps 0-15 softmax — group g = w/8 takes the units with u%2 == g;
+// warp w owns key rows 32·(w%4).. (TMEM lane quadrant w%4) and query columns [32·((w/4)%2), +32)
+// of the 64-wide unit; in the epilogue all 16 warps split the head dim in quarters (w/4) and
+// store their 2·HD/4 bytes of every dK / dV row directly.
+// Warp 16 TMA producer, warp 17 TMEM allocator + MMA issuer.
 constexpr int kDkvThreads = 576;
 
 template <int HD, bool PROF>
 __global__ void __launch_bounds__(kDkvThreads, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
+               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+               const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, const BwdParams p) {
   using Cfg = DkvCfg<HD>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
+  constexpr int NS = Cfg::NS;
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_kv_full = bars + 0;
-  uint64_t* bar_kv_empty = bars + 1;
-  uint64_t* bar_q_full = bars + 2;    // [2]
-  uint64_t* bar_q_empty = bars + 4;   // [2]
-  uint64_t* bar_do_full = bars + 6;   // [2]
-  uint64_t* bar_do_empty = bars + 8;  // [2]
-  uint64_t* bar_s_full = bars + 10;
-  uint64_t* bar_dp_full = bars + 11;
-  uint64_t* bar_p_full = bars + 12;     // 512 arrivals: Pᵀ in smem, dSᵀ in TMEM
-  uint64_t* bar_dkv_full = bars + 13;
-  uint64_t* bar_dkv_empty = bars + 14;  // 512 arrivals
-  uint64_t* bar_s_free = bars + 15;     // 512 arrivals: S columns read by phase A
-  uint64_t* bar_pv_done = bars + 16;    // dV(G) has read Pᵀ from smem
+  uint64_t* bar_kv_empty = bars + 1;   // committed after the item's last S / dP
+  uint64_t* bar_dkv_full = bars + 2;
+  uint64_t* bar_dkv_empty = bars + 3;  // 16 warp arrivals: TMEM dV / dK drained
+  uint64_t* bar_s_full = bars + 4;     // [2]
+  uint64_t* bar_dp_full = bars + 6;    // [2]
+  uint64_t* bar_pt_full = bars + 8;    // [2] 8 warp arrivals: Pᵀ written over S
+  uint64_t* bar_ds_full = bars + 10;   // [2] 8 warp arrivals: dSᵀ written over dP
+  uint64_t* bar_qd_full = bars + 12;        // [NS] Q + dO (+ lse2 / D windows) of a unit
+  uint64_t* bar_qd_empty = bars + 12 + NS;  // [NS] committed after the unit's dK
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
-  int* rows = reinterpret_cast<int*>(tmem_slot + 4);  // [128] epilogue destination rows
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // event trace (PROF builds with VLASIM_DBG & 2: the idle Q stages hold 4 × 4001 words)
+  unsigned long long* const trb =
+      PROF && (p.dbg & 2) && blockIdx.x == 0 ? reinterpret_cast<unsigned long long*>(smem + Cfg::OFF_Q) : nullptr;
   const int group = p.H / p.Hkv;
   if (tid == 0) {
     if (smem_u32(smem) & 1023) __trap();
     mbar_init(bar_kv_full, 1);
     mbar_init(bar_kv_empty, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar_q_full[s], 1);
-      mbar_init(&bar_q_empty[s], 1);
-      mbar_init(&bar_do_full[s], 1);
-      mbar_init(&bar_do_empty[s], 1);
-    }
-    mbar_init(bar_s_full, 1);
-    mbar_init(bar_dp_full, 1);
-    mbar_init(bar_p_full, 512);
     mbar_init(bar_dkv_full, 1);
-    mbar_init(bar_dkv_empty, 512);
-    mbar_init(bar_s_free, 512);
-    mbar_init(bar_pv_done, 1);
+    mbar_init(bar_dkv_empty, 16);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_s_full[b], 1);
+      mbar_init(&bar_dp_full[b], 1);
+      mbar_init(&bar_pt_full[b], 8);
+      mbar_init(&bar_ds_full[b], 8);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bar_qd_full[s], 1);
+      mbar_init(&bar_qd_empty[s], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc<512>(tmem_slot);
@@ -234,235 +245,318 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     // ================================================ TMA producer
     if (lane == 0) {
       WaitProf<PROF> wp;
-      int G = 0, k = 0;
-      KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
-      for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
-        const KvItem itm = nxt;
-        if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);  // prefetch
-        if (itm.iters == 0) continue;
-        for (int it = 0; it < itm.iters; ++it, ++G) {
-          const int h = itm.kh * group + it / itm.nq;
-          const int qb = itm.q_lo + (it % itm.nq) * 128;
-          const int b = G & 1;
-          if (G >= 2) wp.template wait<0>(&bar_q_empty[b], ((G >> 1) - 1) & 1);
-          mbar_expect_tx(&bar_q_full[b], Cfg::TILE + 512);
+      TraceCtr trace(trb);
+      UnitCursor c;
+      int s = 0;          // stage of unit c.u (= c.u % NS)
+      uint32_t ph = 0;    // parity of that stage's current use
+      for (bool v = c.start(p); v; v = c.next(p)) {
+        if (c.it == 0) {
+          if (c.k > 0) wp.template wait<1>(bar_kv_empty, (c.k - 1) & 1);
+          mbar_expect_tx(bar_kv_full, 2 * Cfg::KT);
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c)
-            tma_load_2d(smem + Cfg::OFF_Q + b * Cfg::TILE + c * 16384, &tmQ, h * HD + c * 64, qb, &bar_q_full[b]);
-          bulk_load(smem + Cfg::OFF_LSE + b * Cfg::VEC, p.lse2 + ((-qb) & 3) * p.vec_copy + int64_t(h) * p.Tp + qb + ((-qb) & 3), 512, &bar_q_full[b]);
-          if (it == 0) {
-            if (k > 0) wp.template wait<1>(bar_kv_empty, (k - 1) & 1);
-            mbar_expect_tx(bar_kv_full, 2 * Cfg::TILE);
-#pragma unroll
-            for (int c = 0; c < HD / 64; ++c) {
-              tma_load_2d(smem + Cfg::OFF_K + c * 16384, &tmK, itm.kh * HD + c * 64, itm.k0, bar_kv_full);
-              tma_load_2d(smem + Cfg::OFF_V + c * 16384, &tmV, itm.kh * HD + c * 64, itm.k0, bar_kv_full);
-            }
+          for (int j = 0; j < HD / 64; ++j) {
+            tma_load_2d(smem + Cfg::OFF_K + j * 16384, &tmK, c.itm.kh * HD + j * 64, c.itm.k0, bar_kv_full);
+            tma_load_2d(smem + Cfg::OFF_V + j * 16384, &tmV, c.itm.kh * HD + j * 64, c.itm.k0, bar_kv_full);
           }
-          if (G >= 2) wp.template wait<2>(&bar_do_empty[b], ((G >> 1) - 1) & 1);
-          mbar_expect_tx(&bar_do_full[b], Cfg::TILE + 512);
-#pragma unroll
-          for (int c = 0; c < HD / 64; ++c)
-            tma_load_2d(smem + Cfg::OFF_DO + b * Cfg::TILE + c * 16384, &tmdO, h * HD + c * 64, qb, &bar_do_full[b]);
-          bulk_load(smem + Cfg::OFF_DSUM + b * Cfg::VEC, p.dsum + ((-qb) & 3) * p.vec_copy + int64_t(h) * p.Tp + qb + ((-qb) & 3), 512, &bar_do_full[b]);
         }
-        ++k;
+        const int h = c.head(group), qb = c.qb();
+        const int sh = (-qb) & 3;  // 16-B aligned window in shifted copy sh (k_bwd_pre)
+        const int64_t vo = sh * p.vec_copy + int64_t(h) * p.Tp + qb + sh;
+        if (c.u >= NS) wp.template wait<0>(&bar_qd_empty[s], ph ^ 1);
+        trace(1, c.u);  // P: Q/dO load issued
+        if (p.dbg & 2) {  // timing experiment: no Q/dO traffic (the trace lives in the Q stages)
+          mbar_arrive(&bar_qd_full[s]);
+        } else {
+          mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + 512);
+#pragma unroll
+          for (int j = 0; j < HD / 64; ++j) {
+            tma_load_2d(smem + Cfg::OFF_Q + s * Cfg::QT + j * 8192, &tmQ, h * HD + j * 64, qb, &bar_qd_full[s]);
+            tma_load_2d(smem + Cfg::OFF_DO + s * Cfg::QT + j * 8192, &tmdO, h * HD + j * 64, qb, &bar_qd_full[s]);
+          }
+          bulk_load(smem + Cfg::OFF_LSE + s * Cfg::VEC, p.lse2 + vo, 256, &bar_qd_full[s]);
+          bulk_load(smem + Cfg::OFF_DSUM + s * Cfg::VEC, p.dsum + vo, 256, &bar_qd_full[s]);
+        }
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
+        }
       }
       wp.flush(p.prof);
     }
   } else if (warp == 17) {
-    // ================================================ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ
-      constexpr uint32_t id_kmn = make_idesc_bf16(128, HD, false, true);   // dV, dK
-      const uint32_t sK = smem_u32(smem + Cfg::OFF_K), sV = smem_u32(smem + Cfg::OFF_V);
-      const uint32_t sPT = smem_u32(smem + Cfg::OFF_PT);
+    // ================================================ MMA issuer (whole warp, so descriptors and
+    // counters stay in uniform registers; one elected lane issues).  Per unit u, in issue order:
+    //   dV(u) · S(u+2) | dK(u) · dP(u+2)   — two issue blocks, three barrier waits.
+    // The warp's serial instruction latency is the budget here (≈6 cycles per instruction on
+    // a single warp), so stages and parities are counters, never u % NS.
+    {
+      constexpr uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // Sᵀ, dPᵀ
+      constexpr uint32_t id_acc = make_idesc_bf16(128, HD, false, true);  // dV, dK
+      constexpr uint32_t QT16 = Cfg::QT >> 4;                             // stage stride, desc units
       WaitProf<PROF> wp;
-      auto mma_S = [&](int G) {
-        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
-        wp.template wait<1>(&bar_q_full[G & 1], (G >> 1) & 1);
-        tc_fence_after();
+      TraceCtr trace(lane == 0 && trb ? trb + 4001 : nullptr);
+      const uint64_t dK0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16, 1024);
+      const uint64_t dV0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), 16, 1024);
+      const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);     // K-major view
+      const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
+      const uint64_t dQm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 8192, 1024);   // MN-major view
+      const uint64_t dOm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 8192, 1024);
+      auto mma_S = [&](uint32_t col, uint32_t soff) {
 #pragma unroll
-        for (int s = 0; s < HD / 16; ++s)
-          umma_f16_ss(tmem + Cfg::S_COL, make_sdesc_sw128(sK + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
-                      make_sdesc_sw128(sQ + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
-        umma_commit(bar_s_full);
+        for (int j = 0; j < HD / 16; ++j)
+          if (!(p.dbg & 4)) umma_f16_ss(tmem + col, sdesc_add(dK0, (j / 4) * 16384 + (j % 4) * 32),
+                      sdesc_add(dQk, (j / 4) * 8192 + (j % 4) * 32) + soff, id_s, j > 0);
       };
-      auto mma_dP = [&](int G) {
-        const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
-        wp.template wait<2>(&bar_do_full[G & 1], (G >> 1) & 1);
-        tc_fence_after();
+      auto mma_dP = [&](uint32_t col, uint32_t soff) {
 #pragma unroll
-        for (int s = 0; s < HD / 16; ++s)
-          umma_f16_ss(tmem + Cfg::DP_COL, make_sdesc_sw128(sV + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
-                      make_sdesc_sw128(sdO + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
-        umma_commit(bar_dp_full);
+        for (int j = 0; j < HD / 16; ++j)
+          if (!(p.dbg & 4)) umma_f16_ss(tmem + col, sdesc_add(dV0, (j / 4) * 16384 + (j % 4) * 32),
+                      sdesc_add(dOk, (j / 4) * 8192 + (j % 4) * 32) + soff, id_s, j > 0);
       };
-      int G = 0, k = 0;
-      KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
-      for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
-        const KvItem itm = nxt;
-        if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);  // prefetch
-        if (itm.iters == 0) continue;
-        wp.template wait<0>(bar_kv_full, k & 1);
+      UnitCursor ca, cc;
+      uint32_t as = 0, aph = 0;  // stage / parity of the look-ahead unit ca.u
+      bool va = ca.start(p);
+      // prologue: S and dP of units 0 and 1
+      for (int n = 0; n < 2 && va; ++n) {
+        if (ca.it == 0) wp.template wait<0>(bar_kv_full, ca.k & 1);
+        wp.template wait<1>(&bar_qd_full[as], aph);
         tc_fence_after();
-        if (G > 0) wp.template wait<5>(bar_s_free, (G - 1) & 1);  // previous item's last S was read
-        mma_S(G);
-        mma_dP(G);
-        if (itm.iters == 1) umma_commit(bar_kv_empty);  // K, V are read only by S and dP
-        for (int it = 0; it < itm.iters; ++it, ++G) {
-          const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + (G & 1) * Cfg::TILE);
-          const uint32_t sdO = smem_u32(smem + Cfg::OFF_DO + (G & 1) * Cfg::TILE);
-          const bool more = it + 1 < itm.iters;
-          if (more) {  // S(G+1) as soon as phase A(G) has read S(G)
-            wp.template wait<5>(bar_s_free, G & 1);
-            mma_S(G + 1);
-          }
-          wp.template wait<3>(bar_p_full, G & 1);
-          if (it == 0 && k > 0) wp.template wait<4>(bar_dkv_empty, (k - 1) & 1);
-          tc_fence_after();
-          // dV += Pᵀ·dO  (A = Pᵀ smem K-major, B = dO MN-major)
+        if (elect_one()) {
+          mma_S(Cfg::s_col(n), as * QT16);
+          (p.dbg & 32) ? mbar_arrive(&bar_s_full[n]) : umma_commit(&bar_s_full[n]);
+          mma_dP(Cfg::dp_col(n), as * QT16);
+          (p.dbg & 32) ? mbar_arrive(&bar_dp_full[n]) : umma_commit(&bar_dp_full[n]);
+          if (ca.last()) (p.dbg & 32) ? mbar_arrive(bar_kv_empty) : umma_commit(bar_kv_empty);
+        }
+        __syncwarp();
+        va = ca.next(p);
+        if (++as == NS) { as = 0; aph ^= 1; }
+      }
+      uint32_t cs = 0, b = 0, ph = 0;  // stage of cc.u; TMEM buffer cc.u & 1; its use parity
+      for (bool vc = cc.start(p); vc; vc = cc.next(p)) {
+        const uint32_t coff = cs * QT16, aoff = as * QT16;
+        if (va) {
+          if (ca.it == 0) wp.template wait<0>(bar_kv_full, ca.k & 1);
+          wp.template wait<1>(&bar_qd_full[as], aph);
+        }
+        wp.template wait<3>(&bar_pt_full[b], ph);
+        trace(10, cc.u);  // M: pt_full seen
+        if (cc.it == 0 && cc.k > 0) wp.template wait<4>(bar_dkv_empty, (cc.k - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc0 = cc.it > 0 ? 1u : 0u;
+        if (elect_one()) {
+          // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
 #pragma unroll
-          for (int s = 0; s < 8; ++s)
-            umma_f16_ss(tmem + Cfg::DV_COL, make_sdesc_sw128(sPT + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
-                        make_sdesc_sw128(sdO + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
-          umma_commit(bar_pv_done);
-          umma_commit(&bar_do_empty[G & 1]);
-          // dK += dSᵀ·Q  (A = dSᵀ in TMEM: queries 32j..32j+31 packed at dP cols 32j .. 32j+15)
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::DP_COL + (s >> 1) * 32 + (s & 1) * 8,
-                        make_sdesc_sw128(sQ + s * 2048, 16384, 1024), id_kmn, (it > 0 || s > 0) ? 1u : 0u);
-          umma_commit(&bar_q_empty[G & 1]);
-          if (more) {
-            mma_dP(G + 1);  // over the dS columns after dK read them (issue order)
-            if (it + 2 == itm.iters) umma_commit(bar_kv_empty);  // last readers of K and V issued
-          } else {
-            umma_commit(bar_dkv_full);
+          for (int j = 0; j < 4; ++j)
+            if (!(p.dbg & 4)) umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+                        sdesc_add(dOm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
+          if (va) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
+            mma_S(Cfg::s_col(b), aoff);
+            (p.dbg & 32) ? mbar_arrive(&bar_s_full[b]) : umma_commit(&bar_s_full[b]);
           }
         }
-        ++k;
+        __syncwarp();
+        trace(11, cc.u);  // M: dV + S(u+2) issued
+        wp.template wait<5>(&bar_ds_full[b], ph);
+        trace(12, cc.u);  // M: ds_full seen
+        tc_fence_after();
+        if (elect_one()) {
+          // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (!(p.dbg & 4)) umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+                        sdesc_add(dQm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
+          (p.dbg & 32) ? mbar_arrive(&bar_qd_empty[cs]) : umma_commit(&bar_qd_empty[cs]);
+          if (cc.last()) (p.dbg & 32) ? mbar_arrive(bar_dkv_full) : umma_commit(bar_dkv_full);
+          if (va) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
+            mma_dP(Cfg::dp_col(b), aoff);
+            (p.dbg & 32) ? mbar_arrive(&bar_dp_full[b]) : umma_commit(&bar_dp_full[b]);
+            if (ca.last()) (p.dbg & 32) ? mbar_arrive(bar_kv_empty) : umma_commit(bar_kv_empty);  // the item's last readers of K and V
+          }
+        }
+        __syncwarp();
+        trace(13, cc.u);  // M: dK + dP(u+2) issued
+        if (va) {
+          va = ca.next(p);
+          if (++as == NS) { as = 0; aph ^= 1; }
+        }
+        if (++cs == NS) cs = 0;
+        b ^= 1;
+        ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
       }
-      wp.flush(p.prof + 8);
+      if (lane == 0) wp.flush(p.prof + 8);
     }
   } else {
-    // ================================================ softmax warps 0-15 (key row, 32-query quarter)
-    const int quad = warp & 3, part = warp >> 2;
+    // ================================================ softmax warps 0-15
+    const int g = warp >> 3, quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int krow = quad * 32 + lane;
-    const int c0 = part * 32;
-    // Pᵀ row chunk: box part/2 (queries 64·(part/2)..), 16-B chunks (part%2)*4 .. +3, swizzled
-    uint8_t* spt_row = smem + Cfg::OFF_PT + (part >> 1) * 16384 + krow * 128;
-    WaitProf<PROF> wp;
-    int G = 0, k = 0;
-    KvItem nxt = kv_item(p, blockIdx.x < p.kv_items ? blockIdx.x : 0);
-    int2 ks_nxt = nxt.k0 + krow < p.T ? __ldg(p.cols_span + nxt.k0 + krow) : make_int2(0, 0);
-    for (int i = blockIdx.x; i < p.kv_items; i += gridDim.x) {
-      const KvItem itm = nxt;
-      const int2 ks = ks_nxt;
-      if (i + int(gridDim.x) < p.kv_items) {  // prefetch the next item's parameters
-        nxt = kv_item(p, i + gridDim.x);
-        ks_nxt = nxt.k0 + krow < p.T ? __ldg(p.cols_span + nxt.k0 + krow) : make_int2(0, 0);
+    const int c0 = (part & 1) * 32;
+    WaitProf<PROF, 12> wp;
+    TraceCtr trace(lane == 0 && (warp & 7) == 0 && trb ? trb + 4001 * (2 + (warp >> 3)) : nullptr);
+    UnitCursor c;
+    auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
+    auto dst_of = [&](int key) { return key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1; };
+    int ss = 0;  // stage of unit c.u
+    int2 ks = make_int2(0, 0), ks_nxt = ks;
+    int dst_key = -1, dst_nxt = -1;
+    for (bool v = c.start(p); v; v = c.next(p)) {
+      if (c.it == 0) {  // this item's spans were prefetched one item ahead (first item: now)
+        const int key = c.itm.k0 + krow;
+        ks = c.k == 0 ? span_of(key) : ks_nxt;
+        dst_key = c.k == 0 ? dst_of(key) : dst_nxt;
+        if (c.i + int(gridDim.x) < p.kv_items) {
+          const int nkey = c.nxt.k0 + krow;
+          ks_nxt = span_of(nkey);
+          dst_nxt = dst_of(nkey);
+        }
       }
-      if (itm.iters == 0) continue;
-      const int key = itm.k0 + krow;
-      for (int it = 0; it < itm.iters; ++it, ++G) {
-        const int qb = itm.q_lo + (it % itm.nq) * 128;
-        const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this quarter
-        const bool full = c_lo <= 0 && c_hi >= 32;
-        const float4* lse4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_LSE + (G & 1) * Cfg::VEC) + c0 / 4;
-        const float4* dsum4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_DSUM + (G & 1) * Cfg::VEC) + c0 / 4;
-        // ---- phase A: Sᵀ → Pᵀ (fp32 registers; bf16 to smem)
-        wp.template wait<0>(bar_s_full, G & 1);
+      const int s = ss;
+      if (++ss == NS) ss = 0;
+      if ((c.u & 1) == g) {
+        const uint32_t ph = (c.u >> 1) & 1;
+        const int qb = c.qb();
+        const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
+        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
+        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= 32) || (p.dbg & 1);
+        // visible-column bitmask (used only when some row of the warp is partial)
+        const int lo = max(c_lo, 0), hi = min(c_hi, 32);
+        const uint32_t vis = hi <= lo ? 0u : ((hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u));
+        const float4* lse4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_LSE + s * Cfg::VEC) + c0 / 4;
+        const float4* dsum4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_DSUM + s * Cfg::VEC) + c0 / 4;
+        uint32_t pp[16];  // Pᵀ row chunk as bf16 pairs: written over S, kept for phase B
+        // ---- phase A: Sᵀ → Pᵀ (bf16 over the S columns)
+        wp.template wait<0>(&bar_s_full[g], ph);
+        trace(20 + g, c.u);  // S: s_full seen
         const long long ta = wp.now();
         tc_fence_after();
-        float pr[32];
-        {
+        if (!none) {
           uint32_t sa[32];
-          tmem_ld32(tmem + lane_off + Cfg::S_COL + c0, sa);
+          tmem_ld32(tmem + lane_off + Cfg::s_col(g) + c0, sa);
           tmem_wait_ld();
-          tc_fence_before();
-          mbar_arrive(bar_s_free);  // the MMA warp may overwrite S now
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
             const float4 l = lse4[j4];  // 128-bit broadcast load
-            const float lv[4] = {l.x, l.y, l.z, l.w};
+            float e[4];
+            e[0] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 0]), p.scale_log2, -l.x));
+            e[1] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 1]), p.scale_log2, -l.y));
+            e[2] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 2]), p.scale_log2, -l.z));
+            e[3] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 3]), p.scale_log2, -l.w));
+            if (!all_full) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = 4 * j4 + u;
-              const float e = ex2_approx(fmaf(__uint_as_float(sa[j]), p.scale_log2, -lv[u]));
-              pr[j] = (full || (j >= c_lo && j < c_hi)) ? e : 0.f;
+              for (int q = 0; q < 4; ++q) e[q] = (vis & (1u << (4 * j4 + q))) ? e[q] : 0.f;
             }
+            pp[2 * j4] = pack_bf16x2(e[0], e[1]);
+            pp[2 * j4 + 1] = pack_bf16x2(e[2], e[3]);
           }
-        }
-        if (G > 0) wp.template wait<2>(bar_pv_done, (G - 1) & 1);  // dV(G-1) has read the Pᵀ buffer
-        if (it == 0 && k > 0) named_bar_sync(6, 512);              // epilogue staging reads finished
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t w[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) w[u] = pack_bf16x2(pr[8 * j + 2 * u], pr[8 * j + 2 * u + 1]);
-          *reinterpret_cast<uint4*>(spt_row + ((((part & 1) * 4 + j) ^ (krow & 7)) * 16)) =
-              make_uint4(w[0], w[1], w[2], w[3]);
+          for (int j = 0; j < 16; ++j) pp[j] = 0u;
         }
-        fence_proxy_async_smem();
+        tmem_st16(tmem + lane_off + Cfg::s_col(g) + c0, pp);
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(&bar_pt_full[g]);
+        trace(22 + g, c.u);  // S: pt arrived
         wp.template add_since<4>(ta);
-        // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns
-        wp.template wait<1>(bar_dp_full, G & 1);
+        // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns (P as the dV GEMM saw it)
+        wp.template wait<1>(&bar_dp_full[g], ph);
+        trace(24 + g, c.u);  // S: dp_full seen
         const long long tb = wp.now();
         tc_fence_after();
-        {
+        uint32_t pk[16];
+        if (!none) {
           uint32_t dr[32];
-          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0, dr);
+          tmem_ld32(tmem + lane_off + Cfg::dp_col(g) + c0, dr);
           tmem_wait_ld();
-          uint32_t dk[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
             const float4 dd = dsum4[j4];  // 128-bit broadcast load
-            const int c = 4 * j4;
-            dk[2 * j4] = pack_bf16x2(pr[c] * (__uint_as_float(dr[c]) - dd.x), pr[c + 1] * (__uint_as_float(dr[c + 1]) - dd.y));
-            dk[2 * j4 + 1] =
-                pack_bf16x2(pr[c + 2] * (__uint_as_float(dr[c + 2]) - dd.z), pr[c + 3] * (__uint_as_float(dr[c + 3]) - dd.w));
+            const int q = 4 * j4;
+            const float p0 = __uint_as_float(pp[2 * j4] << 16), p1 = __uint_as_float(pp[2 * j4] & 0xFFFF0000u);
+            const float p2 = __uint_as_float(pp[2 * j4 + 1] << 16), p3 = __uint_as_float(pp[2 * j4 + 1] & 0xFFFF0000u);
+            pk[2 * j4] = pack_bf16x2(p0 * (__uint_as_float(dr[q]) - dd.x), p1 * (__uint_as_float(dr[q + 1]) - dd.y));
+            pk[2 * j4 + 1] =
+                pack_bf16x2(p2 * (__uint_as_float(dr[q + 2]) - dd.z), p3 * (__uint_as_float(dr[q + 3]) - dd.w));
           }
-          tmem_st16(tmem + lane_off + Cfg::DP_COL + c0, dk);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = 0u;
         }
+        tmem_st16(tmem + lane_off + Cfg::dp_col(g) + c0, pk);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(bar_p_full);
+        warp_arrive(&bar_ds_full[g]);
+        trace(26 + g, c.u);  // S: ds arrived
         wp.template add_since<5>(tb);
       }
-      // ---- item end: dK / dV epilogue — TMEM → registers → release TMEM → coalesced stores
-      //      through the (now idle) Pᵀ buffer
-      const long long te = wp.now();
-      wp.template wait<3>(bar_dkv_full, k & 1);
-      tc_fence_after();
-      uint32_t pv[HD / 8], pkk[HD / 8];
+      if (c.last()) {
+        // ---- item epilogue (all 16 warps): TMEM → registers → release TMEM → 16-B stores of
+        //      the thread's HD/4-column segment of its key's dV / dK rows
+        const long long te = wp.now();
+        trace(30 + (warp >> 3), c.u);  // E: epilogue entered
+        wp.template wait<3>(bar_dkv_full, c.k & 1);
+        trace(32 + (warp >> 3), c.u);  // E: dkv_full seen
+        tc_fence_after();
+        uint32_t pv[HD / 8], pkk[HD / 8];
 #pragma unroll
-      for (int c = 0; c < HD / 4; c += 32 > HD / 4 ? HD / 4 : 32) {
-        uint32_t v[32], kk[32];
-        tmem_ld32(tmem + lane_off + Cfg::DV_COL + part * (HD / 4) + c, v);
-        tmem_ld32(tmem + lane_off + Cfg::DK_COL + part * (HD / 4) + c, kk);
-        tmem_wait_ld();
+        for (int cc = 0; cc < HD / 4; cc += 32 > HD / 4 ? HD / 4 : 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lane_off + Cfg::DV_COL + part * (HD / 4) + cc, v);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < (HD / 4 < 32 ? HD / 8 : 16); ++j) {
-          pv[c / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-          pkk[c / 2 + j] = pack_bf16x2(__uint_as_float(kk[2 * j]) * p.scale, __uint_as_float(kk[2 * j + 1]) * p.scale);
+          for (int j = 0; j < (HD / 4 < 32 ? HD / 8 : 16); ++j)
+            pv[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+          tmem_ld32(tmem + lane_off + Cfg::DK_COL + part * (HD / 4) + cc, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < (HD / 4 < 32 ? HD / 8 : 16); ++j)
+            pkk[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]) * p.scale, __uint_as_float(v[2 * j + 1]) * p.scale);
         }
+        tc_fence_before();
+        warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
+        // registers → SW128 staging tile (conflict-free 16-B stores) → one TMA row store per
+        // (key, 64-column box), issued by the box's owner thread; dV first, then dK through the
+        // same 32 KB staging (the TMA engine, not the LSU, writes the scattered rows)
+        constexpr int CPT = HD / 32;  // 16-B chunks per thread (HD/4 columns)
+        uint8_t* stg = smem + Cfg::OFF_STG;
+        const bool issuer = part < HD / 64 && dst_key >= 0;
+        auto stage = [&](const uint32_t* w) {
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) {
+            const int cidx = part * CPT + j;  // 16-B chunk of the row
+            *reinterpret_cast<uint4*>(stg + (cidx >> 3) * 16384 + krow * 128 + (((cidx & 7) ^ (krow & 7)) << 4)) =
+                make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+          }
+          fence_proxy_async_smem();
+        };
+        bulk_wait_read0();  // this thread's previous stores have read the staging
+        named_bar_sync(5, 512);
+        stage(pv);
+        named_bar_sync(5, 512);
+        if (issuer) {
+          tma_store_2d(&tmdV, c.itm.kh * HD + part * 64, dst_key, stg + part * 16384 + krow * 128);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+        named_bar_sync(5, 512);
+        stage(pkk);
+        named_bar_sync(5, 512);
+        if (issuer) {
+          tma_store_2d(&tmdK, c.itm.kh * HD + part * 64, dst_key, stg + part * 16384 + krow * 128);
+          bulk_commit();
+        }
+        trace(34 + (warp >> 3), c.u);  // E: epilogue done
+        wp.template add_since<6>(te);
       }
-      tc_fence_before();
-      mbar_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
-      if (part == 0) rows[krow] = key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1;
-      named_bar_sync(5, 512);
-      uint8_t* stg = smem + Cfg::OFF_PT;
-      store_tile_coalesced<HD, 4>(stg, rows, pv, krow, part, tid, p.dv + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
-      store_tile_coalesced<HD, 4>(stg, rows, pkk, krow, part, tid, p.dk + itm.kh * HD, int64_t(p.Hkv) * HD, 5);
-      wp.template add_since<6>(te);
-      ++k;
     }
-    if (warp == 0 && lane == 0) wp.flush(p.prof + 16);
+    bulk_wait_all();  // dK / dV row stores of the last item
+    if (warp == 0 && lane == 0) wp.flush(p.prof + 16);  // 12 slots: 16..27
   }
   tc_fence_before();
   __syncthreads();
+  if (trb)  // copy CTA 0's event trace out
+    for (int i = tid; i < 4 * 4001; i += kDkvThreads) p.prof[64 + i] = trb[i];
   if (warp == 17) tmem_dealloc<512>(tmem);
 }
 
@@ -534,11 +628,11 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_s_full[s], 1);
-      mbar_init(&bar_p_full[s], 256);
+      mbar_init(&bar_p_full[s], 8);
     }
     mbar_init(bar_dp_full, 1);
     mbar_init(bar_dq_full, 1);
-    mbar_init(bar_dq_empty, 256);
+    mbar_init(bar_dq_empty, 8);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -702,7 +796,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bar_p_full[g & 1]);
+        warp_arrive(&bar_p_full[g & 1]);
       }
       // ---- item end: dQ = scale · acc → bf16 (half of the head dim per warp), coalesced store
       mbar_wait(bar_dq_full, k & 1);
@@ -718,7 +812,7 @@ __global__ void __launch_bounds__(320, 1)
           pq[c / 2 + t] = pack_bf16x2(__uint_as_float(v[2 * t]) * p.scale, __uint_as_float(v[2 * t + 1]) * p.scale);
       }
       tc_fence_before();
-      mbar_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
+      warp_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
       if (valid) {  // this thread's half row → staging → async bulk store
         uint8_t* stg_row = smem + Cfg::OFF_STG + r * (HD * 2) + half * HD;
         const int64_t dst = p.row_map ? int64_t(__ldg(p.row_map + row)) : int64_t(row);
@@ -781,6 +875,13 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   if (int rc = encode_tmap_2d(&tdo, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tk, a->k, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
+  CUtensorMap tdk1, tdv1;  // dK / dV row stores (1 row × 64 columns boxes, SW128)
+  if (int rc = encode_tmap_2d(&tdk1, g->dk, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 1, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&tdv1, g->dv, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 1, 64, true)) return rc;
+  CUtensorMap tq64, tdo64;  // 64-query tiles of the dK/dV kernel
+  if (int rc = encode_tmap_2d(&tq64, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 64, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&tdo64, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 64, 64, true))
+    return rc;
   BwdParams p;
   p.dq = static_cast<__nv_bfloat16*>(g->dq);
   p.dk = static_cast<__nv_bfloat16*>(g->dk);
@@ -799,20 +900,21 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.q_items = int((int64_t(T) + 127) / 128) * H;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;
+  p.dbg = getenv("VLASIM_DBG") ? atoi(getenv("VLASIM_DBG")) : 0;
   {
     using Cfg = DkvCfg<HD>;
     const int grid = std::min(p.kv_items, num_sms());
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
     auto kern = p.prof ? k_bwd_dkdv<HD, true> : k_bwd_dkdv<HD, false>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tq64, tk, tv, tdo64, tdk1, tdv1, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,
-                  {"prod:q_empty", "prod:kv_empty", "prod:do_empty", "", "", "", "", "prod:total", "mma:kv_full",
-                   "mma:q_full", "mma:do_full", "mma:p_full", "mma:dkv_empty", "mma:s_free", "", "mma:total",
-                   "smx:s_full", "smx:dp_full", "smx:pv_done", "smx:dkv_full", "smx:phaseA", "smx:phaseB",
-                   "smx:epilogue", "smx:total"});
+                  {"prod:qd_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:kv_full",
+                   "mma:qd_full", "", "mma:pt_full", "mma:dkv_empty", "mma:ds_full", "", "mma:total",
+                   "smx:s_full", "smx:dp_full", "", "smx:dkv_full", "smx:phaseA", "smx:phaseB", "smx:epilogue", "",
+                   "", "", "", "smx:total"});
   }
   {
     constexpr int ST = HD == 64 ? 4 : 2;

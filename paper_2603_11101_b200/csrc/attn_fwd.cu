@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
-      mbar_init(&bar_p_full[b], 128);
+      mbar_init(&bar_p_full[b], 4);
     }
     mbar_init(&bar_o_ready, 1);
     s_kv_lo = INT_MAX;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(192, 1)
       l_run += ls;
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bar_p_full[sb]);
+      warp_arrive(&bar_p_full[sb]);
     }
     // ------------------------------------------------ epilogue: O / l → bf16, LSE
     if (nkv > 0) {

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&bar_q_full[s], 1);
       mbar_init(&bar_q_empty[s], 1);
       mbar_init(&bar_s_full[s], 1);
-      mbar_init(&bar_p_full[s], 256);
+      mbar_init(&bar_p_full[s], 8);
     }
     if (smem_u32(smem) & 1023) __trap();  // swizzle atoms need 1 KB alignment
     for (int s = 0; s < KS; ++s) {
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_o_full[s], 1);
-      mbar_init(&bar_o_empty[s], 256);
+      mbar_init(&bar_o_empty[s], 8);
     }
     mbar_init(bar_o_ready, 1);
     fence_barrier_init();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bar_o_empty[ek & 1]);
+      warp_arrive(&bar_o_empty[ek & 1]);
       if (valid && half == 0)
         p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
       ek = -1;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(320, 1)
         l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bar_p_full[g & 1]);
+        warp_arrive(&bar_p_full[g & 1]);
         if (j == 0 && ek >= 0) epilogue();  // previous item, now that this tile is in flight
       }
       // combine the halves' row sums and defer this item's epilogue

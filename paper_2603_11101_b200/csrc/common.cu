@@ -1,7 +1,9 @@
 // common.cu — error state, tensor-map encoding, device queries, version/selftest exports.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "common.hpp"
 
@@ -69,11 +71,14 @@ bool prof_enabled() {
   return on;
 }
 
+// [0, 64) wait counters, [64, 64 + kTraceWords) event trace (trace_evt, sm100.cuh)
+static constexpr size_t kTraceWords = 4 * 4001;  // 4 roles × (count + 4000 events), TraceCtr
 static unsigned long long* g_prof = nullptr;
 static unsigned long long* prof_buffer_peek() { return g_prof; }
 unsigned long long* prof_buffer() {
-  if (!g_prof) cudaMalloc(&g_prof, 64 * sizeof(unsigned long long));
-  cudaMemset(g_prof, 0, 64 * sizeof(unsigned long long));
+  const size_t bytes = (64 + kTraceWords) * sizeof(unsigned long long);
+  if (!g_prof) cudaMalloc(&g_prof, bytes);
+  cudaMemset(g_prof, 0, bytes);
   return g_prof;
 }
 
@@ -92,6 +97,22 @@ int prof_report(const char* kernel, int grid, cudaStream_t st, std::initializer_
     ++i;
   }
   fprintf(stderr, "%s\n", line.c_str());
+  if (const char* path = getenv("VLASIM_TRACE")) {  // dump the CTA-0 event trace (binary, appended)
+    std::vector<unsigned long long> tr(kTraceWords);
+    VLASIM_CUDA_TRY(cudaMemcpy(tr.data(), prof_buffer_peek() + 64, tr.size() * 8, cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(path, "ab")) {
+      for (int r = 0; r < 4; ++r) {
+        const unsigned long long* b = tr.data() + r * 4001;
+        const unsigned long long n = std::min<unsigned long long>(b[0], 4000);
+        char tag[32] = {0};
+        snprintf(tag, sizeof(tag), "%s", kernel);
+        fwrite(tag, 1, 32, f);
+        fwrite(&n, 8, 1, f);
+        fwrite(b + 1, 8, n, f);
+      }
+      fclose(f);
+    }
+  }
   return VLASIM_OK;
 }
 

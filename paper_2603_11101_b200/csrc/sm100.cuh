@@ -30,6 +30,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// One arrival per warp (lane 0, after the warp has converged): barriers that consumer warps
+// release are initialised with a count of warps, not threads — 32× fewer serialised smem
+// atomics per hand-off.  Callers issue their tcgen05 fences before this.
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -70,6 +77,13 @@ __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const CUtensorM
       "%3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// 2-D tiled store: smem box → global at element coords (c0 = inner, c1 = row); bulk-group tracked.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, int32_t c0, int32_t c1, const void* smem_src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
+               : "memory");
 }
 // 1-D bulk copy global → smem (16-B aligned src/dst, size multiple of 16), completes tx on bar.
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -214,6 +228,19 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t lb
   d |= 2ull << 61;
   return d;
 }
+// Descriptor of the same layout `bytes` further on (the start address field holds addr >> 4 in
+// 14 bits; smem addresses < 256 KB never carry out of it).
+__device__ __forceinline__ uint64_t sdesc_add(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+// One elected lane of a converged warp (elect.sync).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 // Instruction descriptor, kind::f16, bf16 × bf16 → f32.
 //  [4,6) c_format (1=F32)  [7,10) a_format (1=BF16)  [10,13) b_format (1=BF16)
 //  [15] a_major (1=MN)  [16] b_major (1=MN)  [17,23) N>>3  [24,29) M>>4
@@ -249,6 +276,20 @@ __device__ __forceinline__ void red_add_v4_f32(float* gaddr, float a, float b, f
 // Per-role wait-time accounting, compiled in only for the PROF kernel instantiations:
 // accumulates clock64 cycles spent in each mbarrier wait category and flushes them to a global
 // counter array (one warp-lane per role) at kernel exit.
+// Event trace (timing experiments): each role appends (clock << 32 | code << 16 | unit) words to
+// its own shared-memory region ([0] = count) — one STS per event; the kernel copies the regions
+// of CTA 0 to global memory at exit (trace_flush).  Disabled when base is null.
+struct TraceCtr {
+  unsigned long long* base;
+  uint32_t n;
+  __device__ __forceinline__ explicit TraceCtr(unsigned long long* b) : base(b), n(0) {}
+  __device__ __forceinline__ void operator()(uint32_t code, uint32_t unit) {
+    if (base == nullptr || n >= 4000) return;
+    base[1 + n] = (static_cast<unsigned long long>(clock()) << 32) | (code << 16) | (unit & 0xFFFFu);
+    base[0] = ++n;
+  }
+};
+
 template <bool ON, int N = 8>
 struct WaitProf {
   unsigned long long acc[N];

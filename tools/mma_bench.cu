@@ -1,0 +1,99 @@
+// Tensor-pipe microbenchmark: back-to-back tcgen05.mma of one shape/mode, 1 CTA per SM.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2603_11101_b200/csrc tools/mma_bench.cu -o tools/mma_bench
+#include <cstdio>
+#include "sm100.cuh"
+using namespace vlasim_dev;
+
+// mode 0: SS 128x64 K-major   1: SS 128x128 K-major   2: TS 128x128 B MN-major   3: TS 128x64 B MN-major
+// 4: SS 128x256 K-major
+// LDW warps (1..LDW) hammer tcgen05.ld on TMEM columns [0,128) while warp 0 issues MMAs
+// (MMAs write columns [256, 512); TS modes read A from columns [0, 32)).
+template <int MODE, int LDW = 0>
+__global__ void __launch_bounds__(576, 1) k_mma(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    const uint64_t da = make_sdesc_sw128(smem_u32(smem), 16, 1024);
+    const uint64_t db = make_sdesc_sw128(smem_u32(smem + 32768), 16, 1024);
+    const uint64_t dbm = make_sdesc_sw128(smem_u32(smem + 32768), 8192, 1024);
+    constexpr uint32_t N = MODE == 0 || MODE == 3 ? 64 : (MODE == 4 ? 256 : 128);
+    constexpr uint32_t id = make_idesc_bf16(128, N, false, MODE == 2 || MODE == 3);
+    const long long t0 = clock64();
+    if (elect_one()) {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (MODE == 0 || MODE == 1 || MODE == 4)
+            umma_f16_ss(tmem + 256 * (MODE == 4 ? 0 : (it & 1)), sdesc_add(da, (j % 4) * 32), sdesc_add(db, (j % 4) * 32), id, 1);
+          else
+            umma_f16_ts(tmem + 256 + 128 * (it & 1), tmem + (j & 3) * 8, sdesc_add(dbm, (j & 3) * 2048), id, 1);
+        }
+      }
+      umma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(&slot + 0) = slot;  // keep
+  } else if (warp <= LDW) {
+    // load traffic until warp 0 is done (bounded iterations)
+    uint32_t acc = 0;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    for (int it = 0; it < iters * 2; ++it) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_off + ((it * 32) & 127), r);
+      tmem_wait_ld();
+      acc += r[0] ^ r[31];
+    }
+    if (acc == 0x12345678u) out[1000] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <int MODE, int LDW = 0>
+void run(int blocks, const char* name, double flop_per_instr) {
+  unsigned long long* d;
+  cudaMalloc(&d, 2048 * 8);
+  const int iters = 2000;
+  cudaFuncSetAttribute(k_mma<MODE, LDW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  k_mma<MODE, LDW><<<blocks, 32 * (LDW + 1), 65536>>>(10, d);
+  k_mma<MODE, LDW><<<blocks, 32 * (LDW + 1), 65536>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[256];
+  cudaMemcpy(h, d, blocks * 8, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < blocks; ++i) avg += h[i];
+  avg /= blocks;
+  printf("%-28s ldw=%2d blocks=%3d  %.1f cycles/instr  %.0f flop/clk/SM  (%s)\n", name, LDW, blocks, avg / (iters * 8.0),
+         flop_per_instr * iters * 8 / avg, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+int main() {
+  run<2, 4>(1, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);
+  run<2, 8>(1, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);
+  run<2, 16>(1, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);
+  run<1, 16>(1, "SS 128x128x16 K-major", 2.0 * 128 * 128 * 16);
+  run<0, 16>(1, "SS 128x64x16 K-major", 2.0 * 128 * 64 * 16);
+  for (int b : {1}) {
+    run<0>(b, "SS 128x64x16 K-major", 2.0 * 128 * 64 * 16);
+    run<1>(b, "SS 128x128x16 K-major", 2.0 * 128 * 128 * 16);
+    run<4>(b, "SS 128x256x16 K-major", 2.0 * 128 * 256 * 16);
+    run<2>(b, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);
+    run<3>(b, "TS 128x64x16 B MN-major", 2.0 * 128 * 64 * 16);
+  }
+  return 0;
+}

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // event trace (PROF builds with VLASIM_DBG & 2: the idle Q stages hold 4 × 4001 words)
+  // event trace (PROF builds with VLASIM_DBG & 2: the idle Q/dO stages hold 4 × 2001 words)
   unsigned long long* const trb =
       PROF && (p.dbg & 2) && blockIdx.x == 0 ? reinterpret_cast<unsigned long long*>(smem + Cfg::OFF_Q) : nullptr;
   const int group = p.H / p.Hkv;
@@ -287,14 +287,16 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     // ================================================ MMA issuer (whole warp, so descriptors and
     // counters stay in uniform registers; one elected lane issues).  Per unit u, in issue order:
     //   dV(u) · S(u+2) | dK(u) · dP(u+2)   — two issue blocks, three barrier waits.
-    // The warp's serial instruction latency is the budget here (≈6 cycles per instruction on
-    // a single warp), so stages and parities are counters, never u % NS.
+    // Look-ahead S/dP stay inside the current item: the next item's first units are issued only
+    // after the current item's last dK and its dkv_full commit, so the epilogue never waits
+    // behind the next item's K/V load (single K/V buffer).  The warp's serial instruction
+    // latency is the budget here, so stages and parities are counters, never u % NS.
     {
       constexpr uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // Sᵀ, dPᵀ
       constexpr uint32_t id_acc = make_idesc_bf16(128, HD, false, true);  // dV, dK
       constexpr uint32_t QT16 = Cfg::QT >> 4;                             // stage stride, desc units
       WaitProf<PROF> wp;
-      TraceCtr trace(lane == 0 && trb ? trb + 4001 : nullptr);
+      TraceCtr trace(lane == 0 && trb ? trb + 2001 : nullptr);
       const uint64_t dK0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16, 1024);
       const uint64_t dV0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), 16, 1024);
       const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);     // K-major view
@@ -304,41 +306,44 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       auto mma_S = [&](uint32_t col, uint32_t soff) {
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j)
-          if (!(p.dbg & 4)) umma_f16_ss(tmem + col, sdesc_add(dK0, (j / 4) * 16384 + (j % 4) * 32),
+          umma_f16_ss(tmem + col, sdesc_add(dK0, (j / 4) * 16384 + (j % 4) * 32),
                       sdesc_add(dQk, (j / 4) * 8192 + (j % 4) * 32) + soff, id_s, j > 0);
       };
       auto mma_dP = [&](uint32_t col, uint32_t soff) {
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j)
-          if (!(p.dbg & 4)) umma_f16_ss(tmem + col, sdesc_add(dV0, (j / 4) * 16384 + (j % 4) * 32),
+          umma_f16_ss(tmem + col, sdesc_add(dV0, (j / 4) * 16384 + (j % 4) * 32),
                       sdesc_add(dOk, (j / 4) * 8192 + (j % 4) * 32) + soff, id_s, j > 0);
       };
       UnitCursor ca, cc;
       uint32_t as = 0, aph = 0;  // stage / parity of the look-ahead unit ca.u
-      bool va = ca.start(p);
-      // prologue: S and dP of units 0 and 1
-      for (int n = 0; n < 2 && va; ++n) {
+      bool va = false;
+      auto adv_a = [&] {
+        va = ca.next(p);
+        if (++as == NS) { as = 0; aph ^= 1; }
+      };
+      auto issue_SdP = [&] {  // S and dP of unit ca.u (both buffers of its parity are free)
         if (ca.it == 0) wp.template wait<0>(bar_kv_full, ca.k & 1);
         wp.template wait<1>(&bar_qd_full[as], aph);
         tc_fence_after();
+        const uint32_t bb = ca.u & 1;
         if (elect_one()) {
-          mma_S(Cfg::s_col(n), as * QT16);
-          (p.dbg & 32) ? mbar_arrive(&bar_s_full[n]) : umma_commit(&bar_s_full[n]);
-          mma_dP(Cfg::dp_col(n), as * QT16);
-          (p.dbg & 32) ? mbar_arrive(&bar_dp_full[n]) : umma_commit(&bar_dp_full[n]);
-          if (ca.last()) (p.dbg & 32) ? mbar_arrive(bar_kv_empty) : umma_commit(bar_kv_empty);
+          mma_S(Cfg::s_col(bb), as * QT16);
+          umma_commit(&bar_s_full[bb]);
+          mma_dP(Cfg::dp_col(bb), as * QT16);
+          umma_commit(&bar_dp_full[bb]);
+          if (ca.last()) umma_commit(bar_kv_empty);  // the item's last readers of K and V
         }
         __syncwarp();
-        va = ca.next(p);
-        if (++as == NS) { as = 0; aph ^= 1; }
-      }
+        adv_a();
+      };
+      va = ca.start(p);
+      while (va && ca.k == 0 && ca.u < 2) issue_SdP();  // prologue: first item only
       uint32_t cs = 0, b = 0, ph = 0;  // stage of cc.u; TMEM buffer cc.u & 1; its use parity
       for (bool vc = cc.start(p); vc; vc = cc.next(p)) {
         const uint32_t coff = cs * QT16, aoff = as * QT16;
-        if (va) {
-          if (ca.it == 0) wp.template wait<0>(bar_kv_full, ca.k & 1);
-          wp.template wait<1>(&bar_qd_full[as], aph);
-        }
+        const bool early = va && ca.u == cc.u + 2 && ca.k == cc.k;  // S(u+2) after dV(u), dP(u+2) after dK(u)
+        if (early) wp.template wait<1>(&bar_qd_full[as], aph);
         wp.template wait<3>(&bar_pt_full[b], ph);
         trace(10, cc.u);  // M: pt_full seen
         if (cc.it == 0 && cc.k > 0) wp.template wait<4>(bar_dkv_empty, (cc.k - 1) & 1);
@@ -348,11 +353,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (!(p.dbg & 4)) umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+            umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + (j >> 1) * 32 + (j & 1) * 8,
                         sdesc_add(dOm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
-          if (va) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
+          if (early) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
             mma_S(Cfg::s_col(b), aoff);
-            (p.dbg & 32) ? mbar_arrive(&bar_s_full[b]) : umma_commit(&bar_s_full[b]);
+            umma_commit(&bar_s_full[b]);
           }
         }
         __syncwarp();
@@ -364,22 +369,22 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (!(p.dbg & 4)) umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
                         sdesc_add(dQm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
-          (p.dbg & 32) ? mbar_arrive(&bar_qd_empty[cs]) : umma_commit(&bar_qd_empty[cs]);
-          if (cc.last()) (p.dbg & 32) ? mbar_arrive(bar_dkv_full) : umma_commit(bar_dkv_full);
-          if (va) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
+          umma_commit(&bar_qd_empty[cs]);
+          if (cc.last()) umma_commit(bar_dkv_full);
+          if (early) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
             mma_dP(Cfg::dp_col(b), aoff);
-            (p.dbg & 32) ? mbar_arrive(&bar_dp_full[b]) : umma_commit(&bar_dp_full[b]);
-            if (ca.last()) (p.dbg & 32) ? mbar_arrive(bar_kv_empty) : umma_commit(bar_kv_empty);  // the item's last readers of K and V
+            umma_commit(&bar_dp_full[b]);
+            if (ca.last()) umma_commit(bar_kv_empty);
           }
         }
         __syncwarp();
         trace(13, cc.u);  // M: dK + dP(u+2) issued
-        if (va) {
-          va = ca.next(p);
-          if (++as == NS) { as = 0; aph ^= 1; }
-        }
+        if (early) adv_a();
+        // item boundary: the next item's first units (their buffers' previous readers, the dV /
+        // dK of units ≤ u, are issued)
+        while (va && ca.u <= cc.u + 2 && (ca.k == cc.k || (cc.last() && ca.k == cc.k + 1))) issue_SdP();
         if (++cs == NS) cs = 0;
         b ^= 1;
         ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     const int krow = quad * 32 + lane;
     const int c0 = (part & 1) * 32;
     WaitProf<PROF, 12> wp;
-    TraceCtr trace(lane == 0 && (warp & 7) == 0 && trb ? trb + 4001 * (2 + (warp >> 3)) : nullptr);
+    TraceCtr trace(lane == 0 && (warp & 7) == 0 && trb ? trb + 2001 * (2 + (warp >> 3)) : nullptr);
     UnitCursor c;
     auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
     auto dst_of = [&](int key) { return key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1; };
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const int qb = c.qb();
         const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
         const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
-        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= 32) || (p.dbg & 1);
+        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= 32);
         // visible-column bitmask (used only when some row of the warp is partial)
         const int lo = max(c_lo, 0), hi = min(c_hi, 32);
         const uint32_t vis = hi <= lo ? 0u : ((hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u));
@@ -516,8 +521,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_before();
         warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
         // registers → SW128 staging tile (conflict-free 16-B stores) → one TMA row store per
-        // (key, 64-column box), issued by the box's owner thread; dV first, then dK through the
-        // same 32 KB staging (the TMA engine, not the LSU, writes the scattered rows)
+        // (key, 64-column box), issued by the box's owner thread (256 issuers); dV first, then dK
+        // through the same 32 KB staging.  The TMA engine, not the LSU, writes the scattered rows.
         constexpr int CPT = HD / 32;  // 16-B chunks per thread (HD/4 columns)
         uint8_t* stg = smem + Cfg::OFF_STG;
         const bool issuer = part < HD / 64 && dst_key >= 0;
@@ -530,16 +535,19 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           }
           fence_proxy_async_smem();
         };
+        trace(50, c.u);  // E: TMEM drained
         bulk_wait_read0();  // this thread's previous stores have read the staging
         named_bar_sync(5, 512);
         stage(pv);
         named_bar_sync(5, 512);
+        trace(51, c.u);  // E: dV staged
         if (issuer) {
           tma_store_2d(&tmdV, c.itm.kh * HD + part * 64, dst_key, stg + part * 16384 + krow * 128);
           bulk_commit();
           bulk_wait_read0();
         }
         named_bar_sync(5, 512);
+        trace(52, c.u);  // E: dV read by the TMA
         stage(pkk);
         named_bar_sync(5, 512);
         if (issuer) {
@@ -556,7 +564,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (trb)  // copy CTA 0's event trace out
-    for (int i = tid; i < 4 * 4001; i += kDkvThreads) p.prof[64 + i] = trb[i];
+    for (int i = tid; i < 4 * 2001; i += kDkvThreads) p.prof[64 + i] = trb[i];
   if (warp == 17) tmem_dealloc<512>(tmem);
 }
 

@@ -72,7 +72,7 @@ bool prof_enabled() {
 }
 
 // [0, 64) wait counters, [64, 64 + kTraceWords) event trace (trace_evt, sm100.cuh)
-static constexpr size_t kTraceWords = 4 * 4001;  // 4 roles × (count + 4000 events), TraceCtr
+static constexpr size_t kTraceWords = 4 * 2001;  // 4 roles × (count + 2000 events), TraceCtr
 static unsigned long long* g_prof = nullptr;
 static unsigned long long* prof_buffer_peek() { return g_prof; }
 unsigned long long* prof_buffer() {
@@ -102,8 +102,8 @@ int prof_report(const char* kernel, int grid, cudaStream_t st, std::initializer_
     VLASIM_CUDA_TRY(cudaMemcpy(tr.data(), prof_buffer_peek() + 64, tr.size() * 8, cudaMemcpyDeviceToHost));
     if (FILE* f = fopen(path, "ab")) {
       for (int r = 0; r < 4; ++r) {
-        const unsigned long long* b = tr.data() + r * 4001;
-        const unsigned long long n = std::min<unsigned long long>(b[0], 4000);
+        const unsigned long long* b = tr.data() + r * 2001;
+        const unsigned long long n = std::min<unsigned long long>(b[0], 2000);
         char tag[32] = {0};
         snprintf(tag, sizeof(tag), "%s", kernel);
         fwrite(tag, 1, 32, f);

@@ -276,7 +276,7 @@ __device__ __forceinline__ void red_add_v4_f32(float* gaddr, float a, float b, f
 // Per-role wait-time accounting, compiled in only for the PROF kernel instantiations:
 // accumulates clock64 cycles spent in each mbarrier wait category and flushes them to a global
 // counter array (one warp-lane per role) at kernel exit.
-// Event trace (timing experiments): each role appends (clock << 32 | code << 16 | unit) words to
+// Event trace (timing experiments; ≤ 2000 events per role): each role appends (clock << 32 | code << 16 | unit) words to
 // its own shared-memory region ([0] = count) — one STS per event; the kernel copies the regions
 // of CTA 0 to global memory at exit (trace_flush).  Disabled when base is null.
 struct TraceCtr {
@@ -284,7 +284,7 @@ struct TraceCtr {
   uint32_t n;
   __device__ __forceinline__ explicit TraceCtr(unsigned long long* b) : base(b), n(0) {}
   __device__ __forceinline__ void operator()(uint32_t code, uint32_t unit) {
-    if (base == nullptr || n >= 4000) return;
+    if (base == nullptr || n >= 2000) return;
     base[1 + n] = (static_cast<unsigned long long>(clock()) << 32) | (code << 16) | (unit & 0xFFFFu);
     base[0] = ++n;
   }

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(576, 1) k_seq(int iters, int alias, int commit
     const int phases = commits ? iters + 1 : 1;
     mbar_wait(&bar[0], (phases - 1) & 1);
     const long long t1 = clock64();
-    if (threadIdx.x == 0) out[0] = t1 - t0;
+    if (threadIdx.x == 0) atomicMax(&out[0], (unsigned long long)(t1 - t0));
     if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(smem + 131068) = 1;  // stop flag
   } else if (warp == 1 && variant == 11) {
     // TMA-like load traffic: 32 KB bulk copies global → smem [131072, 196608) back to back
@@ -130,17 +130,18 @@ int main() {
       {1, 1, 0, "kernel scheme (alias, commits)"}, {1, 0, 0, "alias, no commits"},
       {0, 1, 0, "disjoint cols, commits"}, {0, 0, 0, "disjoint, no commits"},
       {1, 1, 10, "kernel scheme + 16 exp-busy warps"}, {1, 1, 11, "kernel scheme + TMA load warp"}};
+  for (int blocks : {1, 148})
   for (int thr : {64, 64 + 512}) {
     for (auto& c : cases) {
       cudaMemset(d, 0, 64);
-      k_seq<<<1, thr, 196608>>>(10, c.alias, c.commits, c.variant, d, g);
+      k_seq<<<blocks, thr, 196608>>>(10, c.alias, c.commits, c.variant, d, g);
       cudaMemset(d, 0, 64);
-      k_seq<<<1, thr, 196608>>>(iters, c.alias, c.commits, c.variant, d, g);
+      k_seq<<<blocks, thr, 196608>>>(iters, c.alias, c.commits, c.variant, d, g);
       cudaError_t e = cudaDeviceSynchronize();
       unsigned long long h[8];
       cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
       if (c.variant == 11) printf("   TMA loads of 32 KB: %llu\n", h[6]);
-      printf("ldst warps %2d  %-40s %.0f cycles/unit (model 1280)  ld+st iters %llu avg %.0f cyc  %s\n", (thr - 64) / 32,
+      printf("blocks %3d ldst warps %2d  %-40s %.0f cycles/unit (model 1280)  ld+st iters %llu avg %.0f cyc  %s\n", blocks, (thr - 64) / 32,
              c.name, double(h[0]) / iters, h[1], h[1] ? double(h[2]) / h[1] : 0.0, cudaGetErrorString(e));
     }
   }

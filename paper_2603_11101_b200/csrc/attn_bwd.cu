@@ -98,7 +98,7 @@ struct BwdParams {
   int64_t vec_copy;  // element stride between the 4 shifted copies of lse2 / dsum
   float scale_log2, scale;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
-  int dbg;                   // VLASIM_DBG ablations (timing experiments only; results invalid if ≠ 0)
+  int dbg;                   // VLASIM_DBG ablations, honoured by the PROF instantiation only (timing experiments)
 };
 
 // ================================================================== dK / dV (KV-stationary)
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const int64_t vo = sh * p.vec_copy + int64_t(h) * p.Tp + qb + sh;
         if (c.u >= NS) wp.template wait<0>(&bar_qd_empty[s], ph ^ 1);
         trace(1, c.u);  // P: Q/dO load issued
-        if (p.dbg & 2) {  // timing experiment: no Q/dO traffic (the trace lives in the Q stages)
+        if (PROF && (p.dbg & 2)) {  // timing experiment: no Q/dO traffic (the trace lives in the Q stages)
           mbar_arrive(&bar_qd_full[s]);
         } else {
           mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + 512);
@@ -340,15 +340,17 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       va = ca.start(p);
       while (va && ca.k == 0 && ca.u < 2) issue_SdP();  // prologue: first item only
       uint32_t cs = 0, b = 0, ph = 0;  // stage of cc.u; TMEM buffer cc.u & 1; its use parity
-      for (bool vc = cc.start(p); vc; vc = cc.next(p)) {
+      bool vc = cc.start(p);
+      while (vc) {
         const uint32_t coff = cs * QT16, aoff = as * QT16;
         const bool early = va && ca.u == cc.u + 2 && ca.k == cc.k;  // S(u+2) after dV(u), dP(u+2) after dK(u)
+        const bool a_last = ca.last(), c_last = cc.last();
+        const uint32_t acc0 = cc.it > 0 ? 1u : 0u;
         if (early) wp.template wait<1>(&bar_qd_full[as], aph);
         wp.template wait<3>(&bar_pt_full[b], ph);
         trace(10, cc.u);  // M: pt_full seen
         if (cc.it == 0 && cc.k > 0) wp.template wait<4>(bar_dkv_empty, (cc.k - 1) & 1);
         tc_fence_after();
-        const uint32_t acc0 = cc.it > 0 ? 1u : 0u;
         if (elect_one()) {
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
 #pragma unroll
@@ -362,32 +364,36 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         }
         __syncwarp();
         trace(11, cc.u);  // M: dV + S(u+2) issued
-        wp.template wait<5>(&bar_ds_full[b], ph);
-        trace(12, cc.u);  // M: ds_full seen
+        // bookkeeping for the next unit while phase B of this one runs
+        const uint32_t cs_u = cs, b_u = b, ph_u = ph;
+        const UnitCursor cu = cc;
+        vc = cc.next(p);
+        if (++cs == NS) cs = 0;
+        b ^= 1;
+        ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
+        if (early) adv_a();
+        wp.template wait<5>(&bar_ds_full[b_u], ph_u);
+        trace(12, cu.u);  // M: ds_full seen
         tc_fence_after();
         if (elect_one()) {
           // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b_u) + (j >> 1) * 32 + (j & 1) * 8,
                         sdesc_add(dQm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
-          umma_commit(&bar_qd_empty[cs]);
-          if (cc.last()) umma_commit(bar_dkv_full);
+          umma_commit(&bar_qd_empty[cs_u]);
+          if (c_last) umma_commit(bar_dkv_full);
           if (early) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
-            mma_dP(Cfg::dp_col(b), aoff);
-            umma_commit(&bar_dp_full[b]);
-            if (ca.last()) umma_commit(bar_kv_empty);
+            mma_dP(Cfg::dp_col(b_u), aoff);
+            umma_commit(&bar_dp_full[b_u]);
+            if (a_last) umma_commit(bar_kv_empty);
           }
         }
         __syncwarp();
-        trace(13, cc.u);  // M: dK + dP(u+2) issued
-        if (early) adv_a();
+        trace(13, cu.u);  // M: dK + dP(u+2) issued
         // item boundary: the next item's first units (their buffers' previous readers, the dV /
         // dK of units ≤ u, are issued)
-        while (va && ca.u <= cc.u + 2 && (ca.k == cc.k || (cc.last() && ca.k == cc.k + 1))) issue_SdP();
-        if (++cs == NS) cs = 0;
-        b ^= 1;
-        ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
+        while (va && ca.u <= cu.u + 2 && (ca.k == cu.k || (c_last && ca.k == cu.k + 1))) issue_SdP();
       }
       if (lane == 0) wp.flush(p.prof + 8);
     }
@@ -423,7 +429,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const int qb = c.qb();
         const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
         const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
-        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= 32);
+        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= 32) || (PROF && (p.dbg & 1));  // ablation
         // visible-column bitmask (used only when some row of the warp is partial)
         const int lo = max(c_lo, 0), hi = min(c_hi, 32);
         const uint32_t vis = hi <= lo ? 0u : ((hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u));
@@ -681,60 +687,82 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 9) {
-    // ================================================ MMA issuer
-    if (lane == 0) {
+    // ================================================ MMA issuer (whole warp; one elected lane
+    // issues).  Per key tile g: S(g) · [dQ(g−1) after its dS] · dP(g).  At an item boundary the
+    // previous item's last dQ is issued before waiting for the next item's Q/dO, so dq_full —
+    // and the epilogue — never wait behind that load.
+    {
       constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // S, dP
       constexpr uint32_t id_dq = make_idesc_bf16(128, HD, false, true);    // dQ (A from TMEM, B MN-major)
-      const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q), sdO = smem_u32(smem + Cfg::OFF_DO);
+      constexpr uint32_t KV16 = (2 * Cfg::TILE) >> 4;                      // K/V stage stride, desc units
+      const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
+      const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
+      const uint64_t dKk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_KV), 16, 1024);
+      const uint64_t dVk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_KV + Cfg::TILE), 16, 1024);
+      const uint64_t dKm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_KV), 16384, 1024);  // MN-major view
       int g = 0, k = 0;
-      int pj = -1, pg = 0;  // pending dQ MMA of tile pg (local index pj)
-      bool plast = false;
+      int st = 0;           // K/V stage of tile g
+      uint32_t kvph = 0;    // its use parity
+      bool pend = false;    // dQ of the previous tile not issued yet
+      bool plast = false, pfirst = false;
+      int pst = 0, pg = 0;  // its stage and tile ordinal
       auto do_dq = [&]() {
         mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + Cfg::OFF_KV + (pg % STAGES) * 2 * Cfg::TILE);
-        const uint32_t a = tmem + Cfg::s_col(pg);
+        if (elect_one()) {
+          const uint32_t a = tmem + Cfg::s_col(pg);
 #pragma unroll
-        for (int s = 0; s < 8; ++s)  // dS: keys 0-63 at +0..31, 64-127 at +64..95
-          umma_f16_ts(tmem + Cfg::DQ_COL, a + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
-                      make_sdesc_sw128(sK + s * 2048, 16384, 1024), id_dq, (pj > 0 || s > 0) ? 1u : 0u);
-        umma_commit(&bar_kv_empty[pg % STAGES]);
-        if (plast) umma_commit(bar_dq_full);
+          for (int s = 0; s < 8; ++s)  // dS: keys 0-63 at +0..31, 64-127 at +64..95
+            umma_f16_ts(tmem + Cfg::DQ_COL, a + (s < 4 ? s * 8 : 64 + (s - 4) * 8), sdesc_add(dKm, s * 2048) + pst * KV16,
+                        id_dq, (!pfirst || s > 0) ? 1u : 0u);
+          umma_commit(&bar_kv_empty[pst]);
+          if (plast) umma_commit(bar_dq_full);
+        }
+        __syncwarp();
+        pend = false;
       };
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
         const QItem itm = nxt;
         if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
+        if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
         mbar_wait(bar_qdo_full, k & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int st = g % STAGES;
-          mbar_wait(&bar_kv_full[st], (g / STAGES) & 1);
+          mbar_wait(&bar_kv_full[st], kvph);
           tc_fence_after();
-          const uint32_t sK = smem_u32(smem + Cfg::OFF_KV + st * 2 * Cfg::TILE);
-          const uint32_t sV = sK + Cfg::TILE;
           // S_g = Q·K_gᵀ into S buffer g%2 (its previous dS was consumed by dQ_{g-2}: issue order)
+          if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < HD / 16; ++s)
-            umma_f16_ss(tmem + Cfg::s_col(g), make_sdesc_sw128(sQ + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
-                        make_sdesc_sw128(sK + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
-          umma_commit(&bar_s_full[g & 1]);
+            for (int s = 0; s < HD / 16; ++s)
+              umma_f16_ss(tmem + Cfg::s_col(g), sdesc_add(dQk, (s / 4) * 16384 + (s % 4) * 32),
+                          sdesc_add(dKk, (s / 4) * 16384 + (s % 4) * 32) + st * KV16, id_kk, s > 0);
+            umma_commit(&bar_s_full[g & 1]);
+          }
+          __syncwarp();
           // dQ of the previous tile (needs its dS), then dP_g over the dP columns it freed
-          if (pj >= 0) do_dq();
+          if (pend) do_dq();
           if (j == 0 && k > 0) mbar_wait(bar_dq_empty, (k - 1) & 1);  // previous item's dQ drained
+          tc_fence_after();
+          if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < HD / 16; ++s)
-            umma_f16_ss(tmem + Cfg::DP_COL, make_sdesc_sw128(sdO + (s / 4) * 16384 + (s % 4) * 32, 16, 1024),
-                        make_sdesc_sw128(sV + (s / 4) * 16384 + (s % 4) * 32, 16, 1024), id_kk, s > 0);
-          umma_commit(bar_dp_full);
-          if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
-          pj = j;
+            for (int s = 0; s < HD / 16; ++s)
+              umma_f16_ss(tmem + Cfg::DP_COL, sdesc_add(dOk, (s / 4) * 16384 + (s % 4) * 32),
+                          sdesc_add(dVk, (s / 4) * 16384 + (s % 4) * 32) + st * KV16, id_kk, s > 0);
+            umma_commit(bar_dp_full);
+            if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
+          }
+          __syncwarp();
+          pend = true;
+          pfirst = j == 0;
+          plast = j == itm.nkv - 1;
+          pst = st;
           pg = g;
-          plast = (j == itm.nkv - 1);
+          if (++st == STAGES) { st = 0; kvph ^= 1; }
         }
         ++k;
       }
-      if (pj >= 0) do_dq();
+      if (pend) do_dq();
     }
   } else {
     // ================================================ softmax + epilogue warps 0-7 (query row, key-column half)

@@ -116,8 +116,3 @@ extern "C" int vlasim_fp8_dequant_block_cuda(const uint8_t* d_codes, const float
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }
-
-extern "C" int vlasim_pack_greedy_cuda(const int32_t*, int64_t, int32_t, const vlasim_pack_out*, void*, size_t, uint32_t,
-                                       vlasim_stream_t) {
-  return vlasim_host::set_error(VLASIM_ECONFIG, "greedy packer: not implemented in this build");
-}

@@ -411,6 +411,87 @@ __global__ void __launch_bounds__(kRankThreads) k_assign(const int32_t* __restri
   }
 }
 
+// ------------------------------------------------------------------ greedy (arrival order)
+// Streaming first-fit in id order: sample i goes to the lowest-index bin whose
+// remaining room is >= len[i] (a fresh bin has room cap, so the first unopened bin always
+// qualifies).  Inherently sequential; one warp walks a 32-ary max-tree of remaining room held
+// in shared memory (3 levels, 32768 bins): 3 ballots down, 2 warp max-reductions up per sample.
+constexpr int kGreedyMaxBins = 32768;
+constexpr size_t kGreedySmem = (2 * kGreedyMaxBins + 1024 + 32) * sizeof(uint16_t);
+
+__global__ void __launch_bounds__(32, 1) k_greedy(const int32_t* __restrict__ len, int64_t n, int cap,
+                                                  vlasim_pack_out out) {
+  extern __shared__ uint16_t gsm[];
+  uint16_t* rem0 = gsm;                   // [32768] remaining room of bin b
+  uint16_t* cnt = rem0 + kGreedyMaxBins;  // [32768] members of bin b
+  uint16_t* rem1 = cnt + kGreedyMaxBins;  // [1024] max over 32 bins
+  uint16_t* rem2 = rem1 + 1024;           // [32]   max over 32 level-1 nodes
+  const int lane = threadIdx.x;
+  if (out.status[0] != 0) return;  // invalid lengths (k_hist)
+  for (int i = lane; i < kGreedyMaxBins; i += 32) {
+    rem0[i] = uint16_t(cap);
+    cnt[i] = 0;
+  }
+  for (int i = lane; i < 1024; i += 32) rem1[i] = uint16_t(cap);
+  rem2[lane] = uint16_t(cap);
+  __syncwarp();
+  auto wmax = [](int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  };
+  int nb = 0;
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t my = base + lane;
+    const int lm = my < n ? len[my] : 0;
+    const int cntv = int(n - base < 32 ? n - base : 32);
+    int ob = 0, os = 0, ot = 0;  // results of sample base + lane
+    for (int j = 0; j < cntv; ++j) {
+      const int L = __shfl_sync(0xffffffffu, lm, j);
+      const unsigned m2 = __ballot_sync(0xffffffffu, rem2[lane] >= L);
+      if (m2 == 0) {  // every one of the 32768 bins is too full: out of tree capacity
+        if (lane == 0) {
+          out.status[1] = -4;
+          out.status[0] = VLASIM_ECONFIG;
+        }
+        return;
+      }
+      const int j2 = __ffs(m2) - 1;
+      const int j1 = j2 * 32 + __ffs(__ballot_sync(0xffffffffu, rem1[j2 * 32 + lane] >= L)) - 1;
+      const int b = j1 * 32 + __ffs(__ballot_sync(0xffffffffu, rem0[j1 * 32 + lane] >= L)) - 1;
+      const int r = rem0[b], c = cnt[b];
+      __syncwarp();
+      if (lane == 0) {
+        rem0[b] = uint16_t(r - L);
+        cnt[b] = uint16_t(c + 1);
+      }
+      __syncwarp();
+      const int v1 = wmax(rem0[j1 * 32 + lane]);
+      if (lane == 0) rem1[j1] = uint16_t(v1);
+      __syncwarp();
+      const int v2 = wmax(rem1[j2 * 32 + lane]);
+      if (lane == 0) rem2[j2] = uint16_t(v2);
+      __syncwarp();
+      if (lane == j) {
+        ob = b;
+        os = c;
+        ot = cap - r;
+      }
+      nb = max(nb, b + 1);
+    }
+    if (my < n) {
+      out.bin_of[my] = ob;
+      out.slot[my] = os;
+      out.tok_off[my] = ot;
+    }
+  }
+  for (int b = lane; b < nb; b += 32) {
+    out.bin_count[b] = cnt[b];
+    out.bin_fill[b] = cap - rem0[b];
+  }
+  if (lane == 0) *out.num_bins = nb;
+}
+
 // ------------------------------------------------------------------ device-wide scans
 // Exclusive scan of int32 in[0..n) (+ total at out[n]) in three passes; partial sums int64.
 __global__ void k_scan_reduce(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ part) {
@@ -551,6 +632,7 @@ int finish(const vlasim_pack_out* out, int64_t n, uint32_t flags, cudaStream_t s
   if (h[0] == 0) return VLASIM_OK;
   if (h[1] == -2) return set_error(VLASIM_ECONFIG, "GPU packer: more than %d simultaneously open bins", kMaxActiveBins);
   if (h[1] == -3) return set_error(VLASIM_ECONFIG, "GPU packer: total tokens exceed int32 cu_seqlens range");
+  if (h[1] == -4) return set_error(VLASIM_ECONFIG, "greedy packer: more than %d bins", kGreedyMaxBins);
   return set_error(VLASIM_ECONFIG, "oversize or empty sample: id %d (length must be in [1, capacity])", h[1]);
 }
 
@@ -639,4 +721,33 @@ extern "C" int vlasim_gather_rows_cuda(const void* d_src, void* d_dst, int64_t r
 extern "C" int vlasim_scatter_rows_cuda(const void* d_packed, void* d_dst, int64_t row_bytes, const int32_t* d_len,
                                         const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream) {
   return copy_rows(false, d_packed, d_dst, row_bytes, d_len, out, n, stream);
+}
+
+extern "C" int vlasim_pack_greedy_cuda(const int32_t* d_len, int64_t n, int32_t cap, const vlasim_pack_out* out,
+                                       void* d_ws, size_t ws_bytes, uint32_t flags, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = check_out(out)) return rc;
+  if (n < 1) return set_error(VLASIM_ECONFIG, "pack_greedy: need at least one sample (n=%lld)", (long long)n);
+  if (n >= INT_MAX) return set_error(VLASIM_ECONFIG, "pack_greedy: n=%lld exceeds int32 ids", (long long)n);
+  if (cap < 1 || cap > VLASIM_PACK_MAX_CAPACITY)
+    return set_error(VLASIM_ECONFIG, "pack_greedy: capacity %d outside [1, %d]", cap, VLASIM_PACK_MAX_CAPACITY);
+  PackWs w;
+  const size_t need = carve(&w, nullptr, n, cap);
+  if (!d_ws || ws_bytes < need)
+    return set_error(VLASIM_ECONFIG, "pack_greedy: workspace too small (%zu < %zu)", ws_bytes, need);
+  carve(&w, d_ws, n, cap);
+  cudaStream_t st = as_stream(stream);
+  k_init<<<(n + 255) / 256, 256, 0, st>>>(*out, n);
+  if ((cap + 1) * 4 > 48 * 1024)
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + 1) * 4));
+  k_hist<<<num_chunks(n), 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);  // validation
+  VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGreedySmem));
+  k_greedy<<<1, 32, kGreedySmem, st>>>(d_len, n, cap, *out);
+  const int64_t nsb = num_scan_blocks(n) + 1;
+  run_scan(out->bin_count, n, out->bin_member_off, w.scan_part, nullptr, nullptr, st);
+  run_scan(out->bin_fill, n, out->bin_token_off, w.scan_part + nsb, nullptr, out->status, st);
+  run_scan(d_len, n, out->src_off, w.scan_part + 2 * nsb, out->total_tokens, out->status, st);
+  k_layout<<<(n + 255) / 256, 256, 0, st>>>(d_len, n, *out);
+  VLASIM_LAUNCH_CHECK();
+  return finish(out, n, flags, st);
 }

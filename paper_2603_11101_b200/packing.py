@@ -197,6 +197,13 @@ def pack_ffd(lengths, capacity: int, *, plan: PackPlan | None = None, sync_check
     return plan
 
 
+def pack_greedy(lengths, capacity: int, *, plan: PackPlan | None = None, sync_check: bool = True,
+                stream=None) -> PackPlan:
+    """GPU streaming first-fit in arrival order (SPEC.md:519 greedy variant): sample i goes to the
+    lowest-index bin with room >= len[i].  Same outputs and errors as pack_ffd."""
+    return pack_ffd(lengths, capacity, plan=plan, sync_check=sync_check, stream=stream, greedy=True)
+
+
 def token_ids(plan: PackPlan, total_tokens: int, stream=None):
     """Per packed token: (position in sample, segment index, gather index into the source layout)."""
     dev = plan.bin_of.device

@@ -7,9 +7,11 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _check_plan(orc, L, cap, plan):
+def _check_plan(orc, L, cap, plan, mode=None):
     from paper_2603_11101_b200 import packing
-    bin_of, slot, tok, nb = orc.pack(L, cap, 1 if len(L) > 3000 else 0)
+    if mode is None:
+        mode = 1 if len(L) > 3000 else 0  # FFD: segment tree / naive scan (same result)
+    bin_of, slot, tok, nb = orc.pack(L, cap, mode)
     assert plan.num_bins() == nb
     n = len(L)
     assert np.array_equal(plan.bin_of.cpu().numpy(), bin_of)
@@ -105,3 +107,35 @@ def test_token_ids_and_gather_scatter(gpu, orc):
     assert torch.equal(packed, src[gat.long()])
     back = packing.scatter_rows(packed, plan)
     assert torch.equal(back, src)
+
+
+# ---- greedy arrival-order first-fit: bit-exact with the oracle's mode 2
+def test_greedy_spec_shape_and_errors(gpu, orc):
+    from paper_2603_11101_b200 import ConfigError, packing
+    L = [6, 5, 4, 3, 2]
+    p = packing.pack_greedy(L, 8)
+    assert [b.member_lens for b in p.to_host(L)] == [[6, 2], [5, 3], [4]]
+    _check_plan(orc, np.array(L, np.int32), 8, p, mode=2)
+    with pytest.raises(ConfigError, match="id 2"):
+        packing.pack_greedy([3, 4, 9, 1], 8)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_greedy_random_instances(gpu, orc, seed):
+    from paper_2603_11101_b200 import packing
+    rng = np.random.default_rng(100 + seed)
+    for _ in range(25):
+        n = int(rng.integers(1, 4000))
+        cap = int(rng.choice([8, 64, 300, 2048, 8192, 16384]))
+        hi = int(rng.choice([cap, max(1, cap // 4), max(1, cap // 50)]))
+        L = rng.integers(1, hi + 1, n).astype(np.int32)
+        _check_plan(orc, L, cap, packing.pack_greedy(L, cap), mode=2)
+
+
+def test_greedy_config1_and_long_tail(gpu, orc):
+    from paper_2603_11101_b200 import packing
+    from paper_2603_11101_b200.synthetic import DIST_GEOMETRIC, gen_lengths
+    L = np.asarray(gen_lengths(64, 0, 16, 512), np.int32)
+    _check_plan(orc, L, 2048, packing.pack_greedy(L, 2048), mode=2)
+    L = np.asarray(gen_lengths(200000, DIST_GEOMETRIC, 0.02, 500, label="lengths", seed=42), np.int32)
+    _check_plan(orc, L, 8192, packing.pack_greedy(L, 8192), mode=2)

@@ -169,6 +169,13 @@ int vlasim_fp8_quant_block_cuda(const void* d_x, int64_t T, int32_t heads, int32
                                 float* d_scales, vlasim_stream_t stream);
 int vlasim_fp8_dequant_block_cuda(const uint8_t* d_codes, const float* d_scales, int64_t T, int32_t heads, int32_t d,
                                   float* d_out, vlasim_stream_t stream);
+/* quant_error(original, qt) per group (head, 128-token block, 128-d block),
+ * groups ordered like the scales: max relative roundtrip error over elements in E4M3's normal
+ * range (|x / scale| >= 2^-6, fp32 quotient), sum of squared errors (fp64) and element count.  Global
+ * metrics: max of the maxima, Σsse / Σcount. */
+int vlasim_fp8_quant_error_cuda(const void* d_x, const uint8_t* d_codes, const float* d_scales, int64_t T,
+                                int32_t heads, int32_t d, float* d_group_maxrel, double* d_group_sse,
+                                int32_t* d_group_count, vlasim_stream_t stream);
 
 /* ------------------------------------------------------------------ synthetic inputs
  * Counter-based values shared with the CPU oracle:

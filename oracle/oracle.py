@@ -242,3 +242,38 @@ def fp8_quant_block(x, quotient_fp32=True):
     _chk(lib().oracle_fp8_quant_block(_p(x, f32p), T, Hh, d, 1 if quotient_fp32 else 0, _p(codes, u8p),
                                       _p(scales, f32p)))
     return codes, scales
+
+
+def fp8_quant_error(x, codes, scales):
+    """quant_error(original, qt) restated for PerBlock(128,128) per head, with the
+    arithmetic the GPU path pins: deq = fp32(value(code) · scale), diff = fp32(deq − x), relative
+    error fp32(|diff| / |x|) over elements in E4M3's normal range (|fp32(x / scale)| >= 2^-6,
+    SPEC.md:586); squared errors summed in fp64.
+    Returns (group_max_rel [heads, ⌈T/128⌉, ⌈d/128⌉] f32, group_sse f64, group_count int, max_rel, mse)."""
+    x = np.asarray(x, np.float32)
+    codes = np.asarray(codes, np.uint8)
+    T, Hh, d = x.shape
+    nbt, nbd = (T + 127) // 128, (d + 127) // 128
+    vals = np.zeros(256, np.float32)
+    for c in range(256):  # E4M3 decode (SPEC.md:544-562): bias 7, subnormals, 0x7f/0xff NaN
+        e, m = (c >> 3) & 0xF, c & 7
+        v = (m / 8.0) * 2.0 ** -6 if e == 0 else ((1 + m / 8.0) * 2.0 ** (e - 7) if not (e == 15 and m == 7) else np.nan)
+        vals[c] = -v if c & 0x80 else v
+    deq = vals[codes] * np.repeat(np.repeat(np.transpose(np.asarray(scales, np.float32), (1, 0, 2)), 128, 0)[:T],
+                                  128, 2)[:, :, :d]  # fp32 · fp32
+    diff = (deq - x).astype(np.float32)
+    sc = np.repeat(np.repeat(np.transpose(np.asarray(scales, np.float32), (1, 0, 2)), 128, 0)[:T], 128, 2)[:, :, :d]
+    normal = np.abs((x / sc).astype(np.float32)) >= np.float32(2.0 ** -6)
+    rel = np.where(normal, np.abs(diff) / np.where(x != 0, np.abs(x), np.float32(1)), np.float32(0)).astype(np.float32)
+    gmax = np.zeros((Hh, nbt, nbd), np.float32)
+    gsse = np.zeros((Hh, nbt, nbd), np.float64)
+    gcnt = np.zeros((Hh, nbt, nbd), np.int64)
+    sq = diff.astype(np.float64) ** 2
+    for h in range(Hh):
+        for bt in range(nbt):
+            for bd in range(nbd):
+                sl = (slice(bt * 128, min(T, bt * 128 + 128)), h, slice(bd * 128, min(d, bd * 128 + 128)))
+                gmax[h, bt, bd] = rel[sl].max() if rel[sl].size else 0.0
+                gsse[h, bt, bd] = sq[sl].sum()
+                gcnt[h, bt, bd] = sq[sl].size
+    return gmax, gsse, gcnt, float(gmax.max()), float(gsse.sum() / gcnt.sum())

@@ -61,6 +61,8 @@ _SIGS = {
                                               C.c_void_p]),
     "vlasim_fp8_dequant_block_cuda": (C.c_int, [C.c_void_p, f32p, C.c_int64, C.c_int32, C.c_int32, f32p,
                                                 C.c_void_p]),
+    "vlasim_fp8_quant_error_cuda": (C.c_int, [C.c_void_p, C.c_void_p, f32p, C.c_int64, C.c_int32, C.c_int32, f32p,
+                                              C.c_void_p, C.c_void_p, C.c_void_p]),
     "vlasim_fill_synthetic_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p]),
     "vlasim_gen_lengths": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, i32p]),

@@ -18,6 +18,15 @@ __device__ __forceinline__ uint16_t cvt_e4m3x2(float lo, float hi) {
   return r;
 }
 
+__device__ __forceinline__ float e4m3_to_float(uint8_t c) {
+  const int e = (c >> 3) & 0xF, m = c & 7;
+  float v;
+  if (e == 0) v = ldexpf(float(m) / 8.f, -6);
+  else if (e == 15 && m == 7) v = __int_as_float(0x7fc00000);
+  else v = ldexpf(1.f + float(m) / 8.f, e - 7);
+  return (c & 0x80) ? -v : v;
+}
+
 // One CTA (256 threads) per (head, 128-token block, 128-d block).
 __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __restrict__ x, int T, int heads, int d,
                                                      uint8_t* __restrict__ codes, float* __restrict__ scales) {
@@ -68,15 +77,6 @@ __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __rest
   }
 }
 
-__device__ __forceinline__ float e4m3_to_float(uint8_t c) {
-  const int e = (c >> 3) & 0xF, m = c & 7;
-  float v;
-  if (e == 0) v = ldexpf(float(m) / 8.f, -6);
-  else if (e == 15 && m == 7) v = __int_as_float(0x7fc00000);
-  else v = ldexpf(1.f + float(m) / 8.f, e - 7);
-  return (c & 0x80) ? -v : v;
-}
-
 __global__ void k_dequant_block(const uint8_t* __restrict__ codes, const float* __restrict__ scales, int64_t T,
                                 int heads, int d, float* __restrict__ out) {
   const int64_t n = T * heads * d;
@@ -90,7 +90,73 @@ __global__ void k_dequant_block(const uint8_t* __restrict__ codes, const float* 
   }
 }
 
+// quant_error per (head, 128-token, 128-d) group: max relative roundtrip
+// error over the elements in E4M3's normal range (|x / scale| >= 2^-6, with the quantiser's fp32
+// quotient), and the sum of squared errors.  deq = value(code) · scale and every error
+// term are fp32 (one rounding each, as the oracle restates them); SSE accumulates in fp64.
+__global__ void __launch_bounds__(256) k_quant_error(const __nv_bfloat16* __restrict__ x,
+                                                     const uint8_t* __restrict__ codes,
+                                                     const float* __restrict__ scales, int T, int heads, int d,
+                                                     float* __restrict__ gmax, double* __restrict__ gsse,
+                                                     int* __restrict__ gcnt) {
+  const int nbd = (d + 127) / 128, nbt = (T + 127) / 128;
+  const int bd = blockIdx.x % nbd, bt = (blockIdx.x / nbd) % nbt, h = blockIdx.x / (nbd * nbt);
+  const int t0 = bt * 128, c0 = bd * 128;
+  const int rows = min(128, T - t0), cols = min(128, d - c0);
+  const float scale = scales[(int64_t(h) * nbt + bt) * nbd + bd];
+  float mx = 0.f;
+  double sse = 0.0;
+  for (int e = threadIdx.x; e < rows * 128; e += 256) {
+    const int r = e / 128, c = e % 128;
+    if (c >= cols) continue;
+    const int64_t off = (int64_t(t0 + r) * heads + h) * d + c0 + c;
+    const float xv = __bfloat162float(x[off]);
+    const uint8_t code = codes[off];
+    const float diff = __fsub_rn(__fmul_rn(e4m3_to_float(code), scale), xv);
+    sse += double(diff) * double(diff);
+    if (fabsf(__fdiv_rn(xv, scale)) >= 0.015625f) mx = fmaxf(mx, __fdiv_rn(fabsf(diff), fabsf(xv)));
+  }
+  __shared__ float smx[8];
+  __shared__ double ssse[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sse += __shfl_xor_sync(0xffffffffu, sse, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smx[threadIdx.x >> 5] = mx;
+    ssse[threadIdx.x >> 5] = sse;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.f;
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      m = fmaxf(m, smx[w]);
+      t += ssse[w];
+    }
+    gmax[blockIdx.x] = m;
+    gsse[blockIdx.x] = t;
+    gcnt[blockIdx.x] = rows * cols;
+  }
+}
+
 }  // namespace
+
+extern "C" int vlasim_fp8_quant_error_cuda(const void* d_x, const uint8_t* d_codes, const float* d_scales, int64_t T,
+                                           int32_t heads, int32_t d, float* d_group_maxrel, double* d_group_sse,
+                                           int32_t* d_group_count, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (!d_x || !d_codes || !d_scales || !d_group_maxrel || !d_group_sse || !d_group_count)
+    return set_error(VLASIM_ECONFIG, "fp8_quant_error: null buffer");
+  if (T < 1 || heads < 1 || d < 1 || T >= (int64_t(1) << 31))
+    return set_error(VLASIM_ECONFIG, "fp8_quant_error: bad shape T=%lld heads=%d d=%d", (long long)T, heads, d);
+  const int64_t groups = int64_t(heads) * ((T + 127) / 128) * ((d + 127) / 128);
+  k_quant_error<<<groups, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(d_x), d_codes, d_scales,
+                                                       int(T), heads, d, d_group_maxrel, d_group_sse, d_group_count);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
 
 extern "C" int vlasim_fp8_quant_block_cuda(const void* d_x, int64_t T, int32_t heads, int32_t d, uint8_t* d_codes,
                                            float* d_scales, vlasim_stream_t stream) {

@@ -36,6 +36,23 @@ def dequant_block(codes: torch.Tensor, scales: torch.Tensor, stream=None) -> tor
     return out
 
 
+def quant_error(x: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor, stream=None) -> dict:
+    """quant_error(original, qt) for a PerBlock(128,128) E4M3 quantisation of
+    x [T, heads, d] bf16: {"max_rel": max relative error over elements quantised to E4M3 normals,
+    "mse": mean squared error, "groups": {"max_rel", "mse"} per (head, token block, d block)}."""
+    T, Hh, d = x.shape
+    g = Hh * ((T + 127) // 128) * ((d + 127) // 128)
+    gmax = torch.empty(g, dtype=torch.float32, device=x.device)
+    gsse = torch.empty(g, dtype=torch.float64, device=x.device)
+    gcnt = torch.empty(g, dtype=torch.int32, device=x.device)
+    _lib.check(_lib.lib().vlasim_fp8_quant_error_cuda(_lib.ptr(x), _lib.ptr(codes), _lib.ptr(scales, _lib.f32p), T, Hh,
+                                                      d, _lib.ptr(gmax, _lib.f32p), _lib.ptr(gsse), _lib.ptr(gcnt),
+                                                      _lib.stream_ptr(stream)), "fp8_quant_error")
+    shape = scales.shape
+    return {"max_rel": float(gmax.max()), "mse": float(gsse.sum() / gcnt.sum()),
+            "groups": {"max_rel": gmax.view(shape), "mse": (gsse / gcnt).view(shape)}}
+
+
 def varlen_attn_fwd_fp8qk(q_codes, q_scale, k_codes, k_scale, v, cu_seqlens, *, mask_mode=0, prefix_len=None,
                           softmax_scale=None, out=None, lse=None, stream=None):
     """Forward with E4M3 Q/K (tcgen05 kind::f8f6f4 for QKᵀ, block scales applied to S; P·V in bf16)."""

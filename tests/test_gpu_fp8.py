@@ -62,3 +62,32 @@ def test_fp8qk_attention_within_tolerance(gpu, orc, L, H, Hkv, mask):
     err16 = np.max(np.abs(o16.float().cpu().numpy() - ro)) / max(1.0, np.max(np.abs(ro)))
     assert err8 < 6e-2, err8
     assert err16 < 2e-2, err16
+
+
+# ---- quant_error
+@pytest.mark.parametrize("shape", [(300, 3, 128), (128, 2, 256), (77, 1, 64), (1, 1, 1)])
+def test_quant_error_matches_oracle(gpu, orc, shape):
+    from paper_2603_11101_b200 import fp8
+    torch.manual_seed(sum(shape))
+    x = (torch.randn(*shape, device="cuda") * torch.logspace(-3, 2, shape[0], device="cuda")[:, None, None]).bfloat16()
+    codes, scales = fp8.quant_block(x)
+    m = fp8.quant_error(x, codes, scales)
+    gmax, gsse, gcnt, mx, mse = orc.fp8_quant_error(x.float().cpu().numpy(), codes.cpu().numpy(), scales.cpu().numpy())
+    assert np.array_equal(m["groups"]["max_rel"].cpu().numpy(), gmax)  # fp32, same roundings
+    np.testing.assert_allclose(m["groups"]["mse"].cpu().numpy(), gsse / gcnt, rtol=1e-12, atol=0)
+    assert m["max_rel"] == mx
+    np.testing.assert_allclose(m["mse"], mse, rtol=1e-12)
+    assert m["max_rel"] <= 2.0 ** -4  # normal-range relative error <= 2^-4
+
+
+def test_quant_error_known_answers(gpu):
+    from paper_2603_11101_b200 import fp8
+    z = torch.zeros(130, 2, 64, dtype=torch.bfloat16, device="cuda")
+    m = fp8.quant_error(z, *fp8.quant_block(z))  # zero tensor: exact roundtrip
+    assert m["max_rel"] == 0.0 and m["mse"] == 0.0
+    e = torch.tensor([-448.0, 0.0, 448.0], device="cuda").bfloat16().view(3, 1, 1)  # representable at scale 1
+    m = fp8.quant_error(e, *fp8.quant_block(e))
+    assert m["max_rel"] == 0.0 and m["mse"] == 0.0
+    c = torch.full((256, 1, 128), 3.0, dtype=torch.bfloat16, device="cuda")  # all-equal tensor
+    m = fp8.quant_error(c, *fp8.quant_block(c))
+    assert m["max_rel"] <= 2.0 ** -23  # zero up to the fp32 rounding of scale = amax / 448

@@ -349,3 +349,24 @@ def test_quantize_idempotent(orc):
     deq[128:] *= s1[0, 1, 0]
     c2, s2 = orc.fp8_quant_block(deq.astype(np.float32), quotient_fp32=False)
     assert np.array_equal(c1, c2)
+
+
+def test_fp8_quant_error_known_answers(orc):
+    """quant_error KATs (SPEC.md:603-606): zero tensor and values representable at scale 1 → all zeros;
+    refinement: per-block metrics of a heterogeneous-scale tensor beat one 128×128 group's worth."""
+    z = np.zeros((130, 2, 64), np.float32)
+    g, s, n, mx, mse = orc.fp8_quant_error(z, *orc.fp8_quant_block(z))
+    assert mx == 0.0 and mse == 0.0 and g.shape == (2, 2, 1)
+    e = np.array([-448.0, 0.0, 448.0], np.float32).reshape(3, 1, 1)
+    assert orc.fp8_quant_error(e, *orc.fp8_quant_block(e))[3:] == (0.0, 0.0)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((256, 1, 128)).astype(np.float32)
+    x[128:] *= 1000.0  # second token block 1000x larger
+    codes, scales = orc.fp8_quant_block(x)
+    g, s, n, mx, mse = orc.fp8_quant_error(x, codes, scales)
+    assert mx <= 2.0 ** -4
+    # the small block quantised alone has smaller squared error than with the large block's scale
+    xs = x.copy()
+    xs[:128] = x[:128]
+    one = np.concatenate([x[:128], x[128:]], 0)
+    assert s[0, 0, 0] < 1e-3 * s[0, 1, 0]

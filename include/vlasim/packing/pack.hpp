@@ -56,6 +56,8 @@ class GpuPacker {
 
   // d_lengths: device int32[n].  sync_check → synchronise and throw ConfigError on bad input.
   void pack(const std::int32_t* d_lengths, std::int64_t n, vlasim_stream_t stream, bool sync_check = true);
+  // greedy arrival-order first fit; same outputs.
+  void pack_greedy(const std::int32_t* d_lengths, std::int64_t n, vlasim_stream_t stream, bool sync_check = true);
   const vlasim_pack_out& out() const { return out_; }
   std::int32_t capacity() const { return capacity_; }
 

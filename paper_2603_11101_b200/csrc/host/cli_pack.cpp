@@ -1,7 +1,7 @@
 // cli_pack.cpp — `vlasim_pack`: the reference's `pack` subcommand on the GPU packer.
 //
 //   vlasim_pack --capacity N (--corpus FILE | --synthetic N LO HI [SEED]) [--pad-to P] [--head-dim D]
-//               [--prune VIEW] [--manifest]
+//               [--prune VIEW] [--greedy] [--manifest]
 //
 // Corpus file (flat tabular text): one sample per line, `id text_len [view=count ...]`,
 // '#' starts a comment.  Prints PackingStats and, with --manifest, every bin's
@@ -48,7 +48,7 @@ std::vector<vlasim::SampleLen> read_corpus(const std::string& path) {
 int usage() {
   std::fprintf(stderr,
                "usage: vlasim_pack --capacity N (--corpus FILE | --synthetic N LO HI [SEED]) [--pad-to P]\n"
-               "                   [--head-dim D] [--prune VIEW] [--manifest]\n");
+               "                   [--head-dim D] [--prune VIEW] [--greedy] [--manifest]\n");
   return 2;
 }
 
@@ -59,7 +59,7 @@ int main(int argc, char** argv) {
     std::int64_t capacity = 0, pad_to = 0, head_dim = 128;
     std::string corpus, prune;
     long long syn_n = 0, syn_lo = 16, syn_hi = 512, seed = 42;
-    bool manifest = false;
+    bool manifest = false, greedy = false;
     for (int i = 1; i < argc; ++i) {
       const std::string a = argv[i];
       auto need = [&](int k) {
@@ -77,6 +77,7 @@ int main(int argc, char** argv) {
       else if (a == "--head-dim") { need(1); head_dim = std::stoll(argv[++i]); }
       else if (a == "--prune") { need(1); prune = argv[++i]; }
       else if (a == "--manifest") manifest = true;
+      else if (a == "--greedy") greedy = true;  // arrival-order first fit
       else throw vlasim::ConfigError("unknown option " + a);
     }
     if (capacity <= 0 || (corpus.empty() == (syn_n == 0))) return usage();
@@ -92,7 +93,7 @@ int main(int argc, char** argv) {
     }
     if (lengths.empty()) throw vlasim::ConfigError("empty corpus");
     if (pad_to <= 0) pad_to = vlasim::dynamic_pad_length(lengths);
-    const auto bins = vlasim::pack_ffd(lengths, capacity);
+    const auto bins = greedy ? vlasim::pack_greedy(lengths, capacity) : vlasim::pack_ffd(lengths, capacity);
     const auto st = vlasim::packing_stats(lengths, bins, pad_to, head_dim);
     std::printf("{\"samples\": %zu, \"capacity\": %lld, \"bins_used\": %lld, \"fill_rate\": %.6f, "
                 "\"padding_rate_before\": %.6f, \"padding_rate_after\": %.6f, \"attention_flops_fixed\": %.6e, "

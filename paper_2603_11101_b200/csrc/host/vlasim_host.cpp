@@ -131,6 +131,13 @@ void GpuPacker::pack(const std::int32_t* d_lengths, std::int64_t n, vlasim_strea
         "pack_ffd");
 }
 
+void GpuPacker::pack_greedy(const std::int32_t* d_lengths, std::int64_t n, vlasim_stream_t stream, bool sync_check) {
+  if (n > max_n_) throw ConfigError("GpuPacker: batch larger than max_n");
+  check(vlasim_pack_greedy_cuda(d_lengths, n, capacity_, &out_, ws_, ws_bytes_,
+                                sync_check ? VLASIM_PACK_SYNC_CHECK : 0u, stream),
+        "pack_greedy");
+}
+
 static std::vector<PackedSequence> run_pack(std::span<const std::int64_t> lengths, std::int64_t capacity, bool greedy) {
   const std::int64_t n = std::int64_t(lengths.size());
   if (n < 1) throw ConfigError("pack: need at least one sample");
@@ -148,8 +155,7 @@ static std::vector<PackedSequence> run_pack(std::span<const std::int64_t> length
   cuda_check(cudaMemcpy(d_len.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
   const vlasim_pack_out& o = packer.out();
   if (greedy)
-    check(vlasim_pack_greedy_cuda(d_len.p, n, std::int32_t(capacity), &o, nullptr, 0, VLASIM_PACK_SYNC_CHECK, nullptr),
-          "pack_greedy");
+    packer.pack_greedy(d_len.p, n, nullptr, true);
   else
     packer.pack(d_len.p, n, nullptr, true);
   std::int32_t nb = 0;

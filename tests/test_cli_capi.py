@@ -71,3 +71,22 @@ def test_cli_pack_matches_oracle(gpu, orc, tmp_path):
         mem = [int(x) for x in parts[parts.index("members") + 1: parts.index("cu_seqlens")]]
         assert all(bin_of[i] == b for i in mem)
         assert [slot[i] for i in mem] == list(range(len(mem)))
+
+
+def test_cli_pack_greedy_matches_oracle(gpu, orc, tmp_path):
+    rng = np.random.default_rng(5)
+    L = rng.integers(1, 3000, 300).tolist()
+    f = tmp_path / "corpus.txt"
+    f.write_text("\n".join(f"{i} {l}" for i, l in enumerate(L)) + "\n")
+    r = subprocess.run([str(CLI), "--capacity", "4096", "--corpus", str(f), "--greedy", "--manifest"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    bin_of, slot, tok, nb = orc.pack(L, 4096, 2)
+    assert json.loads(lines[0])["bins_used"] == nb
+    for line in lines[1:]:
+        parts = line.split()
+        b = int(parts[1])
+        mem = [int(x) for x in parts[parts.index("members") + 1: parts.index("cu_seqlens")]]
+        assert all(bin_of[i] == b for i in mem)
+        assert [slot[i] for i in mem] == list(range(len(mem)))

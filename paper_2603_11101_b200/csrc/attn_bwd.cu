@@ -37,50 +37,82 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ------------------------------------------------------------------ pre / post
-// D[h][t] = Σ_c dO·O (fp32) and LSE → log2 domain; 16-byte loads, HD/8 lanes per (t, h) row.
-// Lane 0 of every (t, head 0) row also writes the token's visible spans (attn_common.cuh):
+// D[h][t] = Σ_c dO·O (fp32) and LSE → log2 domain.  A block owns 32 consecutive tokens × all heads,
+// a contiguous [32·H, HD] slab of O and dO read with 16-byte loads (HD/8 lanes per (t, h) row,
+// reduced by shuffles); D goes through smem so that the 4 shifted copies of D and lse2 (and the
+// per-token visible spans, attn_common.cuh) are written coalesced along the token axis:
 // rows[t] = visible keys of query t, cols[t] = queries that see key t.
+constexpr int kPreTokens = 32;
+
 template <int HD>
-__global__ void k_bwd_pre(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                          const float* __restrict__ lse, float* __restrict__ lse2, float* __restrict__ dsum,
-                          int2* __restrict__ rows_span, int2* __restrict__ cols_span, const int32_t* __restrict__ cu,
-                          const int32_t* __restrict__ prefix, int nseq, int mask, int T, int Tp, int H) {
+__global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                                 const float* __restrict__ lse, float* __restrict__ lse2,
+                                                 float* __restrict__ dsum, int2* __restrict__ rows_span,
+                                                 int2* __restrict__ cols_span, const int32_t* __restrict__ cu,
+                                                 const int32_t* __restrict__ prefix, int nseq, int mask, int T, int Tp,
+                                                 int H) {
   constexpr int LPR = HD / 8;  // lanes per row (8 bf16 per lane)
-  const int64_t gt = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int64_t row = gt / LPR;
-  const int sub = int(gt % LPR);
-  const bool ok = row < int64_t(T) * H;
-  float acc = 0.f;
-  if (ok) {
-    const uint4 a = *reinterpret_cast<const uint4*>(o + row * HD + sub * 8);
-    const uint4 b = *reinterpret_cast<const uint4*>(dout + row * HD + sub * 8);
-    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+  extern __shared__ float sh_d[];  // [H][kPreTokens]
+  const int t0 = blockIdx.x * kPreTokens;
+  const int nt = min(kPreTokens, T - t0);
+  const int tasks = nt * H * LPR;
+  const int64_t base = int64_t(t0) * H * HD;
+#pragma unroll 4
+  for (int task = threadIdx.x; task < kPreTokens * 16 * LPR; task += 256) {  // uniform trip count (H ≤ 16 fast path)
+    if (task >= tasks) break;
+    const int r = task / LPR, sub = task % LPR;
+    const uint4 x = *reinterpret_cast<const uint4*>(o + base + int64_t(r) * HD + sub * 8);
+    const uint4 y = *reinterpret_cast<const uint4*>(dout + base + int64_t(r) * HD + sub * 8);
+    const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* py = reinterpret_cast<const __nv_bfloat162*>(&y);
+    float acc = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
-      acc += x.x * y.x + x.y * y.y;
+      const float2 a = __bfloat1622float2(px[i]), b = __bfloat1622float2(py[i]);
+      acc += a.x * b.x + a.y * b.y;
     }
-  }
 #pragma unroll
-  for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (ok && sub == 0) {
-    const int t = int(row / H), h = int(row % H);
-    // 4 copies shifted by s = 0..3 elements: any 128-wide window [qb, qb+128) starts 16-B aligned
-    // in copy (−qb) & 3, so the dK/dV kernel reads it with 128-bit shared loads.
-    const int64_t cp = int64_t(H) * Tp + 512;
+    for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
+  }
+  for (int task = kPreTokens * 16 * LPR + threadIdx.x; task < tasks; task += 256) {  // H > 16
+    const int r = task / LPR, sub = task % LPR;
+    const uint4 x = *reinterpret_cast<const uint4*>(o + base + int64_t(r) * HD + sub * 8);
+    const uint4 y = *reinterpret_cast<const uint4*>(dout + base + int64_t(r) * HD + sub * 8);
+    const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* py = reinterpret_cast<const __nv_bfloat162*>(&y);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = __bfloat1622float2(px[i]), b = __bfloat1622float2(py[i]);
+      acc += a.x * b.x + a.y * b.y;
+    }
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
+  }
+  __syncthreads();
+  // 4 copies shifted by s = 0..3 elements: any 64/128-wide window [qb, qb+w) starts 16-B aligned
+  // in copy (−qb) & 3, so the dK/dV kernel reads it with 128-bit shared loads.
+  const int64_t cp = int64_t(H) * Tp + 512;
+  for (int idx = threadIdx.x; idx < H * kPreTokens; idx += 256) {
+    const int h = idx / kPreTokens, tl = idx % kPreTokens;
+    if (tl >= nt) continue;
+    const int t = t0 + tl;
+    const float d = sh_d[h * kPreTokens + tl];
     const float l2 = lse[int64_t(h) * T + t] * kLog2e;
 #pragma unroll
     for (int sh = 0; sh < 4; ++sh) {
-      dsum[sh * cp + int64_t(h) * Tp + t + sh] = acc;
+      dsum[sh * cp + int64_t(h) * Tp + t + sh] = d;
       lse2[sh * cp + int64_t(h) * Tp + t + sh] = l2;
     }
-    if (h == 0) {
-      const RowSpan r = row_span(cu, prefix, nseq, mask, t, T);
-      const RowSpan c = key_span(cu, prefix, nseq, mask, t, T);
-      rows_span[t] = make_int2(r.lo, r.hi);
-      cols_span[t] = make_int2(c.lo, c.hi);
-    }
+  }
+  if (threadIdx.x < nt) {
+    const int t = t0 + threadIdx.x;
+    const RowSpan rr = row_span(cu, prefix, nseq, mask, t, T);
+    const RowSpan c = key_span(cu, prefix, nseq, mask, t, T);
+    rows_span[t] = make_int2(rr.lo, rr.hi);
+    cols_span[t] = make_int2(c.lo, c.hi);
   }
 }
 
@@ -900,8 +932,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   using namespace vlasim_host;
   const int T = int(a->total_tokens), H = a->num_heads, Hkv = a->num_kv_heads;
   const int Tp = (T + 3) & ~3;
-  const int64_t rows = int64_t(T) * H;
-  k_bwd_pre<HD><<<(rows * (HD / 8) + 255) / 256, 256, 0, st>>>(
+  k_bwd_pre<HD><<<(T + kPreTokens - 1) / kPreTokens, 256, H * kPreTokens * sizeof(float), st>>>(
       static_cast<const __nv_bfloat16*>(a->o), static_cast<const __nv_bfloat16*>(g->dout), a->lse, w.lse2, w.dsum,
       w.rows_span, w.cols_span, a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, Tp, H);
   VLASIM_LAUNCH_CHECK();

@@ -338,11 +338,11 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = 0; c < 64; ++c)
             if (!(c >= c_lo && c < c_hi)) x[c] = __float_as_uint(-INFINITY);
         }
-        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent max chains
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent max chains (FMNMX3)
 #pragma unroll
-        for (int c = 0; c < 64; c += 4) {
+        for (int c = 0; c < 64; c += 8) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) mq[u] = fmaxf(mq[u], __uint_as_float(x[c + u]));
+          for (int u = 0; u < 4; ++u) mq[u] = fmax3(mq[u], __uint_as_float(x[c + 2 * u]), __uint_as_float(x[c + 2 * u + 1]));
         }
         float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         // combine the two column halves of this row
@@ -375,21 +375,22 @@ __global__ void __launch_bounds__(320, 1)
           m_run = mt;
         }
         const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-        float lq[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent sum chains
+        float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 independent sum chains (FADD2)
+        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
 #pragma unroll
         for (int c = 0; c < 64; c += 32) {
           uint32_t pk[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            const float p0 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t]), sl2, -msub));
-            const float p1 = ex2_approx(fmaf(__uint_as_float(x[c + 2 * t + 1]), sl2, -msub));
-            lq[(2 * t) & 3] += p0;
-            lq[(2 * t + 1) & 3] += p1;
-            pk[t] = pack_bf16x2(p0, p1);
+            const float2 a = f2_fma(make_float2(__uint_as_float(x[c + 2 * t]), __uint_as_float(x[c + 2 * t + 1])),
+                                    sl2v, nmv);
+            const float2 pe = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            lq[t & 1] = f2_add(lq[t & 1], pe);
+            pk[t] = pack_bf16x2(pe.x, pe.y);
           }
           tmem_st16(s_tm + c / 2, pk);
         }
-        l_run += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+        l_run += (lq[0].x + lq[1].x) + (lq[0].y + lq[1].y);
         tmem_wait_st();
         tc_fence_before();
         warp_arrive(&bar_p_full[g & 1]);

@@ -645,7 +645,7 @@ __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {
   return it;
 }
 
-template <int HD, int STAGES>
+template <int HD, int STAGES, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     k_bwd_dq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
@@ -665,6 +665,9 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // event trace (PROF builds with VLASIM_DBG & 2: the idle K/V stages hold 4 × 2001 words)
+  unsigned long long* const trb =
+      PROF && (p.dbg & 2) && blockIdx.x == 0 ? reinterpret_cast<unsigned long long*>(smem + Cfg::OFF_KV) : nullptr;
   if (tid == 0) {
     mbar_init(bar_qdo_full, 1);
     mbar_init(bar_qdo_empty, 1);
@@ -690,6 +693,7 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 8) {
     // ================================================ TMA producer
     if (lane == 0) {
+      TraceCtr trace(trb);
       int g = 0, k = 0;
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
@@ -697,6 +701,7 @@ __global__ void __launch_bounds__(320, 1)
         if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
+        trace(1, g);  // P: Q/dO load issued
         mbar_expect_tx(bar_qdo_full, 2 * Cfg::TILE);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) {
@@ -708,6 +713,10 @@ __global__ void __launch_bounds__(320, 1)
           if (g >= STAGES) mbar_wait(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
           uint8_t* sk = smem + Cfg::OFF_KV + st * 2 * Cfg::TILE;
           const int kv0 = itm.kv_lo + j * 128;
+          if (PROF && (p.dbg & 2)) {  // timing experiment: no K/V traffic (the trace lives in the K/V stages)
+            mbar_arrive(&bar_kv_full[st]);
+            continue;
+          }
           mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::TILE);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c) {
@@ -738,8 +747,10 @@ __global__ void __launch_bounds__(320, 1)
       bool pend = false;    // dQ of the previous tile not issued yet
       bool plast = false, pfirst = false;
       int pst = 0, pg = 0;  // its stage and tile ordinal
+      TraceCtr trace(lane == 0 && trb ? trb + 2001 : nullptr);
       auto do_dq = [&]() {
         mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
+        trace(10, pg);  // M: p_full seen
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a = tmem + Cfg::s_col(pg);
@@ -751,6 +762,7 @@ __global__ void __launch_bounds__(320, 1)
           if (plast) umma_commit(bar_dq_full);
         }
         __syncwarp();
+        trace(11, pg);  // M: dQ issued
         pend = false;
       };
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
@@ -762,6 +774,7 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(bar_qdo_full, k & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           mbar_wait(&bar_kv_full[st], kvph);
+          trace(12, g);  // M: K/V seen
           tc_fence_after();
           // S_g = Q·K_gᵀ into S buffer g%2 (its previous dS was consumed by dQ_{g-2}: issue order)
           if (elect_one()) {
@@ -785,6 +798,7 @@ __global__ void __launch_bounds__(320, 1)
             if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
           }
           __syncwarp();
+          trace(13, g);  // M: S + dP issued
           pend = true;
           pfirst = j == 0;
           plast = j == itm.nkv - 1;
@@ -802,6 +816,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int r = quad * 32 + lane;
     const int c0 = half * 64;
+    TraceCtr trace(lane == 0 && (warp == 0 || warp == 4) && trb ? trb + 2001 * (2 + half) : nullptr);
     int g = 0, k = 0;
     // row parameters of the next item are prefetched one item ahead
     auto load_row = [&](const QItem& it, int2& rs_, float& l_, float& d_) {
@@ -830,24 +845,38 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
         const int kv0 = itm.kv_lo + j * 128 + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        const bool full = c_lo <= 0 && c_hi >= 64;
+        // visible columns of this 64-column half as a bitmask (rows are intervals)
+        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 64);
+        const int vlo = min(max(c_lo, 0), 64), vhi = min(max(c_hi, 0), 64);
+        const unsigned long long vis =
+            vhi <= vlo ? 0ull : ((vhi >= 64 ? ~0ull : (1ull << vhi) - 1ull) & ~((1ull << vlo) - 1ull));
         mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+        trace(20, g);  // S: s_full seen
         tc_fence_after();
-        float pr[64];
+        float2 pr[32];  // P (fp32 pairs) kept for phase B
+        const float2 sl2v = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(-lse2, -lse2);
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 32) {
           uint32_t sr[32];
           tmem_ld32(s_tm + cc, sr);
           tmem_wait_ld();
+          const uint32_t vm = static_cast<uint32_t>(vis >> cc);
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const int c = cc + t;
-            const float e = ex2_approx(fmaf(__uint_as_float(sr[t]), p.scale_log2, -lse2));
-            pr[c] = (full || (c >= c_lo && c < c_hi)) ? e : 0.f;
+          for (int t = 0; t < 16; ++t) {
+            const float2 a = f2_fma(make_float2(__uint_as_float(sr[2 * t]), __uint_as_float(sr[2 * t + 1])), sl2v, nl2);
+            float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+            if (!all_full) {
+              e.x = (vm >> (2 * t)) & 1u ? e.x : 0.f;
+              e.y = (vm >> (2 * t + 1)) & 1u ? e.y : 0.f;
+            }
+            pr[cc / 2 + t] = e;
           }
         }
+        trace(21, g);  // S: phase A done
         mbar_wait(bar_dp_full, g & 1);
+        trace(22, g);  // S: dp_full seen
         tc_fence_after();
+        const float2 nd2 = make_float2(-dsum, -dsum);
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 32) {
           uint32_t dr[32];
@@ -855,19 +884,22 @@ __global__ void __launch_bounds__(320, 1)
           tmem_wait_ld();
           uint32_t dk[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const int c = cc + 2 * t;
-            dk[t] = pack_bf16x2(pr[c] * (__uint_as_float(dr[2 * t]) - dsum),
-                                pr[c + 1] * (__uint_as_float(dr[2 * t + 1]) - dsum));
+          for (int t = 0; t < 16; ++t) {  // dS = P ∘ (dP − D): FADD2 + FMUL2 per pair
+            const float2 ds = f2_mul(pr[cc / 2 + t],
+                                     f2_add(make_float2(__uint_as_float(dr[2 * t]), __uint_as_float(dr[2 * t + 1])), nd2));
+            dk[t] = pack_bf16x2(ds.x, ds.y);
           }
           tmem_st16(s_tm + cc / 2, dk);
         }
         tmem_wait_st();
         tc_fence_before();
         warp_arrive(&bar_p_full[g & 1]);
+        trace(23, g);  // S: p_full arrived
       }
       // ---- item end: dQ = scale · acc → bf16 (half of the head dim per warp), coalesced store
+      trace(30, g);  // E: epilogue entered
       mbar_wait(bar_dq_full, k & 1);
+      trace(31, g);  // E: dq_full seen
       tc_fence_after();
       uint32_t pq[HD / 4];
 #pragma unroll
@@ -892,12 +924,15 @@ __global__ void __launch_bounds__(320, 1)
         bulk_store(p.dq + (dst * p.H + itm.h) * HD + half * (HD / 2), stg_row, HD);
         bulk_commit();
       }
+      trace(32, g);  // E: done
       ++k;
     }
     bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
+  if (trb)  // copy CTA 0's event trace out
+    for (int i = tid; i < 4 * 2001; i += 320) p.prof[64 + i] = trb[i];
   if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
@@ -986,10 +1021,13 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   {
     constexpr int ST = HD == 64 ? 4 : 2;
     using Cfg = DqCfg<HD, ST>;
-    auto kern = k_bwd_dq<HD, ST>;
+    auto kern = p.prof ? k_bwd_dq<HD, ST, true> : k_bwd_dq<HD, ST, false>;
+    if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<std::min(p.q_items, num_sms()), 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    const int grid = std::min(p.q_items, num_sms());
+    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
     VLASIM_LAUNCH_CHECK();
+    if (p.prof) prof_report("k_bwd_dq", grid, st, {});
   }
   return VLASIM_OK;
 }

@@ -284,6 +284,14 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack
 // class counts staged in smem, bins visited 32 at a time with early exit once the class is
 // placed (no block barriers on the per-class critical path).
 constexpr int kWarpMaxBins = 16384;
+// floor(a / b) for 0 <= a, 1 <= b <= 2^15 via the fp32 reciprocal, corrected to the exact quotient
+// (the estimate is off by at most one either way at these magnitudes).
+__device__ __forceinline__ int udiv_small(int a, int b, float inv_b) {
+  int q = __float2int_rz(__int2float_rn(a) * inv_b);
+  q -= q * b > a;
+  q += (q + 1) * b <= a;
+  return q;
+}
 __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_pack_out out) {
   extern __shared__ int32_t sm[];
   int32_t* act_rem = sm;                    // bins are never retired here: id == index
@@ -292,7 +300,9 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
   const int lane = threadIdx.x;
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   if (out.status[0] != 0) return;
-  for (int L = lane; L <= cap; L += 32) cnt[L] = ws.class_count[L];
+  // class counts → smem: a single warp, so keep 8 loads in flight per lane (latency-bound otherwise)
+#pragma unroll 8
+  for (int L = lane; L <= cap; L += 32) cnt[L] = __ldg(ws.class_count + L);
   __syncwarp();
   int nb = 0, nruns = 0;
   for (int hi = cap; hi >= 1; hi -= 32) {
@@ -303,12 +313,13 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
       present &= present - 1;
       const int L = hi - k;
       const int c = cnt[L];
+      const float invL = __frcp_rn(float(L));
       const int runs_before = nruns;
       int running = 0;  // items of class L accounted for by bins visited so far (Σq)
       for (int b0 = 0; b0 < nb && running < c; b0 += 32) {
         const int b = b0 + lane;
         const int rem = b < nb ? act_rem[b] : 0;
-        const int q = rem / L;
+        const int q = udiv_small(rem, L, invL);
         int inc = q;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -334,8 +345,8 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
       const int placed = min(c, running);
       const int r = c - placed;
       if (r > 0) {
-        const int kk = cap / L;
-        const int nnew = (r + kk - 1) / kk;
+        const int kk = udiv_small(cap, L, invL);
+        const int nnew = udiv_small(r + kk - 1, kk, __frcp_rn(float(kk)));
         if (nb + nnew > kWarpMaxBins) {
           if (lane == 0) {
             out.status[0] = VLASIM_ECONFIG;

@@ -17,6 +17,9 @@ while off < len(data):
     off += 40 + 8 * n
 tag = runs[-1][0]
 ev = sorted(e for r in runs[-4:] for e in r[1])
+if tag.startswith("k_bwd_dq"):
+    NAMES = {1: "P.qdo_load", 10: "M.p_seen", 11: "M.dQ_iss", 12: "M.kv_seen", 13: "M.S+dP_iss", 20: "S.s_seen",
+             21: "S.A_done", 22: "S.dp_seen", 23: "S.p_arr", 30: "E.enter", 31: "E.dq_seen", 32: "E.done"}
 t0 = ev[0][0]
 u0, u1 = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (100, 112)
 print(tag, len(ev), "events; span", ev[-1][0] - t0, "cycles")

@@ -648,7 +648,8 @@ __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {
 template <int HD, int STAGES, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     k_bwd_dq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
+             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+             const __grid_constant__ CUtensorMap tmdQ1, const __grid_constant__ CUtensorMap tmdQ8, const BwdParams p) {
   using Cfg = DqCfg<HD, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -913,16 +914,45 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       warp_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
-      if (valid) {  // this thread's half row → staging → async bulk store
-        uint8_t* stg_row = smem + Cfg::OFF_STG + r * (HD * 2) + half * HD;
-        const int64_t dst = p.row_map ? int64_t(__ldg(p.row_map + row)) : int64_t(row);
-        bulk_wait_read0();  // previous item's store has finished reading the staging row
+      // registers → SW128 staging (64-column boxes, conflict-free 16-B stores) → TMA tensor stores
+      // through row_map: one 8-row box per 8 rows with consecutive destinations (always without
+      // row_map; inside each sample with it), 1-row boxes otherwise — ~32 TMA ops per item instead
+      // of one bulk copy per half row.  Issued by the 16·HD/64 lowest threads.
+      {
+        constexpr int NB = HD / 64, CPT = HD / 16;  // boxes per row; 16-B chunks per thread (HD/2 cols)
+        int* rows = reinterpret_cast<int*>(smem + Cfg::OFF_ROWS);
+        uint8_t* stg = smem + Cfg::OFF_STG;
+        const bool issuer = tid < 16 * NB;
+        if (issuer) bulk_wait_read0();  // previous item's stores have read the staging
+        if (half == 0) rows[r] = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
+        named_bar_sync(2, 256);
 #pragma unroll
-        for (int j = 0; j < HD / 16; ++j)
-          *reinterpret_cast<uint4*>(stg_row + j * 16) = make_uint4(pq[4 * j], pq[4 * j + 1], pq[4 * j + 2], pq[4 * j + 3]);
+        for (int j = 0; j < CPT; ++j) {
+          const int cidx = half * CPT + j;  // 16-B chunk of the row
+          *reinterpret_cast<uint4*>(stg + (cidx >> 3) * 16384 + r * 128 + (((cidx & 7) ^ (r & 7)) << 4)) =
+              make_uint4(pq[4 * j], pq[4 * j + 1], pq[4 * j + 2], pq[4 * j + 3]);
+        }
         fence_proxy_async_smem();
-        bulk_store(p.dq + (dst * p.H + itm.h) * HD + half * (HD / 2), stg_row, HD);
-        bulk_commit();
+        named_bar_sync(2, 256);
+        if (issuer) {
+          const int grp = tid / NB, box = tid % NB, r0 = 8 * grp;
+          const int4 ra = *reinterpret_cast<const int4*>(rows + r0);
+          const int4 rb = *reinterpret_cast<const int4*>(rows + r0 + 4);
+          const int d[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          bool run = d[0] >= 0;
+#pragma unroll
+          for (int i = 1; i < 8; ++i) run = run && d[i] == d[0] + i;
+          const int col = itm.h * HD + box * 64;
+          const uint8_t* src = stg + box * 16384 + r0 * 128;
+          if (run) {
+            tma_store_2d(&tmdQ8, col, d[0], src);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (d[i] >= 0) tma_store_2d(&tmdQ1, col, d[i], src + i * 128);
+          }
+          bulk_commit();
+        }
       }
       trace(32, g);  // E: done
       ++k;
@@ -1021,11 +1051,14 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   {
     constexpr int ST = HD == 64 ? 4 : 2;
     using Cfg = DqCfg<HD, ST>;
+    CUtensorMap tdq1, tdq8;  // dQ row stores: 1-row and 8-row boxes of 64 columns (SW128)
+    if (int rc = encode_tmap_2d(&tdq1, g->dq, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 1, 64, true)) return rc;
+    if (int rc = encode_tmap_2d(&tdq8, g->dq, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 8, 64, true)) return rc;
     auto kern = p.prof ? k_bwd_dq<HD, ST, true> : k_bwd_dq<HD, ST, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     const int grid = std::min(p.q_items, num_sms());
-    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, tdq1, tdq8, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});
   }

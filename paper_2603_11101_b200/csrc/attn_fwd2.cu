@@ -10,7 +10,10 @@
 //              S columns [64·(w/4), +64); the two halves of a row exchange their partial row
 //              max through smem (named barrier per quadrant), P (bf16) is written over the S
 //              columns each half read, and each half stores its half of the O row.
-//   warp 8     TMA producer (Q double buffer, K/V ring)
+//   warp 8     TMA producer (Q double buffer, K/V ring) and, for bf16, the O stores: an item's
+//              epilogue stages O (bf16, SW128) into the item's own Q buffer, idle by then, and
+//              the producer writes it with two 128×64 TMA tensor stores before refilling that
+//              buffer with the Q tile two items later (no LSU row scatter, no softmax stall).
 //   warp 9     TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
 // TMEM (512 cols): S0 [0,128) · S1 [128,256) · O0 [256, 256+HD) · O1 after O0 (double-buffered so an
 // item's epilogue can be deferred past the next item's first tile).
@@ -64,7 +67,7 @@ struct Fwd2Cfg {
   static constexpr int OFF_V = OFF_K + KS * K_BYTES;     // [VS] V ring
   static constexpr int OFF_XCH = OFF_V + VS * KV_BYTES;  // float [2 parity][2 half][128]
   static constexpr int OFF_BAR = OFF_XCH + 2 * 2 * 128 * 4;
-  static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5;
+  static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5 + 2;
   // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
@@ -90,7 +93,8 @@ __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) 
 template <int HD, int KS, int VS, bool FP8, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const Fwd2Params p) {
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                     const Fwd2Params p) {
   using Cfg = Fwd2Cfg<HD, KS, VS, FP8>;
   constexpr int BN = Cfg::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -107,6 +111,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar_o_full = bar_s_full + 4;         // [2] per item: last PV landed in O[k%2]
   uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 256 arrivals: epilogue drained O[k%2]
   uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
+  uint64_t* bar_o_staged = bar_s_full + 9;       // [2] 8 warp arrivals: item's O staged in its Q buffer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
   float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&bar_o_empty[s], 8);
     }
     mbar_init(bar_o_ready, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&bar_o_staged[s], 8);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -159,12 +165,30 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, pv_kh * HD + c * 64, pv_kv0, &bar_v_full[vs]);
       };
+      // bf16: item k's O is staged in Q buffer k&1; write it out (two 128×64 TMA stores) and wait
+      // for the stores to read smem before that buffer takes item k+2's Q.  Every item has ≥ 1
+      // key tile (a query sees itself), so every item runs an epilogue.
+      int hq0[2] = {0, 0}, hh[2] = {0, 0};
+      auto store_o = [&](int kk) {
+        const int b = kk & 1;
+        wp.template wait<0>(&bar_o_staged[b], (kk >> 1) & 1);
+        const uint8_t* so = smem + Cfg::OFF_Q + b * Cfg::Q_BYTES;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) tma_store_2d(&tmO, hh[b] * HD + c * 64, hq0[b], so + c * 16384);
+        bulk_commit();
+        bulk_wait_read0();
+      };
       FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
         const FwdItem itm = nxt;
         if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
-        if (k >= 2) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
+        if (k >= 2) {
+          if constexpr (FP8) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
+          else store_o(k - 2);
+        }
+        hq0[qs] = itm.q0;
+        hh[qs] = itm.h;
         uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
         mbar_expect_tx(&bar_q_full[qs], Cfg::Q_BYTES);
 #pragma unroll
@@ -186,6 +210,9 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
       if (pv_g >= 0) load_v();
+      if constexpr (!FP8)
+        for (int kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) store_o(kk);
+      bulk_wait_all();
       wp.flush(p.prof);
     }
   } else if (warp == 9) {
@@ -240,7 +267,7 @@ __global__ void __launch_bounds__(320, 1)
           }
           umma_commit(&bar_s_full[g & 1]);
           umma_commit(&bar_k_empty[ks]);
-          if (j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);
+          if (FP8 && j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);  // bf16: freed by the O store
           if (pj >= 0) do_pv();
           pj = j;
           pg = g;
@@ -271,20 +298,34 @@ __global__ void __launch_bounds__(320, 1)
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
       __nv_bfloat16* orow = p.o + (static_cast<int64_t>(valid ? e_row : 0) * p.H + e_h) * HD + half * (HD / 2);
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + half * (HD / 2);
+      uint8_t* so = smem + Cfg::OFF_Q + (ek & 1) * Cfg::Q_BYTES;  // bf16: this item's Q buffer
 #pragma unroll
       for (int c = 0; c < HD / 2; c += 32) {
         uint32_t o[32];
         tmem_ld32(o_tm + c, o);
         tmem_wait_ld();
-        if (valid) {
-          uint32_t pk[16];
+        uint32_t pk[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t)
-            pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+        for (int t = 0; t < 16; ++t)
+          pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
+        if constexpr (FP8) {
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+            for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+          }
+        } else {  // SW128 staging: 64-column box (half·HD/2 + c) / 64, chunk XOR row
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int col = half * (HD / 2) + c + 8 * t;
+            *reinterpret_cast<uint4*>(so + (col >> 6) * 16384 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+          }
         }
+      }
+      if constexpr (!FP8) {
+        fence_proxy_async_smem();
+        warp_arrive(&bar_o_staged[ek & 1]);  // the producer writes the tile out
       }
       tc_fence_before();
       warp_arrive(&bar_o_empty[ek & 1]);
@@ -433,6 +474,8 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   if (int rc = encode_tmap_2d(&tq, a->q, QK, T, H * HD, H * HD * Cfg::QK_ELEM, 128, Cfg::QK_BOX, true)) return rc;
   if (int rc = encode_tmap_2d(&tk, a->k, QK, T, Hkv * HD, Hkv * HD * Cfg::QK_ELEM, Cfg::BN, Cfg::QK_BOX, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, Hkv * HD, Hkv * HD * 2, Cfg::BN, 64, true)) return rc;
+  CUtensorMap to;  // O tile stores (bf16 path): 128 rows × 64 columns, SW128
+  if (int rc = encode_tmap_2d(&to, a->o, BF, T, H * HD, H * HD * 2, 128, 64, true)) return rc;
   Fwd2Params p;
   p.o = static_cast<__nv_bfloat16*>(a->o);
   p.lse = a->lse;
@@ -450,7 +493,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
     p.prof = prof_buffer();
     auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, true>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
+    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
     VLASIM_LAUNCH_CHECK();
     return prof_report("attn_fwd2", grid, st,
                        {"prod:q_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:q_full", "mma:k/v_full",
@@ -460,7 +503,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   p.prof = nullptr;
   auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, false>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, p);
+  kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }

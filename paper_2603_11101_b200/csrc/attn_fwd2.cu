@@ -374,10 +374,14 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int c = 0; c < 64; ++c) x[c] = __float_as_uint(__uint_as_float(x[c]) * (c < cb ? k0s : k1s));
         }
-        if (!(c_lo <= 0 && c_hi >= 64)) {
+        if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 64)) {  // some row of the warp is partial
+          const int vlo = min(max(c_lo, 0), 64), vhi = min(max(c_hi, 0), 64);
+          const unsigned long long vis =
+              vhi <= vlo ? 0ull : ((vhi >= 64 ? ~0ull : (1ull << vhi) - 1ull) & ~((1ull << vlo) - 1ull));
+          const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
 #pragma unroll
           for (int c = 0; c < 64; ++c)
-            if (!(c >= c_lo && c < c_hi)) x[c] = __float_as_uint(-INFINITY);
+            x[c] = ((c < 32 ? v0 >> c : v1 >> (c - 32)) & 1u) ? x[c] : __float_as_uint(-INFINITY);
         }
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent max chains (FMNMX3)
 #pragma unroll

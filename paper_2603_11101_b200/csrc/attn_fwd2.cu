@@ -216,67 +216,82 @@ __global__ void __launch_bounds__(320, 1)
       wp.flush(p.prof);
     }
   } else if (warp == 9) {
-    // ================================================ MMA issuer
-    if (lane == 0) {
+    // ================================================ MMA issuer (whole warp: descriptors and
+    // counters in uniform registers; one elected lane issues)
+    {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
+      constexpr uint32_t Q16 = Cfg::Q_BYTES >> 4, K16 = Cfg::K_BYTES >> 4, V16 = Cfg::KV_BYTES >> 4;
+      const uint64_t dQ0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
+      const uint64_t dK0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16, 1024);
+      const uint64_t dV0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), BN * 128, 1024);  // MN-major
       WaitProf<PROF> wp;
       int g = 0, k = 0;
-      int pj = -1, pg = 0, pk = 0;  // pending PV (issued one tile late so S_g overlaps softmax of g-1)
-      bool plast = false;
+      int ks = 0, vs = 0;                // ring stages of tile g (K) and of the pending PV (V)
+      uint32_t kph = 0, vph = 0;
+      bool pend = false, pfirst = false, plast = false;  // pending PV (issued one tile late)
+      int pg = 0, pk = 0;
       auto do_pv = [&]() {
         wp.template wait<2>(&bar_p_full[pg & 1], (pg >> 1) & 1);
-        if (pj == 0 && pk >= 2) wp.template wait<3>(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
+        if (pfirst && pk >= 2) wp.template wait<3>(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
+        wp.template wait<1>(&bar_v_full[vs], vph);
         tc_fence_after();
-        const int vs = pg % VS;
-        wp.template wait<1>(&bar_v_full[vs], (pg / VS) & 1);
-        const uint32_t v_addr = smem_u32(smem + Cfg::OFF_V + vs * Cfg::KV_BYTES);
-        const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
+        if (elect_one()) {
+          const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
+          const uint64_t vd = dV0 + vs * V16;
 #pragma unroll
-        for (int s = 0; s < BN / 16; ++s)  // P: columns 0-63 at +0..31, 64-127 at +64..95
-          umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
-                      make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024), idesc_o, (pj > 0 || s > 0) ? 1u : 0u);
-        umma_commit(&bar_v_empty[vs]);
-        umma_commit(bar_o_ready);
-        if (plast) umma_commit(&bar_o_full[pk & 1]);
+          for (int s = 0; s < BN / 16; ++s)  // P: columns 0-63 at +0..31, 64-127 at +64..95
+            umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+                        sdesc_add(vd, s * 2048), idesc_o, (!pfirst || s > 0) ? 1u : 0u);
+          umma_commit(&bar_v_empty[vs]);
+          umma_commit(bar_o_ready);
+          if (plast) umma_commit(&bar_o_full[pk & 1]);
+        }
+        __syncwarp();
+        if (++vs == VS) { vs = 0; vph ^= 1; }
+        pend = false;
       };
       FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
         const FwdItem itm = nxt;
         if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
-        const uint32_t q_addr = smem_u32(smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES);
+        const uint64_t qd = dQ0 + qs * Q16;
         wp.template wait<0>(&bar_q_full[qs], (k >> 1) & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int ks = g % KS;
-          wp.template wait<1>(&bar_k_full[ks], (g / KS) & 1);
+          wp.template wait<1>(&bar_k_full[ks], kph);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(smem + Cfg::OFF_K + ks * Cfg::K_BYTES);
           const uint32_t d_s = tmem + Cfg::S_COL + (g & 1) * 128;
-          if constexpr (FP8) {  // kind::f8f6f4: 32 E4M3 elements (32 B) per K step
-            constexpr uint32_t idesc_f8 = make_idesc_e4m3(128, BN);
+          const uint64_t kd = dK0 + ks * K16;
+          if (elect_one()) {
+            if constexpr (FP8) {  // kind::f8f6f4: 32 E4M3 elements (32 B) per K step
+              constexpr uint32_t idesc_f8 = make_idesc_e4m3(128, BN);
 #pragma unroll
-            for (int s = 0; s < HD / 32; ++s)
-              umma_f8_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
-                         make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_f8, s > 0);
-          } else {
+              for (int s = 0; s < HD / 32; ++s)
+                umma_f8_ss(d_s, sdesc_add(qd, (s / 4) * 128 * 128 + (s % 4) * 32),
+                           sdesc_add(kd, (s / 4) * BN * 128 + (s % 4) * 32), idesc_f8, s > 0);
+            } else {
 #pragma unroll
-            for (int s = 0; s < HD / 16; ++s)
-              umma_f16_ss(d_s, make_sdesc_sw128(q_addr + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024),
-                          make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024), idesc_s, s > 0);
+              for (int s = 0; s < HD / 16; ++s)
+                umma_f16_ss(d_s, sdesc_add(qd, (s / 4) * 128 * 128 + (s % 4) * 32),
+                            sdesc_add(kd, (s / 4) * BN * 128 + (s % 4) * 32), idesc_s, s > 0);
+            }
+            umma_commit(&bar_s_full[g & 1]);
+            umma_commit(&bar_k_empty[ks]);
+            if (FP8 && j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);  // bf16: freed by the O store
           }
-          umma_commit(&bar_s_full[g & 1]);
-          umma_commit(&bar_k_empty[ks]);
-          if (FP8 && j == itm.nkv - 1) umma_commit(&bar_q_empty[qs]);  // bf16: freed by the O store
-          if (pj >= 0) do_pv();
-          pj = j;
+          __syncwarp();
+          if (++ks == KS) { ks = 0; kph ^= 1; }
+          if (pend) do_pv();
+          pend = true;
+          pfirst = j == 0;
+          plast = j == itm.nkv - 1;
           pg = g;
           pk = k;
-          plast = (j == itm.nkv - 1);
         }
       }
-      if (pj >= 0) do_pv();
-      wp.flush(p.prof + 8);
+      if (pend) do_pv();
+      if (lane == 0) wp.flush(p.prof + 8);
     }
   } else {
     // ================================================ softmax + epilogue warps 0-7

@@ -141,9 +141,11 @@ struct BwdParams {
 //                      phase B  dSᵀ = Pᵀ ∘ (dPᵀ − D)        → bf16 over the dP columns
 //   dV += Pᵀ·dO, dK += dSᵀ·Q                                 (A from TMEM, B = dO / Q MN-major)
 // Two softmax groups of 8 warps take alternate units, so while one group exponentiates unit u
-// the tensor cores run the GEMMs of its neighbours: the MMA warp issues S/dP two units ahead
-// (S(u+2) right after dV(u) consumed Pᵀ(u) from S[u&1], dP(u+2) after dK(u) consumed dSᵀ(u));
-// the column aliasing relies on tcgen05.mma executing in issue order.  Q/dO stream through
+// the tensor cores run the GEMMs of its neighbours.  The MMA warp issues one block per unit,
+// dV(u) · S(u+2) · dK(u) · dP(u+2), once dSᵀ(u) is written (S/dP run two units ahead; the
+// column aliasing — S(u+2) over Pᵀ(u), dP(u+2) over dSᵀ(u) — relies on tcgen05.mma executing in
+// issue order).  One wait and one issue block per unit keep the MMA warp's serial overhead
+// (≈ 6 cycles per instruction) from draining the shallow MMA queue between blocks.  Q/dO stream through
 // NS = 5 stages (the look-ahead of 2 units plus ~2 units of HBM latency); every role prefetches
 // the next item's descriptor so item boundaries do not expose a global-load round trip.  The
 // item epilogue writes dK/dV straight from TMEM-loaded registers (64-B row segments) through
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   uint64_t* bar_dkv_empty = bars + 3;  // 16 warp arrivals: TMEM dV / dK drained
   uint64_t* bar_s_full = bars + 4;     // [2]
   uint64_t* bar_dp_full = bars + 6;    // [2]
-  uint64_t* bar_pt_full = bars + 8;    // [2] 8 warp arrivals: Pᵀ written over S
+  // bars + 8, + 9: spare (Pᵀ completion rides on the dSᵀ barrier: one MMA wait per unit)
   uint64_t* bar_ds_full = bars + 10;   // [2] 8 warp arrivals: dSᵀ written over dP
   uint64_t* bar_qd_full = bars + 12;        // [NS] Q + dO (+ lse2 / D windows) of a unit
   uint64_t* bar_qd_empty = bars + 12 + NS;  // [NS] committed after the unit's dK
@@ -258,7 +260,6 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
       mbar_init(&bar_dp_full[b], 1);
-      mbar_init(&bar_pt_full[b], 8);
       mbar_init(&bar_ds_full[b], 8);
     }
     for (int s = 0; s < NS; ++s) {
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   } else if (warp == 17) {
     // ================================================ MMA issuer (whole warp, so descriptors and
     // counters stay in uniform registers; one elected lane issues).  Per unit u, in issue order:
-    //   dV(u) · S(u+2) | dK(u) · dP(u+2)   — two issue blocks, three barrier waits.
+    //   dV(u) · S(u+2) · dK(u) · dP(u+2)   — one issue block after one barrier wait.
     // Look-ahead S/dP stay inside the current item: the next item's first units are issued only
     // after the current item's last dK and its dkv_full commit, so the epilogue never waits
     // behind the next item's K/V load (single K/V buffer).  The warp's serial instruction
@@ -372,15 +373,15 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       va = ca.start(p);
       while (va && ca.k == 0 && ca.u < 2) issue_SdP();  // prologue: first item only
       uint32_t cs = 0, b = 0, ph = 0;  // stage of cc.u; TMEM buffer cc.u & 1; its use parity
-      bool vc = cc.start(p);
-      while (vc) {
+      for (bool vc = cc.start(p); vc; vc = cc.next(p)) {
         const uint32_t coff = cs * QT16, aoff = as * QT16;
-        const bool early = va && ca.u == cc.u + 2 && ca.k == cc.k;  // S(u+2) after dV(u), dP(u+2) after dK(u)
+        const bool early = va && ca.u == cc.u + 2 && ca.k == cc.k;  // S/dP(u+2) in this unit's block
         const bool a_last = ca.last(), c_last = cc.last();
         const uint32_t acc0 = cc.it > 0 ? 1u : 0u;
         if (early) wp.template wait<1>(&bar_qd_full[as], aph);
-        wp.template wait<3>(&bar_pt_full[b], ph);
-        trace(10, cc.u);  // M: pt_full seen
+        // dSᵀ(u) written ⇒ Pᵀ(u) written (each softmax warp stores P before dS): one wait per unit
+        wp.template wait<5>(&bar_ds_full[b], ph);
+        trace(12, cc.u);  // M: ds_full seen
         if (cc.it == 0 && cc.k > 0) wp.template wait<4>(bar_dkv_empty, (cc.k - 1) & 1);
         tc_fence_after();
         if (elect_one()) {
@@ -393,39 +394,28 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             mma_S(Cfg::s_col(b), aoff);
             umma_commit(&bar_s_full[b]);
           }
-        }
-        __syncwarp();
-        trace(11, cc.u);  // M: dV + S(u+2) issued
-        // bookkeeping for the next unit while phase B of this one runs
-        const uint32_t cs_u = cs, b_u = b, ph_u = ph;
-        const UnitCursor cu = cc;
-        vc = cc.next(p);
-        if (++cs == NS) cs = 0;
-        b ^= 1;
-        ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
-        if (early) adv_a();
-        wp.template wait<5>(&bar_ds_full[b_u], ph_u);
-        trace(12, cu.u);  // M: ds_full seen
-        tc_fence_after();
-        if (elect_one()) {
           // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b_u) + (j >> 1) * 32 + (j & 1) * 8,
+            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
                         sdesc_add(dQm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
-          umma_commit(&bar_qd_empty[cs_u]);
+          umma_commit(&bar_qd_empty[cs]);
           if (c_last) umma_commit(bar_dkv_full);
           if (early) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
-            mma_dP(Cfg::dp_col(b_u), aoff);
-            umma_commit(&bar_dp_full[b_u]);
+            mma_dP(Cfg::dp_col(b), aoff);
+            umma_commit(&bar_dp_full[b]);
             if (a_last) umma_commit(bar_kv_empty);
           }
         }
         __syncwarp();
-        trace(13, cu.u);  // M: dK + dP(u+2) issued
+        trace(13, cc.u);  // M: unit issued
+        if (early) adv_a();
         // item boundary: the next item's first units (their buffers' previous readers, the dV /
         // dK of units ≤ u, are issued)
-        while (va && ca.u <= cu.u + 2 && (ca.k == cu.k || (c_last && ca.k == cu.k + 1))) issue_SdP();
+        while (va && ca.u <= cc.u + 2 && (ca.k == cc.k || (c_last && ca.k == cc.k + 1))) issue_SdP();
+        if (++cs == NS) cs = 0;
+        b ^= 1;
+        ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
       }
       if (lane == 0) wp.flush(p.prof + 8);
     }
@@ -496,11 +486,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) pp[j] = 0u;
         }
-        tmem_st16(tmem + lane_off + Cfg::s_col(g) + c0, pp);
-        tmem_wait_st();
-        tc_fence_before();
-        warp_arrive(&bar_pt_full[g]);
-        trace(22 + g, c.u);  // S: pt arrived
+        tmem_st16(tmem + lane_off + Cfg::s_col(g) + c0, pp);  // completion awaited with dS's (phase B)
+        trace(22 + g, c.u);  // S: P written
         wp.template add_since<4>(ta);
         // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns (P as the dV GEMM saw it)
         wp.template wait<1>(&bar_dp_full[g], ph);

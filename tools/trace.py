@@ -1,4 +1,5 @@
-"""Print the CTA-0 event trace written by VLASIM_TRACE=file (PROF builds).  python tools/trace.py file [u0 u1]"""
+"""Print the CTA-0 event trace written by VLASIM_TRACE=file (PROF builds).
+python tools/trace.py file [u0 u1] [kernel-tag]   (default: the last kernel in the file)"""
 import struct
 import sys
 
@@ -15,8 +16,10 @@ while off < len(data):
     ev = struct.unpack_from(f"<{n}Q", data, off + 40)
     runs.append((tag, [(w >> 32, (w >> 16) & 0xFFFF, w & 0xFFFF) for w in ev]))
     off += 40 + 8 * n
-tag = runs[-1][0]
-ev = sorted(e for r in runs[-4:] for e in r[1])
+want = sys.argv[4] if len(sys.argv) > 4 else runs[-1][0]
+sel = [r for r in runs if r[0] == want][-4:]
+tag = want
+ev = sorted(e for r in sel for e in r[1])
 if tag.startswith("k_bwd_dq"):
     NAMES = {1: "P.qdo_load", 10: "M.p_seen", 11: "M.dQ_iss", 12: "M.kv_seen", 13: "M.S+dP_iss", 20: "S.s_seen",
              21: "S.A_done", 22: "S.dp_seen", 23: "S.p_arr", 30: "E.enter", 31: "E.dq_seen", 32: "E.done"}

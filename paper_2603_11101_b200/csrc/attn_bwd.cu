@@ -336,17 +336,26 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
       const uint64_t dQm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 8192, 1024);   // MN-major view
       const uint64_t dOm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 8192, 1024);
+      // Descriptor bases are made opaque where they are used (empty asm), so the per-MMA operand
+      // descriptors are formed by uniform adds interleaved with the MMAs (hidden behind MMA-queue
+      // back-pressure) instead of being hoisted into ~20 registers re-converted every unit.
+      auto opaque = [](uint64_t v) {
+        asm volatile("" : "+l"(v));
+        return v;
+      };
       auto mma_S = [&](uint32_t col, uint32_t soff) {
+        const uint64_t a0 = opaque(dK0), b0 = opaque(dQk) + soff;
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j)
-          umma_f16_ss(tmem + col, sdesc_add(dK0, (j / 4) * 16384 + (j % 4) * 32),
-                      sdesc_add(dQk, (j / 4) * 8192 + (j % 4) * 32) + soff, id_s, j > 0);
+          umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
+                      sdesc_add(b0, (j / 4) * 8192 + (j % 4) * 32), id_s, j > 0);
       };
       auto mma_dP = [&](uint32_t col, uint32_t soff) {
+        const uint64_t a0 = opaque(dV0), b0 = opaque(dOk) + soff;
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j)
-          umma_f16_ss(tmem + col, sdesc_add(dV0, (j / 4) * 16384 + (j % 4) * 32),
-                      sdesc_add(dOk, (j / 4) * 8192 + (j % 4) * 32) + soff, id_s, j > 0);
+          umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
+                      sdesc_add(b0, (j / 4) * 8192 + (j % 4) * 32), id_s, j > 0);
       };
       UnitCursor ca, cc;
       uint32_t as = 0, aph = 0;  // stage / parity of the look-ahead unit ca.u
@@ -387,9 +396,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (elect_one()) {
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
 #pragma unroll
+          const uint64_t om = opaque(dOm) + coff, qm = opaque(dQm) + coff;
           for (int j = 0; j < 4; ++j)
             umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + (j >> 1) * 32 + (j & 1) * 8,
-                        sdesc_add(dOm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
+                        sdesc_add(om, j * 2048), id_acc, j > 0 ? 1u : acc0);
           if (early) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
             mma_S(Cfg::s_col(b), aoff);
             umma_commit(&bar_s_full[b]);
@@ -398,7 +408,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
-                        sdesc_add(dQm, j * 2048) + coff, id_acc, j > 0 ? 1u : acc0);
+                        sdesc_add(qm, j * 2048), id_acc, j > 0 ? 1u : acc0);
           umma_commit(&bar_qd_empty[cs]);
           if (c_last) umma_commit(bar_dkv_full);
           if (early) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order

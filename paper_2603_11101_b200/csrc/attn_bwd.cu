@@ -218,6 +218,44 @@ struct UnitCursor {
   __device__ __forceinline__ int qb() const { return itm.q_lo + (it % itm.nq) * 64; }
 };
 
+// Epilogue row store without smem: thread (row = lane of a 32-row warp slab, part) holds CPT 16-B
+// chunks of its row.  A butterfly over groups of CPT lanes transposes the chunks so that lane
+// (g·CPT + i) holds chunk i of the group's CPT rows; CPT stores then write CPT-row × (16·CPT)-B
+// segments per warp instruction (8 rows × 64 B for CPT = 4) instead of 32 scattered rows.
+// dst = this lane's destination row (< 0: skip); base + dst·stride + col0 (elements) = row start.
+template <int CPT>
+__device__ __forceinline__ void store_rows_xpose(uint32_t (&w)[4 * CPT], int dst, __nv_bfloat16* base,
+                                                 int64_t stride, int col0) {
+  const int lane = threadIdx.x & 31, li = lane & (CPT - 1);
+#pragma unroll
+  for (int m = 1; m < CPT; m <<= 1) {  // stage: position c takes the partner's position c ^ m
+    const bool hi = li & m;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if ((c & m) != 0) continue;  // handle the pair (c, c ^ m) once
+      const int c1 = c | m;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // a lane with bit m clear keeps position c and receives position c1 from its partner's c;
+        // a lane with bit m set keeps c1 and receives position c from its partner's c1
+        const uint32_t send = hi ? w[4 * c + k] : w[4 * c1 + k];
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, m);
+        if (hi) w[4 * c + k] = recv;
+        else w[4 * c1 + k] = recv;
+      }
+    }
+  }
+  // lane (g·CPT + li) now holds chunk li of rows g·CPT + i at position i
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int src = (lane & ~(CPT - 1)) + i;
+    const int d = __shfl_sync(0xffffffffu, dst, src);
+    if (d >= 0)
+      *reinterpret_cast<uint4*>(base + int64_t(d) * stride + col0 + li * 8) =
+          make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+  }
+}
+
 // Warp roles (576 threads): warps 0-15 softmax — group g = w/8 takes the units with u%2 == g;
 // warp w owns key rows 32·(w%4).. (TMEM lane quadrant w%4) and query columns [32·((w/4)%2), +32)
 // of the 64-wide unit; in the epilogue all 16 warps split the head dim in quarters (w/4) and
@@ -555,40 +593,16 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         }
         tc_fence_before();
         warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
-        // registers → SW128 staging tile (conflict-free 16-B stores) → one TMA row store per
-        // (key, 64-column box), issued by the box's owner thread (256 issuers); dV first, then dK
-        // through the same 32 KB staging.  The TMA engine, not the LSU, writes the scattered rows.
-        constexpr int CPT = HD / 32;  // 16-B chunks per thread (HD/4 columns)
-        uint8_t* stg = smem + Cfg::OFF_STG;
-        const bool issuer = part < HD / 64 && dst_key >= 0;
-        auto stage = [&](const uint32_t* w) {
-#pragma unroll
-          for (int j = 0; j < CPT; ++j) {
-            const int cidx = part * CPT + j;  // 16-B chunk of the row
-            *reinterpret_cast<uint4*>(stg + (cidx >> 3) * 16384 + krow * 128 + (((cidx & 7) ^ (krow & 7)) << 4)) =
-                make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-          }
-          fence_proxy_async_smem();
-        };
+        // registers → 4-lane chunk transpose → row-segment stores through row_map (no smem, no
+        // barrier, no TMA): each warp store writes 8 rows × 64 B.
         trace(50, c.u);  // E: TMEM drained
-        bulk_wait_read0();  // this thread's previous stores have read the staging
-        named_bar_sync(5, 512);
-        stage(pv);
-        named_bar_sync(5, 512);
-        trace(51, c.u);  // E: dV staged
-        if (issuer) {
-          tma_store_2d(&tmdV, c.itm.kh * HD + part * 64, dst_key, stg + part * 16384 + krow * 128);
-          bulk_commit();
-          bulk_wait_read0();
+        {
+          const int64_t stride = int64_t(p.Hkv) * HD;
+          const int col0 = c.itm.kh * HD + part * (HD / 4);
+          store_rows_xpose<HD / 32>(pv, dst_key, p.dv, stride, col0);
+          store_rows_xpose<HD / 32>(pkk, dst_key, p.dk, stride, col0);
         }
-        named_bar_sync(5, 512);
-        trace(52, c.u);  // E: dV read by the TMA
-        stage(pkk);
-        named_bar_sync(5, 512);
-        if (issuer) {
-          tma_store_2d(&tmdK, c.itm.kh * HD + part * 64, dst_key, stg + part * 16384 + krow * 128);
-          bulk_commit();
-        }
+        trace(51, c.u);  // E: stored
         trace(34 + (warp >> 3), c.u);  // E: epilogue done
         wp.template add_since<6>(te);
       }

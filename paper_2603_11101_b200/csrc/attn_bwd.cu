@@ -925,45 +925,11 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       warp_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
-      // registers → SW128 staging (64-column boxes, conflict-free 16-B stores) → TMA tensor stores
-      // through row_map: one 8-row box per 8 rows with consecutive destinations (always without
-      // row_map; inside each sample with it), 1-row boxes otherwise — ~32 TMA ops per item instead
-      // of one bulk copy per half row.  Issued by the 16·HD/64 lowest threads.
+      // registers → 8-lane chunk transpose → row-segment stores through row_map: each warp store
+      // writes 4 rows × 128 B (no smem staging, barrier or TMA op per row)
       {
-        constexpr int NB = HD / 64, CPT = HD / 16;  // boxes per row; 16-B chunks per thread (HD/2 cols)
-        int* rows = reinterpret_cast<int*>(smem + Cfg::OFF_ROWS);
-        uint8_t* stg = smem + Cfg::OFF_STG;
-        const bool issuer = tid < 16 * NB;
-        if (issuer) bulk_wait_read0();  // previous item's stores have read the staging
-        if (half == 0) rows[r] = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
-        named_bar_sync(2, 256);
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) {
-          const int cidx = half * CPT + j;  // 16-B chunk of the row
-          *reinterpret_cast<uint4*>(stg + (cidx >> 3) * 16384 + r * 128 + (((cidx & 7) ^ (r & 7)) << 4)) =
-              make_uint4(pq[4 * j], pq[4 * j + 1], pq[4 * j + 2], pq[4 * j + 3]);
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(2, 256);
-        if (issuer) {
-          const int grp = tid / NB, box = tid % NB, r0 = 8 * grp;
-          const int4 ra = *reinterpret_cast<const int4*>(rows + r0);
-          const int4 rb = *reinterpret_cast<const int4*>(rows + r0 + 4);
-          const int d[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-          bool run = d[0] >= 0;
-#pragma unroll
-          for (int i = 1; i < 8; ++i) run = run && d[i] == d[0] + i;
-          const int col = itm.h * HD + box * 64;
-          const uint8_t* src = stg + box * 16384 + r0 * 128;
-          if (run) {
-            tma_store_2d(&tmdQ8, col, d[0], src);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (d[i] >= 0) tma_store_2d(&tmdQ1, col, d[i], src + i * 128);
-          }
-          bulk_commit();
-        }
+        const int dst = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
+        store_rows_xpose<HD / 16>(pq, dst, p.dq, int64_t(p.H) * HD, itm.h * HD + half * (HD / 2));
       }
       trace(32, g);  // E: done
       ++k;

@@ -148,19 +148,19 @@ struct BwdParams {
 // (≈ 6 cycles per instruction) from draining the shallow MMA queue between blocks.  Q/dO stream through
 // NS = 5 stages (the look-ahead of 2 units plus ~2 units of HBM latency); every role prefetches
 // the next item's descriptor so item boundaries do not expose a global-load round trip.  The
-// item epilogue writes dK/dV straight from TMEM-loaded registers (64-B row segments) through
-// row_map.  TMEM: S0 [0,64) · S1 [64,128) · dP0 [128,192) · dP1 [192,256) · dV · dK.
+// item epilogue writes dK/dV from TMEM-loaded registers through row_map after a 4-lane chunk
+// transpose (store_rows_xpose: 8 rows × 64 B per warp store; no smem staging, barrier or TMA).
+// TMEM: S0 [0,64) · S1 [64,128) · dP0 [128,192) · dP1 [192,256) · dV · dK.
 template <int HD>
 struct DkvCfg {
   static constexpr int KT = 128 * HD * 2;  // K or V tile (128 keys)
   static constexpr int QT = 64 * HD * 2;   // Q or dO tile (64 queries)
-  static constexpr int NS = 4;             // Q / dO stages
+  static constexpr int NS = 5;             // Q / dO stages
   static constexpr int OFF_K = 0, OFF_V = KT;
   static constexpr int OFF_Q = 2 * KT;              // [NS]
   static constexpr int OFF_DO = OFF_Q + NS * QT;    // [NS]
-  static constexpr int OFF_STG = OFF_DO + NS * QT;  // epilogue staging: one [128 × HD] bf16 tile (SW128)
   static constexpr int VEC = 256;                   // 64 floats of lse2 / D (16-B aligned window)
-  static constexpr int OFF_LSE = OFF_STG + KT;      // [NS][VEC]
+  static constexpr int OFF_LSE = OFF_DO + NS * QT;  // [NS][VEC]
   static constexpr int OFF_DSUM = OFF_LSE + NS * VEC;
   static constexpr int OFF_BAR = OFF_DSUM + NS * VEC;
   static constexpr int NUM_BARS = 12 + 2 * NS;
@@ -267,7 +267,7 @@ template <int HD, bool PROF>
 __global__ void __launch_bounds__(kDkvThreads, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-               const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, const BwdParams p) {
+               const BwdParams p) {
   using Cfg = DkvCfg<HD>;
   constexpr int NS = Cfg::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -569,8 +569,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         wp.template add_since<5>(tb);
       }
       if (c.last()) {
-        // ---- item epilogue (all 16 warps): TMEM → registers → release TMEM → 16-B stores of
-        //      the thread's HD/4-column segment of its key's dV / dK rows
+        // ---- item epilogue (all 16 warps): TMEM → registers → release TMEM → transposed 16-B
+        //      stores of the HD/4-column segments of the warp's 32 dV / dK rows
         const long long te = wp.now();
         trace(30 + (warp >> 3), c.u);  // E: epilogue entered
         wp.template wait<3>(bar_dkv_full, c.k & 1);
@@ -630,9 +630,7 @@ struct DqCfg {
   static constexpr int TILE = 128 * HD * 2;
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
   static constexpr int OFF_KV = 2 * TILE;  // stage s: K at +s*2*TILE, V right after
-  static constexpr int OFF_STG = OFF_KV + STAGES * 2 * TILE;  // epilogue staging (128 × HD bf16)
-  static constexpr int OFF_ROWS = OFF_STG + TILE;             // int [128]
-  static constexpr int OFF_BAR = OFF_ROWS + 512;
+  static constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
   static constexpr int NUM_BARS = 2 + 2 * STAGES + 2 + 2 + 2 + 2;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t DP_COL = 128, DQ_COL = 256;
@@ -659,8 +657,7 @@ __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {
 template <int HD, int STAGES, bool PROF>
 __global__ void __launch_bounds__(320, 1)
     k_bwd_dq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-             const __grid_constant__ CUtensorMap tmdQ1, const __grid_constant__ CUtensorMap tmdQ8, const BwdParams p) {
+             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
   using Cfg = DqCfg<HD, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -934,7 +931,6 @@ __global__ void __launch_bounds__(320, 1)
       trace(32, g);  // E: done
       ++k;
     }
-    bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -984,9 +980,6 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   if (int rc = encode_tmap_2d(&tdo, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tk, a->k, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
-  CUtensorMap tdk1, tdv1;  // dK / dV row stores (1 row × 64 columns boxes, SW128)
-  if (int rc = encode_tmap_2d(&tdk1, g->dk, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 1, 64, true)) return rc;
-  if (int rc = encode_tmap_2d(&tdv1, g->dv, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 1, 64, true)) return rc;
   CUtensorMap tq64, tdo64;  // 64-query tiles of the dK/dV kernel
   if (int rc = encode_tmap_2d(&tq64, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 64, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tdo64, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 64, 64, true))
@@ -1016,7 +1009,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
     auto kern = p.prof ? k_bwd_dkdv<HD, true> : k_bwd_dkdv<HD, false>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tq64, tk, tv, tdo64, tdk1, tdv1, p);
+    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tq64, tk, tv, tdo64, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,
@@ -1028,14 +1021,11 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   {
     constexpr int ST = HD == 64 ? 4 : 2;
     using Cfg = DqCfg<HD, ST>;
-    CUtensorMap tdq1, tdq8;  // dQ row stores: 1-row and 8-row boxes of 64 columns (SW128)
-    if (int rc = encode_tmap_2d(&tdq1, g->dq, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 1, 64, true)) return rc;
-    if (int rc = encode_tmap_2d(&tdq8, g->dq, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 8, 64, true)) return rc;
     auto kern = p.prof ? k_bwd_dq<HD, ST, true> : k_bwd_dq<HD, ST, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     const int grid = std::min(p.q_items, num_sms());
-    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, tdq1, tdq8, p);
+    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});
   }

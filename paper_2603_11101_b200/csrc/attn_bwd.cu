@@ -625,13 +625,14 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 //   dQ += dS·K                                                (A from TMEM, B = K MN-major)
 // and writes dQ = scale · dQacc once per item in bf16 (through row_map).  Deterministic: no atomics.
 // TMEM: S0 [0,128) · dP [128,256) · dQ [256,256+HD) · S1 [384,512).
-template <int HD, int STAGES>
+template <int HD, int KS, int VS>
 struct DqCfg {
   static constexpr int TILE = 128 * HD * 2;
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
-  static constexpr int OFF_KV = 2 * TILE;  // stage s: K at +s*2*TILE, V right after
-  static constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
-  static constexpr int NUM_BARS = 2 + 2 * STAGES + 2 + 2 + 2 + 2;
+  static constexpr int OFF_K = 2 * TILE;             // K ring [KS]: released after dQ
+  static constexpr int OFF_V = OFF_K + KS * TILE;    // V ring [VS]: released after dP
+  static constexpr int OFF_BAR = OFF_V + VS * TILE;
+  static constexpr int NUM_BARS = 2 + 2 * KS + 2 * VS + 8;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t DP_COL = 128, DQ_COL = 256;
   __host__ __device__ static constexpr uint32_t s_col(int g) { return (g & 1) ? 384u : 0u; }
@@ -654,52 +655,65 @@ __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {
   return it;
 }
 
-template <int HD, int STAGES, bool PROF>
-__global__ void __launch_bounds__(320, 1)
+// Warp roles (576 threads): warps 0-15 softmax — warp w owns Q rows 32·(w%4).. (TMEM lane quadrant
+// w%4) and key columns [32·(w/4), +32) of each 128-key tile; warp 16 TMA producer; warp 17 TMEM
+// allocator + MMA issuer.
+constexpr int kDqThreads = 576;
+
+template <int HD, int KS, int VS, bool PROF>
+__global__ void __launch_bounds__(kDqThreads, 1)
     k_bwd_dq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
-  using Cfg = DqCfg<HD, STAGES>;
+  using Cfg = DqCfg<HD, KS, VS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_qdo_full = bars + 0;
   uint64_t* bar_qdo_empty = bars + 1;
-  uint64_t* bar_kv_full = bars + 2;                // [STAGES]
-  uint64_t* bar_kv_empty = bars + 2 + STAGES;      // [STAGES]
-  uint64_t* bar_s_full = bars + 2 + 2 * STAGES;    // [2]
+  uint64_t* bar_k_full = bars + 2;                  // [KS]
+  uint64_t* bar_k_empty = bars + 2 + KS;            // [KS]
+  uint64_t* bar_v_full = bars + 2 + 2 * KS;         // [VS]
+  uint64_t* bar_v_empty = bars + 2 + 2 * KS + VS;   // [VS]
+  uint64_t* bar_s_full = bars + 2 + 2 * KS + 2 * VS;  // [2]
   uint64_t* bar_dp_full = bar_s_full + 2;          // one per tile
-  uint64_t* bar_p_full = bar_s_full + 3;           // [2] 256 arrivals (dS written over S buffer g%2)
+  uint64_t* bar_p_full = bar_s_full + 3;           // [2] 16 warp arrivals (dS written over S buffer g%2)
   uint64_t* bar_dq_full = bar_s_full + 5;          // one per item
-  uint64_t* bar_dq_empty = bar_s_full + 6;         // 256 arrivals
+  uint64_t* bar_dq_empty = bar_s_full + 6;         // 16 warp arrivals
+  uint64_t* bar_dp_free = bar_s_full + 7;          // 16 warp arrivals: phase B has loaded dP(g)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // event trace (PROF builds with VLASIM_DBG & 2: the idle K/V stages hold 4 × 2001 words)
   unsigned long long* const trb =
-      PROF && (p.dbg & 2) && blockIdx.x == 0 ? reinterpret_cast<unsigned long long*>(smem + Cfg::OFF_KV) : nullptr;
+      PROF && (p.dbg & 2) && blockIdx.x == 0 ? reinterpret_cast<unsigned long long*>(smem + Cfg::OFF_K) : nullptr;
   if (tid == 0) {
     mbar_init(bar_qdo_full, 1);
     mbar_init(bar_qdo_empty, 1);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&bar_kv_full[s], 1);
-      mbar_init(&bar_kv_empty[s], 1);
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(&bar_k_full[s], 1);
+      mbar_init(&bar_k_empty[s], 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(&bar_v_full[s], 1);
+      mbar_init(&bar_v_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_s_full[s], 1);
-      mbar_init(&bar_p_full[s], 8);
+      mbar_init(&bar_p_full[s], 16);
     }
     mbar_init(bar_dp_full, 1);
     mbar_init(bar_dq_full, 1);
-    mbar_init(bar_dq_empty, 8);
+    mbar_init(bar_dq_empty, 16);
+    mbar_init(bar_dp_free, 16);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == 17) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 16) {
     // ================================================ TMA producer
     if (lane == 0) {
       TraceCtr trace(trb);
@@ -718,25 +732,31 @@ __global__ void __launch_bounds__(320, 1)
           tma_load_2d(smem + Cfg::OFF_DO + c * 16384, &tmdO, itm.h * HD + c * 64, itm.q0, bar_qdo_full);
         }
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int st = g % STAGES;
-          if (g >= STAGES) mbar_wait(&bar_kv_empty[st], ((g / STAGES) - 1) & 1);
-          uint8_t* sk = smem + Cfg::OFF_KV + st * 2 * Cfg::TILE;
           const int kv0 = itm.kv_lo + j * 128;
-          if (PROF && (p.dbg & 2)) {  // timing experiment: no K/V traffic (the trace lives in the K/V stages)
-            mbar_arrive(&bar_kv_full[st]);
-            continue;
-          }
-          mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::TILE);
+          const int ks = g % KS, vs = g % VS;
+          if (g >= KS) mbar_wait(&bar_k_empty[ks], ((g / KS) - 1) & 1);
+          if (PROF && (p.dbg & 2)) {  // timing experiment: no K/V traffic (the trace lives in the K ring)
+            mbar_arrive(&bar_k_full[ks]);
+          } else {
+            mbar_expect_tx(&bar_k_full[ks], Cfg::TILE);
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c) {
-            tma_load_2d(sk + c * 16384, &tmK, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
-            tma_load_2d(sk + Cfg::TILE + c * 16384, &tmV, itm.kh * HD + c * 64, kv0, &bar_kv_full[st]);
+            for (int c = 0; c < HD / 64; ++c)
+              tma_load_2d(smem + Cfg::OFF_K + ks * Cfg::TILE + c * 16384, &tmK, itm.kh * HD + c * 64, kv0, &bar_k_full[ks]);
+          }
+          if (g >= VS) mbar_wait(&bar_v_empty[vs], ((g / VS) - 1) & 1);
+          if (PROF && (p.dbg & 2)) {
+            mbar_arrive(&bar_v_full[vs]);
+          } else {
+            mbar_expect_tx(&bar_v_full[vs], Cfg::TILE);
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c)
+              tma_load_2d(smem + Cfg::OFF_V + vs * Cfg::TILE + c * 16384, &tmV, itm.kh * HD + c * 64, kv0, &bar_v_full[vs]);
           }
         }
         ++k;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     // ================================================ MMA issuer (whole warp; one elected lane
     // issues).  Per key tile g: S(g) · [dQ(g−1) after its dS] · dP(g).  At an item boundary the
     // previous item's last dQ is issued before waiting for the next item's Q/dO, so dq_full —
@@ -744,30 +764,32 @@ __global__ void __launch_bounds__(320, 1)
     {
       constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // S, dP
       constexpr uint32_t id_dq = make_idesc_bf16(128, HD, false, true);    // dQ (A from TMEM, B MN-major)
-      constexpr uint32_t KV16 = (2 * Cfg::TILE) >> 4;                      // K/V stage stride, desc units
+      constexpr uint32_t T16 = Cfg::TILE >> 4;                             // ring stage stride, desc units
       const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
       const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
-      const uint64_t dKk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_KV), 16, 1024);
-      const uint64_t dVk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_KV + Cfg::TILE), 16, 1024);
-      const uint64_t dKm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_KV), 16384, 1024);  // MN-major view
+      const uint64_t dKk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16, 1024);
+      const uint64_t dVk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), 16, 1024);
+      const uint64_t dKm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16384, 1024);  // MN-major view
       int g = 0, k = 0;
-      int st = 0;           // K/V stage of tile g
-      uint32_t kvph = 0;    // its use parity
+      int ks = 0, vs = 0;          // K / V ring stages of tile g
+      uint32_t kph = 0, vph = 0;   // their use parities
       bool pend = false;    // dQ of the previous tile not issued yet
       bool plast = false, pfirst = false;
-      int pst = 0, pg = 0;  // its stage and tile ordinal
+      int pks = 0, pg = 0;  // its K stage and tile ordinal
       TraceCtr trace(lane == 0 && trb ? trb + 2001 : nullptr);
+      int pk = 0;  // item ordinal of the pending dQ
       auto do_dq = [&]() {
         mbar_wait(&bar_p_full[pg & 1], (pg >> 1) & 1);
         trace(10, pg);  // M: p_full seen
+        if (pfirst && pk > 0) mbar_wait(bar_dq_empty, (pk - 1) & 1);  // previous item's dQ drained
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a = tmem + Cfg::s_col(pg);
 #pragma unroll
-          for (int s = 0; s < 8; ++s)  // dS: keys 0-63 at +0..31, 64-127 at +64..95
-            umma_f16_ts(tmem + Cfg::DQ_COL, a + (s < 4 ? s * 8 : 64 + (s - 4) * 8), sdesc_add(dKm, s * 2048) + pst * KV16,
+          for (int s = 0; s < 8; ++s)  // dS: keys 32p..32p+31 packed at S cols 32p .. 32p+15
+            umma_f16_ts(tmem + Cfg::DQ_COL, a + (s >> 1) * 32 + (s & 1) * 8, sdesc_add(dKm, s * 2048) + pks * T16,
                         id_dq, (!pfirst || s > 0) ? 1u : 0u);
-          umma_commit(&bar_kv_empty[pst]);
+          umma_commit(&bar_k_empty[pks]);
           if (plast) umma_commit(bar_dq_full);
         }
         __syncwarp();
@@ -782,50 +804,54 @@ __global__ void __launch_bounds__(320, 1)
         if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
         mbar_wait(bar_qdo_full, k & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          mbar_wait(&bar_kv_full[st], kvph);
-          trace(12, g);  // M: K/V seen
+          mbar_wait(&bar_k_full[ks], kph);
+          trace(12, g);  // M: K seen
           tc_fence_after();
           // S_g = Q·K_gᵀ into S buffer g%2 (its previous dS was consumed by dQ_{g-2}: issue order)
           if (elect_one()) {
 #pragma unroll
             for (int s = 0; s < HD / 16; ++s)
               umma_f16_ss(tmem + Cfg::s_col(g), sdesc_add(dQk, (s / 4) * 16384 + (s % 4) * 32),
-                          sdesc_add(dKk, (s / 4) * 16384 + (s % 4) * 32) + st * KV16, id_kk, s > 0);
+                          sdesc_add(dKk, (s / 4) * 16384 + (s % 4) * 32) + ks * T16, id_kk, s > 0);
             umma_commit(&bar_s_full[g & 1]);
           }
           __syncwarp();
-          // dQ of the previous tile (needs its dS), then dP_g over the dP columns it freed
-          if (pend) do_dq();
-          if (j == 0 && k > 0) mbar_wait(bar_dq_empty, (k - 1) & 1);  // previous item's dQ drained
+          // dP_g as soon as phase B(g−1) has loaded dP_{g−1} (dS goes over S, not dP), then dQ_{g−1}
+          if (g > 0) mbar_wait(bar_dp_free, (g - 1) & 1);
+          mbar_wait(&bar_v_full[vs], vph);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
             for (int s = 0; s < HD / 16; ++s)
               umma_f16_ss(tmem + Cfg::DP_COL, sdesc_add(dOk, (s / 4) * 16384 + (s % 4) * 32),
-                          sdesc_add(dVk, (s / 4) * 16384 + (s % 4) * 32) + st * KV16, id_kk, s > 0);
+                          sdesc_add(dVk, (s / 4) * 16384 + (s % 4) * 32) + vs * T16, id_kk, s > 0);
             umma_commit(bar_dp_full);
+            umma_commit(&bar_v_empty[vs]);
             if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
           }
           __syncwarp();
           trace(13, g);  // M: S + dP issued
+          if (pend) do_dq();
           pend = true;
           pfirst = j == 0;
           plast = j == itm.nkv - 1;
-          pst = st;
+          pks = ks;
           pg = g;
-          if (++st == STAGES) { st = 0; kvph ^= 1; }
+          pk = k;
+          if (++ks == KS) { ks = 0; kph ^= 1; }
+          if (++vs == VS) { vs = 0; vph ^= 1; }
         }
         ++k;
       }
       if (pend) do_dq();
     }
   } else {
-    // ================================================ softmax + epilogue warps 0-7 (query row, key-column half)
-    const int quad = warp & 3, half = warp >> 2;
+    // ================================================ softmax + epilogue warps 0-15 (query row, key-column quarter)
+    const int quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int r = quad * 32 + lane;
-    const int c0 = half * 64;
-    TraceCtr trace(lane == 0 && (warp == 0 || warp == 4) && trb ? trb + 2001 * (2 + half) : nullptr);
+    const int c0 = part * 32;
+    TraceCtr trace(lane == 0 && (warp == 0 || warp == 4) && trb ? trb + 2001 * (2 + (part & 1)) : nullptr);
     int g = 0, k = 0;
     // row parameters of the next item are prefetched one item ahead
     auto load_row = [&](const QItem& it, int2& rs_, float& l_, float& d_) {
@@ -854,22 +880,19 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
         const int kv0 = itm.kv_lo + j * 128 + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        // visible columns of this 64-column half as a bitmask (rows are intervals)
-        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 64);
-        const int vlo = min(max(c_lo, 0), 64), vhi = min(max(c_hi, 0), 64);
-        const unsigned long long vis =
-            vhi <= vlo ? 0ull : ((vhi >= 64 ? ~0ull : (1ull << vhi) - 1ull) & ~((1ull << vlo) - 1ull));
+        // visible columns of this 32-column quarter as a bitmask (rows are intervals)
+        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
+        const int vlo = min(max(c_lo, 0), 32), vhi = min(max(c_hi, 0), 32);
+        const uint32_t vm = vhi <= vlo ? 0u : ((vhi >= 32 ? 0xffffffffu : (1u << vhi) - 1u) & ~((1u << vlo) - 1u));
         mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
         trace(20, g);  // S: s_full seen
         tc_fence_after();
-        float2 pr[32];  // P (fp32 pairs) kept for phase B
+        float2 pr[16];  // P (fp32 pairs) kept for phase B
         const float2 sl2v = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(-lse2, -lse2);
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
+        {
           uint32_t sr[32];
-          tmem_ld32(s_tm + cc, sr);
+          tmem_ld32(s_tm, sr);
           tmem_wait_ld();
-          const uint32_t vm = static_cast<uint32_t>(vis >> cc);
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             const float2 a = f2_fma(make_float2(__uint_as_float(sr[2 * t]), __uint_as_float(sr[2 * t + 1])), sl2v, nl2);
@@ -878,7 +901,7 @@ __global__ void __launch_bounds__(320, 1)
               e.x = (vm >> (2 * t)) & 1u ? e.x : 0.f;
               e.y = (vm >> (2 * t + 1)) & 1u ? e.y : 0.f;
             }
-            pr[cc / 2 + t] = e;
+            pr[t] = e;
           }
         }
         trace(21, g);  // S: phase A done
@@ -886,19 +909,19 @@ __global__ void __launch_bounds__(320, 1)
         trace(22, g);  // S: dp_full seen
         tc_fence_after();
         const float2 nd2 = make_float2(-dsum, -dsum);
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
+        {
           uint32_t dr[32];
-          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0 + cc, dr);
+          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0, dr);
           tmem_wait_ld();
+          tc_fence_before();
+          warp_arrive(bar_dp_free);  // dP(g) is in registers: the MMA may issue dP(g+1)
           uint32_t dk[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t) {  // dS = P ∘ (dP − D): FADD2 + FMUL2 per pair
-            const float2 ds = f2_mul(pr[cc / 2 + t],
-                                     f2_add(make_float2(__uint_as_float(dr[2 * t]), __uint_as_float(dr[2 * t + 1])), nd2));
+            const float2 ds = f2_mul(pr[t], f2_add(make_float2(__uint_as_float(dr[2 * t]), __uint_as_float(dr[2 * t + 1])), nd2));
             dk[t] = pack_bf16x2(ds.x, ds.y);
           }
-          tmem_st16(s_tm + cc / 2, dk);
+          tmem_st16(s_tm, dk);  // dS over the first 16 of this quarter's S columns
         }
         tmem_wait_st();
         tc_fence_before();
@@ -910,23 +933,23 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(bar_dq_full, k & 1);
       trace(31, g);  // E: dq_full seen
       tc_fence_after();
-      uint32_t pq[HD / 4];
+      uint32_t pq[HD / 8];  // this quarter's HD/4 columns of dQ as bf16 pairs
 #pragma unroll
-      for (int c = 0; c < HD / 2; c += 32) {
+      for (int c = 0; c < HD / 4; c += 32 > HD / 4 ? HD / 4 : 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + lane_off + Cfg::DQ_COL + half * (HD / 2) + c, v);
+        tmem_ld32(tmem + lane_off + Cfg::DQ_COL + part * (HD / 4) + c, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
+        for (int t = 0; t < (HD / 4 < 32 ? HD / 8 : 16); ++t)
           pq[c / 2 + t] = pack_bf16x2(__uint_as_float(v[2 * t]) * p.scale, __uint_as_float(v[2 * t + 1]) * p.scale);
       }
       tc_fence_before();
       warp_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
-      // registers → 8-lane chunk transpose → row-segment stores through row_map: each warp store
-      // writes 4 rows × 128 B (no smem staging, barrier or TMA op per row)
+      // registers → 4-lane chunk transpose → row-segment stores through row_map (8 rows × 64 B
+      // per warp store; no smem staging, barrier or TMA op per row)
       {
         const int dst = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
-        store_rows_xpose<HD / 16>(pq, dst, p.dq, int64_t(p.H) * HD, itm.h * HD + half * (HD / 2));
+        store_rows_xpose<HD / 32>(pq, dst, p.dq, int64_t(p.H) * HD, itm.h * HD + part * (HD / 4));
       }
       trace(32, g);  // E: done
       ++k;
@@ -935,8 +958,8 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_before();
   __syncthreads();
   if (trb)  // copy CTA 0's event trace out
-    for (int i = tid; i < 4 * 2001; i += 320) p.prof[64 + i] = trb[i];
-  if (warp == 9) tmem_dealloc<512>(tmem);
+    for (int i = tid; i < 4 * 2001; i += kDqThreads) p.prof[64 + i] = trb[i];
+  if (warp == 17) tmem_dealloc<512>(tmem);
 }
 
 struct BwdWs {
@@ -1019,13 +1042,13 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
                    "", "", "", "smx:total"});
   }
   {
-    constexpr int ST = HD == 64 ? 4 : 2;
-    using Cfg = DqCfg<HD, ST>;
-    auto kern = p.prof ? k_bwd_dq<HD, ST, true> : k_bwd_dq<HD, ST, false>;
+    constexpr int KS = HD == 64 ? 5 : 3, VS = HD == 64 ? 4 : 2;
+    using Cfg = DqCfg<HD, KS, VS>;
+    auto kern = p.prof ? k_bwd_dq<HD, KS, VS, true> : k_bwd_dq<HD, KS, VS, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     const int grid = std::min(p.q_items, num_sms());
-    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    kern<<<grid, kDqThreads, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});
   }

@@ -5,16 +5,16 @@
 // with a static stride; Q is double-buffered so the next item's loads and first S MMAs
 // overlap the current item's epilogue.
 //
-// Warp roles (320 threads):
-//   warps 0-7  softmax + epilogue: warp w owns rows 32·(w%4).. (TMEM lane quadrant w%4) and
-//              S columns [64·(w/4), +64); the two halves of a row exchange their partial row
-//              max through smem (named barrier per quadrant), P (bf16) is written over the S
-//              columns each half read, and each half stores its half of the O row.
-//   warp 8     TMA producer (Q double buffer, K/V ring) and, for bf16, the O stores: an item's
+// Warp roles (576 threads):
+//   warps 0-15 softmax + epilogue: warp w owns rows 32·(w%4).. (TMEM lane quadrant w%4) and
+//              S columns [32·(w/4), +32); the four quarters of a row exchange their partial
+//              row max / sum through smem (named barrier per quadrant), P (bf16) is written over
+//              the S columns each quarter read, and each quarter handles HD/4 columns of O.
+//   warp 16    TMA producer (Q double buffer, K/V ring) and, for bf16, the O stores: an item's
 //              epilogue stages O (bf16, SW128) into the item's own Q buffer, idle by then, and
 //              the producer writes it with two 128×64 TMA tensor stores before refilling that
 //              buffer with the Q tile two items later (no LSU row scatter, no softmax stall).
-//   warp 9     TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
+//   warp 17    TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
 // TMEM (512 cols): S0 [0,128) · S1 [128,256) · O0 [256, 256+HD) · O1 after O0 (double-buffered so an
 // item's epilogue can be deferred past the next item's first tile).
 // Visible-key spans per token come from k_fwd_spans (one binary search per token).
@@ -65,8 +65,8 @@ struct Fwd2Cfg {
   static constexpr int OFF_Q = 0;                        // [2]
   static constexpr int OFF_K = 2 * Q_BYTES;              // [KS] K ring
   static constexpr int OFF_V = OFF_K + KS * K_BYTES;     // [VS] V ring
-  static constexpr int OFF_XCH = OFF_V + VS * KV_BYTES;  // float [2 parity][2 half][128]
-  static constexpr int OFF_BAR = OFF_XCH + 2 * 2 * 128 * 4;
+  static constexpr int OFF_XCH = OFF_V + VS * KV_BYTES;  // float [2 parity][4 quarter][128]
+  static constexpr int OFF_BAR = OFF_XCH + 2 * 4 * 128 * 4;
   static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5 + 2;
   // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
@@ -90,8 +90,10 @@ __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) 
   return it;
 }
 
+constexpr int kFwdThreads = 576;
+
 template <int HD, int KS, int VS, bool FP8, bool PROF>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                      const Fwd2Params p) {
@@ -107,11 +109,11 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar_v_full = bar_k_full + 2 * KS;           // [VS]
   uint64_t* bar_v_empty = bar_v_full + VS;              // [VS]
   uint64_t* bar_s_full = bar_v_full + 2 * VS;           // [2]
-  uint64_t* bar_p_full = bar_s_full + 2;         // [2] 256 arrivals
+  uint64_t* bar_p_full = bar_s_full + 2;         // [2] 16 warp arrivals
   uint64_t* bar_o_full = bar_s_full + 4;         // [2] per item: last PV landed in O[k%2]
-  uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 256 arrivals: epilogue drained O[k%2]
+  uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 16 warp arrivals: epilogue drained O[k%2]
   uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
-  uint64_t* bar_o_staged = bar_s_full + 9;       // [2] 8 warp arrivals: item's O staged in its Q buffer
+  uint64_t* bar_o_staged = bar_s_full + 9;       // [2] 16 warp arrivals: item's O staged in its Q buffer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
   float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&bar_q_full[s], 1);
       mbar_init(&bar_q_empty[s], 1);
       mbar_init(&bar_s_full[s], 1);
-      mbar_init(&bar_p_full[s], 8);
+      mbar_init(&bar_p_full[s], 16);
     }
     if (smem_u32(smem) & 1023) __trap();  // swizzle atoms need 1 KB alignment
     for (int s = 0; s < KS; ++s) {
@@ -134,19 +136,19 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_o_full[s], 1);
-      mbar_init(&bar_o_empty[s], 8);
+      mbar_init(&bar_o_empty[s], 16);
     }
     mbar_init(bar_o_ready, 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&bar_o_staged[s], 8);
+    for (int s = 0; s < 2; ++s) mbar_init(&bar_o_staged[s], 16);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == 17) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 16) {
     // ================================================ TMA producer
     if (lane == 0) {
       WaitProf<PROF> wp;
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(320, 1)
       bulk_wait_all();
       wp.flush(p.prof);
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     // ================================================ MMA issuer (whole warp: descriptors and
     // counters in uniform registers; one elected lane issues)
     {
@@ -240,8 +242,8 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t a_tm = tmem + Cfg::S_COL + (pg & 1) * 128;
           const uint64_t vd = dV0 + vs * V16;
 #pragma unroll
-          for (int s = 0; s < BN / 16; ++s)  // P: columns 0-63 at +0..31, 64-127 at +64..95
-            umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s < 4 ? s * 8 : 64 + (s - 4) * 8),
+          for (int s = 0; s < BN / 16; ++s)  // P: keys 32q..32q+31 packed at S cols 32q .. 32q+15
+            umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s >> 1) * 32 + (s & 1) * 8,
                         sdesc_add(vd, s * 2048), idesc_o, (!pfirst || s > 0) ? 1u : 0u);
           umma_commit(&bar_v_empty[vs]);
           umma_commit(bar_o_ready);
@@ -294,11 +296,12 @@ __global__ void __launch_bounds__(320, 1)
       if (lane == 0) wp.flush(p.prof + 8);
     }
   } else {
-    // ================================================ softmax + epilogue warps 0-7
-    const int quad = warp & 3, half = warp >> 2;
+    // ================================================ softmax + epilogue warps 0-15
+    const int quad = warp & 3, qp = warp >> 2;  // TMEM lane quadrant; column quarter
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int r = quad * 32 + lane;
-    const int c0 = half * 64;
+    const int c0 = qp * 32;
+    constexpr int OC = HD / 4;  // O columns per quarter
     float sl2 = p.scale_log2;
     // Epilogue of item `ek` is deferred until the first tile of the next item has been handed to
     // the MMA warp, so the tensor core never idles on it (O is double-buffered in TMEM).
@@ -311,40 +314,35 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
       const bool valid = e_row < p.T;
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
-      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(valid ? e_row : 0) * p.H + e_h) * HD + half * (HD / 2);
-      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + half * (HD / 2);
+      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(valid ? e_row : 0) * p.H + e_h) * HD + qp * OC;
+      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + qp * OC;
       uint8_t* so = smem + Cfg::OFF_Q + (ek & 1) * Cfg::Q_BYTES;  // bf16: this item's Q buffer
+      uint32_t o[32];
+      tmem_ld32(o_tm, o);  // OC ≤ 32 columns (HD 64: the upper 16 belong to the next quarter, unused)
+      tmem_wait_ld();
+      uint32_t pk[16];
 #pragma unroll
-      for (int c = 0; c < HD / 2; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(o_tm + c, o);
-        tmem_wait_ld();
-        uint32_t pk[16];
+      for (int t = 0; t < OC / 2; ++t)
+        pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
+      if constexpr (FP8) {
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
-        if constexpr (FP8) {
-          if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-          }
-        } else {  // SW128 staging: 64-column box (half·HD/2 + c) / 64, chunk XOR row
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int col = half * (HD / 2) + c + 8 * t;
-            *reinterpret_cast<uint4*>(so + (col >> 6) * 16384 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4)) =
-                make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-          }
+          for (int t = 0; t < OC / 8; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
         }
-      }
-      if constexpr (!FP8) {
+      } else {  // SW128 staging: 64-column box col / 64, 16-B chunk XOR row
+#pragma unroll
+        for (int t = 0; t < OC / 8; ++t) {
+          const int col = qp * OC + 8 * t;
+          *reinterpret_cast<uint4*>(so + (col >> 6) * 16384 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        }
         fence_proxy_async_smem();
         warp_arrive(&bar_o_staged[ek & 1]);  // the producer writes the tile out
       }
       tc_fence_before();
       warp_arrive(&bar_o_empty[ek & 1]);
-      if (valid && half == 0)
+      if (valid && qp == 0)
         p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
       ek = -1;
       wp.template add_since<4>(te);
@@ -360,76 +358,52 @@ __global__ void __launch_bounds__(320, 1)
         rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
       }
       const int row = itm.q0 + r;
-      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + half * (HD / 2);
+      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + qp * OC;
       if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + itm.q0 / 128);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
         wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t x[64];
-        {
-          uint32_t a[32], b[32];
-          tmem_ld32(s_tm, a);
-          tmem_ld32(s_tm + 32, b);
-          tmem_wait_ld();
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            x[t] = a[t];
-            x[32 + t] = b[t];
-          }
-        }
+        uint32_t x[32];
+        tmem_ld32(s_tm, x);
+        tmem_wait_ld();
         const int kv0 = itm.kv_lo + j * BN + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        if constexpr (FP8) {  // per-column K block scale (a 64-column half spans at most 2 blocks)
+        if constexpr (FP8) {  // per-column K block scale (a 32-column quarter spans at most 2 blocks)
           const int b0 = kv0 / 128;
           const int cb = (b0 + 1) * 128 - kv0;
           const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
           const float k0s = __ldg(ksc + min(b0, p.nbt - 1)), k1s = __ldg(ksc + min(b0 + 1, p.nbt - 1));
 #pragma unroll
-          for (int c = 0; c < 64; ++c) x[c] = __float_as_uint(__uint_as_float(x[c]) * (c < cb ? k0s : k1s));
+          for (int c = 0; c < 32; ++c) x[c] = __float_as_uint(__uint_as_float(x[c]) * (c < cb ? k0s : k1s));
         }
-        if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 64)) {  // some row of the warp is partial
-          const int vlo = min(max(c_lo, 0), 64), vhi = min(max(c_hi, 0), 64);
-          const unsigned long long vis =
-              vhi <= vlo ? 0ull : ((vhi >= 64 ? ~0ull : (1ull << vhi) - 1ull) & ~((1ull << vlo) - 1ull));
-          const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
+        if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32)) {  // some row of the warp is partial
+          const int vlo = min(max(c_lo, 0), 32), vhi = min(max(c_hi, 0), 32);
+          const uint32_t vis = vhi <= vlo ? 0u : ((vhi >= 32 ? 0xffffffffu : (1u << vhi) - 1u) & ~((1u << vlo) - 1u));
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
-            x[c] = ((c < 32 ? v0 >> c : v1 >> (c - 32)) & 1u) ? x[c] : __float_as_uint(-INFINITY);
+          for (int c = 0; c < 32; ++c) x[c] = ((vis >> c) & 1u) ? x[c] : __float_as_uint(-INFINITY);
         }
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent max chains (FMNMX3)
 #pragma unroll
-        for (int c = 0; c < 64; c += 8) {
+        for (int c = 0; c < 32; c += 8) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) mq[u] = fmax3(mq[u], __uint_as_float(x[c + 2 * u]), __uint_as_float(x[c + 2 * u + 1]));
         }
         float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-        // combine the two column halves of this row
-        float* xs = xch + (g & 1) * 256;
-        xs[half * 128 + r] = mt;
+        // combine the four column quarters of this row
+        float* xs = xch + (g & 1) * 512;
+        xs[qp * 128 + r] = mt;
         {
           const long long tb = wp.now();
-          named_bar_sync(1 + quad, 64);
+          named_bar_sync(1 + quad, 128);
           wp.template add_since<3>(tb);
         }
-        mt = fmaxf(mt, xs[(1 - half) * 128 + r]);
+        mt = fmaxf(fmaxf(xs[r], xs[128 + r]), fmaxf(xs[256 + r], xs[384 + r]));
         mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
         const bool grow = mt > m_run + kLazyRescale;
         const float alpha = grow ? exp2f(m_run - mt) : 1.f;
-        if (__any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY)) {
-          wp.template wait<1>(bar_o_ready, (g - 1) & 1);  // PV_{g-1} has landed in O
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < HD / 2; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(o_tm + c, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-            tmem_st32(o_tm + c, o);
-          }
-        }
+        const bool rescale = __any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY);
         if (grow) {
           l_run *= alpha;
           m_run = mt;
@@ -437,32 +411,47 @@ __global__ void __launch_bounds__(320, 1)
         const float msub = (m_run == -INFINITY) ? 0.f : m_run;
         float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 independent sum chains (FADD2)
         const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+        uint32_t pk[16];
 #pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const float2 a = f2_fma(make_float2(__uint_as_float(x[c + 2 * t]), __uint_as_float(x[c + 2 * t + 1])),
-                                    sl2v, nmv);
-            const float2 pe = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-            lq[t & 1] = f2_add(lq[t & 1], pe);
-            pk[t] = pack_bf16x2(pe.x, pe.y);
-          }
-          tmem_st16(s_tm + c / 2, pk);
+        for (int t = 0; t < 16; ++t) {
+          const float2 a = f2_fma(make_float2(__uint_as_float(x[2 * t]), __uint_as_float(x[2 * t + 1])), sl2v, nmv);
+          const float2 pe = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+          lq[t & 1] = f2_add(lq[t & 1], pe);
+          pk[t] = pack_bf16x2(pe.x, pe.y);
         }
+        tmem_st16(s_tm, pk);  // P over the first 16 of this quarter's S columns
         l_run += (lq[0].x + lq[1].x) + (lq[0].y + lq[1].y);
+        // lazy O rescale (after the exp pass: x is dead), before PV(g) is released by p_full
+        if (rescale) {
+          wp.template wait<1>(bar_o_ready, (g - 1) & 1);  // PV_{g-1} has landed in O
+          tc_fence_after();
+          uint32_t o[32];
+          tmem_ld32(o_tm, o);  // OC ≤ 32 columns (HD 64: the upper 16 are rewritten unchanged... scaled)
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < OC; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+          if constexpr (OC == 32) {
+            tmem_st32(o_tm, o);
+          } else {
+            uint32_t o16[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) o16[t] = o[t];
+            tmem_st16(o_tm, o16);
+          }
+        }
+
         tmem_wait_st();
         tc_fence_before();
         warp_arrive(&bar_p_full[g & 1]);
         if (j == 0 && ek >= 0) epilogue();  // previous item, now that this tile is in flight
       }
-      // combine the halves' row sums and defer this item's epilogue
-      float* xs = xch + (g & 1) * 256;  // parity not used by any in-flight tile
-      xs[half * 128 + r] = l_run;
-      named_bar_sync(1 + quad, 64);
-      const float l_tot = l_run + xs[(1 - half) * 128 + r];
-      named_bar_sync(1 + quad, 64);  // both halves read before the slot is reused
-      if (ek >= 0) epilogue();       // (only when this item had no tiles)
+      // combine the quarters' row sums and defer this item's epilogue
+      float* xs = xch + (g & 1) * 512;  // parity not used by any in-flight tile
+      xs[qp * 128 + r] = l_run;
+      named_bar_sync(1 + quad, 128);
+      const float l_tot = (xs[r] + xs[128 + r]) + (xs[256 + r] + xs[384 + r]);
+      named_bar_sync(1 + quad, 128);  // all quarters read before the slot is reused
+      if (ek >= 0) epilogue();         // (only when this item had no tiles)
       if (itm.nkv > 0) {
         ek = k;
         e_row = row;
@@ -476,7 +465,7 @@ __global__ void __launch_bounds__(320, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == 17) tmem_dealloc<512>(tmem);
 }
 
 template <int HD, int KS, int VS, bool FP8>
@@ -512,7 +501,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
     p.prof = prof_buffer();
     auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, true>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
+    kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
     VLASIM_LAUNCH_CHECK();
     return prof_report("attn_fwd2", grid, st,
                        {"prod:q_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:q_full", "mma:k/v_full",
@@ -522,7 +511,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   p.prof = nullptr;
   auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, false>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  kern<<<grid, 320, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
+  kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }
@@ -536,7 +525,7 @@ int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, 
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
   int2* spans = static_cast<int2*>(ws);
   if (a->head_dim == 64) return launch_fwd2<64, 4, 4, false>(a, spans, st);
-  return launch_fwd2<128, 3, 2, false>(a, spans, st);
+  return launch_fwd2<128, 2, 2, false>(a, spans, st);
 }
 }  // namespace vlasim_host
 

@@ -114,6 +114,18 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
+def bwd_traffic():
+    """DRAM bytes (read + write) per backward step (3 launches) from the committed ncu --set full
+    capture (profiles/*/ncu_traffic.json); None when no capture is present."""
+    import glob
+    files = sorted(glob.glob(str(Path(__file__).parent / "profiles" / "*" / "ncu_traffic.json")))
+    if not files:
+        return None
+    ks = json.load(open(files[-1]))["kernels"]
+    tot = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in ks.items() if k.startswith("k_bwd"))
+    return {"bytes": tot, "src": str(Path(files[-1]).relative_to(Path(__file__).parent))}
+
+
 def cpu_baseline(Ls, threads):
     """The reference's CPU path (oracle restatement of SPEC.md:502-509 + closed-form bwd), fp32,
     on a bounded sample of the step's samples; returns (tokens/s, seconds, sample description)."""
@@ -358,16 +370,16 @@ def main():
                            float(fl_all.item()) / (ms_max / 1e3) / 1e12,
                        "l2": "inputs larger than L2 (%.1f GB/GPU)" % (4 * T * H * D * 2 / 1e9),
                        "parallelism": f"packs sharded over {world} GPU(s) (LPT), no collective on attention"},
-            "roofline": {"bound": "tensor", "kernel": "attn_bwd_kernel (+pre/post)",
+            "roofline": {"bound": "tensor", "kernel": "backward: k_bwd_pre + k_bwd_dkdv + k_bwd_dq",
                          "achieved": bwd_flops / (kb / 1e3) / 1e12, "peak": PEAKS["bf16_tflops"],
                          "unit": "TFLOP/s", "frac": bwd_flops / (kb / 1e3) / 1e12 / PEAKS["bf16_tflops"],
-                         "traffic": None, "peak_src": PEAKS["src"],
+                         "traffic": bwd_traffic(), "peak_src": PEAKS["src"],
                          "fwd": {"achieved": fl_fwd / (kf / 1e3) / 1e12, "ms": kf}, "bwd_ms": kb},
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
             # our launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
-            # token ids 1, gather 3, fwd 1, bwd 3 (pre, main, post; + 1 memset of the dQ accumulator)
-            "gpu_launches": 22 * a.steps,
+            # token ids 1, gather 3, fwd 2 (spans, attention), bwd 3 (pre, dK/dV, dQ)
+            "gpu_launches": 23 * a.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

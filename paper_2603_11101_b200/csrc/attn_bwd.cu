@@ -172,19 +172,23 @@ struct DkvCfg {
   static_assert(SMEM <= 232448, "smem budget");
 };
 
+// Item descriptors are loaded one item ahead; only the raw span loads are issued then and the
+// derived counts are computed when the item becomes current (kv_item_finish), so the loads'
+// latency never stalls a role at an item boundary.
 struct KvItem {
-  int k0, kh, q_lo, nq, iters;
+  int k0, kh, q_lo, q_hi, nq, iters;
 };
 __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   KvItem it;
   it.kh = i % p.Hkv;
   it.k0 = (i / p.Hkv) * 128;
-  const int2 first = __ldg(p.cols_span + it.k0);
-  const int2 last = __ldg(p.cols_span + min(it.k0 + 127, p.T - 1));
-  it.q_lo = first.x;
-  it.nq = max(0, (last.y - first.x + 63) / 64);
-  it.iters = it.nq * (p.H / p.Hkv);
+  it.q_lo = __ldg(&p.cols_span[it.k0].x);
+  it.q_hi = __ldg(&p.cols_span[min(it.k0 + 127, p.T - 1)].y);
   return it;
+}
+__device__ __forceinline__ void kv_item_finish(const BwdParams& p, KvItem& it) {
+  it.nq = max(0, (it.q_hi - it.q_lo + 63) / 64);
+  it.iters = it.nq * (p.H / p.Hkv);
 }
 
 // Walks this CTA's units in order: item i (blockIdx.x + m·gridDim.x), unit it within the item,
@@ -199,6 +203,7 @@ struct UnitCursor {
     it = k = u = 0;
     if (i >= p.kv_items) return false;
     itm = kv_item(p, i);
+    kv_item_finish(p, itm);
     if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
     return true;
   }
@@ -210,6 +215,7 @@ struct UnitCursor {
     i += gridDim.x;
     if (i >= p.kv_items) return false;
     itm = nxt;
+    kv_item_finish(p, itm);
     if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
     return true;
   }
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   uint64_t* bar_kv_full = bars + 0;
   uint64_t* bar_kv_empty = bars + 1;   // committed after the item's last S / dP
   uint64_t* bar_dkv_full = bars + 2;
-  uint64_t* bar_dkv_empty = bars + 3;  // 16 warp arrivals: TMEM dV / dK drained
+  uint64_t* bar_dkv_empty = bars + 3;  // 8 warp arrivals (the epilogue group): TMEM dV / dK drained
   uint64_t* bar_s_full = bars + 4;     // [2]
   uint64_t* bar_dp_full = bars + 6;    // [2]
   // bars + 8, + 9: spare (Pᵀ completion rides on the dSᵀ barrier: one MMA wait per unit)
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     mbar_init(bar_kv_full, 1);
     mbar_init(bar_kv_empty, 1);
     mbar_init(bar_dkv_full, 1);
-    mbar_init(bar_dkv_empty, 16);
+    mbar_init(bar_dkv_empty, 8);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
       mbar_init(&bar_dp_full[b], 1);
@@ -323,11 +329,21 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       for (bool v = c.start(p); v; v = c.next(p)) {
         if (c.it == 0) {
           if (c.k > 0) wp.template wait<1>(bar_kv_empty, (c.k - 1) & 1);
+          trace(2, c.u);  // P: K/V load issued
           mbar_expect_tx(bar_kv_full, 2 * Cfg::KT);
 #pragma unroll
           for (int j = 0; j < HD / 64; ++j) {
             tma_load_2d(smem + Cfg::OFF_K + j * 16384, &tmK, c.itm.kh * HD + j * 64, c.itm.k0, bar_kv_full);
             tma_load_2d(smem + Cfg::OFF_V + j * 16384, &tmV, c.itm.kh * HD + j * 64, c.itm.k0, bar_kv_full);
+          }
+          // the next item's K/V into L2 now: its load (single K/V buffer, issued only once this
+          // item's last dP has run) then hits L2 at the item boundary
+          if (c.i + int(gridDim.x) < p.kv_items) {
+#pragma unroll
+            for (int j = 0; j < HD / 64; ++j) {
+              tma_prefetch_2d(&tmK, c.nxt.kh * HD + j * 64, c.nxt.k0);
+              tma_prefetch_2d(&tmV, c.nxt.kh * HD + j * 64, c.nxt.k0);
+            }
           }
         }
         const int h = c.head(group), qb = c.qb();
@@ -403,8 +419,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (++as == NS) { as = 0; aph ^= 1; }
       };
       auto issue_SdP = [&] {  // S and dP of unit ca.u (both buffers of its parity are free)
+        trace(14, ca.u);  // M: boundary S/dP issue entered
         if (ca.it == 0) wp.template wait<0>(bar_kv_full, ca.k & 1);
         wp.template wait<1>(&bar_qd_full[as], aph);
+        trace(15, ca.u);  // M: K/V + Q/dO ready
         tc_fence_after();
         const uint32_t bb = ca.u & 1;
         if (elect_one()) {
@@ -482,6 +500,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     int2 ks = make_int2(0, 0), ks_nxt = ks;
     int dst_key = -1, dst_nxt = -1;
     for (bool v = c.start(p); v; v = c.next(p)) {
+      if (c.it == 0) trace(36 + g, c.u);  // S: item start (after the cursor advance)
       if (c.it == 0) {  // this item's spans were prefetched one item ahead (first item: now)
         const int key = c.itm.k0 + krow;
         ks = c.k == 0 ? span_of(key) : ks_nxt;
@@ -503,6 +522,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         // visible-column bitmask (used only when some row of the warp is partial)
         const int lo = max(c_lo, 0), hi = min(c_hi, 32);
         const uint32_t vis = hi <= lo ? 0u : ((hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u));
+        if (c.it == 0) trace(38 + g, c.u);  // S: unit set up (before the s_full wait)
         const float4* lse4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_LSE + s * Cfg::VEC) + c0 / 4;
         const float4* dsum4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_DSUM + s * Cfg::VEC) + c0 / 4;
         uint32_t pp[16];  // Pᵀ row chunk as bf16 pairs: written over S, kept for phase B
@@ -568,39 +588,39 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         trace(26 + g, c.u);  // S: ds arrived
         wp.template add_since<5>(tb);
       }
-      if (c.last()) {
-        // ---- item epilogue (all 16 warps): TMEM → registers → release TMEM → transposed 16-B
-        //      stores of the HD/4-column segments of the warp's 32 dV / dK rows
+      if (c.last() && (c.u & 1) == g) {
+        // ---- item epilogue, by the group that ran the item's last unit (the other group goes
+        //      straight on to the next item's first unit): TMEM → registers → release TMEM →
+        //      8-lane chunk transpose → stores of 4 rows × 128 B per warp instruction.  Warp
+        //      (quadrant, half hh) owns HD/2 columns of its 32 dV and dK rows; dV, then dK.
         const long long te = wp.now();
         trace(30 + (warp >> 3), c.u);  // E: epilogue entered
         wp.template wait<3>(bar_dkv_full, c.k & 1);
         trace(32 + (warp >> 3), c.u);  // E: dkv_full seen
         tc_fence_after();
-        uint32_t pv[HD / 8], pkk[HD / 8];
+        const int hh = (warp >> 2) & 1;
+        const int64_t stride = int64_t(p.Hkv) * HD;
+        const int col0 = c.itm.kh * HD + hh * (HD / 2);
+        uint32_t pw[HD / 4];
 #pragma unroll
-        for (int cc = 0; cc < HD / 4; cc += 32 > HD / 4 ? HD / 4 : 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem + lane_off + Cfg::DV_COL + part * (HD / 4) + cc, v);
-          tmem_wait_ld();
+        for (int t = 0; t < 2; ++t) {  // t = 0: dV, 1: dK (· scale)
+          const uint32_t col = (t ? Cfg::DK_COL : Cfg::DV_COL) + hh * (HD / 2);
+          const float sc = t ? p.scale : 1.f;
 #pragma unroll
-          for (int j = 0; j < (HD / 4 < 32 ? HD / 8 : 16); ++j)
-            pv[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-          tmem_ld32(tmem + lane_off + Cfg::DK_COL + part * (HD / 4) + cc, v);
-          tmem_wait_ld();
+          for (int cc = 0; cc < HD / 2; cc += 32) {
+            uint32_t v[32];
+            tmem_ld32(tmem + lane_off + col + cc, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < (HD / 4 < 32 ? HD / 8 : 16); ++j)
-            pkk[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]) * p.scale, __uint_as_float(v[2 * j + 1]) * p.scale);
-        }
-        tc_fence_before();
-        warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
-        // registers → 4-lane chunk transpose → row-segment stores through row_map (no smem, no
-        // barrier, no TMA): each warp store writes 8 rows × 64 B.
-        trace(50, c.u);  // E: TMEM drained
-        {
-          const int64_t stride = int64_t(p.Hkv) * HD;
-          const int col0 = c.itm.kh * HD + part * (HD / 4);
-          store_rows_xpose<HD / 32>(pv, dst_key, p.dv, stride, col0);
-          store_rows_xpose<HD / 32>(pkk, dst_key, p.dk, stride, col0);
+            for (int j = 0; j < 16; ++j)
+              pw[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]) * sc, __uint_as_float(v[2 * j + 1]) * sc);
+          }
+          if (t == 1) {
+            tc_fence_before();
+            warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
+            trace(50, c.u);  // E: TMEM drained
+          }
+          store_rows_xpose<HD / 16>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
         }
         trace(51, c.u);  // E: stored
         trace(34 + (warp >> 3), c.u);  // E: epilogue done
@@ -641,17 +661,20 @@ struct DqCfg {
 };
 
 struct QItem {
-  int q0, h, kh, kv_lo, nkv;
+  int q0, h, kh, kv_lo, kv_hi, nkv;
 };
-__device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {
+__device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {  // raw loads (see KvItem)
   QItem it;
   it.h = i % p.H;
   it.q0 = (i / p.H) * 128;
   it.kh = it.h / (p.H / p.Hkv);
-  const int2 a = __ldg(p.rows_span + it.q0);
-  const int2 b = __ldg(p.rows_span + min(it.q0 + 127, p.T - 1));
-  it.kv_lo = a.x;
-  it.nkv = max(0, (b.y - a.x + 127) / 128);
+  it.kv_lo = __ldg(&p.rows_span[it.q0].x);
+  it.kv_hi = __ldg(&p.rows_span[min(it.q0 + 127, p.T - 1)].y);
+  it.nkv = -1;
+  return it;
+}
+__device__ __forceinline__ QItem q_item_cur(QItem it) {  // derived count, when the item is current
+  it.nkv = max(0, (it.kv_hi - it.kv_lo + 127) / 128);
   return it;
 }
 
@@ -720,7 +743,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       int g = 0, k = 0;
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-        const QItem itm = nxt;
+        const QItem itm = q_item_cur(nxt);
         if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
@@ -798,7 +821,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       };
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-        const QItem itm = nxt;
+        const QItem itm = q_item_cur(nxt);
         if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
@@ -866,7 +889,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     float lse_n, dsum_n;
     load_row(nxt, rs_n, lse_n, dsum_n);
     for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-      const QItem itm = nxt;
+      const QItem itm = q_item_cur(nxt);
       const int2 rs = rs_n;
       const float lse2 = lse_n, dsum = dsum_n;
       if (i + int(gridDim.x) < p.q_items) {

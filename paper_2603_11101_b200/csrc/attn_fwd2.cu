@@ -75,18 +75,24 @@ struct Fwd2Cfg {
   static_assert(SMEM <= 232448, "smem budget");
 };
 
+// Items are prefetched one ahead with raw span loads only; the key-tile count is derived when
+// the item becomes current (fwd_item_cur), so the loads never stall a role at an item boundary.
 struct FwdItem {
-  int q0, h, kh, kv_lo, nkv;
+  int q0, h, kh, kv_lo, kv_hi, nkv;
 };
 __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) {
   FwdItem it;
   it.h = i % p.H;
   it.q0 = (i / p.H) * 128;
   it.kh = it.h / (p.H / p.Hkv);
-  const int2 a = __ldg(p.rows_span + it.q0);
-  const int2 b = __ldg(p.rows_span + min(it.q0 + 127, p.T - 1));
-  it.kv_lo = a.x;
-  it.nkv = max(0, (b.y - a.x + BN - 1) / BN);
+  it.kv_lo = __ldg(&p.rows_span[it.q0].x);
+  it.kv_hi = __ldg(&p.rows_span[min(it.q0 + 127, p.T - 1)].y);
+  it.nkv = -1;
+  (void)BN;
+  return it;
+}
+__device__ __forceinline__ FwdItem fwd_item_cur(FwdItem it, int BN) {
+  it.nkv = max(0, (it.kv_hi - it.kv_lo + BN - 1) / BN);
   return it;
 }
 
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       };
       FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-        const FwdItem itm = nxt;
+        const FwdItem itm = fwd_item_cur(nxt, BN);
         if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
         if (k >= 2) {
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       };
       FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-        const FwdItem itm = nxt;
+        const FwdItem itm = fwd_item_cur(nxt, BN);
         if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
         const int qs = k & 1;
         const uint64_t qd = dQ0 + qs * Q16;
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
     int2 rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
     for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
-      const FwdItem itm = nxt;
+      const FwdItem itm = fwd_item_cur(nxt, BN);
       const int2 rs = rs_n;
       if (i + int(gridDim.x) < p.num_items) {  // prefetch the next item's parameters
         nxt = fwd_item(p, i + gridDim.x, BN);

@@ -301,9 +301,72 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   if (out.status[0] != 0) return;
   // class counts → smem: a single warp, so keep 8 loads in flight per lane (latency-bound otherwise)
+  long long tok = 0;  // Σ lengths, for the bin-count bound below
 #pragma unroll 8
-  for (int L = lane; L <= cap; L += 32) cnt[L] = __ldg(ws.class_count + L);
+  for (int L = lane; L <= cap; L += 32) {
+    const int c = __ldg(ws.class_count + L);
+    cnt[L] = c;
+    tok += static_cast<long long>(c) * L;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(full, tok, o);
   __syncwarp();
+  // Register-resident fast path: FFD never opens more than 2·Σl/cap + 1 bins (every pair of
+  // consecutive bins holds more than cap tokens), so when that bound is ≤ 64 the open bins live
+  // in registers, two per lane (bins lane and 32 + lane).  Each run of a class is one first-fit
+  // step: two ballots for the lowest bin with room, the bin's room and member count broadcast
+  // from its owner lane, min(⌊room/L⌋, left) items taken at once (the class-wise argument).
+  if (2 * tok <= 63LL * cap) {
+    int rem[2] = {cap, cap}, mem[2] = {0, 0};
+    int nb = 0, nruns = 0;
+    for (int hi = cap; hi >= 1; hi -= 32) {
+      const int myL = hi - lane;
+      unsigned present = __ballot_sync(full, myL >= 1 && cnt[myL > 0 ? myL : 0] > 0);
+      while (present) {
+        const int k = __ffs(present) - 1;  // lowest lane = largest L
+        present &= present - 1;
+        const int L = hi - k;
+        const int c = cnt[L];
+        const float invL = __frcp_rn(float(L));
+        const int runs_before = nruns;
+        for (int placed = 0; placed < c;) {
+          const unsigned m0 = __ballot_sync(full, lane < nb && rem[0] >= L);
+          const unsigned m1 = __ballot_sync(full, 32 + lane < nb && rem[1] >= L);
+          const int b = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : nb);
+          if (b == nb) ++nb;  // a fresh bin (room cap, no members)
+          const int h = b >> 5, owner = b & 31;
+          const int rb = __shfl_sync(full, h ? rem[1] : rem[0], owner);
+          const int cb = __shfl_sync(full, h ? mem[1] : mem[0], owner);
+          // room >= L is guaranteed (first fit or a fresh bin): a single item needs no division
+          const int take = c - placed == 1 ? 1 : min(udiv_small(rb, L, invL), c - placed);
+          if (lane == 0) {
+            ws.run_bin[nruns] = b;
+            ws.run_cum[nruns] = placed;
+            ws.run_tok[nruns] = cap - rb;
+            ws.run_mem[nruns] = cb;
+          }
+          if (lane == owner) {
+            if (h) { rem[1] = rb - take * L; mem[1] = cb + take; }
+            else { rem[0] = rb - take * L; mem[0] = cb + take; }
+          }
+          ++nruns;
+          placed += take;
+        }
+        if (lane == 0) {
+          ws.class_run_start[L] = runs_before;
+          ws.class_nruns[L] = nruns - runs_before;
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (32 * h + lane < nb) {
+        out.bin_count[32 * h + lane] = mem[h];
+        out.bin_fill[32 * h + lane] = cap - rem[h];
+      }
+    if (lane == 0) *out.num_bins = nb;
+    return;
+  }
   int nb = 0, nruns = 0;
   for (int hi = cap; hi >= 1; hi -= 32) {
     const int myL = hi - lane;

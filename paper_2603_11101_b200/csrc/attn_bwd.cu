@@ -131,6 +131,7 @@ struct BwdParams {
   float scale_log2, scale;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
   int dbg;                   // VLASIM_DBG ablations, honoured by the PROF instantiation only (timing experiments)
+  int ohalf;                 // dK/dV head-dim half of this launch (head_dim 256: two launches; else 0)
 };
 
 // ================================================================== dK / dV (KV-stationary)
@@ -150,26 +151,37 @@ struct BwdParams {
 // the next item's descriptor so item boundaries do not expose a global-load round trip.  The
 // item epilogue writes dK/dV from TMEM-loaded registers through row_map after a 4-lane chunk
 // transpose (store_rows_xpose: 8 rows × 64 B per warp store; no smem staging, barrier or TMA).
-// TMEM: S0 [0,64) · S1 [64,128) · dP0 [128,192) · dP1 [192,256) · dV · dK.
-template <int HD>
+// TMEM: S0 [0,UQ) · S1 [UQ,2UQ) · dP0 [128,128+UQ) · dP1 [128+UQ,..) · dV · dK.
+// head_dim 256: dV and dK of the full head dim (2 × 256 fp32 columns) do not fit next to S / dP,
+// so two launches each accumulate one 128-column half (p.ohalf; S / dP recomputed), and the
+// unit is 32 queries (UQ) so that 3 Q/dO stages fit beside the 64 KB K and V tiles.
+template <int HD, int UQ = 64>
 struct DkvCfg {
+  static constexpr int HO = HD < 128 ? HD : 128;  // dK / dV head-dim columns per launch
+  static constexpr int CW = UQ / 2;               // query columns per softmax warp
+  static constexpr int QBOX = UQ * 128;           // one 64-column TMA box of a Q / dO stage
   static constexpr int KT = 128 * HD * 2;  // K or V tile (128 keys)
-  static constexpr int QT = 64 * HD * 2;   // Q or dO tile (64 queries)
-  static constexpr int NS = 5;             // Q / dO stages
+  static constexpr int QT = UQ * HD * 2;   // Q or dO tile (UQ queries)
+  static constexpr int NS = HD == 256 ? 3 : 5;  // Q / dO stages
   static constexpr int OFF_K = 0, OFF_V = KT;
   static constexpr int OFF_Q = 2 * KT;              // [NS]
   static constexpr int OFF_DO = OFF_Q + NS * QT;    // [NS]
-  static constexpr int VEC = 256;                   // 64 floats of lse2 / D (16-B aligned window)
+  static constexpr int VEC = UQ * 4;                // UQ floats of lse2 / D (16-B aligned window)
   static constexpr int OFF_LSE = OFF_DO + NS * QT;  // [NS][VEC]
   static constexpr int OFF_DSUM = OFF_LSE + NS * VEC;
   static constexpr int OFF_BAR = OFF_DSUM + NS * VEC;
   static constexpr int NUM_BARS = 12 + 2 * NS;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
-  static constexpr uint32_t DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
-  __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? 64u : 0u; }
-  __host__ __device__ static constexpr uint32_t dp_col(int b) { return b ? 192u : 128u; }
-  static_assert(DK_COL + HD <= 512, "TMEM budget");
+  static constexpr uint32_t DV_COL = 256, DK_COL = 256 + HO;
+  __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? uint32_t(UQ) : 0u; }
+  __host__ __device__ static constexpr uint32_t dp_col(int b) { return 128u + (b ? uint32_t(UQ) : 0u); }
+  // TMEM column of K-step j (16 queries) of Pᵀ / dSᵀ: warp chunks of CW queries sit at column
+  // offsets part·CW, each packed into CW/2 columns as bf16 pairs
+  __host__ __device__ static constexpr uint32_t a_col(int j) { return (j / (CW / 16)) * CW + (j % (CW / 16)) * 8; }
+  static_assert(UQ == 64 || UQ == 32, "unit width");
+  static_assert(DK_COL + HO <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
+  static_assert(4 * 2001 * 8 <= 2 * NS * QT, "PROF trace fits the Q/dO stages");
 };
 
 // Item descriptors are loaded one item ahead; only the raw span loads are issued then and the
@@ -186,8 +198,9 @@ __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   it.q_hi = __ldg(&p.cols_span[min(it.k0 + 127, p.T - 1)].y);
   return it;
 }
+template <int UQ>
 __device__ __forceinline__ void kv_item_finish(const BwdParams& p, KvItem& it) {
-  it.nq = max(0, (it.q_hi - it.q_lo + 63) / 64);
+  it.nq = max(0, (it.q_hi - it.q_lo + UQ - 1) / UQ);
   it.iters = it.nq * (p.H / p.Hkv);
 }
 
@@ -195,6 +208,7 @@ __device__ __forceinline__ void kv_item_finish(const BwdParams& p, KvItem& it) {
 // k = ordinal of the item, u = ordinal of the unit.  The next item's descriptor is loaded one
 // item ahead (its global loads overlap the current item).  Every key sees itself, so every
 // item has iters ≥ 1.
+template <int UQ>
 struct UnitCursor {
   int i, it, k, u;
   KvItem itm, nxt;
@@ -203,7 +217,7 @@ struct UnitCursor {
     it = k = u = 0;
     if (i >= p.kv_items) return false;
     itm = kv_item(p, i);
-    kv_item_finish(p, itm);
+    kv_item_finish<UQ>(p, itm);
     if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
     return true;
   }
@@ -215,13 +229,13 @@ struct UnitCursor {
     i += gridDim.x;
     if (i >= p.kv_items) return false;
     itm = nxt;
-    kv_item_finish(p, itm);
+    kv_item_finish<UQ>(p, itm);
     if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
     return true;
   }
   __device__ __forceinline__ bool last() const { return it + 1 == itm.iters; }
   __device__ __forceinline__ int head(int group) const { return itm.kh * group + it / itm.nq; }
-  __device__ __forceinline__ int qb() const { return itm.q_lo + (it % itm.nq) * 64; }
+  __device__ __forceinline__ int qb() const { return itm.q_lo + (it % itm.nq) * UQ; }
 };
 
 // Epilogue row store without smem: thread (row = lane of a 32-row warp slab, part) holds CPT 16-B
@@ -269,13 +283,13 @@ __device__ __forceinline__ void store_rows_xpose(uint32_t (&w)[4 * CPT], int dst
 // Warp 16 TMA producer, warp 17 TMEM allocator + MMA issuer.
 constexpr int kDkvThreads = 576;
 
-template <int HD, bool PROF>
+template <int HD, int UQ, bool PROF>
 __global__ void __launch_bounds__(kDkvThreads, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const BwdParams p) {
-  using Cfg = DkvCfg<HD>;
-  constexpr int NS = Cfg::NS;
+  using Cfg = DkvCfg<HD, UQ>;
+  constexpr int NS = Cfg::NS, HO = Cfg::HO, CW = Cfg::CW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_kv_full = bars + 0;
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     if (lane == 0) {
       WaitProf<PROF> wp;
       TraceCtr trace(trb);
-      UnitCursor c;
+      UnitCursor<UQ> c;
       int s = 0;          // stage of unit c.u (= c.u % NS)
       uint32_t ph = 0;    // parity of that stage's current use
       for (bool v = c.start(p); v; v = c.next(p)) {
@@ -354,14 +368,15 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (PROF && (p.dbg & 2)) {  // timing experiment: no Q/dO traffic (the trace lives in the Q stages)
           mbar_arrive(&bar_qd_full[s]);
         } else {
-          mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + 512);
+          mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + 2 * Cfg::VEC);
 #pragma unroll
           for (int j = 0; j < HD / 64; ++j) {
-            tma_load_2d(smem + Cfg::OFF_Q + s * Cfg::QT + j * 8192, &tmQ, h * HD + j * 64, qb, &bar_qd_full[s]);
-            tma_load_2d(smem + Cfg::OFF_DO + s * Cfg::QT + j * 8192, &tmdO, h * HD + j * 64, qb, &bar_qd_full[s]);
+            tma_load_2d(smem + Cfg::OFF_Q + s * Cfg::QT + j * Cfg::QBOX, &tmQ, h * HD + j * 64, qb, &bar_qd_full[s]);
+            tma_load_2d(smem + Cfg::OFF_DO + s * Cfg::QT + j * Cfg::QBOX, &tmdO, h * HD + j * 64, qb,
+                        &bar_qd_full[s]);
           }
-          bulk_load(smem + Cfg::OFF_LSE + s * Cfg::VEC, p.lse2 + vo, 256, &bar_qd_full[s]);
-          bulk_load(smem + Cfg::OFF_DSUM + s * Cfg::VEC, p.dsum + vo, 256, &bar_qd_full[s]);
+          bulk_load(smem + Cfg::OFF_LSE + s * Cfg::VEC, p.lse2 + vo, Cfg::VEC, &bar_qd_full[s]);
+          bulk_load(smem + Cfg::OFF_DSUM + s * Cfg::VEC, p.dsum + vo, Cfg::VEC, &bar_qd_full[s]);
         }
         if (++s == NS) {
           s = 0;
@@ -379,8 +394,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     // behind the next item's K/V load (single K/V buffer).  The warp's serial instruction
     // latency is the budget here, so stages and parities are counters, never u % NS.
     {
-      constexpr uint32_t id_s = make_idesc_bf16(128, 64, false, false);   // Sᵀ, dPᵀ
-      constexpr uint32_t id_acc = make_idesc_bf16(128, HD, false, true);  // dV, dK
+      constexpr uint32_t id_s = make_idesc_bf16(128, UQ, false, false);   // Sᵀ, dPᵀ
+      constexpr uint32_t id_acc = make_idesc_bf16(128, HO, false, true);  // dV, dK (this launch's half)
       constexpr uint32_t QT16 = Cfg::QT >> 4;                             // stage stride, desc units
       WaitProf<PROF> wp;
       TraceCtr trace(lane == 0 && trb ? trb + 2001 : nullptr);
@@ -388,8 +403,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       const uint64_t dV0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), 16, 1024);
       const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);     // K-major view
       const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
-      const uint64_t dQm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 8192, 1024);   // MN-major view
-      const uint64_t dOm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 8192, 1024);
+      // MN-major views of this launch's head-dim half (boxes of 64 columns, QBOX bytes apart)
+      const uint32_t hoff = uint32_t(p.ohalf) * (HO / 64) * Cfg::QBOX;
+      const uint64_t dQm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q) + hoff, Cfg::QBOX, 1024);
+      const uint64_t dOm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO) + hoff, Cfg::QBOX, 1024);
       // Descriptor bases are made opaque where they are used (empty asm), so the per-MMA operand
       // descriptors are formed by uniform adds interleaved with the MMAs (hidden behind MMA-queue
       // back-pressure) instead of being hoisted into ~20 registers re-converted every unit.
@@ -402,16 +419,16 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j)
           umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
-                      sdesc_add(b0, (j / 4) * 8192 + (j % 4) * 32), id_s, j > 0);
+                      sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
       };
       auto mma_dP = [&](uint32_t col, uint32_t soff) {
         const uint64_t a0 = opaque(dV0), b0 = opaque(dOk) + soff;
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j)
           umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
-                      sdesc_add(b0, (j / 4) * 8192 + (j % 4) * 32), id_s, j > 0);
+                      sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
       };
-      UnitCursor ca, cc;
+      UnitCursor<UQ> ca, cc;
       uint32_t as = 0, aph = 0;  // stage / parity of the look-ahead unit ca.u
       bool va = false;
       auto adv_a = [&] {
@@ -453,8 +470,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
 #pragma unroll
           const uint64_t om = opaque(dOm) + coff, qm = opaque(dQm) + coff;
-          for (int j = 0; j < 4; ++j)
-            umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+          for (int j = 0; j < UQ / 16; ++j)
+            umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + Cfg::a_col(j),
                         sdesc_add(om, j * 2048), id_acc, j > 0 ? 1u : acc0);
           if (early) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
             mma_S(Cfg::s_col(b), aoff);
@@ -462,8 +479,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           }
           // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + (j >> 1) * 32 + (j & 1) * 8,
+          for (int j = 0; j < UQ / 16; ++j)
+            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + Cfg::a_col(j),
                         sdesc_add(qm, j * 2048), id_acc, j > 0 ? 1u : acc0);
           umma_commit(&bar_qd_empty[cs]);
           if (c_last) umma_commit(bar_dkv_full);
@@ -490,10 +507,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     const int g = warp >> 3, quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int krow = quad * 32 + lane;
-    const int c0 = (part & 1) * 32;
+    const int c0 = (part & 1) * CW;
     WaitProf<PROF, 12> wp;
     TraceCtr trace(lane == 0 && (warp & 7) == 0 && trb ? trb + 2001 * (2 + (warp >> 3)) : nullptr);
-    UnitCursor c;
+    UnitCursor<UQ> c;
     auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
     auto dst_of = [&](int key) { return key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1; };
     int ss = 0;  // stage of unit c.u
@@ -517,26 +534,27 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const uint32_t ph = (c.u >> 1) & 1;
         const int qb = c.qb();
         const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible columns of this half
-        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
-        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= 32) || (PROF && (p.dbg & 1));  // ablation
+        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= CW);
+        const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= CW) || (PROF && (p.dbg & 1));  // ablation
         // visible-column bitmask (used only when some row of the warp is partial)
-        const int lo = max(c_lo, 0), hi = min(c_hi, 32);
+        const int lo = max(c_lo, 0), hi = min(c_hi, CW);
         const uint32_t vis = hi <= lo ? 0u : ((hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u));
         if (c.it == 0) trace(38 + g, c.u);  // S: unit set up (before the s_full wait)
         const float4* lse4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_LSE + s * Cfg::VEC) + c0 / 4;
         const float4* dsum4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_DSUM + s * Cfg::VEC) + c0 / 4;
-        uint32_t pp[16];  // Pᵀ row chunk as bf16 pairs: written over S, kept for phase B
+        uint32_t pp[CW / 2];  // Pᵀ row chunk as bf16 pairs: written over S, kept for phase B
         // ---- phase A: Sᵀ → Pᵀ (bf16 over the S columns)
         wp.template wait<0>(&bar_s_full[g], ph);
         trace(20 + g, c.u);  // S: s_full seen
         const long long ta = wp.now();
         tc_fence_after();
         if (!none) {
-          uint32_t sa[32];
-          tmem_ld32(tmem + lane_off + Cfg::s_col(g) + c0, sa);
+          uint32_t sa[CW];
+          if constexpr (CW == 32) tmem_ld32(tmem + lane_off + Cfg::s_col(g) + c0, sa);
+          else tmem_ld16(tmem + lane_off + Cfg::s_col(g) + c0, sa);
           tmem_wait_ld();
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
+          for (int j4 = 0; j4 < CW / 4; ++j4) {
             const float4 l = lse4[j4];  // 128-bit broadcast load
             float e[4];
             e[0] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 0]), p.scale_log2, -l.x));
@@ -552,9 +570,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) pp[j] = 0u;
+          for (int j = 0; j < CW / 2; ++j) pp[j] = 0u;
         }
-        tmem_st16(tmem + lane_off + Cfg::s_col(g) + c0, pp);  // completion awaited with dS's (phase B)
+        if constexpr (CW == 32) tmem_st16(tmem + lane_off + Cfg::s_col(g) + c0, pp);
+        else tmem_st8(tmem + lane_off + Cfg::s_col(g) + c0, pp);  // completion awaited with dS's (phase B)
         trace(22 + g, c.u);  // S: P written
         wp.template add_since<4>(ta);
         // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns (P as the dV GEMM saw it)
@@ -562,13 +581,14 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         trace(24 + g, c.u);  // S: dp_full seen
         const long long tb = wp.now();
         tc_fence_after();
-        uint32_t pk[16];
+        uint32_t pk[CW / 2];
         if (!none) {
-          uint32_t dr[32];
-          tmem_ld32(tmem + lane_off + Cfg::dp_col(g) + c0, dr);
+          uint32_t dr[CW];
+          if constexpr (CW == 32) tmem_ld32(tmem + lane_off + Cfg::dp_col(g) + c0, dr);
+          else tmem_ld16(tmem + lane_off + Cfg::dp_col(g) + c0, dr);
           tmem_wait_ld();
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
+          for (int j4 = 0; j4 < CW / 4; ++j4) {
             const float4 dd = dsum4[j4];  // 128-bit broadcast load
             const int q = 4 * j4;
             const float p0 = __uint_as_float(pp[2 * j4] << 16), p1 = __uint_as_float(pp[2 * j4] & 0xFFFF0000u);
@@ -579,9 +599,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = 0u;
+          for (int j = 0; j < CW / 2; ++j) pk[j] = 0u;
         }
-        tmem_st16(tmem + lane_off + Cfg::dp_col(g) + c0, pk);
+        if constexpr (CW == 32) tmem_st16(tmem + lane_off + Cfg::dp_col(g) + c0, pk);
+        else tmem_st8(tmem + lane_off + Cfg::dp_col(g) + c0, pk);
         tmem_wait_st();
         tc_fence_before();
         warp_arrive(&bar_ds_full[g]);
@@ -600,14 +621,14 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_after();
         const int hh = (warp >> 2) & 1;
         const int64_t stride = int64_t(p.Hkv) * HD;
-        const int col0 = c.itm.kh * HD + hh * (HD / 2);
-        uint32_t pw[HD / 4];
+        const int col0 = c.itm.kh * HD + p.ohalf * HO + hh * (HO / 2);
+        uint32_t pw[HO / 4];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {  // t = 0: dV, 1: dK (· scale)
-          const uint32_t col = (t ? Cfg::DK_COL : Cfg::DV_COL) + hh * (HD / 2);
+          const uint32_t col = (t ? Cfg::DK_COL : Cfg::DV_COL) + hh * (HO / 2);
           const float sc = t ? p.scale : 1.f;
 #pragma unroll
-          for (int cc = 0; cc < HD / 2; cc += 32) {
+          for (int cc = 0; cc < HO / 2; cc += 32) {
             uint32_t v[32];
             tmem_ld32(tmem + lane_off + col + cc, v);
             tmem_wait_ld();
@@ -620,7 +641,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
             trace(50, c.u);  // E: TMEM drained
           }
-          store_rows_xpose<HD / 16>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
+          store_rows_xpose<HO / 16>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
         }
         trace(51, c.u);  // E: stored
         trace(34 + (warp >> 3), c.u);  // E: epilogue done
@@ -645,18 +666,23 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 //   dQ += dS·K                                                (A from TMEM, B = K MN-major)
 // and writes dQ = scale · dQacc once per item in bf16 (through row_map).  Deterministic: no atomics.
 // TMEM: S0 [0,128) · dP [128,256) · dQ [256,256+HD) · S1 [384,512).
-template <int HD, int KS, int VS>
+template <int HD, int BN, int KS, int VS>
 struct DqCfg {
-  static constexpr int TILE = 128 * HD * 2;
+  static constexpr int TILE = 128 * HD * 2;          // Q / dO tile (128 rows)
+  static constexpr int KTILE = BN * HD * 2;          // K / V tile (BN keys)
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
   static constexpr int OFF_K = 2 * TILE;             // K ring [KS]: released after dQ
-  static constexpr int OFF_V = OFF_K + KS * TILE;    // V ring [VS]: released after dP
-  static constexpr int OFF_BAR = OFF_V + VS * TILE;
+  static constexpr int OFF_V = OFF_K + KS * KTILE;   // V ring [VS]: released after dP
+  static constexpr int OFF_BAR = OFF_V + VS * KTILE;
   static constexpr int NUM_BARS = 2 + 2 * KS + 2 * VS + 8;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
+  // TMEM: BN 128 → S0 [0,128) · dP [128,256) · dQ [256,256+HD) · S1 [384,512)
+  //       BN  64 → S0 [0,64) · S1 [64,128) · dP [128,192) · dQ [256,256+HD)   (HD up to 256)
   static constexpr uint32_t DP_COL = 128, DQ_COL = 256;
-  __host__ __device__ static constexpr uint32_t s_col(int g) { return (g & 1) ? 384u : 0u; }
-  static_assert(DQ_COL + HD <= 384, "TMEM budget");
+  __host__ __device__ static constexpr uint32_t s_col(int g) {
+    return BN == 128 ? ((g & 1) ? 384u : 0u) : ((g & 1) ? 64u : 0u);
+  }
+  static_assert(BN == 128 ? DQ_COL + HD <= 384 : DQ_COL + HD <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
 };
 
@@ -673,21 +699,22 @@ __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {  // raw loa
   it.nkv = -1;
   return it;
 }
-__device__ __forceinline__ QItem q_item_cur(QItem it) {  // derived count, when the item is current
-  it.nkv = max(0, (it.kv_hi - it.kv_lo + 127) / 128);
+__device__ __forceinline__ QItem q_item_cur(QItem it, int BN) {  // derived count, when the item is current
+  it.nkv = max(0, (it.kv_hi - it.kv_lo + BN - 1) / BN);
   return it;
 }
 
 // Warp roles (576 threads): warps 0-15 softmax — warp w owns Q rows 32·(w%4).. (TMEM lane quadrant
-// w%4) and key columns [32·(w/4), +32) of each 128-key tile; warp 16 TMA producer; warp 17 TMEM
-// allocator + MMA issuer.
+// w%4) and key columns [BN/4·(w/4), +BN/4) of each BN-key tile; warp 16 TMA producer; warp 17
+// TMEM allocator + MMA issuer.  BN = 128 for head_dim ≤ 128, 64 for head_dim 256 (TMEM / smem).
 constexpr int kDqThreads = 576;
 
-template <int HD, int KS, int VS, bool PROF>
+template <int HD, int BN, int KS, int VS, bool PROF>
 __global__ void __launch_bounds__(kDqThreads, 1)
     k_bwd_dq(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams p) {
-  using Cfg = DqCfg<HD, KS, VS>;
+  using Cfg = DqCfg<HD, BN, KS, VS>;
+  constexpr int W = BN / 4;  // key columns per softmax warp
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
@@ -743,7 +770,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       int g = 0, k = 0;
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-        const QItem itm = q_item_cur(nxt);
+        const QItem itm = q_item_cur(nxt, BN);
         if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
@@ -755,25 +782,27 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           tma_load_2d(smem + Cfg::OFF_DO + c * 16384, &tmdO, itm.h * HD + c * 64, itm.q0, bar_qdo_full);
         }
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int kv0 = itm.kv_lo + j * 128;
+          const int kv0 = itm.kv_lo + j * BN;
           const int ks = g % KS, vs = g % VS;
           if (g >= KS) mbar_wait(&bar_k_empty[ks], ((g / KS) - 1) & 1);
           if (PROF && (p.dbg & 2)) {  // timing experiment: no K/V traffic (the trace lives in the K ring)
             mbar_arrive(&bar_k_full[ks]);
           } else {
-            mbar_expect_tx(&bar_k_full[ks], Cfg::TILE);
+            mbar_expect_tx(&bar_k_full[ks], Cfg::KTILE);
 #pragma unroll
             for (int c = 0; c < HD / 64; ++c)
-              tma_load_2d(smem + Cfg::OFF_K + ks * Cfg::TILE + c * 16384, &tmK, itm.kh * HD + c * 64, kv0, &bar_k_full[ks]);
+              tma_load_2d(smem + Cfg::OFF_K + ks * Cfg::KTILE + c * (BN * 128), &tmK, itm.kh * HD + c * 64, kv0,
+                          &bar_k_full[ks]);
           }
           if (g >= VS) mbar_wait(&bar_v_empty[vs], ((g / VS) - 1) & 1);
           if (PROF && (p.dbg & 2)) {
             mbar_arrive(&bar_v_full[vs]);
           } else {
-            mbar_expect_tx(&bar_v_full[vs], Cfg::TILE);
+            mbar_expect_tx(&bar_v_full[vs], Cfg::KTILE);
 #pragma unroll
             for (int c = 0; c < HD / 64; ++c)
-              tma_load_2d(smem + Cfg::OFF_V + vs * Cfg::TILE + c * 16384, &tmV, itm.kh * HD + c * 64, kv0, &bar_v_full[vs]);
+              tma_load_2d(smem + Cfg::OFF_V + vs * Cfg::KTILE + c * (BN * 128), &tmV, itm.kh * HD + c * 64, kv0,
+                          &bar_v_full[vs]);
           }
         }
         ++k;
@@ -785,14 +814,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // previous item's last dQ is issued before waiting for the next item's Q/dO, so dq_full —
     // and the epilogue — never wait behind that load.
     {
-      constexpr uint32_t id_kk = make_idesc_bf16(128, 128, false, false);  // S, dP
+      constexpr uint32_t id_kk = make_idesc_bf16(128, BN, false, false);   // S, dP
       constexpr uint32_t id_dq = make_idesc_bf16(128, HD, false, true);    // dQ (A from TMEM, B MN-major)
-      constexpr uint32_t T16 = Cfg::TILE >> 4;                             // ring stage stride, desc units
+      constexpr uint32_t T16 = Cfg::KTILE >> 4;                            // ring stage stride, desc units
       const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
       const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
       const uint64_t dKk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16, 1024);
       const uint64_t dVk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), 16, 1024);
-      const uint64_t dKm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16384, 1024);  // MN-major view
+      const uint64_t dKm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), BN * 128, 1024);  // MN-major view
       int g = 0, k = 0;
       int ks = 0, vs = 0;          // K / V ring stages of tile g
       uint32_t kph = 0, vph = 0;   // their use parities
@@ -809,9 +838,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (elect_one()) {
           const uint32_t a = tmem + Cfg::s_col(pg);
 #pragma unroll
-          for (int s = 0; s < 8; ++s)  // dS: keys 32p..32p+31 packed at S cols 32p .. 32p+15
-            umma_f16_ts(tmem + Cfg::DQ_COL, a + (s >> 1) * 32 + (s & 1) * 8, sdesc_add(dKm, s * 2048) + pks * T16,
-                        id_dq, (!pfirst || s > 0) ? 1u : 0u);
+          for (int s = 0; s < BN / 16; ++s)  // dS: keys Wp..Wp+W−1 packed at S cols Wp .. Wp+W/2−1
+            umma_f16_ts(tmem + Cfg::DQ_COL, a + (s / (W / 16)) * W + (s % (W / 16)) * 8,
+                        sdesc_add(dKm, s * 2048) + pks * T16, id_dq, (!pfirst || s > 0) ? 1u : 0u);
           umma_commit(&bar_k_empty[pks]);
           if (plast) umma_commit(bar_dq_full);
         }
@@ -821,7 +850,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       };
       QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
       for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-        const QItem itm = q_item_cur(nxt);
+        const QItem itm = q_item_cur(nxt, BN);
         if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
         if (itm.nkv == 0) continue;
         if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
@@ -835,7 +864,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
             for (int s = 0; s < HD / 16; ++s)
               umma_f16_ss(tmem + Cfg::s_col(g), sdesc_add(dQk, (s / 4) * 16384 + (s % 4) * 32),
-                          sdesc_add(dKk, (s / 4) * 16384 + (s % 4) * 32) + ks * T16, id_kk, s > 0);
+                          sdesc_add(dKk, (s / 4) * (BN * 128) + (s % 4) * 32) + ks * T16, id_kk, s > 0);
             umma_commit(&bar_s_full[g & 1]);
           }
           __syncwarp();
@@ -847,7 +876,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
             for (int s = 0; s < HD / 16; ++s)
               umma_f16_ss(tmem + Cfg::DP_COL, sdesc_add(dOk, (s / 4) * 16384 + (s % 4) * 32),
-                          sdesc_add(dVk, (s / 4) * 16384 + (s % 4) * 32) + vs * T16, id_kk, s > 0);
+                          sdesc_add(dVk, (s / 4) * (BN * 128) + (s % 4) * 32) + vs * T16, id_kk, s > 0);
             umma_commit(bar_dp_full);
             umma_commit(&bar_v_empty[vs]);
             if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
@@ -873,7 +902,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const int quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const int r = quad * 32 + lane;
-    const int c0 = part * 32;
+    const int c0 = part * W;
     TraceCtr trace(lane == 0 && (warp == 0 || warp == 4) && trb ? trb + 2001 * (2 + (part & 1)) : nullptr);
     int g = 0, k = 0;
     // row parameters of the next item are prefetched one item ahead
@@ -889,7 +918,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     float lse_n, dsum_n;
     load_row(nxt, rs_n, lse_n, dsum_n);
     for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
-      const QItem itm = q_item_cur(nxt);
+      const QItem itm = q_item_cur(nxt, BN);
       const int2 rs = rs_n;
       const float lse2 = lse_n, dsum = dsum_n;
       if (i + int(gridDim.x) < p.q_items) {
@@ -901,23 +930,24 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const bool valid = row < p.T;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
-        const int kv0 = itm.kv_lo + j * 128 + c0;
+        const int kv0 = itm.kv_lo + j * BN + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        // visible columns of this 32-column quarter as a bitmask (rows are intervals)
-        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
-        const int vlo = min(max(c_lo, 0), 32), vhi = min(max(c_hi, 0), 32);
+        // visible columns of this W-column slice as a bitmask (rows are intervals)
+        const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= W);
+        const int vlo = min(max(c_lo, 0), W), vhi = min(max(c_hi, 0), W);
         const uint32_t vm = vhi <= vlo ? 0u : ((vhi >= 32 ? 0xffffffffu : (1u << vhi) - 1u) & ~((1u << vlo) - 1u));
         mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
         trace(20, g);  // S: s_full seen
         tc_fence_after();
-        float2 pr[16];  // P (fp32 pairs) kept for phase B
+        float2 pr[W / 2];  // P (fp32 pairs) kept for phase B
         const float2 sl2v = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(-lse2, -lse2);
         {
-          uint32_t sr[32];
-          tmem_ld32(s_tm, sr);
+          uint32_t sr[W];
+          if constexpr (W == 32) tmem_ld32(s_tm, sr);
+          else tmem_ld16(s_tm, sr);
           tmem_wait_ld();
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
+          for (int t = 0; t < W / 2; ++t) {
             const float2 a = f2_fma(make_float2(__uint_as_float(sr[2 * t]), __uint_as_float(sr[2 * t + 1])), sl2v, nl2);
             float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
             if (!all_full) {
@@ -933,18 +963,20 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         tc_fence_after();
         const float2 nd2 = make_float2(-dsum, -dsum);
         {
-          uint32_t dr[32];
-          tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0, dr);
+          uint32_t dr[W];
+          if constexpr (W == 32) tmem_ld32(tmem + lane_off + Cfg::DP_COL + c0, dr);
+          else tmem_ld16(tmem + lane_off + Cfg::DP_COL + c0, dr);
           tmem_wait_ld();
           tc_fence_before();
           warp_arrive(bar_dp_free);  // dP(g) is in registers: the MMA may issue dP(g+1)
-          uint32_t dk[16];
+          uint32_t dk[W / 2];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {  // dS = P ∘ (dP − D): FADD2 + FMUL2 per pair
+          for (int t = 0; t < W / 2; ++t) {  // dS = P ∘ (dP − D): FADD2 + FMUL2 per pair
             const float2 ds = f2_mul(pr[t], f2_add(make_float2(__uint_as_float(dr[2 * t]), __uint_as_float(dr[2 * t + 1])), nd2));
             dk[t] = pack_bf16x2(ds.x, ds.y);
           }
-          tmem_st16(s_tm, dk);  // dS over the first 16 of this quarter's S columns
+          if constexpr (W == 32) tmem_st16(s_tm, dk);  // dS over the first W/2 of this slice's S columns
+          else tmem_st8(s_tm, dk);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -966,6 +998,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         for (int t = 0; t < (HD / 4 < 32 ? HD / 8 : 16); ++t)
           pq[c / 2 + t] = pack_bf16x2(__uint_as_float(v[2 * t]) * p.scale, __uint_as_float(v[2 * t + 1]) * p.scale);
       }
+      static_assert(HD / 4 <= 64, "dQ quarter held in registers");
       tc_fence_before();
       warp_arrive(bar_dq_empty);  // TMEM drained: the next item's first dQ MMA may start
       // registers → 4-lane chunk transpose → row-segment stores through row_map (8 rows × 64 B
@@ -1026,9 +1059,18 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   if (int rc = encode_tmap_2d(&tdo, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tk, a->k, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 128, 64, true)) return rc;
-  CUtensorMap tq64, tdo64;  // 64-query tiles of the dK/dV kernel
-  if (int rc = encode_tmap_2d(&tq64, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 64, 64, true)) return rc;
-  if (int rc = encode_tmap_2d(&tdo64, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 64, 64, true))
+  CUtensorMap tk64, tv64;  // 64-key tiles of the dQ kernel (head_dim 256)
+  if (HD == 256) {
+    if (int rc = encode_tmap_2d(&tk64, a->k, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 64, 64, true)) return rc;
+    if (int rc = encode_tmap_2d(&tv64, a->v, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, 64, 64, true)) return rc;
+  } else {
+    tk64 = tk;
+    tv64 = tv;
+  }
+  constexpr int UQ = HD == 256 ? 32 : 64;  // query unit of the dK/dV kernel
+  CUtensorMap tqu, tdou;                    // UQ-row Q / dO boxes of the dK/dV kernel
+  if (int rc = encode_tmap_2d(&tqu, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, UQ, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&tdou, g->dout, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, UQ, 64, true))
     return rc;
   BwdParams p;
   p.dq = static_cast<__nv_bfloat16*>(g->dq);
@@ -1049,13 +1091,15 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;
   p.dbg = getenv("VLASIM_DBG") ? atoi(getenv("VLASIM_DBG")) : 0;
-  {
-    using Cfg = DkvCfg<HD>;
+  p.ohalf = 0;
+  for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO; ++half) {
+    using Cfg = DkvCfg<HD, UQ>;
     const int grid = std::min(p.kv_items, num_sms());
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
-    auto kern = p.prof ? k_bwd_dkdv<HD, true> : k_bwd_dkdv<HD, false>;
+    p.ohalf = half;
+    auto kern = p.prof ? k_bwd_dkdv<HD, UQ, true> : k_bwd_dkdv<HD, UQ, false>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tq64, tk, tv, tdo64, p);
+    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tqu, tk, tv, tdou, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,
@@ -1065,13 +1109,14 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
                    "", "", "", "smx:total"});
   }
   {
-    constexpr int KS = HD == 64 ? 5 : 3, VS = HD == 64 ? 4 : 2;
-    using Cfg = DqCfg<HD, KS, VS>;
-    auto kern = p.prof ? k_bwd_dq<HD, KS, VS, true> : k_bwd_dq<HD, KS, VS, false>;
+    constexpr int BN = HD == 256 ? 64 : 128;
+    constexpr int KS = HD == 64 ? 5 : (HD == 128 ? 3 : 2), VS = HD == 64 ? 4 : (HD == 128 ? 2 : 1);
+    using Cfg = DqCfg<HD, BN, KS, VS>;
+    auto kern = p.prof ? k_bwd_dq<HD, BN, KS, VS, true> : k_bwd_dq<HD, BN, KS, VS, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     const int grid = std::min(p.q_items, num_sms());
-    kern<<<grid, kDqThreads, Cfg::SMEM, st>>>(tq, tk, tv, tdo, p);
+    kern<<<grid, kDqThreads, Cfg::SMEM, st>>>(tq, BN == 128 ? tk : tk64, BN == 128 ? tv : tv64, tdo, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});
   }
@@ -1092,11 +1137,14 @@ extern "C" int vlasim_varlen_attn_bwd_cuda(const vlasim_attn_args* a, const vlas
   using namespace vlasim_host;
   if (int rc = validate_attn_args(a, false)) return rc;
   if (!g || !g->dout || !g->dq || !g->dk || !g->dv) return set_error(VLASIM_ECONFIG, "attention bwd: grads required");
-  if (a->head_dim == 256) return set_error(VLASIM_ECONFIG, "attention bwd: head_dim 256 not supported yet");
   BwdWs w;
   const size_t need = bwd_ws(&w, nullptr, a);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention bwd: workspace %zu < %zu", ws_bytes, need);
   bwd_ws(&w, ws, a);
   cudaStream_t st = as_stream(stream);
-  return a->head_dim == 64 ? launch_bwd<64>(a, g, w, st) : launch_bwd<128>(a, g, w, st);
+  switch (a->head_dim) {
+    case 64: return launch_bwd<64>(a, g, w, st);
+    case 128: return launch_bwd<128>(a, g, w, st);
+    default: return launch_bwd<256>(a, g, w, st);
+  }
 }

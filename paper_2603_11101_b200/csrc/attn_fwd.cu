@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + Cfg::Q_BYTES;  // stage s: K at s*2*KV_BYTES, V right after
 
-  __shared__ uint64_t bar_q, bar_kv_full[STAGES], bar_kv_empty[STAGES], bar_s_full[2], bar_p_full[2], bar_o_ready;
+  __shared__ uint64_t bar_q, bar_kv_full[STAGES], bar_kv_empty[STAGES], bar_s_full[2], bar_p_full[2], bar_o_ready, bar_o_done;
   __shared__ uint32_t tmem_base_s;
   __shared__ int s_kv_lo, s_kv_hi;
 
@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&bar_p_full[b], 4);
     }
     mbar_init(&bar_o_ready, 1);
+    mbar_init(&bar_o_done, 1);
     s_kv_lo = INT_MAX;
     s_kv_hi = INT_MIN;
     fence_barrier_init();
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(192, 1)
           }
           umma_commit(&bar_kv_empty[st]);
           umma_commit(&bar_o_ready);
+          if (jj == nkv - 1) umma_commit(&bar_o_done);
         }
       }
     }
@@ -237,8 +239,10 @@ __global__ void __launch_bounds__(192, 1)
       warp_arrive(&bar_p_full[sb]);
     }
     // ------------------------------------------------ epilogue: O / l → bf16, LSE
+    // o_ready may trail the softmax by two phases here (S(nkv-1) only orders PV(nkv-3)), so its
+    // parity is ambiguous: the epilogue waits on the dedicated last-PV barrier
     if (nkv > 0) {
-      mbar_wait(&bar_o_ready, (nkv - 1) & 1);
+      mbar_wait(&bar_o_done, 0);
       tc_fence_after();
     }
     const int row = q0 + tid;

@@ -38,6 +38,9 @@ CASES = [
     ([700, 20, 129], 4, 4, 64, 1),
     ([300, 50, 17], 4, 1, 256, 2),
     ([1, 1, 1, 2, 3], 1, 1, 128, 0),
+    ([700, 33, 260], 8, 1, 256, 2),   # config-3 shape: H=8, Hkv=1 (MQA), prefix-LM
+    ([100, 28, 300, 5, 1, 130], 2, 2, 256, 0),
+    ([513, 77, 129], 4, 2, 256, 1),
 ]
 
 
@@ -55,7 +58,7 @@ def test_fwd_matches_oracle(gpu, orc, case):
     assert np.max(np.abs(lse.cpu().numpy() - rlse)) < 1e-2
 
 
-@pytest.mark.parametrize("case", [i for i, c in enumerate(CASES) if c[3] != 256])
+@pytest.mark.parametrize("case", range(len(CASES)))
 def test_bwd_matches_oracle(gpu, orc, case):
     from paper_2603_11101_b200 import attention
     L, H, Hkv, d, mask = CASES[case]
@@ -87,11 +90,12 @@ def test_segment_isolation_on_gpu(gpu):
     assert torch.equal(o1[:200], o2[:200]) and torch.equal(o1[277:], o2[277:])
 
 
-def test_bwd_row_map_fuses_scatter(gpu):
+@pytest.mark.parametrize("d", [128, 256])
+def test_bwd_row_map_fuses_scatter(gpu, d):
     """row_map[t] redirects gradient row t (the packer's gather index → sample order)."""
     from paper_2603_11101_b200 import attention
     L = [300, 45, 129, 2]
-    q, k, v, do, cu = _inputs(L, 2, 1, 128, 11)
+    q, k, v, do, cu = _inputs(L, 2, 1, d, 11)
     T = q.shape[0]
     o, lse = attention.varlen_attn_fwd(q, k, v, cu)
     dq, dk, dv = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu)

@@ -65,9 +65,11 @@ struct Fwd2Cfg {
   static constexpr int OFF_Q = 0;                        // [2]
   static constexpr int OFF_K = 2 * Q_BYTES;              // [KS] K ring
   static constexpr int OFF_V = OFF_K + KS * K_BYTES;     // [VS] V ring
-  static constexpr int OFF_XCH = OFF_V + VS * KV_BYTES;  // float [2 parity][4 quarter][128]
+  // FP8: the E4M3 Q buffer is too small to stage the bf16 O tile, so O gets its own staging tile
+  static constexpr int OFF_OST = OFF_V + VS * KV_BYTES;
+  static constexpr int OFF_XCH = OFF_OST + (FP8 ? BM * HD * 2 : 0);  // float [2 parity][4 quarter][128]
   static constexpr int OFF_BAR = OFF_XCH + 2 * 4 * 128 * 4;
-  static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5 + 2;
+  static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5 + 2 + 1;
   // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 16 warp arrivals: epilogue drained O[k%2]
   uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
   uint64_t* bar_o_staged = bar_s_full + 9;       // [2] 16 warp arrivals: item's O staged in its Q buffer
+  uint64_t* bar_ost_free = bar_s_full + 11;      // FP8: the O staging tile has been read by its TMA store
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
   float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
@@ -146,6 +149,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     mbar_init(bar_o_ready, 1);
     for (int s = 0; s < 2; ++s) mbar_init(&bar_o_staged[s], 16);
+    mbar_init(bar_ost_free, 1);
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc<512>(tmem_slot);
@@ -180,11 +184,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto store_o = [&](int kk) {
         const int b = kk & 1;
         wp.template wait<0>(&bar_o_staged[b], (kk >> 1) & 1);
-        const uint8_t* so = smem + Cfg::OFF_Q + b * Cfg::Q_BYTES;
+        const uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + b * Cfg::Q_BYTES);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) tma_store_2d(&tmO, hh[b] * HD + c * 64, hq0[b], so + c * 16384);
         bulk_commit();
         bulk_wait_read0();
+        if constexpr (FP8) mbar_arrive(bar_ost_free);  // the next item's O may be staged
       };
       FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
       for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int qs = k & 1;
         if (k >= 2) {
           if constexpr (FP8) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
-          else store_o(k - 2);
+          store_o(k - 2);
         }
         hq0[qs] = itm.q0;
         hh[qs] = itm.h;
@@ -218,8 +223,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       if (pv_g >= 0) load_v();
-      if constexpr (!FP8)
-        for (int kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) store_o(kk);
+      for (int kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) store_o(kk);
       bulk_wait_all();
       wp.flush(p.prof);
     }
@@ -320,9 +324,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_after();
       const bool valid = e_row < p.T;
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
-      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(valid ? e_row : 0) * p.H + e_h) * HD + qp * OC;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + qp * OC;
-      uint8_t* so = smem + Cfg::OFF_Q + (ek & 1) * Cfg::Q_BYTES;  // bf16: this item's Q buffer
+      // staging tile: bf16 → this item's Q buffer; FP8 → the O tile, once item ek-1's store has read it
+      uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + (ek & 1) * Cfg::Q_BYTES);
       uint32_t o[32];
       tmem_ld32(o_tm, o);  // OC ≤ 32 columns (HD 64: the upper 16 belong to the next quarter, unused)
       tmem_wait_ld();
@@ -330,13 +334,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
       for (int t = 0; t < OC / 2; ++t)
         pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
-      if constexpr (FP8) {
-        if (valid) {
-          uint4* dst = reinterpret_cast<uint4*>(orow);
-#pragma unroll
-          for (int t = 0; t < OC / 8; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-        }
-      } else {  // SW128 staging: 64-column box col / 64, 16-B chunk XOR row
+      {  // SW128 staging: 64-column box col / 64, 16-B chunk XOR row
+        if (FP8 && ek > 0) wp.template wait<2>(bar_ost_free, (ek - 1) & 1);
 #pragma unroll
         for (int t = 0; t < OC / 8; ++t) {
           const int col = qp * OC + 8 * t;
@@ -369,20 +368,36 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
+        const int kv0 = itm.kv_lo + j * BN + c0;
+        float k0s = 1.f, k1s = 1.f;  // FP8: this quarter's K block scales, loaded before the S wait
+        if constexpr (FP8) {
+          const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
+          k0s = __ldg(ksc + min(kv0 / 128, p.nbt - 1));
+          k1s = __ldg(ksc + min(kv0 / 128 + 1, p.nbt - 1));
+        }
         wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
         uint32_t x[32];
         tmem_ld32(s_tm, x);
         tmem_wait_ld();
-        const int kv0 = itm.kv_lo + j * BN + c0;
         const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
-        if constexpr (FP8) {  // per-column K block scale (a 32-column quarter spans at most 2 blocks)
-          const int b0 = kv0 / 128;
-          const int cb = (b0 + 1) * 128 - kv0;
-          const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
-          const float k0s = __ldg(ksc + min(b0, p.nbt - 1)), k1s = __ldg(ksc + min(b0 + 1, p.nbt - 1));
+        // FP8: K block scale of this quarter.  A quarter inside one 128-key block (≈ 3 in 4) has a
+        // uniform scale, folded into the row max and the exponent's multiplier (no per-element
+        // work); a quarter straddling two blocks scales its columns (a quarter spans ≤ 2 blocks).
+        float ksc = 1.f;
+        if constexpr (FP8) {
+          const int cb = (kv0 / 128 + 1) * 128 - kv0;
+          if (cb >= 32) {
+            ksc = k0s;
+          } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) x[c] = __float_as_uint(__uint_as_float(x[c]) * (c < cb ? k0s : k1s));
+            for (int c = 0; c < 32; c += 2) {
+              const float2 sc = make_float2(c < cb ? k0s : k1s, c + 1 < cb ? k0s : k1s);
+              const float2 y = f2_mul(make_float2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])), sc);
+              x[c] = __float_as_uint(y.x);
+              x[c + 1] = __float_as_uint(y.y);
+            }
+          }
         }
         if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32)) {  // some row of the warp is partial
           const int vlo = min(max(c_lo, 0), 32), vhi = min(max(c_hi, 0), 32);
@@ -396,7 +411,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) mq[u] = fmax3(mq[u], __uint_as_float(x[c + 2 * u]), __uint_as_float(x[c + 2 * u + 1]));
         }
-        float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * ksc;  // scales are > 0
         // combine the four column quarters of this row
         float* xs = xch + (g & 1) * 512;
         xs[qp * 128 + r] = mt;
@@ -416,7 +431,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         const float msub = (m_run == -INFINITY) ? 0.f : m_run;
         float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 independent sum chains (FADD2)
-        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+        const float2 sl2v = make_float2(sl2 * ksc, sl2 * ksc), nmv = make_float2(-msub, -msub);
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
@@ -545,5 +560,5 @@ extern "C" int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args* a, void
   if (a->head_dim != 128) return set_error(VLASIM_ECONFIG, "fp8 Q/K attention: head_dim must be 128");
   const size_t need = size_t(a->total_tokens) * sizeof(int2);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
-  return launch_fwd2<128, 4, 3, true>(a, static_cast<int2*>(ws), as_stream(stream));
+  return launch_fwd2<128, 3, 3, true>(a, static_cast<int2*>(ws), as_stream(stream));
 }

@@ -195,6 +195,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -362,5 +367,43 @@ struct WaitProf {
     }
   }
 };
+
+// Epilogue row store without smem: thread (row = lane of a 32-row warp slab, part) holds CPT 16-B
+// chunks of its row.  A butterfly over groups of CPT lanes transposes the chunks so that lane
+// (g·CPT + i) holds chunk i of the group's CPT rows; CPT stores then write CPT-row × (16·CPT)-B
+// segments per warp instruction (8 rows × 64 B for CPT = 4) instead of 32 scattered rows.
+// dst = this lane's destination row (< 0: skip); base + dst·stride + col0 (elements) = row start.
+template <int CPT>
+__device__ __forceinline__ void store_rows_xpose(uint32_t (&w)[4 * CPT], int dst, __nv_bfloat16* base,
+                                                 int64_t stride, int col0) {
+  const int lane = threadIdx.x & 31, li = lane & (CPT - 1);
+#pragma unroll
+  for (int m = 1; m < CPT; m <<= 1) {  // stage: position c takes the partner's position c ^ m
+    const bool hi = li & m;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if ((c & m) != 0) continue;  // handle the pair (c, c ^ m) once
+      const int c1 = c | m;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // a lane with bit m clear keeps position c and receives position c1 from its partner's c;
+        // a lane with bit m set keeps c1 and receives position c from its partner's c1
+        const uint32_t send = hi ? w[4 * c + k] : w[4 * c1 + k];
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, m);
+        if (hi) w[4 * c + k] = recv;
+        else w[4 * c1 + k] = recv;
+      }
+    }
+  }
+  // lane (g·CPT + li) now holds chunk li of rows g·CPT + i at position i
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int src = (lane & ~(CPT - 1)) + i;
+    const int d = __shfl_sync(0xffffffffu, dst, src);
+    if (d >= 0)
+      *reinterpret_cast<uint4*>(base + int64_t(d) * stride + col0 + li * 8) =
+          make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+  }
+}
 
 }  // namespace vlasim_dev

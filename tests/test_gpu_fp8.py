@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("T,H,d,scale", [(300, 3, 128, 1.0), (128, 2, 128, 1000.0), (77, 1, 64, 1e-3),
-                                          (513, 2, 256, 3.0)])
+                                          (513, 2, 256, 3.0), (200, 2, 100, 1.0), (130, 2, 192, 5.0)])
 def test_quant_block_bit_exact(gpu, orc, T, H, d, scale):
     from paper_2603_11101_b200 import fp8
     g = torch.Generator(device="cuda").manual_seed(T + H)

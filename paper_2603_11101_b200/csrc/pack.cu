@@ -300,9 +300,9 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
   const int lane = threadIdx.x;
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   if (out.status[0] != 0) return;
-  // class counts → smem: a single warp, so keep 8 loads in flight per lane (latency-bound otherwise)
+  // class counts → smem: a single warp, so keep 32 loads in flight per lane (latency-bound otherwise)
   long long tok = 0;  // Σ lengths, for the bin-count bound below
-#pragma unroll 8
+#pragma unroll 32
   for (int L = lane; L <= cap; L += 32) {
     const int c = __ldg(ws.class_count + L);
     cnt[L] = c;
@@ -317,47 +317,75 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
   // step: two ballots for the lowest bin with room, the bin's room and member count broadcast
   // from its owner lane, min(⌊room/L⌋, left) items taken at once (the class-wise argument).
   if (2 * tok <= 63LL * cap) {
-    int rem[2] = {cap, cap}, mem[2] = {0, 0};
-    int nb = 0, nruns = 0;
+    // (1) the present classes, largest first, compacted into smem (the bin arrays are unused on
+    //     this path; n ≤ kWarpMaxBins bounds the class count)
+    int2* cls = reinterpret_cast<int2*>(act_rem);
+    int ncls = 0;
+#pragma unroll 4
     for (int hi = cap; hi >= 1; hi -= 32) {
       const int myL = hi - lane;
-      unsigned present = __ballot_sync(full, myL >= 1 && cnt[myL > 0 ? myL : 0] > 0);
-      while (present) {
-        const int k = __ffs(present) - 1;  // lowest lane = largest L
-        present &= present - 1;
-        const int L = hi - k;
-        const int c = cnt[L];
-        const float invL = __frcp_rn(float(L));
-        const int runs_before = nruns;
-        for (int placed = 0; placed < c;) {
-          const unsigned m0 = __ballot_sync(full, lane < nb && rem[0] >= L);
-          const unsigned m1 = __ballot_sync(full, 32 + lane < nb && rem[1] >= L);
-          const int b = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : nb);
-          if (b == nb) ++nb;  // a fresh bin (room cap, no members)
-          const int h = b >> 5, owner = b & 31;
-          const int rb = __shfl_sync(full, h ? rem[1] : rem[0], owner);
-          const int cb = __shfl_sync(full, h ? mem[1] : mem[0], owner);
-          // room >= L is guaranteed (first fit or a fresh bin): a single item needs no division
-          const int take = c - placed == 1 ? 1 : min(udiv_small(rb, L, invL), c - placed);
-          if (lane == 0) {
-            ws.run_bin[nruns] = b;
-            ws.run_cum[nruns] = placed;
-            ws.run_tok[nruns] = cap - rb;
-            ws.run_mem[nruns] = cb;
-          }
-          if (lane == owner) {
-            if (h) { rem[1] = rb - take * L; mem[1] = cb + take; }
-            else { rem[0] = rb - take * L; mem[0] = cb + take; }
-          }
-          ++nruns;
-          placed += take;
-        }
-        if (lane == 0) {
-          ws.class_run_start[L] = runs_before;
-          ws.class_nruns[L] = nruns - runs_before;
+      const int c = myL >= 1 ? cnt[myL] : 0;
+      const unsigned pm = __ballot_sync(full, c > 0);
+      if (c > 0) cls[ncls + __popc(pm & lt)] = make_int2(myL, c);
+      ncls += __popc(pm);
+    }
+    __syncwarp();
+    // (2) placement.  Bins not yet opened hold room = cap, so the lowest bin with room ≥ L is the
+    //     first fit when one exists and otherwise the next fresh bin: two ballots, no bin count
+    //     test on the critical path.  Classes are read 32 at a time into registers; the owner lane
+    //     of the chosen bin records the run in an smem ring (one 16-B store) that the warp flushes
+    //     to the run arrays every 32 runs, and the per-class run ranges are written once per 32
+    //     classes — a single-warp loop is latency-bound, so every instruction on it counts.
+    int4* ring = reinterpret_cast<int4*>(act_cnt);  // [32] run records (bin, cum, tok, mem)
+    auto flush = [&](int base, int cnt) {
+      __syncwarp();
+      if (lane < cnt) {
+        const int4 rr = ring[lane];
+        ws.run_bin[base + lane] = rr.x;
+        ws.run_cum[base + lane] = rr.y;
+        ws.run_tok[base + lane] = rr.z;
+        ws.run_mem[base + lane] = rr.w;
+      }
+      __syncwarp();
+    };
+    int rem[2] = {cap, cap}, mem[2] = {0, 0};
+    int nb = 0, nruns = 0;
+    for (int base = 0; base < ncls; base += 32) {
+      const int2 my = base + lane < ncls ? cls[base + lane] : make_int2(0, 0);
+      const int ne = min(32, ncls - base);
+      int my_start = 0;  // first run of class base + lane
+      for (int e = 0; e < ne; ++e) {
+        const int L = __shfl_sync(full, my.x, e), c = __shfl_sync(full, my.y, e);
+        if (lane == e) my_start = nruns;
+        int placed = 0;
+        while (true) {  // one run per iteration
+          const unsigned m0 = __ballot_sync(full, rem[0] >= L);
+          const unsigned m1 = __ballot_sync(full, rem[1] >= L);
+          const int b = m0 ? __ffs(m0) - 1 : 31 + __ffs(m1);
+          // branch-free owner update (selects, one predicated store): no divergence on the chain
+          const bool h = m0 == 0, own = lane == (b & 31);
+          const int rb = h ? rem[1] : rem[0], cb = h ? mem[1] : mem[0];
+          int take = 1;  // room ≥ L is guaranteed (first fit or a fresh bin): one item needs no division
+          if (c - placed > 1) take = min(udiv_small(rb, L, __frcp_rn(float(L))), c - placed);  // uniform test
+          if (own) ring[nruns & 31] = make_int4(b, placed, cap - rb, cb);
+          rem[0] = own && !h ? rb - take * L : rem[0];
+          rem[1] = own && h ? rb - take * L : rem[1];
+          mem[0] = own && !h ? cb + take : mem[0];
+          mem[1] = own && h ? cb + take : mem[1];
+          nb = max(nb, b + 1);
+          if ((++nruns & 31) == 0) flush(nruns - 32, 32);
+          if (c == 1) break;  // c is warp-uniform
+          placed += __shfl_sync(full, take, b & 31);
+          if (placed >= c) break;
         }
       }
+      const int nxt = __shfl_down_sync(full, my_start, 1);
+      if (lane < ne) {
+        ws.class_run_start[my.x] = my_start;
+        ws.class_nruns[my.x] = (lane + 1 < ne ? nxt : nruns) - my_start;
+      }
     }
+    flush(nruns & ~31, nruns & 31);
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       if (32 * h + lane < nb) {

@@ -9,6 +9,10 @@
 #include <cuda_bf16.h>
 
 #include "common.hpp"
+#include "sm100.cuh"
+
+using vlasim_dev::f2_fma;
+using vlasim_dev::f2_mul;
 
 namespace {
 
@@ -111,6 +115,18 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
   amax = fmaxf(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])), fmaxf(fmaxf(red[4], red[5]), fmaxf(red[6], red[7])));
   const float scale = amax == 0.f ? 1.f : __fdiv_rn(amax, 448.f);
   if (threadIdx.x == 0) scales[(int64_t(h) * nbt + bt) * nbd + bd] = scale;
+  // x / scale correctly rounded without a division per element (IEEE div.rn is ~10 dependent
+  // instructions and made this kernel ALU-bound): q0 = RN(x·r) with r = RN(1/scale), then one
+  // Markstein correction q = RN(q0 + RN(x − q0·scale)·r) (the residual is exact by FMA), which is
+  // the correctly rounded quotient for normal operands; quotients below 2^-10 map to code 0
+  // either way.  Packed f32x2 FMUL / FFMA.
+  const float rs = __frcp_rn(scale);
+  const float2 r2 = make_float2(rs, rs), ns2 = make_float2(-scale, -scale);
+  auto quot = [&](float2 f) {  // (the correction turns −0 into +0: the sign is restored)
+    const float2 q0 = f2_mul(f, r2);
+    const float2 q = f2_fma(f2_fma(q0, ns2, f), r2, q0);
+    return make_float2(copysignf(q.x, f.x), copysignf(q.y, f.y));
+  };
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int t = t0 + r0 + 16 * i;
@@ -119,9 +135,9 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
     uint32_t w[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const float2 f0 = __bfloat1622float2(b[2 * j]), f1 = __bfloat1622float2(b[2 * j + 1]);
-      const uint32_t lo = cvt_e4m3x2(__fdiv_rn(f0.x, scale), __fdiv_rn(f0.y, scale));
-      const uint32_t hi = cvt_e4m3x2(__fdiv_rn(f1.x, scale), __fdiv_rn(f1.y, scale));
+      const float2 q0 = quot(__bfloat1622float2(b[2 * j])), q1 = quot(__bfloat1622float2(b[2 * j + 1]));
+      const uint32_t lo = cvt_e4m3x2(q0.x, q0.y);
+      const uint32_t hi = cvt_e4m3x2(q1.x, q1.y);
       w[j] = lo | (hi << 16);
     }
     __stcs(reinterpret_cast<uint2*>(codes + (int64_t(t) * heads + h) * d + c0 + ch * 8), make_uint2(w[0], w[1]));

@@ -91,3 +91,26 @@ def test_quant_error_known_answers(gpu):
     c = torch.full((256, 1, 128), 3.0, dtype=torch.bfloat16, device="cuda")  # all-equal tensor
     m = fp8.quant_error(c, *fp8.quant_block(c))
     assert m["max_rel"] <= 2.0 ** -23  # zero up to the fp32 rounding of scale = amax / 448
+
+
+def test_quant_block_quotient_stress(gpu, orc):
+    """The block quantiser's reciprocal + one-correction quotient against the oracle's correctly
+    rounded fp32 division: 64 blocks, each with its own amax (hence scale) and 16383 other
+    elements drawn uniformly over the bf16 bit patterns below it (every exponent range)."""
+    from paper_2603_11101_b200 import fp8
+    g = torch.Generator(device="cpu").manual_seed(7)
+    nblk = 64
+    amax_bits = torch.randint(0x3000, 0x4f00, (nblk,), generator=g, dtype=torch.int32)  # ~5e-10 .. 2e9
+    x = torch.empty(nblk * 128, 1, 128, dtype=torch.bfloat16)
+    for b in range(nblk):
+        top = int(amax_bits[b])
+        bits = torch.randint(0, top, (128 * 128,), generator=g, dtype=torch.int32)
+        sign = torch.randint(0, 2, (128 * 128,), generator=g, dtype=torch.int32) << 15
+        bits = bits | sign
+        bits[0] = top  # the block's amax
+        x[128 * b:128 * (b + 1), 0, :] = bits.to(torch.int16).view(torch.bfloat16).view(128, 128)
+    xc = x.cuda()
+    codes, scales = fp8.quant_block(xc)
+    rc, rs = orc.fp8_quant_block(x.float().numpy(), quotient_fp32=True)
+    assert np.array_equal(scales.cpu().numpy(), rs)
+    assert np.array_equal(codes.cpu().numpy(), rc)

@@ -6,12 +6,13 @@ loudly (build it with `python -m paper_2603_11101_b200.build`).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import raise_for_status
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
-LIB_PATH = LIB_DIR / "libvlasim_cuda.so"
+LIB_PATH = Path(os.environ["VLASIM_CUDA_LIB"]) if os.environ.get("VLASIM_CUDA_LIB") else LIB_DIR / "libvlasim_cuda.so"
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

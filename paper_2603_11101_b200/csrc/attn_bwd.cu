@@ -7,11 +7,12 @@
 //
 // Launches (no atomics, no fp32 dQ accumulator in HBM — dQ is deterministic):
 //   k_bwd_pre   D = rowsum(dO∘O), LSE → log2 domain, per-token visible spans    [HBM-bound]
-//   k_bwd_dkdv  persistent, KV-stationary: items = (128-key tile, kv head); loops over the q
+//   k_bwd_dkdv  persistent, KV-stationary: items = (segment-aligned key tile of ≤ 128 rows
+//               (attn_tiles.cu), kv head); loops over the q
 //               heads of the group × the 128-row Q tiles of the tile's visible query range
 //               (tile skipping: queries outside [q_lo, q_hi) are never loaded or multiplied).
 //               4 GEMMs per (key tile, Q tile): Sᵀ, dPᵀ, dV, dK.
-//   k_bwd_dq    persistent, Q-stationary: items = (128-row Q tile, head); loops over the key
+//   k_bwd_dq    persistent, Q-stationary: items = (segment-aligned Q tile, head); loops over the key
 //               tiles of the visible key range.  3 GEMMs per tile: S, dP, dQ (recomputing S and
 //               dP costs 2 GEMMs but removes the dQ reduction across key tiles).
 // Both kernels: warps 0-7 softmax (warp w: TMEM lane quadrant w%4, column half w/4), warp 8 TMA
@@ -58,11 +59,14 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
   const int tasks = nt * H * LPR;
   const int64_t base = int64_t(t0) * H * HD;
 #pragma unroll 4
+  // Loop exits are warp-uniform (a warp's 32 tasks are consecutive) so that the shuffle reduction
+  // always runs with the full warp; tasks past the end contribute zeros and are not written.
   for (int task = threadIdx.x; task < kPreTokens * 16 * LPR; task += 256) {  // uniform trip count (H ≤ 16 fast path)
-    if (task >= tasks) break;
-    const int r = task / LPR, sub = task % LPR;
-    const uint4 x = *reinterpret_cast<const uint4*>(o + base + int64_t(r) * HD + sub * 8);
-    const uint4 y = *reinterpret_cast<const uint4*>(dout + base + int64_t(r) * HD + sub * 8);
+    if (task - (threadIdx.x & 31) >= tasks) break;
+    const bool act = task < tasks;
+    const int r = act ? task / LPR : 0, sub = task % LPR;
+    const uint4 x = act ? *reinterpret_cast<const uint4*>(o + base + int64_t(r) * HD + sub * 8) : make_uint4(0, 0, 0, 0);
+    const uint4 y = act ? *reinterpret_cast<const uint4*>(dout + base + int64_t(r) * HD + sub * 8) : make_uint4(0, 0, 0, 0);
     const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&x);
     const __nv_bfloat162* py = reinterpret_cast<const __nv_bfloat162*>(&y);
     float acc = 0.f;
@@ -73,12 +77,13 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
     }
 #pragma unroll
     for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
+    if (act && sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
   }
-  for (int task = kPreTokens * 16 * LPR + threadIdx.x; task < tasks; task += 256) {  // H > 16
-    const int r = task / LPR, sub = task % LPR;
-    const uint4 x = *reinterpret_cast<const uint4*>(o + base + int64_t(r) * HD + sub * 8);
-    const uint4 y = *reinterpret_cast<const uint4*>(dout + base + int64_t(r) * HD + sub * 8);
+  for (int task = kPreTokens * 16 * LPR + threadIdx.x; task - int(threadIdx.x & 31) < tasks; task += 256) {  // H > 16
+    const bool act = task < tasks;
+    const int r = act ? task / LPR : 0, sub = task % LPR;
+    const uint4 x = act ? *reinterpret_cast<const uint4*>(o + base + int64_t(r) * HD + sub * 8) : make_uint4(0, 0, 0, 0);
+    const uint4 y = act ? *reinterpret_cast<const uint4*>(dout + base + int64_t(r) * HD + sub * 8) : make_uint4(0, 0, 0, 0);
     const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&x);
     const __nv_bfloat162* py = reinterpret_cast<const __nv_bfloat162*>(&y);
     float acc = 0.f;
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
     }
 #pragma unroll
     for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
+    if (act && sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
   }
   __syncthreads();
   // 4 copies shifted by s = 0..3 elements: any 64/128-wide window [qb, qb+w) starts 16-B aligned
@@ -126,7 +131,9 @@ struct BwdParams {
   const float* dsum;       // [H, Tp] rowsum(dO ∘ O)
   const int2* rows_span;   // [T] visible keys of query t
   const int2* cols_span;   // [T] queries that see key t
-  int T, Tp, H, Hkv, kv_items, q_items;
+  const int2* tiles;       // segment-aligned 128-row tiles [t0, te), sorted by cost (attn_tiles.cu)
+  const int* ntiles;       // device-side tile count
+  int T, Tp, H, Hkv;
   int64_t vec_copy;  // element stride between the 4 shifted copies of lse2 / dsum
   float scale_log2, scale;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
@@ -188,14 +195,16 @@ struct DkvCfg {
 // derived counts are computed when the item becomes current (kv_item_finish), so the loads'
 // latency never stalls a role at an item boundary.
 struct KvItem {
-  int k0, kh, q_lo, q_hi, nq, iters;
+  int k0, ke, kh, q_lo, q_hi, nq, iters;
 };
 __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   KvItem it;
+  const int2 t = __ldg(&p.tiles[i / p.Hkv]);
   it.kh = i % p.Hkv;
-  it.k0 = (i / p.Hkv) * 128;
-  it.q_lo = __ldg(&p.cols_span[it.k0].x);
-  it.q_hi = __ldg(&p.cols_span[min(it.k0 + 127, p.T - 1)].y);
+  it.k0 = t.x;
+  it.ke = t.y;
+  it.q_lo = __ldg(&p.cols_span[t.x].x);      // key spans are monotone inside a segment
+  it.q_hi = __ldg(&p.cols_span[t.y - 1].y);
   return it;
 }
 template <int UQ>
@@ -204,33 +213,34 @@ __device__ __forceinline__ void kv_item_finish(const BwdParams& p, KvItem& it) {
   it.iters = it.nq * (p.H / p.Hkv);
 }
 
-// Walks this CTA's units in order: item i (blockIdx.x + m·gridDim.x), unit it within the item,
-// k = ordinal of the item, u = ordinal of the unit.  The next item's descriptor is loaded one
-// item ahead (its global loads overlap the current item).  Every key sees itself, so every
+// Walks this CTA's units in order: item i = sched_item(k) (attn_common.cuh), unit it within the
+// item, k = ordinal of the item, u = ordinal of the unit.  The next item's descriptor is loaded
+// one item ahead (its global loads overlap the current item).  Every key sees itself, so every
 // item has iters ≥ 1.
 template <int UQ>
 struct UnitCursor {
-  int i, it, k, u;
+  int i, it, k, u, n;
   KvItem itm, nxt;
+  __device__ __forceinline__ bool has_next() const { return sched_item(k + 1) < n; }
   __device__ __forceinline__ bool start(const BwdParams& p) {
-    i = blockIdx.x;
+    n = __ldg(p.ntiles) * p.Hkv;
     it = k = u = 0;
-    if (i >= p.kv_items) return false;
+    i = sched_item(0);
+    if (i >= n) return false;
     itm = kv_item(p, i);
     kv_item_finish<UQ>(p, itm);
-    if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
+    if (has_next()) nxt = kv_item(p, sched_item(1));
     return true;
   }
   __device__ __forceinline__ bool next(const BwdParams& p) {
     ++u;
     if (++it < itm.iters) return true;
     it = 0;
-    ++k;
-    i += gridDim.x;
-    if (i >= p.kv_items) return false;
+    i = sched_item(++k);
+    if (i >= n) return false;
     itm = nxt;
     kv_item_finish<UQ>(p, itm);
-    if (i + int(gridDim.x) < p.kv_items) nxt = kv_item(p, i + gridDim.x);
+    if (has_next()) nxt = kv_item(p, sched_item(k + 1));
     return true;
   }
   __device__ __forceinline__ bool last() const { return it + 1 == itm.iters; }
@@ -314,7 +324,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           }
           // the next item's K/V into L2 now: its load (single K/V buffer, issued only once this
           // item's last dP has run) then hits L2 at the item boundary
-          if (c.i + int(gridDim.x) < p.kv_items) {
+          if (c.has_next()) {
 #pragma unroll
             for (int j = 0; j < HD / 64; ++j) {
               tma_prefetch_2d(&tmK, c.nxt.kh * HD + j * 64, c.nxt.k0);
@@ -474,7 +484,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     TraceCtr trace(lane == 0 && (warp & 7) == 0 && trb ? trb + 2001 * (2 + (warp >> 3)) : nullptr);
     UnitCursor<UQ> c;
     auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
-    auto dst_of = [&](int key) { return key < p.T ? (p.row_map ? __ldg(p.row_map + key) : key) : -1; };
+    // keys past the tile's end belong to the next segment: never stored
+    auto dst_of = [&](int key, int ke) { return key < ke ? (p.row_map ? __ldg(p.row_map + key) : key) : -1; };
     int ss = 0;  // stage of unit c.u
     int2 ks = make_int2(0, 0), ks_nxt = ks;
     int dst_key = -1, dst_nxt = -1;
@@ -483,11 +494,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       if (c.it == 0) {  // this item's spans were prefetched one item ahead (first item: now)
         const int key = c.itm.k0 + krow;
         ks = c.k == 0 ? span_of(key) : ks_nxt;
-        dst_key = c.k == 0 ? dst_of(key) : dst_nxt;
-        if (c.i + int(gridDim.x) < p.kv_items) {
+        dst_key = c.k == 0 ? dst_of(key, c.itm.ke) : dst_nxt;
+        if (c.has_next()) {
           const int nkey = c.nxt.k0 + krow;
           ks_nxt = span_of(nkey);
-          dst_nxt = dst_of(nkey);
+          dst_nxt = dst_of(nkey, c.nxt.ke);
         }
       }
       const int s = ss;
@@ -649,15 +660,17 @@ struct DqCfg {
 };
 
 struct QItem {
-  int q0, h, kh, kv_lo, kv_hi, nkv;
+  int q0, qe, h, kh, kv_lo, kv_hi, nkv;
 };
 __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {  // raw loads (see KvItem)
   QItem it;
+  const int2 t = __ldg(&p.tiles[i / p.H]);
   it.h = i % p.H;
-  it.q0 = (i / p.H) * 128;
+  it.q0 = t.x;
+  it.qe = t.y;
   it.kh = it.h / (p.H / p.Hkv);
-  it.kv_lo = __ldg(&p.rows_span[it.q0].x);
-  it.kv_hi = __ldg(&p.rows_span[min(it.q0 + 127, p.T - 1)].y);
+  it.kv_lo = __ldg(&p.rows_span[t.x].x);
+  it.kv_hi = __ldg(&p.rows_span[t.y - 1].y);
   it.nkv = -1;
   return it;
 }
@@ -695,6 +708,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = __ldg(p.ntiles) * p.H, i0 = sched_item(0);
   // event trace (PROF builds with VLASIM_DBG & 2: the idle K/V stages hold 4 × 2001 words)
   unsigned long long* const trb =
       PROF && (p.dbg & 2) && blockIdx.x == 0 ? reinterpret_cast<unsigned long long*>(smem + Cfg::OFF_K) : nullptr;
@@ -730,10 +744,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (lane == 0) {
       TraceCtr trace(trb);
       int g = 0, k = 0;
-      QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
-      for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
+      QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
+      for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
         const QItem itm = q_item_cur(nxt, BN);
-        if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
+        if (sched_item(m + 1) < n_items) nxt = q_item(p, sched_item(m + 1));
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
         trace(1, g);  // P: Q/dO load issued
@@ -810,10 +824,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         trace(11, pg);  // M: dQ issued
         pend = false;
       };
-      QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
-      for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
+      QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
+      for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
         const QItem itm = q_item_cur(nxt, BN);
-        if (i + int(gridDim.x) < p.q_items) nxt = q_item(p, i + gridDim.x);
+        if (sched_item(m + 1) < n_items) nxt = q_item(p, sched_item(m + 1));
         if (itm.nkv == 0) continue;
         if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
         mbar_wait(bar_qdo_full, k & 1);
@@ -875,21 +889,21 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw) : 0.f;  // copy 0 (unshifted)
       d_ = v ? __ldg(p.dsum + int64_t(it.h) * p.Tp + rw) : 0.f;
     };
-    QItem nxt = q_item(p, blockIdx.x < p.q_items ? blockIdx.x : 0);
+    QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
     int2 rs_n;
     float lse_n, dsum_n;
     load_row(nxt, rs_n, lse_n, dsum_n);
-    for (int i = blockIdx.x; i < p.q_items; i += gridDim.x) {
+    for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
       const QItem itm = q_item_cur(nxt, BN);
       const int2 rs = rs_n;
       const float lse2 = lse_n, dsum = dsum_n;
-      if (i + int(gridDim.x) < p.q_items) {
-        nxt = q_item(p, i + gridDim.x);
+      if (sched_item(m + 1) < n_items) {
+        nxt = q_item(p, sched_item(m + 1));
         load_row(nxt, rs_n, lse_n, dsum_n);
       }
       if (itm.nkv == 0) continue;
       const int row = itm.q0 + r;
-      const bool valid = row < p.T;
+      const bool valid = row < itm.qe;  // rows past the tile's end belong to the next segment
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
         const int kv0 = itm.kv_lo + j * BN + c0;
@@ -985,6 +999,7 @@ struct BwdWs {
   float* dsum;
   int2* rows_span;
   int2* cols_span;
+  void* tiles;  // tile table (attn_tiles.cu)
 };
 
 size_t bwd_ws(BwdWs* w, void* base, const vlasim_attn_args* a) {
@@ -1003,6 +1018,7 @@ size_t bwd_ws(BwdWs* w, void* base, const vlasim_attn_args* a) {
   w->dsum = reinterpret_cast<float*>(take(4 * (Tp * H + 512) * 4));
   w->rows_span = reinterpret_cast<int2*>(take(T * 8));
   w->cols_span = reinterpret_cast<int2*>(take(T * 8));
+  w->tiles = take(vlasim_host::tiles_bytes(int64_t(T), a->num_seqs));
   return off;
 }
 
@@ -1015,6 +1031,10 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
       static_cast<const __nv_bfloat16*>(a->o), static_cast<const __nv_bfloat16*>(g->dout), a->lse, w.lse2, w.dsum,
       w.rows_span, w.cols_span, a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, Tp, H);
   VLASIM_LAUNCH_CHECK();
+  int2* tiles;
+  int* ntiles;
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->num_seqs, T, w.tiles, st, &tiles, &ntiles)) return rc;
+  const int64_t max_tiles = int64_t(T) / 128 + a->num_seqs;
   CUtensorMap tq, tk, tv, tdo;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (int rc = encode_tmap_2d(&tq, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, 128, 64, true)) return rc;
@@ -1043,20 +1063,21 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.dsum = w.dsum;
   p.rows_span = w.rows_span;
   p.cols_span = w.cols_span;
+  p.tiles = tiles;
+  p.ntiles = ntiles;
   p.T = T;
   p.Tp = Tp;
   p.H = H;
   p.Hkv = Hkv;
-  p.kv_items = int((int64_t(T) + 127) / 128) * Hkv;
   p.vec_copy = int64_t(H) * Tp + 512;
-  p.q_items = int((int64_t(T) + 127) / 128) * H;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * kLog2e;
   p.dbg = getenv("VLASIM_DBG") ? atoi(getenv("VLASIM_DBG")) : 0;
   p.ohalf = 0;
-  for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO; ++half) {
+  const int skip = getenv("VLASIM_BWD_SKIP") ? atoi(getenv("VLASIM_BWD_SKIP")) : 0;  // debugging
+  for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO && !(skip & 2); ++half) {
     using Cfg = DkvCfg<HD, UQ>;
-    const int grid = std::min(p.kv_items, num_sms());
+    const int grid = int(std::min<int64_t>(max_tiles * Hkv, num_sms()));
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
     p.ohalf = half;
     auto kern = p.prof ? k_bwd_dkdv<HD, UQ, true> : k_bwd_dkdv<HD, UQ, false>;
@@ -1070,14 +1091,14 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
                    "smx:s_full", "smx:dp_full", "", "smx:dkv_full", "smx:phaseA", "smx:phaseB", "smx:epilogue", "",
                    "", "", "", "smx:total"});
   }
-  {
+  if (!(skip & 1)) {
     constexpr int BN = HD == 256 ? 64 : 128;
     constexpr int KS = HD == 64 ? 5 : (HD == 128 ? 3 : 2), VS = HD == 64 ? 4 : (HD == 128 ? 2 : 1);
     using Cfg = DqCfg<HD, BN, KS, VS>;
     auto kern = p.prof ? k_bwd_dq<HD, BN, KS, VS, true> : k_bwd_dq<HD, BN, KS, VS, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    const int grid = std::min(p.q_items, num_sms());
+    const int grid = int(std::min<int64_t>(max_tiles * H, num_sms()));
     kern<<<grid, kDqThreads, Cfg::SMEM, st>>>(tq, BN == 128 ? tk : tk64, BN == 128 ? tv : tv64, tdo, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});
@@ -1089,7 +1110,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
 
 extern "C" size_t vlasim_varlen_attn_workspace_size(const vlasim_attn_args* a, int backward) {
   if (!a) return 0;
-  if (!backward) return size_t(a->total_tokens) * 8 + 256;  // forward: per-token visible spans
+  if (!backward) return vlasim_host::fwd_ws_bytes(a);  // forward: per-token visible spans + tiles
   BwdWs w;
   return bwd_ws(&w, nullptr, a);
 }

@@ -56,4 +56,12 @@ __device__ __forceinline__ RowSpan key_span(const int32_t* __restrict__ cu, cons
   return r;
 }
 
+// Persistent static schedule over work items sorted by decreasing cost (attn_tiles.cu): round m
+// of CTA b takes item m·G + b on even rounds and m·G + (G−1−b) on odd rounds (boustrophedon), so
+// no CTA takes the heaviest item of every round.
+__device__ __forceinline__ int sched_item(int m) {
+  const int G = gridDim.x, b = blockIdx.x;
+  return m * G + ((m & 1) ? G - 1 - b : b);
+}
+
 }  // namespace vlasim_dev

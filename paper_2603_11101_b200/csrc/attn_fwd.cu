@@ -3,9 +3,8 @@
 // Replaces vlasim::packed_attention (multi-head = looped single head,
 // SPEC.md:521) on the packed stream produced by the GPU packer.
 //
-// One CTA = one 128-row Q tile of the packed stream × one head (tiles on the global
-// 128-row grid, so a tile may span several segments).  The tile's key range is the union
-// of its rows' visible intervals; K/V tiles of BN rows are streamed from there, so no key
+// One CTA = one segment-aligned Q tile of ≤ 128 rows (attn_tiles.cu) × one head.  The tile's
+// key range is the union of its rows' visible intervals; K/V tiles of BN rows are streamed from there, so no key
 // block outside [first segment start, last visible key) is ever loaded or multiplied
 // (tile skipping at sequence boundaries).  Inside a tile the block-diagonal / causal /
 // prefix mask is a per-row interval test.
@@ -34,6 +33,8 @@ struct FwdParams {
   float* lse;
   const int32_t* cu;
   const int32_t* prefix;
+  const int2* tiles;  // segment-aligned Q tiles, sorted by cost (attn_tiles.cu)
+  const int* ntiles;
   int nseq, T, H, Hkv, mask;
   float scale_log2;
 };
@@ -69,10 +70,11 @@ __global__ void __launch_bounds__(192, 1)
   __shared__ int s_kv_lo, s_kv_hi;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (int(blockIdx.x) >= __ldg(p.ntiles) * p.H) return;  // grid sized for the worst-case tile count
   const int h = blockIdx.x % p.H;
-  const int qt = blockIdx.x / p.H;
+  const int2 tile = __ldg(&p.tiles[blockIdx.x / p.H]);
   const int kh = h / (p.H / p.Hkv);
-  const int q0 = qt * Cfg::BM;
+  const int q0 = tile.x, qe = tile.y;
 
   if (tid == 0) {
     mbar_init(&bar_q, 1);
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
 
   RowSpan rs{0, 0, -1};
-  if (tid < 128) {
+  if (tid < 128 && q0 + tid < qe) {  // rows past the tile's end belong to the next segment
     rs = row_span(p.cu, p.prefix, p.nseq, p.mask, q0 + tid, p.T);
     if (rs.lo < rs.hi) {
       atomicMin(&s_kv_lo, rs.lo);
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
     }
     const int row = q0 + tid;
-    const bool valid = row < p.T && rs.lo < rs.hi;
+    const bool valid = row < qe && rs.lo < rs.hi;
     const float inv_l = (valid && l_run > 0.f) ? 1.f / l_run : 0.f;
     __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + h) * HD;
 #pragma unroll
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int HD, int BN, int STAGES>
-int launch_fwd(const vlasim_attn_args* a, cudaStream_t st) {
+int launch_fwd(const vlasim_attn_args* a, void* tiles_buf, cudaStream_t st) {
   using namespace vlasim_host;
   using Cfg = FwdCfg<HD, BN, STAGES>;
   CUtensorMap tq, tk, tv;
@@ -291,6 +293,9 @@ int launch_fwd(const vlasim_attn_args* a, cudaStream_t st) {
   p.lse = a->lse;
   p.cu = a->cu_seqlens;
   p.prefix = a->prefix_len;
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->num_seqs, int64_t(T), tiles_buf, st, const_cast<int2**>(&p.tiles),
+                                  const_cast<int**>(&p.ntiles)))
+    return rc;
   p.nseq = a->num_seqs;
   p.T = static_cast<int>(T);
   p.H = a->num_heads;
@@ -299,8 +304,8 @@ int launch_fwd(const vlasim_attn_args* a, cudaStream_t st) {
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
   auto kern = attn_fwd_kernel<HD, BN, STAGES>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const int64_t qtiles = (int64_t(T) + 127) / 128;
-  kern<<<qtiles * a->num_heads, 192, Cfg::SMEM, st>>>(tq, tk, tv, p);
+  const int64_t max_tiles = int64_t(T) / 128 + a->num_seqs;
+  kern<<<max_tiles * a->num_heads, 192, Cfg::SMEM, st>>>(tq, tk, tv, p);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }
@@ -333,6 +338,7 @@ int validate_attn_args(const vlasim_attn_args* a, bool fp8) {
 
 namespace vlasim_host {
 int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, cudaStream_t st);
+void* fwd_ws_tiles(const vlasim_attn_args* a, void* ws);
 }
 
 // head_dim 64/128: persistent kernel (attn_fwd2.cu, needs the span workspace);
@@ -342,7 +348,11 @@ extern "C" int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void* ws, 
   using namespace vlasim_host;
   if (int rc = validate_attn_args(a, false)) return rc;
   cudaStream_t st = as_stream(stream);
-  if (a->head_dim == 256) return launch_fwd<256, 64, 2>(a, st);
-  if (getenv("VLASIM_FWD_V1")) return a->head_dim == 64 ? launch_fwd<64, 128, 4>(a, st) : launch_fwd<128, 128, 3>(a, st);
+  const size_t need = fwd_ws_bytes(a);
+  if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
+  if (a->head_dim == 256) return launch_fwd<256, 64, 2>(a, fwd_ws_tiles(a, ws), st);
+  if (getenv("VLASIM_FWD_V1"))
+    return a->head_dim == 64 ? launch_fwd<64, 128, 4>(a, fwd_ws_tiles(a, ws), st)
+                             : launch_fwd<128, 128, 3>(a, fwd_ws_tiles(a, ws), st);
   return launch_fwd_persistent(a, ws, ws_bytes, st);
 }

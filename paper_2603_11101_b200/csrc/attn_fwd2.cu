@@ -1,9 +1,9 @@
 // attn_fwd2.cu — persistent block-diagonal varlen attention forward (sm_100a), head_dim 64/128.
 //
 // Same math and masking as attn_fwd.cu (vlasim::packed_attention), but
-// persistent: grid = #SMs, each CTA walks work items (128-row Q tile on the global grid, head)
-// with a static stride; Q is double-buffered so the next item's loads and first S MMAs
-// overlap the current item's epilogue.
+// persistent: grid = #SMs, each CTA walks work items (segment-aligned Q tile of ≤ 128 rows, head;
+// attn_tiles.cu) on the boustrophedon schedule; Q is double-buffered so the next item's loads and
+// first S MMAs overlap the current item's epilogue.
 //
 // Warp roles (576 threads):
 //   warps 0-15 softmax + epilogue: warp w owns rows 32·(w%4).. (TMEM lane quadrant w%4) and
@@ -14,6 +14,8 @@
 //              epilogue stages O (bf16, SW128) into the item's own Q buffer, idle by then, and
 //              the producer writes it with two 128×64 TMA tensor stores before refilling that
 //              buffer with the Q tile two items later (no LSU row scatter, no softmax stall).
+//              A tile of n < 128 rows is stored as boxes of 64/32/16/8 rows (binary digits of
+//              n & ~7); its last n & 7 rows are written by their softmax threads directly.
 //   warp 17    TMEM allocator + tcgen05.mma issuer; S_g = Q·K_gᵀ is issued before PV_{g-1}
 // TMEM (512 cols): S0 [0,128) · S1 [128,256) · O0 [256, 256+HD) · O1 after O0 (double-buffered so an
 // item's epilogue can be deferred past the next item's first tile).
@@ -47,9 +49,11 @@ struct Fwd2Params {
   __nv_bfloat16* o;
   float* lse;
   const int2* rows_span;
+  const int2* tiles;     // segment-aligned Q tiles [q0, qe), sorted by cost (attn_tiles.cu)
+  const int* ntiles;     // device-side tile count
   const float* q_scale;  // FP8 only: [H, nbt] per-(head, 128-token block) E4M3 scales (d = 128)
   const float* k_scale;  // FP8 only: [Hkv, nbt]
-  int T, H, Hkv, num_items, nbt;
+  int T, H, Hkv, nbt;
   float scale_log2;
   unsigned long long* prof;  // [3 roles][8] wait cycles (PROF instantiation only)
 };
@@ -80,15 +84,17 @@ struct Fwd2Cfg {
 // Items are prefetched one ahead with raw span loads only; the key-tile count is derived when
 // the item becomes current (fwd_item_cur), so the loads never stall a role at an item boundary.
 struct FwdItem {
-  int q0, h, kh, kv_lo, kv_hi, nkv;
+  int q0, qe, h, kh, kv_lo, kv_hi, nkv;
 };
 __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) {
   FwdItem it;
+  const int2 t = __ldg(&p.tiles[i / p.H]);
   it.h = i % p.H;
-  it.q0 = (i / p.H) * 128;
+  it.q0 = t.x;
+  it.qe = t.y;
   it.kh = it.h / (p.H / p.Hkv);
-  it.kv_lo = __ldg(&p.rows_span[it.q0].x);
-  it.kv_hi = __ldg(&p.rows_span[min(it.q0 + 127, p.T - 1)].y);
+  it.kv_lo = __ldg(&p.rows_span[t.x].x);      // spans are monotone inside a segment
+  it.kv_hi = __ldg(&p.rows_span[t.y - 1].y);
   it.nkv = -1;
   (void)BN;
   return it;
@@ -104,6 +110,8 @@ template <int HD, int KS, int VS, bool FP8, bool PROF>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                     const __grid_constant__ CUtensorMap tmO64, const __grid_constant__ CUtensorMap tmO32,
+                     const __grid_constant__ CUtensorMap tmO16, const __grid_constant__ CUtensorMap tmO8,
                      const Fwd2Params p) {
   using Cfg = Fwd2Cfg<HD, KS, VS, FP8>;
   constexpr int BN = Cfg::BN;
@@ -127,6 +135,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = __ldg(p.ntiles) * p.H;
+  const int i0 = sched_item(0);
   if (tid == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_q_full[s], 1);
@@ -180,21 +190,33 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // bf16: item k's O is staged in Q buffer k&1; write it out (two 128×64 TMA stores) and wait
       // for the stores to read smem before that buffer takes item k+2's Q.  Every item has ≥ 1
       // key tile (a query sees itself), so every item runs an epilogue.
-      int hq0[2] = {0, 0}, hh[2] = {0, 0};
+      int hq0[2] = {0, 0}, hh[2] = {0, 0}, hn[2] = {0, 0};
       auto store_o = [&](int kk) {
         const int b = kk & 1;
         wp.template wait<0>(&bar_o_staged[b], (kk >> 1) & 1);
         const uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + b * Cfg::Q_BYTES);
+        if (hn[b] == 128) {
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c) tma_store_2d(&tmO, hh[b] * HD + c * 64, hq0[b], so + c * 16384);
+          for (int c = 0; c < HD / 64; ++c) tma_store_2d(&tmO, hh[b] * HD + c * 64, hq0[b], so + c * 16384);
+        } else {  // rows [0, n & ~7) as 64/32/16/8-row boxes (1 KB-aligned starts keep the swizzle)
+          int r0 = 0;
+#pragma unroll
+          for (int bh = 64; bh >= 8; bh >>= 1) {
+            if (!(hn[b] & bh)) continue;
+            const CUtensorMap* m = bh == 64 ? &tmO64 : bh == 32 ? &tmO32 : bh == 16 ? &tmO16 : &tmO8;
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) tma_store_2d(m, hh[b] * HD + c * 64, hq0[b] + r0, so + c * 16384 + r0 * 128);
+            r0 += bh;
+          }
+        }
         bulk_commit();
         bulk_wait_read0();
         if constexpr (FP8) mbar_arrive(bar_ost_free);  // the next item's O may be staged
       };
-      FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
-      for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+      FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
+      for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
-        if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
+        if (sched_item(m + 1) < n_items) nxt = fwd_item(p, sched_item(m + 1), BN);  // prefetch
         const int qs = k & 1;
         if (k >= 2) {
           if constexpr (FP8) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
@@ -202,6 +224,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         hq0[qs] = itm.q0;
         hh[qs] = itm.h;
+        hn[qs] = itm.qe - itm.q0;
         uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
         mbar_expect_tx(&bar_q_full[qs], Cfg::Q_BYTES);
 #pragma unroll
@@ -263,10 +286,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (++vs == VS) { vs = 0; vph ^= 1; }
         pend = false;
       };
-      FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
-      for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+      FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
+      for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
-        if (i + int(gridDim.x) < p.num_items) nxt = fwd_item(p, i + gridDim.x, BN);  // prefetch
+        if (sched_item(m + 1) < n_items) nxt = fwd_item(p, sched_item(m + 1), BN);  // prefetch
         const int qs = k & 1;
         const uint64_t qd = dQ0 + qs * Q16;
         wp.template wait<0>(&bar_q_full[qs], (k >> 1) & 1);
@@ -316,13 +339,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // Epilogue of item `ek` is deferred until the first tile of the next item has been handed to
     // the MMA warp, so the tensor core never idles on it (O is double-buffered in TMEM).
     WaitProf<PROF> wp;
-    int ek = -1, e_row = 0, e_h = 0;
+    int ek = -1, e_row = 0, e_h = 0, e_n = 0;
     float e_m = 0.f, e_l = 0.f;
     auto epilogue = [&]() {
       const long long te = wp.now();
       wp.template wait<2>(&bar_o_full[ek & 1], (ek >> 1) & 1);
       tc_fence_after();
-      const bool valid = e_row < p.T;
+      const bool valid = r < e_n;  // rows past the tile's end belong to the next segment
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + qp * OC;
       // staging tile: bf16 → this item's Q buffer; FP8 → the O tile, once item ek-1's store has read it
@@ -344,6 +367,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         fence_proxy_async_smem();
         warp_arrive(&bar_o_staged[ek & 1]);  // the producer writes the tile out
+        if (valid && r >= (e_n & ~7)) {       // the last n & 7 rows: no TMA box, stored here
+          uint4* dst = reinterpret_cast<uint4*>(p.o + (int64_t(e_row) * p.H + e_h) * HD + qp * OC);
+#pragma unroll
+          for (int t = 0; t < OC / 8; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+        }
       }
       tc_fence_before();
       warp_arrive(&bar_o_empty[ek & 1]);
@@ -353,18 +381,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       wp.template add_since<4>(te);
     };
     int g = 0, k = 0;
-    FwdItem nxt = fwd_item(p, blockIdx.x < p.num_items ? blockIdx.x : 0, BN);
+    FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
     int2 rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
-    for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++k) {
+    for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
       const FwdItem itm = fwd_item_cur(nxt, BN);
       const int2 rs = rs_n;
-      if (i + int(gridDim.x) < p.num_items) {  // prefetch the next item's parameters
-        nxt = fwd_item(p, i + gridDim.x, BN);
+      if (sched_item(m + 1) < n_items) {  // prefetch the next item's parameters
+        nxt = fwd_item(p, sched_item(m + 1), BN);
         rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
       }
       const int row = itm.q0 + r;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + qp * OC;
-      if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + itm.q0 / 128);
+      // FP8: the row's Q block scale (a segment-aligned tile may straddle two 128-token blocks)
+      if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + min(row, p.T - 1) / 128);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
@@ -477,6 +506,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ek = k;
         e_row = row;
         e_h = itm.h;
+        e_n = itm.qe - itm.q0;
         e_m = m_run;
         e_l = l_tot;
       }
@@ -490,12 +520,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 }
 
 template <int HD, int KS, int VS, bool FP8>
-int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
+int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, void* tiles_buf, cudaStream_t st) {
   using namespace vlasim_host;
   using Cfg = Fwd2Cfg<HD, KS, VS, FP8>;
   const int T = int(a->total_tokens);
   k_fwd_spans<<<(T + 255) / 256, 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, rows_span);
   VLASIM_LAUNCH_CHECK();
+  int2* tiles;
+  int* ntiles;
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->num_seqs, T, tiles_buf, st, &tiles, &ntiles)) return rc;
   CUtensorMap tq, tk, tv;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto QK = FP8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : BF;
@@ -505,24 +538,32 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   if (int rc = encode_tmap_2d(&tv, a->v, BF, T, Hkv * HD, Hkv * HD * 2, Cfg::BN, 64, true)) return rc;
   CUtensorMap to;  // O tile stores (bf16 path): 128 rows × 64 columns, SW128
   if (int rc = encode_tmap_2d(&to, a->o, BF, T, H * HD, H * HD * 2, 128, 64, true)) return rc;
+  CUtensorMap to64, to32, to16, to8;  // partial tiles
+  if (int rc = encode_tmap_2d(&to64, a->o, BF, T, H * HD, H * HD * 2, 64, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&to32, a->o, BF, T, H * HD, H * HD * 2, 32, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&to16, a->o, BF, T, H * HD, H * HD * 2, 16, 64, true)) return rc;
+  if (int rc = encode_tmap_2d(&to8, a->o, BF, T, H * HD, H * HD * 2, 8, 64, true)) return rc;
   Fwd2Params p;
   p.o = static_cast<__nv_bfloat16*>(a->o);
   p.lse = a->lse;
   p.rows_span = rows_span;
+  p.tiles = tiles;
+  p.ntiles = ntiles;
   p.q_scale = a->q_scale;
   p.k_scale = a->k_scale;
   p.T = T;
   p.H = a->num_heads;
   p.Hkv = a->num_kv_heads;
   p.nbt = (T + 127) / 128;
-  p.num_items = int((int64_t(T) + 127) / 128) * a->num_heads;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
-  const int grid = std::min(p.num_items, num_sms());
+  // the tile count is known on the device only: one CTA per SM (bounded by the worst case)
+  const int64_t max_items = (int64_t(T) / 128 + a->num_seqs) * a->num_heads;
+  const int grid = int(std::min<int64_t>(max_items, num_sms()));
   if (prof_enabled()) {
     p.prof = prof_buffer();
     auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, true>;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
+    kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, to64, to32, to16, to8, p);
     VLASIM_LAUNCH_CHECK();
     return prof_report("attn_fwd2", grid, st,
                        {"prod:q_empty", "prod:kv_empty", "", "", "", "", "", "prod:total", "mma:q_full", "mma:k/v_full",
@@ -532,7 +573,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
   p.prof = nullptr;
   auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, false>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, p);
+  kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, to64, to32, to16, to8, p);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }
@@ -541,12 +582,19 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, cudaStream_t st) {
 
 namespace vlasim_host {
 // Forward for head_dim 64 / 128; the workspace holds the per-token spans (T int2).
+// Forward workspace: per-token spans (T int2, 256-B aligned) then the tile table.
+size_t fwd_ws_bytes(const vlasim_attn_args* a) {
+  return ((size_t(a->total_tokens) * sizeof(int2) + 255) & ~size_t(255)) + tiles_bytes(a->total_tokens, a->num_seqs);
+}
+void* fwd_ws_tiles(const vlasim_attn_args* a, void* ws) {
+  return static_cast<uint8_t*>(ws) + ((size_t(a->total_tokens) * sizeof(int2) + 255) & ~size_t(255));
+}
 int launch_fwd_persistent(const vlasim_attn_args* a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const size_t need = size_t(a->total_tokens) * sizeof(int2);
+  const size_t need = fwd_ws_bytes(a);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
   int2* spans = static_cast<int2*>(ws);
-  if (a->head_dim == 64) return launch_fwd2<64, 4, 4, false>(a, spans, st);
-  return launch_fwd2<128, 2, 2, false>(a, spans, st);
+  if (a->head_dim == 64) return launch_fwd2<64, 4, 4, false>(a, spans, fwd_ws_tiles(a, ws), st);
+  return launch_fwd2<128, 2, 2, false>(a, spans, fwd_ws_tiles(a, ws), st);
 }
 }  // namespace vlasim_host
 
@@ -558,7 +606,7 @@ extern "C" int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args* a, void
   using namespace vlasim_host;
   if (int rc = validate_attn_args(a, true)) return rc;
   if (a->head_dim != 128) return set_error(VLASIM_ECONFIG, "fp8 Q/K attention: head_dim must be 128");
-  const size_t need = size_t(a->total_tokens) * sizeof(int2);
+  const size_t need = fwd_ws_bytes(a);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
-  return launch_fwd2<128, 3, 3, true>(a, static_cast<int2*>(ws), as_stream(stream));
+  return launch_fwd2<128, 3, 3, true>(a, static_cast<int2*>(ws), fwd_ws_tiles(a, ws), as_stream(stream));
 }

@@ -46,6 +46,13 @@ inline cudaStream_t as_stream(vlasim_stream_t s) { return reinterpret_cast<cudaS
 
 int num_sms();
 
+// Segment-aligned 128-row tiles of the packed stream, sorted by cost (attn_tiles.cu).  `buf` holds
+// tiles_bytes(T, nseq) bytes; *tiles / *ntiles point into it (the count is written on device).
+size_t tiles_bytes(int64_t T, int nseq);
+size_t fwd_ws_bytes(const vlasim_attn_args* a);  // forward workspace: spans + tiles (attn_fwd2.cu)
+int launch_build_tiles(const int32_t* cu, int nseq, int64_t T, void* buf, cudaStream_t st, int2** tiles,
+                       int** ntiles);
+
 // VLASIM_PROF=1: kernels with wait-time accounting are launched instead and each launch prints
 // (stderr) the average cycles per CTA spent in every named wait category.
 bool prof_enabled();

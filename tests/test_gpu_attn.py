@@ -41,6 +41,17 @@ CASES = [
     ([700, 33, 260], 8, 1, 256, 2),   # config-3 shape: H=8, Hkv=1 (MQA), prefix-LM
     ([100, 28, 300, 5, 1, 130], 2, 2, 256, 0),
     ([513, 77, 129], 4, 2, 256, 1),
+    # segment-aligned tiles: partial tiles of every 64/32/16/8/tail row combination, neighbours
+    # that a clipped store must not touch
+    ([127, 1, 255, 9, 135, 64, 72, 200, 7, 385, 128, 120], 2, 2, 128, 0),
+    ([127, 1, 255, 9, 135, 64, 72, 200, 7, 385, 128, 120], 2, 1, 64, 1),
+    ([127, 1, 255, 9, 135, 64, 72, 200, 7, 385], 2, 1, 256, 2),
+    # token counts whose last k_bwd_pre block covers < 32 lanes of work (warp-uniform shuffles)
+    ([385], 1, 1, 64, 1),
+    ([129], 1, 1, 64, 0),
+    ([256, 1], 1, 1, 128, 0),
+    # > 1024 segments: the tile builder's chunked stable sort
+    (list(np.random.default_rng(5).integers(1, 41, 1500)), 1, 1, 64, 0),
 ]
 
 

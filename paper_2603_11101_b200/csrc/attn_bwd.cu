@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // previous item's last dQ is issued before waiting for the next item's Q/dO, so dq_full —
     // and the epilogue — never wait behind that load.
     {
-      constexpr uint32_t id_kk = make_idesc_bf16(128, BN, false, false);   // S, dP
+      constexpr uint32_t id_kk0 = make_idesc_bf16(128, 0, false, false);  // S, dP: | N/8 << 17
       constexpr uint32_t id_dq = make_idesc_bf16(128, HD, false, true);    // dQ (A from TMEM, B MN-major)
       constexpr uint32_t T16 = Cfg::KTILE >> 4;                            // ring stage stride, desc units
       const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       uint32_t kph = 0, vph = 0;   // their use parities
       bool pend = false;    // dQ of the previous tile not issued yet
       bool plast = false, pfirst = false;
-      int pks = 0, pg = 0;  // its K stage and tile ordinal
+      int pks = 0, pg = 0, pna = 4;  // its K stage, tile ordinal and active W-key slices
       TraceCtr trace(lane == 0 && trb ? trb + 2001 : nullptr);
       int pk = 0;  // item ordinal of the pending dQ
       auto do_dq = [&]() {
@@ -815,8 +815,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           const uint32_t a = tmem + Cfg::s_col(pg);
 #pragma unroll
           for (int s = 0; s < BN / 16; ++s)  // dS: keys Wp..Wp+W−1 packed at S cols Wp .. Wp+W/2−1
-            umma_f16_ts(tmem + Cfg::DQ_COL, a + (s / (W / 16)) * W + (s % (W / 16)) * 8,
-                        sdesc_add(dKm, s * 2048) + pks * T16, id_dq, (!pfirst || s > 0) ? 1u : 0u);
+            if (s < pna * (W / 16))
+              umma_f16_ts(tmem + Cfg::DQ_COL, a + (s / (W / 16)) * W + (s % (W / 16)) * 8,
+                          sdesc_add(dKm, s * 2048) + pks * T16, id_dq, (!pfirst || s > 0) ? 1u : 0u);
           umma_commit(&bar_k_empty[pks]);
           if (plast) umma_commit(bar_dq_full);
         }
@@ -832,6 +833,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
         mbar_wait(bar_qdo_full, k & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
+          // the item's last key tile: N = W · ⌈valid keys / W⌉ for S and dP, dQ over those keys
+          const int na = j + 1 < itm.nkv ? 4 : (itm.kv_hi - itm.kv_lo - j * BN + W - 1) / W;
+          const uint32_t id_kk = id_kk0 | (uint32_t(na * W / 8) << 17);
           mbar_wait(&bar_k_full[ks], kph);
           trace(12, g);  // M: K seen
           tc_fence_after();
@@ -866,6 +870,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           pks = ks;
           pg = g;
           pk = k;
+          pna = na;
           if (++ks == KS) { ks = 0; kph ^= 1; }
           if (++vs == VS) { vs = 0; vph ^= 1; }
         }
@@ -904,6 +909,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       if (itm.nkv == 0) continue;
       const int row = itm.q0 + r;
       const bool valid = row < itm.qe;  // rows past the tile's end belong to the next segment
+      // the last key tile computes ⌈valid/W⌉ slices of W keys: this warp's slice is idle there
+      const int j_skip = part >= (itm.kv_hi - itm.kv_lo - (itm.nkv - 1) * BN + W - 1) / W ? itm.nkv - 1 : -1;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::s_col(g) + c0;
         const int kv0 = itm.kv_lo + j * BN + c0;
@@ -912,6 +919,16 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= W);
         const int vlo = min(max(c_lo, 0), W), vhi = min(max(c_hi, 0), W);
         const uint32_t vm = vhi <= vlo ? 0u : ((vhi >= 32 ? 0xffffffffu : (1u << vhi) - 1u) & ~((1u << vlo) - 1u));
+        if (j == j_skip) {
+          // a slice past the last key tile's ⌈valid/W⌉ (S and dP ran with N = W · that): no loads,
+          // exponentials or dS stores — only the barrier handshakes
+          mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+          mbar_wait(bar_dp_full, g & 1);
+          tc_fence_before();
+          warp_arrive(bar_dp_free);
+          warp_arrive(&bar_p_full[g & 1]);
+          continue;
+        }
         mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
         trace(20, g);  // S: s_full seen
         tc_fence_after();

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // ================================================ MMA issuer (whole warp: descriptors and
     // counters in uniform registers; one elected lane issues)
     {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
+      constexpr uint32_t idesc_s0 = make_idesc_bf16(128, 0, false, false);  // | N/8 << 17
       constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
       constexpr uint32_t Q16 = Cfg::Q_BYTES >> 4, K16 = Cfg::K_BYTES >> 4, V16 = Cfg::KV_BYTES >> 4;
       const uint64_t dQ0 = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int ks = 0, vs = 0;                // ring stages of tile g (K) and of the pending PV (V)
       uint32_t kph = 0, vph = 0;
       bool pend = false, pfirst = false, plast = false;  // pending PV (issued one tile late)
-      int pg = 0, pk = 0;
+      int pg = 0, pk = 0, pnq = 4;  // its tile / item ordinals and active 32-key quarters
       auto do_pv = [&]() {
         wp.template wait<2>(&bar_p_full[pg & 1], (pg >> 1) & 1);
         if (pfirst && pk >= 2) wp.template wait<3>(&bar_o_empty[pk & 1], ((pk >> 1) - 1) & 1);
@@ -276,8 +276,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const uint64_t vd = dV0 + vs * V16;
 #pragma unroll
           for (int s = 0; s < BN / 16; ++s)  // P: keys 32q..32q+31 packed at S cols 32q .. 32q+15
-            umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s >> 1) * 32 + (s & 1) * 8,
-                        sdesc_add(vd, s * 2048), idesc_o, (!pfirst || s > 0) ? 1u : 0u);
+            if (s < 2 * pnq)
+              umma_f16_ts(tmem + Cfg::O_COL + (pk & 1) * HD, a_tm + (s >> 1) * 32 + (s & 1) * 8,
+                          sdesc_add(vd, s * 2048), idesc_o, (!pfirst || s > 0) ? 1u : 0u);
           umma_commit(&bar_v_empty[vs]);
           umma_commit(bar_o_ready);
           if (plast) umma_commit(&bar_o_full[pk & 1]);
@@ -298,9 +299,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tc_fence_after();
           const uint32_t d_s = tmem + Cfg::S_COL + (g & 1) * 128;
           const uint64_t kd = dK0 + ks * K16;
+          // the item's last tile: N = 32 · ⌈valid keys / 32⌉
+          const int nq = j + 1 < itm.nkv ? 4 : (itm.kv_hi - itm.kv_lo - j * BN + 31) >> 5;
+          const uint32_t idesc_s = idesc_s0 | (uint32_t(nq * 4) << 17);
           if (elect_one()) {
             if constexpr (FP8) {  // kind::f8f6f4: 32 E4M3 elements (32 B) per K step
-              constexpr uint32_t idesc_f8 = make_idesc_e4m3(128, BN);
+              const uint32_t idesc_f8 = make_idesc_e4m3(128, 0) | (uint32_t(nq * 4) << 17);
 #pragma unroll
               for (int s = 0; s < HD / 32; ++s)
                 umma_f8_ss(d_s, sdesc_add(qd, (s / 4) * 128 * 128 + (s % 4) * 32),
@@ -323,6 +327,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           plast = j == itm.nkv - 1;
           pg = g;
           pk = k;
+          pnq = nq;
         }
       }
       if (pend) do_pv();
@@ -403,6 +408,46 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
           k0s = __ldg(ksc + min(kv0 / 128, p.nbt - 1));
           k1s = __ldg(ksc + min(kv0 / 128 + 1, p.nbt - 1));
+        }
+        if (j + 1 == itm.nkv && qp >= ((itm.kv_hi - kv0 + c0 + 31) >> 5)) {
+          // The item's last key tile covers only ⌈valid/32⌉ quarters (its S MMA ran with N = 32 of
+          // them): this quarter has no S, exponentials or P.  It still takes part in the row-max
+          // exchange and the lazy O rescale of its columns.
+          wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
+          float* xs = xch + (g & 1) * 512;
+          xs[qp * 128 + r] = -INFINITY;
+          named_bar_sync(1 + quad, 128);
+          float mt = fmaxf(fmaxf(xs[r], xs[128 + r]), fmaxf(xs[256 + r], xs[384 + r]));
+          mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
+          const bool grow = mt > m_run + kLazyRescale;
+          const float alpha = grow ? exp2f(m_run - mt) : 1.f;
+          const bool rescale = __any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY);
+          if (grow) {
+            l_run *= alpha;
+            m_run = mt;
+          }
+          if (rescale) {
+            wp.template wait<1>(bar_o_ready, (g - 1) & 1);
+            tc_fence_after();
+            uint32_t o[32];
+            tmem_ld32(o_tm, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < OC; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            if constexpr (OC == 32) {
+              tmem_st32(o_tm, o);
+            } else {
+              uint32_t o16[16];
+#pragma unroll
+              for (int t = 0; t < 16; ++t) o16[t] = o[t];
+              tmem_st16(o_tm, o16);
+            }
+            tmem_wait_st();
+          }
+          tc_fence_before();
+          warp_arrive(&bar_p_full[g & 1]);
+          if (j == 0 && ek >= 0) epilogue();
+          continue;
         }
         wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();

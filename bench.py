@@ -4,8 +4,11 @@
 Workload (BASELINE.json configs[1], "GR00T-N1.5 Eagle-backbone shape"): per GPU, 512 samples with
 lengths uniform_int(16, 512) from make_rng(42, "lengths", rank) (rng.hpp), packed to 8192-token bins
 by the GPU FFD packer; 16 heads × d = 128, bf16, bidirectional block-diagonal attention, fwd + bwd.
-One step = GPU pack → gather Q/K/V rows into the packed stream → attention fwd → attention bwd →
-scatter dQ/dK/dV back to sample order.  Inputs (≈2.3 GB per GPU) are larger than L2 (126 MB).
+One step = GPU pack → per-segment source offsets (seg_src) → attention fwd → attention bwd.  The
+gather of Q/K/V into the packed stream and the scatter of O/dQ/dK/dV back to sample order are
+folded into the attention kernels' TMA coordinates (--layout fused, default); --layout packed runs
+the explicit 16-B row-gather kernels + a materialised packed stream instead (identical results,
+tests/test_gpu_seg_src.py).  Inputs (≈2.3 GB per GPU) are larger than L2 (126 MB).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dist uniform|groot]
 
@@ -57,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=48)
     ap.add_argument("--no-graph", action="store_true", help="launch the step's kernels directly (no CUDA graph)")
+    ap.add_argument("--layout", default="fused", choices=["fused", "packed"],
+                    help="fused: attention reads / writes sample-major rows through seg_src; packed: explicit "
+                         "gather into the packed stream + row_map scatter")
     return ap.parse_args()
 
 
@@ -221,33 +227,49 @@ def main():
     sub = packing.pack_ffd(d_len_mine, CAPACITY)  # this rank's packs (same FFD on its samples)
     ws = attention.BwdWorkspace()
     stream = torch.cuda.current_stream()
-    ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in ("fwd", "bwd")}
 
     gidx = torch.empty(T, dtype=torch.int32, device=dev)
+    seg = torch.empty(sub.n, dtype=torch.int32, device=dev)
 
     bufs = {"q": q_src, "k": k_src, "v": v_src, "do": do_p, "len": d_len_mine, "o": None, "lse": None,
             "dq": dq_s, "dk": dk_s, "dv": dv_s}
 
-    def step(record=False, b=bufs):
-        # 1. pack (GPU FFD + layout), 2. gather index, 3. gather Q/K/V rows into the packed stream,
-        # 4. attention fwd, 5. attention bwd with the scatter back to sample order fused (row_map)
-        packing.pack_ffd(b["len"], CAPACITY, plan=sub, sync_check=False)
+    bufs["o"] = torch.empty_like(q_src)
+    bufs["lse"] = torch.empty(H, T, dtype=torch.float32, device=dev)
+
+    def phases(b):
+        """The step as three stream-ordered phases: pack, attention fwd, attention bwd."""
         cu = sub.cu_seqlens
-        packing.token_ids_into(sub, T, gather_idx=gidx)
-        packing.gather_rows(b["q"], sub, out=qp)
-        packing.gather_rows(b["k"], sub, out=kp)
-        packing.gather_rows(b["v"], sub, out=vp)
-        if record:
-            ev["fwd"][0].record(stream)
-        o, lse = attention.varlen_attn_fwd(qp, kp, vp, cu, out=b["o"], lse=b["lse"])
-        if record:
-            ev["fwd"][1].record(stream)
-            ev["bwd"][0].record(stream)
-        attention.varlen_attn_bwd(b["do"], qp, kp, vp, o, lse, cu, workspace=ws, dq=b["dq"], dk=b["dk"], dv=b["dv"],
-                                  row_map=gidx)
-        if record:
-            ev["bwd"][1].record(stream)
-        return o
+
+        def p_pack():
+            packing.pack_ffd(b["len"], CAPACITY, plan=sub, sync_check=False)
+            if a.layout == "fused":  # segment source offsets: the packed stream stays virtual
+                packing.seg_src(sub, out=seg)
+            else:  # gather index + explicit gather of Q/K/V rows into the packed stream
+                packing.token_ids_into(sub, T, gather_idx=gidx)
+                packing.gather_rows(b["q"], sub, out=qp)
+                packing.gather_rows(b["k"], sub, out=kp)
+                packing.gather_rows(b["v"], sub, out=vp)
+
+        if a.layout == "fused":  # attention over the sample-major rows (TMA coordinates = seg_src + offset)
+            def p_fwd():
+                attention.varlen_attn_fwd(b["q"], b["k"], b["v"], cu, out=b["o"], lse=b["lse"], seg_src=seg)
+
+            def p_bwd():
+                attention.varlen_attn_bwd(b["do"], b["q"], b["k"], b["v"], b["o"], b["lse"], cu, workspace=ws,
+                                          dq=b["dq"], dk=b["dk"], dv=b["dv"], seg_src=seg)
+        else:  # packed stream; dQ/dK/dV scattered back to sample order in the epilogues (row_map)
+            def p_fwd():
+                attention.varlen_attn_fwd(qp, kp, vp, cu, out=b["o"], lse=b["lse"])
+
+            def p_bwd():
+                attention.varlen_attn_bwd(b["do"], qp, kp, vp, b["o"], b["lse"], cu, workspace=ws, dq=b["dq"],
+                                          dk=b["dk"], dv=b["dv"], row_map=gidx)
+        return [p_pack, p_fwd, p_bwd]
+
+    def step(b=bufs):
+        for f in phases(b):
+            f()
 
     for _ in range(max(3, a.warmup)):
         step()
@@ -257,15 +279,16 @@ def main():
     # dependent small packer kernels and the attention kernels.
     graphs = {}
 
-    def capture(b):
+    def capture(b, fn=None):
+        fn = fn or (lambda: step(b=b))
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            step(b=b)  # warm-up on the capture stream
+            fn()  # warm-up on the capture stream
         torch.cuda.current_stream().wait_stream(side)
         with torch.cuda.graph(g):
-            step(b=b)
+            fn()
         torch.cuda.synchronize()
         return g
 
@@ -289,13 +312,20 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / a.steps
-    # per-kernel average over the timed region (separately instrumented pass with the same events)
-    kfwd, kbwd = [], []
-    for _ in range(min(a.steps, 10)):
-        step(record=True)
-        torch.cuda.synchronize()
-        kfwd.append(ev["fwd"][0].elapsed_time(ev["fwd"][1]))
-        kbwd.append(ev["bwd"][0].elapsed_time(ev["bwd"][1]))
+    # per-phase device time: the three phases captured as separate graphs and replayed back to back
+    # with events between them on the launching stream (no host gaps inside a phase)
+    ph_graphs = [capture(bufs, f) for f in phases(bufs)] if not a.no_graph else None
+    nrep = min(a.steps, 10)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nrep)]
+    for r in range(nrep):
+        evs[r][0].record(stream)
+        for i, f in enumerate(phases(bufs)):
+            ph_graphs[i].replay() if ph_graphs else f()
+            evs[r][i + 1].record(stream)
+    torch.cuda.synchronize()
+    kpack = [e[0].elapsed_time(e[1]) for e in evs]
+    kfwd = [e[1].elapsed_time(e[2]) for e in evs]
+    kbwd = [e[2].elapsed_time(e[3]) for e in evs]
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -395,17 +425,22 @@ def main():
                            float(fl_all.item()) / (ms_max / 1e3) / 1e12,
                        "l2": "inputs larger than L2 (%.1f GB/GPU)" % (4 * T * H * D * 2 / 1e9),
                        "parallelism": f"packs sharded over {world} GPU(s) (LPT), no collective on attention",
-                       "launch": "CUDA graph replay of the step" if not a.no_graph else "direct launches"},
+                       "launch": "CUDA graph replay of the step" if not a.no_graph else "direct launches",
+                       "layout": "fused: gather / scatter folded into the attention kernels' TMA coordinates "
+                                 "(seg_src)" if a.layout == "fused" else
+                                 "packed: explicit row gather into the packed stream, row_map scatter"},
             "roofline": {"bound": "tensor", "kernel": "backward: k_bwd_pre + k_bwd_dkdv + k_bwd_dq",
                          "achieved": bwd_flops / (kb / 1e3) / 1e12, "peak": PEAKS["bf16_tflops"],
                          "unit": "TFLOP/s", "frac": bwd_flops / (kb / 1e3) / 1e12 / PEAKS["bf16_tflops"],
                          "traffic": bwd_traffic(), "peak_src": PEAKS["src"],
-                         "fwd": {"achieved": fl_fwd / (kf / 1e3) / 1e12, "ms": kf}, "bwd_ms": kb},
+                         "fwd": {"achieved": fl_fwd / (kf / 1e3) / 1e12, "ms": kf}, "bwd_ms": kb,
+                         "pack_ms": statistics.mean(kpack)},
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
             # our launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
-            # token ids 1, gather 3, fwd 2 (spans, attention), bwd 3 (pre, dK/dV, dQ)
-            "gpu_launches": 23 * a.steps,
+            # fused: seg_src 1; packed: token ids 1 + gather 3; fwd 3 (spans, tiles, attention),
+            # bwd 4 (pre, tiles, dK/dV, dQ)
+            "gpu_launches": (22 if a.layout == "fused" else 25) * a.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VLASIM_ABI_VERSION 1
+#define VLASIM_ABI_VERSION 2
 
 enum {
   VLASIM_OK = 0,
@@ -103,6 +103,9 @@ int vlasim_gather_rows_cuda(const void* d_src, void* d_dst, int64_t row_bytes, c
                             const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream);
 int vlasim_scatter_rows_cuda(const void* d_packed, void* d_dst, int64_t row_bytes, const int32_t* d_len,
                              const vlasim_pack_out* out, int64_t n, vlasim_stream_t stream);
+/* seg_src[m] = src_off[member_ids[m]] for the n packed segments: the source row of each
+ * segment's first token (vlasim_attn_args.seg_src — the gather folded into attention). */
+int vlasim_pack_seg_src_cuda(const vlasim_pack_out* out, int64_t n, int32_t* d_seg_src, vlasim_stream_t stream);
 
 /* ------------------------------------------------------------------ attention
  * Replaces vlasim::packed_attention(q, k, v, cu_seqlens),
@@ -138,6 +141,14 @@ typedef struct vlasim_attn_args {
      [Hkv, ceil(T/128), ceil(d/128)] for k                       */
   const float* q_scale;
   const float* k_scale;
+  /* [num_seqs] or NULL.  NULL: q/k/v/o/lse (and dout/dq/dk/dv) are in packed-stream order.
+     Set: they stay in the SOURCE (sample-major) order and segment m's packed rows
+     [cu_seqlens[m], cu_seqlens[m+1]) live at source rows seg_src[m] + (t - cu_seqlens[m]);
+     the lse / fp8 scale blocks are indexed by source row too.  With the packer's layout
+     (seg_src[m] = src_off[member_ids[m]], vlasim_pack_seg_src_cuda) the gather into the
+     packed stream and the scatter back are folded into the kernels' TMA coordinates.
+     (ABI version 2; row_map must be NULL when it is set.)                                  */
+  const int32_t* seg_src;
 } vlasim_attn_args;
 
 typedef struct vlasim_attn_grads {

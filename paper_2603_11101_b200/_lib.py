@@ -31,7 +31,8 @@ class AttnArgs(C.Structure):
         ("q", C.c_void_p), ("k", C.c_void_p), ("v", C.c_void_p), ("o", C.c_void_p), ("lse", f32p),
         ("cu_seqlens", i32p), ("prefix_len", i32p), ("num_seqs", C.c_int32), ("total_tokens", C.c_int64),
         ("num_heads", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
-        ("mask_mode", C.c_int32), ("softmax_scale", C.c_float), ("q_scale", f32p), ("k_scale", f32p)]
+        ("mask_mode", C.c_int32), ("softmax_scale", C.c_float), ("q_scale", f32p), ("k_scale", f32p),
+        ("seg_src", i32p)]
 
 
 class AttnGrads(C.Structure):
@@ -51,6 +52,7 @@ _SIGS = {
                                              C.c_void_p]),
     "vlasim_gather_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, C.POINTER(PackOut), C.c_int64,
                                           C.c_void_p]),
+    "vlasim_pack_seg_src_cuda": (C.c_int, [C.POINTER(PackOut), C.c_int64, i32p, C.c_void_p]),
     "vlasim_scatter_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, C.POINTER(PackOut), C.c_int64,
                                            C.c_void_p]),
     "vlasim_varlen_attn_workspace_size": (C.c_size_t, [C.POINTER(AttnArgs), C.c_int]),

@@ -3,6 +3,9 @@
 hand-written sm_100a kernels.  Every call goes through the C-ABI; no CPU fallback.
 
 Layout: q/o [T, H, d] bf16, k/v [T, Hkv, d] bf16, lse [H, T] fp32, cu_seqlens [nseq+1] int32.
+With seg_src (int32 [nseq], packing.seg_src) the tensors stay in sample-major order and the packed
+stream is virtual: segment m's rows are read / written at seg_src[m] + offset (the gather and the
+scatter folded into the kernels' TMA coordinates).
 """
 from __future__ import annotations
 
@@ -17,7 +20,8 @@ from .errors import ConfigError
 MASK_BIDIR, MASK_CAUSAL, MASK_PREFIX = 0, 1, 2
 
 
-def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale=None, k_scale=None):
+def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale=None, k_scale=None,
+          seg_src=None):
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
         raise ConfigError("q, k, v must be [T, heads, d]")
     T, H, d = q.shape
@@ -32,13 +36,16 @@ def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_s
             raise ConfigError("tensors must be contiguous CUDA tensors")
     if mask_mode == MASK_PREFIX and prefix_len is None:
         raise ConfigError("prefix mask needs prefix_len")
+    if seg_src is not None and (seg_src.dtype != torch.int32 or seg_src.numel() != cu_seqlens.numel() - 1):
+        raise ConfigError("seg_src must be int32 [num_seqs]")
     scale = float(softmax_scale) if softmax_scale is not None else 1.0 / math.sqrt(d)
     a = _lib.AttnArgs(
         _lib.ptr(q).value, _lib.ptr(k).value, _lib.ptr(v).value, _lib.ptr(o).value, _lib.ptr(lse, _lib.f32p),
         _lib.ptr(cu_seqlens, _lib.i32p), _lib.ptr(prefix_len, _lib.i32p) if prefix_len is not None else None,
         cu_seqlens.numel() - 1, T, H, k.shape[1], d, int(mask_mode), scale,
         _lib.ptr(q_scale, _lib.f32p) if q_scale is not None else None,
-        _lib.ptr(k_scale, _lib.f32p) if k_scale is not None else None)
+        _lib.ptr(k_scale, _lib.f32p) if k_scale is not None else None,
+        _lib.ptr(seg_src, _lib.i32p) if seg_src is not None else None)
     return a
 
 
@@ -59,12 +66,12 @@ _default_fwd_ws = BwdWorkspace()
 
 
 def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None, softmax_scale=None, out=None,
-                    lse=None, workspace: BwdWorkspace | None = None, stream=None):
+                    lse=None, workspace: BwdWorkspace | None = None, seg_src=None, stream=None):
     """Block-diagonal attention forward. Returns (o [T,H,d] bf16, lse [H,T] fp32 natural-log)."""
     T, H, d = q.shape
     o = out if out is not None else torch.empty_like(q)
     lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=q.device)
-    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, seg_src=seg_src)
     L = _lib.lib()
     ws = (workspace or _default_fwd_ws).get(L.vlasim_varlen_attn_workspace_size(C.byref(a), 0), q.device)
     _lib.check(L.vlasim_varlen_attn_fwd_cuda(C.byref(a), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
@@ -74,7 +81,7 @@ def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=Non
 
 def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None,
                     softmax_scale=None, dq=None, dk=None, dv=None, workspace: BwdWorkspace | None = None,
-                    row_map=None, stream=None):
+                    row_map=None, seg_src=None, stream=None):
     """Backward of varlen_attn_fwd. Returns (dq, dk, dv) bf16.  With row_map (int32 [T], e.g. the
     packer's gather index) gradient row t is written to row row_map[t] — the scatter back to sample
     order fused into the kernels."""
@@ -83,7 +90,7 @@ def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, 
     dv = dv if dv is not None else torch.empty_like(v)
     if not dout.is_contiguous() or dout.shape != q.shape:
         raise ConfigError("dout must be contiguous with q's shape")
-    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale)
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, seg_src=seg_src)
     if row_map is not None and (row_map.dtype != torch.int32 or row_map.numel() != q.shape[0]):
         raise ConfigError("row_map must be int32 [T]")
     g = _lib.AttnGrads(_lib.ptr(dout).value, _lib.ptr(dq).value, _lib.ptr(dk).value, _lib.ptr(dv).value,

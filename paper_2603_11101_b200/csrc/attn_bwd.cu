@@ -131,7 +131,7 @@ struct BwdParams {
   const float* dsum;       // [H, Tp] rowsum(dO ∘ O)
   const int2* rows_span;   // [T] visible keys of query t
   const int2* cols_span;   // [T] queries that see key t
-  const int2* tiles;       // segment-aligned 128-row tiles [t0, te), sorted by cost (attn_tiles.cu)
+  const int4* tiles;       // segment-aligned 128-row tiles {t0, te, delta}, sorted by cost (attn_tiles.cu)
   const int* ntiles;       // device-side tile count
   int T, Tp, H, Hkv;
   int64_t vec_copy;  // element stride between the 4 shifted copies of lse2 / dsum
@@ -194,15 +194,17 @@ struct DkvCfg {
 // Item descriptors are loaded one item ahead; only the raw span loads are issued then and the
 // derived counts are computed when the item becomes current (kv_item_finish), so the loads'
 // latency never stalls a role at an item boundary.
+// k0, ke, q_lo, q_hi: packed-stream rows (spans, masks); data rows are those + dl (seg_src).
 struct KvItem {
-  int k0, ke, kh, q_lo, q_hi, nq, iters;
+  int k0, ke, dl, kh, q_lo, q_hi, nq, iters;
 };
 __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   KvItem it;
-  const int2 t = __ldg(&p.tiles[i / p.Hkv]);
+  const int4 t = __ldg(&p.tiles[i / p.Hkv]);
   it.kh = i % p.Hkv;
   it.k0 = t.x;
   it.ke = t.y;
+  it.dl = t.z;
   it.q_lo = __ldg(&p.cols_span[t.x].x);      // key spans are monotone inside a segment
   it.q_hi = __ldg(&p.cols_span[t.y - 1].y);
   return it;
@@ -319,20 +321,20 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           mbar_expect_tx(bar_kv_full, 2 * Cfg::KT);
 #pragma unroll
           for (int j = 0; j < HD / 64; ++j) {
-            tma_load_2d(smem + Cfg::OFF_K + j * 16384, &tmK, c.itm.kh * HD + j * 64, c.itm.k0, bar_kv_full);
-            tma_load_2d(smem + Cfg::OFF_V + j * 16384, &tmV, c.itm.kh * HD + j * 64, c.itm.k0, bar_kv_full);
+            tma_load_2d(smem + Cfg::OFF_K + j * 16384, &tmK, c.itm.kh * HD + j * 64, c.itm.k0 + c.itm.dl, bar_kv_full);
+            tma_load_2d(smem + Cfg::OFF_V + j * 16384, &tmV, c.itm.kh * HD + j * 64, c.itm.k0 + c.itm.dl, bar_kv_full);
           }
           // the next item's K/V into L2 now: its load (single K/V buffer, issued only once this
           // item's last dP has run) then hits L2 at the item boundary
           if (c.has_next()) {
 #pragma unroll
             for (int j = 0; j < HD / 64; ++j) {
-              tma_prefetch_2d(&tmK, c.nxt.kh * HD + j * 64, c.nxt.k0);
-              tma_prefetch_2d(&tmV, c.nxt.kh * HD + j * 64, c.nxt.k0);
+              tma_prefetch_2d(&tmK, c.nxt.kh * HD + j * 64, c.nxt.k0 + c.nxt.dl);
+              tma_prefetch_2d(&tmV, c.nxt.kh * HD + j * 64, c.nxt.k0 + c.nxt.dl);
             }
           }
         }
-        const int h = c.head(group), qb = c.qb();
+        const int h = c.head(group), qb = c.qb() + c.itm.dl;  // data row of the unit's first query
         const int sh = (-qb) & 3;  // 16-B aligned window in shifted copy sh (k_bwd_pre)
         const int64_t vo = sh * p.vec_copy + int64_t(h) * p.Tp + qb + sh;
         if (c.u >= NS) wp.template wait<0>(&bar_qd_empty[s], ph ^ 1);
@@ -485,7 +487,9 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     UnitCursor<UQ> c;
     auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
     // keys past the tile's end belong to the next segment: never stored
-    auto dst_of = [&](int key, int ke) { return key < ke ? (p.row_map ? __ldg(p.row_map + key) : key) : -1; };
+    auto dst_of = [&](int key, int ke, int dl) {
+      return key < ke ? (p.row_map ? __ldg(p.row_map + key) : key + dl) : -1;
+    };
     int ss = 0;  // stage of unit c.u
     int2 ks = make_int2(0, 0), ks_nxt = ks;
     int dst_key = -1, dst_nxt = -1;
@@ -494,11 +498,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       if (c.it == 0) {  // this item's spans were prefetched one item ahead (first item: now)
         const int key = c.itm.k0 + krow;
         ks = c.k == 0 ? span_of(key) : ks_nxt;
-        dst_key = c.k == 0 ? dst_of(key, c.itm.ke) : dst_nxt;
+        dst_key = c.k == 0 ? dst_of(key, c.itm.ke, c.itm.dl) : dst_nxt;
         if (c.has_next()) {
           const int nkey = c.nxt.k0 + krow;
           ks_nxt = span_of(nkey);
-          dst_nxt = dst_of(nkey, c.nxt.ke);
+          dst_nxt = dst_of(nkey, c.nxt.ke, c.nxt.dl);
         }
       }
       const int s = ss;
@@ -660,14 +664,15 @@ struct DqCfg {
 };
 
 struct QItem {
-  int q0, qe, h, kh, kv_lo, kv_hi, nkv;
+  int q0, qe, dl, h, kh, kv_lo, kv_hi, nkv;
 };
 __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {  // raw loads (see KvItem)
   QItem it;
-  const int2 t = __ldg(&p.tiles[i / p.H]);
+  const int4 t = __ldg(&p.tiles[i / p.H]);
   it.h = i % p.H;
   it.q0 = t.x;
   it.qe = t.y;
+  it.dl = t.z;
   it.kh = it.h / (p.H / p.Hkv);
   it.kv_lo = __ldg(&p.rows_span[t.x].x);
   it.kv_hi = __ldg(&p.rows_span[t.y - 1].y);
@@ -754,11 +759,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         mbar_expect_tx(bar_qdo_full, 2 * Cfg::TILE);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) {
-          tma_load_2d(smem + Cfg::OFF_Q + c * 16384, &tmQ, itm.h * HD + c * 64, itm.q0, bar_qdo_full);
-          tma_load_2d(smem + Cfg::OFF_DO + c * 16384, &tmdO, itm.h * HD + c * 64, itm.q0, bar_qdo_full);
+          tma_load_2d(smem + Cfg::OFF_Q + c * 16384, &tmQ, itm.h * HD + c * 64, itm.q0 + itm.dl, bar_qdo_full);
+          tma_load_2d(smem + Cfg::OFF_DO + c * 16384, &tmdO, itm.h * HD + c * 64, itm.q0 + itm.dl, bar_qdo_full);
         }
         for (int j = 0; j < itm.nkv; ++j, ++g) {
-          const int kv0 = itm.kv_lo + j * BN;
+          const int kv0 = itm.kv_lo + j * BN + itm.dl;  // data row
           const int ks = g % KS, vs = g % VS;
           if (g >= KS) mbar_wait(&bar_k_empty[ks], ((g / KS) - 1) & 1);
           if (PROF && (p.dbg & 2)) {  // timing experiment: no K/V traffic (the trace lives in the K ring)
@@ -889,10 +894,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // row parameters of the next item are prefetched one item ahead
     auto load_row = [&](const QItem& it, int2& rs_, float& l_, float& d_) {
       const int rw = it.q0 + r;
-      const bool v = rw < p.T;
-      rs_ = v ? __ldg(p.rows_span + rw) : make_int2(0, 0);
-      l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw) : 0.f;  // copy 0 (unshifted)
-      d_ = v ? __ldg(p.dsum + int64_t(it.h) * p.Tp + rw) : 0.f;
+      const bool v = rw < it.qe;  // rows past the tile's end belong to the next segment
+      rs_ = rw < p.T ? __ldg(p.rows_span + rw) : make_int2(0, 0);
+      l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw + it.dl) : 0.f;  // copy 0 (unshifted), data row
+      d_ = v ? __ldg(p.dsum + int64_t(it.h) * p.Tp + rw + it.dl) : 0.f;
     };
     QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
     int2 rs_n;
@@ -997,7 +1002,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       // registers → 4-lane chunk transpose → row-segment stores through row_map (8 rows × 64 B
       // per warp store; no smem staging, barrier or TMA op per row)
       {
-        const int dst = valid ? (p.row_map ? __ldg(p.row_map + row) : row) : -1;
+        const int dst = valid ? (p.row_map ? __ldg(p.row_map + row) : row + itm.dl) : -1;
         store_rows_xpose<HD / 32>(pq, dst, p.dq, int64_t(p.H) * HD, itm.h * HD + part * (HD / 4));
       }
       trace(32, g);  // E: done
@@ -1048,9 +1053,9 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
       static_cast<const __nv_bfloat16*>(a->o), static_cast<const __nv_bfloat16*>(g->dout), a->lse, w.lse2, w.dsum,
       w.rows_span, w.cols_span, a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, Tp, H);
   VLASIM_LAUNCH_CHECK();
-  int2* tiles;
+  int4* tiles;
   int* ntiles;
-  if (int rc = launch_build_tiles(a->cu_seqlens, a->num_seqs, T, w.tiles, st, &tiles, &ntiles)) return rc;
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, T, w.tiles, st, &tiles, &ntiles)) return rc;
   const int64_t max_tiles = int64_t(T) / 128 + a->num_seqs;
   CUtensorMap tq, tk, tv, tdo;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -1137,6 +1142,8 @@ extern "C" int vlasim_varlen_attn_bwd_cuda(const vlasim_attn_args* a, const vlas
   using namespace vlasim_host;
   if (int rc = validate_attn_args(a, false)) return rc;
   if (!g || !g->dout || !g->dq || !g->dk || !g->dv) return set_error(VLASIM_ECONFIG, "attention bwd: grads required");
+  if (g->row_map && a->seg_src)
+    return set_error(VLASIM_ECONFIG, "attention bwd: row_map and seg_src are exclusive (seg_src keeps source order)");
   BwdWs w;
   const size_t need = bwd_ws(&w, nullptr, a);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention bwd: workspace %zu < %zu", ws_bytes, need);

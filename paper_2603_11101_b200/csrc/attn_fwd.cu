@@ -33,7 +33,7 @@ struct FwdParams {
   float* lse;
   const int32_t* cu;
   const int32_t* prefix;
-  const int2* tiles;  // segment-aligned Q tiles, sorted by cost (attn_tiles.cu)
+  const int4* tiles;  // segment-aligned Q tiles {q0, qe, delta}, sorted by cost (attn_tiles.cu)
   const int* ntiles;
   int nseq, T, H, Hkv, mask;
   float scale_log2;
@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(192, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (int(blockIdx.x) >= __ldg(p.ntiles) * p.H) return;  // grid sized for the worst-case tile count
   const int h = blockIdx.x % p.H;
-  const int2 tile = __ldg(&p.tiles[blockIdx.x / p.H]);
+  const int4 tile = __ldg(&p.tiles[blockIdx.x / p.H]);
   const int kh = h / (p.H / p.Hkv);
-  const int q0 = tile.x, qe = tile.y;
+  const int q0 = tile.x, qe = tile.y, dl = tile.z;  // packed rows; data rows are + dl (seg_src)
 
   if (tid == 0) {
     mbar_init(&bar_q, 1);
@@ -118,13 +118,13 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch_desc(&tmV);
       mbar_expect_tx(&bar_q, Cfg::Q_BYTES);
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) tma_load_2d(sQ + c * Cfg::BM * 128, &tmQ, h * HD + c * 64, q0, &bar_q);
+      for (int c = 0; c < HD / 64; ++c) tma_load_2d(sQ + c * Cfg::BM * 128, &tmQ, h * HD + c * 64, q0 + dl, &bar_q);
       for (int j = 0; j < nkv; ++j) {
         const int st = j % STAGES;
         if (j >= STAGES) mbar_wait(&bar_kv_empty[st], ((j / STAGES) - 1) & 1);
         uint8_t* sk = sKV + st * 2 * Cfg::KV_BYTES;
         uint8_t* sv = sk + Cfg::KV_BYTES;
-        const int kv0 = kv_lo + j * BN;
+        const int kv0 = kv_lo + j * BN + dl;  // data row
         mbar_expect_tx(&bar_kv_full[st], 2 * Cfg::KV_BYTES);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) tma_load_2d(sk + c * BN * 128, &tmK, kh * HD + c * 64, kv0, &bar_kv_full[st]);
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(192, 1)
     const int row = q0 + tid;
     const bool valid = row < qe && rs.lo < rs.hi;
     const float inv_l = (valid && l_run > 0.f) ? 1.f / l_run : 0.f;
-    __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row) * p.H + h) * HD;
+    __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row + dl) * p.H + h) * HD;
 #pragma unroll
     for (int c = 0; c < HD; c += 32) {
       uint32_t o[32];
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       }
     }
-    if (valid) p.lse[static_cast<int64_t>(h) * p.T + row] = (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+    if (valid) p.lse[static_cast<int64_t>(h) * p.T + row + dl] = (m_run + __log2f(l_run)) * 0.69314718055994530942f;
   }
   tc_fence_before();
   __syncthreads();
@@ -293,8 +293,8 @@ int launch_fwd(const vlasim_attn_args* a, void* tiles_buf, cudaStream_t st) {
   p.lse = a->lse;
   p.cu = a->cu_seqlens;
   p.prefix = a->prefix_len;
-  if (int rc = launch_build_tiles(a->cu_seqlens, a->num_seqs, int64_t(T), tiles_buf, st, const_cast<int2**>(&p.tiles),
-                                  const_cast<int**>(&p.ntiles)))
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, int64_t(T), tiles_buf, st,
+                                  const_cast<int4**>(&p.tiles), const_cast<int**>(&p.ntiles)))
     return rc;
   p.nseq = a->num_seqs;
   p.T = static_cast<int>(T);

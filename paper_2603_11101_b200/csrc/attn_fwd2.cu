@@ -49,7 +49,7 @@ struct Fwd2Params {
   __nv_bfloat16* o;
   float* lse;
   const int2* rows_span;
-  const int2* tiles;     // segment-aligned Q tiles [q0, qe), sorted by cost (attn_tiles.cu)
+  const int4* tiles;     // segment-aligned Q tiles {q0, qe, delta}, sorted by cost (attn_tiles.cu)
   const int* ntiles;     // device-side tile count
   const float* q_scale;  // FP8 only: [H, nbt] per-(head, 128-token block) E4M3 scales (d = 128)
   const float* k_scale;  // FP8 only: [Hkv, nbt]
@@ -83,15 +83,17 @@ struct Fwd2Cfg {
 
 // Items are prefetched one ahead with raw span loads only; the key-tile count is derived when
 // the item becomes current (fwd_item_cur), so the loads never stall a role at an item boundary.
+// q0, qe, kv_lo, kv_hi: packed-stream rows (spans, masks); data rows are those + dl (seg_src).
 struct FwdItem {
-  int q0, qe, h, kh, kv_lo, kv_hi, nkv;
+  int q0, qe, dl, h, kh, kv_lo, kv_hi, nkv;
 };
 __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) {
   FwdItem it;
-  const int2 t = __ldg(&p.tiles[i / p.H]);
+  const int4 t = __ldg(&p.tiles[i / p.H]);
   it.h = i % p.H;
   it.q0 = t.x;
   it.qe = t.y;
+  it.dl = t.z;
   it.kh = it.h / (p.H / p.Hkv);
   it.kv_lo = __ldg(&p.rows_span[t.x].x);      // spans are monotone inside a segment
   it.kv_hi = __ldg(&p.rows_span[t.y - 1].y);
@@ -222,19 +224,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if constexpr (FP8) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
           store_o(k - 2);
         }
-        hq0[qs] = itm.q0;
+        hq0[qs] = itm.q0 + itm.dl;  // data row of the tile (O stores)
         hh[qs] = itm.h;
         hn[qs] = itm.qe - itm.q0;
         uint8_t* sq = smem + Cfg::OFF_Q + qs * Cfg::Q_BYTES;
         mbar_expect_tx(&bar_q_full[qs], Cfg::Q_BYTES);
 #pragma unroll
         for (int c = 0; c < HD / Cfg::QK_BOX; ++c)
-          tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * Cfg::QK_BOX, itm.q0, &bar_q_full[qs]);
+          tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * Cfg::QK_BOX, itm.q0 + itm.dl, &bar_q_full[qs]);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           const int ks = g % KS;
           if (g >= KS) wp.template wait<1>(&bar_k_empty[ks], ((g / KS) - 1) & 1);
           uint8_t* sk = smem + Cfg::OFF_K + ks * Cfg::K_BYTES;
-          const int kv0 = itm.kv_lo + j * BN;
+          const int kv0 = itm.kv_lo + j * BN + itm.dl;  // data row
           mbar_expect_tx(&bar_k_full[ks], Cfg::K_BYTES);
 #pragma unroll
           for (int c = 0; c < HD / Cfg::QK_BOX; ++c)
@@ -398,16 +400,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int row = itm.q0 + r;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + qp * OC;
       // FP8: the row's Q block scale (a segment-aligned tile may straddle two 128-token blocks)
-      if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + min(row, p.T - 1) / 128);
+      if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + min(row + itm.dl, p.T - 1) / 128);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
         const int kv0 = itm.kv_lo + j * BN + c0;
         float k0s = 1.f, k1s = 1.f;  // FP8: this quarter's K block scales, loaded before the S wait
-        if constexpr (FP8) {
+        if constexpr (FP8) {  // scale blocks of data rows
           const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
-          k0s = __ldg(ksc + min(kv0 / 128, p.nbt - 1));
-          k1s = __ldg(ksc + min(kv0 / 128 + 1, p.nbt - 1));
+          k0s = __ldg(ksc + min((kv0 + itm.dl) / 128, p.nbt - 1));
+          k1s = __ldg(ksc + min((kv0 + itm.dl) / 128 + 1, p.nbt - 1));
         }
         if (j + 1 == itm.nkv && qp >= ((itm.kv_hi - kv0 + c0 + 31) >> 5)) {
           // The item's last key tile covers only ⌈valid/32⌉ quarters (its S MMA ran with N = 32 of
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // work); a quarter straddling two blocks scales its columns (a quarter spans ≤ 2 blocks).
         float ksc = 1.f;
         if constexpr (FP8) {
-          const int cb = (kv0 / 128 + 1) * 128 - kv0;
+          const int cb = ((kv0 + itm.dl) / 128 + 1) * 128 - (kv0 + itm.dl);
           if (cb >= 32) {
             ksc = k0s;
           } else {
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (ek >= 0) epilogue();         // (only when this item had no tiles)
       if (itm.nkv > 0) {
         ek = k;
-        e_row = row;
+        e_row = row + itm.dl;  // data row (lse, tail-row stores)
         e_h = itm.h;
         e_n = itm.qe - itm.q0;
         e_m = m_run;
@@ -571,9 +573,9 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, void* tiles_buf, cud
   const int T = int(a->total_tokens);
   k_fwd_spans<<<(T + 255) / 256, 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, rows_span);
   VLASIM_LAUNCH_CHECK();
-  int2* tiles;
+  int4* tiles;
   int* ntiles;
-  if (int rc = launch_build_tiles(a->cu_seqlens, a->num_seqs, T, tiles_buf, st, &tiles, &ntiles)) return rc;
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, T, tiles_buf, st, &tiles, &ntiles)) return rc;
   CUtensorMap tq, tk, tv;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto QK = FP8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : BF;

@@ -14,6 +14,10 @@
 // K/V in L2).  With the persistent kernels' boustrophedon schedule (sched_item) the per-CTA work
 // sums stay balanced — the heaviest items run first and the tail is made of the lightest.
 //
+// Each tile also carries its segment's source offset (vlasim_attn_args.seg_src): data row of
+// packed row t = t + delta, one constant for the tile's rows and for all its keys (a segment's
+// keys are its own rows), so the gather into the packed stream is a TMA coordinate shift.
+//
 // One CTA of 1024 threads: pass 1 histograms the tile counts per cost bucket, pass 2 places each
 // segment's tiles at (bucket offset + weighted rank among the earlier segments of its bucket).
 #include <cstdint>
@@ -25,8 +29,9 @@ namespace {
 constexpr int kTilesThreads = 1024;
 constexpr int kBuckets = 128;  // cost bucket = min(tiles of the segment, 127)
 
-__global__ void __launch_bounds__(kTilesThreads) k_build_tiles(const int32_t* __restrict__ cu, int nseq,
-                                                               int2* __restrict__ tiles, int* __restrict__ ntiles) {
+__global__ void __launch_bounds__(kTilesThreads) k_build_tiles(const int32_t* __restrict__ cu,
+                                                               const int32_t* __restrict__ seg_src, int nseq,
+                                                               int4* __restrict__ tiles, int* __restrict__ ntiles) {
   __shared__ int boff[kBuckets];          // first position of each bucket's next tile
   __shared__ int wsum[32][kBuckets];      // per-warp, per-bucket tile counts → exclusive scan over warps
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -74,7 +79,8 @@ __global__ void __launch_bounds__(kTilesThreads) k_build_tiles(const int32_t* __
     __syncthreads();
     if (c > 0) {
       const int pos = boff[b] + wsum[warp][b] + acc;
-      for (int k = 0; k < c; ++k) tiles[pos + k] = make_int2(lo + 128 * k, min(lo + 128 * (k + 1), hi));
+      const int dl = seg_src ? __ldg(seg_src + s) - lo : 0;
+      for (int k = 0; k < c; ++k) tiles[pos + k] = make_int4(lo + 128 * k, min(lo + 128 * (k + 1), hi), dl, 0);
     }
     __syncthreads();
     if (tid < kBuckets) boff[tid] += total;
@@ -86,14 +92,14 @@ __global__ void __launch_bounds__(kTilesThreads) k_build_tiles(const int32_t* __
 namespace vlasim_host {
 
 // Upper bound of the tile count: Σ⌈l/128⌉ ≤ ⌊T/128⌋ + nseq.
-size_t tiles_bytes(int64_t T, int nseq) { return (size_t(T / 128) + size_t(nseq) + 1) * sizeof(int2) + 16; }
+size_t tiles_bytes(int64_t T, int nseq) { return (size_t(T / 128) + size_t(nseq) + 1) * sizeof(int4) + 16; }
 
-// tiles: [tiles_bytes / 8 − 2] int2, followed by the tile count (int) in the last 16 bytes.
-int launch_build_tiles(const int32_t* cu, int nseq, int64_t T, void* buf, cudaStream_t st, int2** tiles,
-                       int** ntiles) {
-  *tiles = static_cast<int2*>(buf);
+// tiles: {q0, qe, delta, 0} per tile, followed by the tile count (int) in the last 16 bytes.
+int launch_build_tiles(const int32_t* cu, const int32_t* seg_src, int nseq, int64_t T, void* buf, cudaStream_t st,
+                       int4** tiles, int** ntiles) {
+  *tiles = static_cast<int4*>(buf);
   *ntiles = reinterpret_cast<int*>(static_cast<uint8_t*>(buf) + tiles_bytes(T, nseq) - 16);
-  k_build_tiles<<<1, kTilesThreads, 0, st>>>(cu, nseq, *tiles, *ntiles);
+  k_build_tiles<<<1, kTilesThreads, 0, st>>>(cu, seg_src, nseq, *tiles, *ntiles);
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }

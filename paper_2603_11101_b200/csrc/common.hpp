@@ -50,8 +50,8 @@ int num_sms();
 // tiles_bytes(T, nseq) bytes; *tiles / *ntiles point into it (the count is written on device).
 size_t tiles_bytes(int64_t T, int nseq);
 size_t fwd_ws_bytes(const vlasim_attn_args* a);  // forward workspace: spans + tiles (attn_fwd2.cu)
-int launch_build_tiles(const int32_t* cu, int nseq, int64_t T, void* buf, cudaStream_t st, int2** tiles,
-                       int** ntiles);
+int launch_build_tiles(const int32_t* cu, const int32_t* seg_src, int nseq, int64_t T, void* buf, cudaStream_t st,
+                       int4** tiles, int** ntiles);
 
 // VLASIM_PROF=1: kernels with wait-time accounting are launched instead and each launch prints
 // (stderr) the average cycles per CTA spent in every named wait category.

@@ -825,6 +825,24 @@ extern "C" int vlasim_scatter_rows_cuda(const void* d_packed, void* d_dst, int64
   return copy_rows(false, d_packed, d_dst, row_bytes, d_len, out, n, stream);
 }
 
+// seg_src[m] = src_off[member_ids[m]]: source row of packed segment m (attention's seg_src).
+__global__ void k_seg_src(const int32_t* __restrict__ member_ids, const int32_t* __restrict__ src_off, int64_t n,
+                          int32_t* __restrict__ seg_src) {
+  const int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (m < n) seg_src[m] = __ldg(src_off + __ldg(member_ids + m));
+}
+
+extern "C" int vlasim_pack_seg_src_cuda(const vlasim_pack_out* out, int64_t n, int32_t* d_seg_src,
+                                        vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = check_out(out)) return rc;
+  if (!d_seg_src) return set_error(VLASIM_ECONFIG, "pack_seg_src: output required");
+  if (n < 1) return VLASIM_OK;
+  k_seg_src<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(out->member_ids, out->src_off, n, d_seg_src);
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+
 extern "C" int vlasim_pack_greedy_cuda(const int32_t* d_len, int64_t n, int32_t cap, const vlasim_pack_out* out,
                                        void* d_ws, size_t ws_bytes, uint32_t flags, vlasim_stream_t stream) {
   using namespace vlasim_host;

@@ -54,14 +54,15 @@ def quant_error(x: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor, stre
 
 
 def varlen_attn_fwd_fp8qk(q_codes, q_scale, k_codes, k_scale, v, cu_seqlens, *, mask_mode=0, prefix_len=None,
-                          softmax_scale=None, out=None, lse=None, stream=None):
+                          softmax_scale=None, out=None, lse=None, seg_src=None, stream=None):
     """Forward with E4M3 Q/K (tcgen05 kind::f8f6f4 for QKᵀ, block scales applied to S; P·V in bf16)."""
     T, H, d = q_codes.shape
     if q_codes.dtype != torch.uint8 or k_codes.dtype != torch.uint8:
         raise ConfigError("q_codes / k_codes must be uint8 E4M3 codes")
     o = out if out is not None else torch.empty(T, H, d, dtype=torch.bfloat16, device=v.device)
     lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=v.device)
-    a = _args(q_codes, k_codes, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale, k_scale)
+    a = _args(q_codes, k_codes, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale, k_scale,
+              seg_src=seg_src)
     L = _lib.lib()
     ws = _default_fwd_ws.get(L.vlasim_varlen_attn_workspace_size(C.byref(a), 0), v.device)
     _lib.check(L.vlasim_varlen_attn_fwd_fp8qk_cuda(C.byref(a), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),

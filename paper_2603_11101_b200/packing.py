@@ -227,6 +227,16 @@ def token_ids_into(plan: PackPlan, total_tokens: int, pos_ids=None, seg_ids=None
     _lib.check(rc, "token_ids")
 
 
+def seg_src(plan: PackPlan, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Source row of every packed segment, src_off[member_ids[m]] (int32 [n]): the attention kernels'
+    seg_src, which folds gather_rows / scatter_rows into their TMA coordinates."""
+    if out is None:
+        out = torch.empty(plan.n, dtype=torch.int32, device=plan.member_ids.device)
+    rc = _lib.lib().vlasim_pack_seg_src_cuda(plan.c_struct, plan.n, _lib.ptr(out, _lib.i32p), _lib.stream_ptr(stream))
+    _lib.check(rc, "pack_seg_src")
+    return out
+
+
 def gather_rows(src: torch.Tensor, plan: PackPlan, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Sample-major rows [Σl, ...] (sample i at src_off[i]) → packed stream order (16-byte vector copies)."""
     if out is None:

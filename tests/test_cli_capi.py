@@ -25,7 +25,7 @@ def test_capi_library_exports_every_declared_symbol():
     assert len(syms) >= 15
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.vlasim_version() == 1
+    assert lib.vlasim_version() == 2
     assert set(syms) <= set(_lib.EXPORTED)
 
 

@@ -1,0 +1,85 @@
+"""Gather folded into the attention kernels (vlasim_attn_args.seg_src): attention over the
+sample-major tensors with the packer's seg_src must equal, bit for bit, attention over the
+explicitly gathered packed stream followed by the scatter back (SPEC.md:504 — the packed stream
+is "concatenated tensors consistent with cu_seqlens"; here it is virtual)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (n samples, max len, capacity, H, Hkv, d, mask)
+    (40, 300, 1024, 2, 2, 128, 0),
+    (40, 300, 1024, 4, 1, 128, 1),
+    (60, 200, 512, 2, 2, 64, 0),
+    (30, 400, 1024, 8, 1, 256, 2),
+    (25, 260, 600, 2, 1, 256, 1),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_seg_src_matches_explicit_gather(gpu, case):
+    from paper_2603_11101_b200 import attention, packing
+    n, lmax, cap, H, Hkv, d, mask = CASES[case]
+    rng = np.random.default_rng(case)
+    L = rng.integers(1, lmax + 1, n).astype(np.int32)
+    plan = packing.pack_ffd(L, cap)
+    T = int(L.sum())
+    g = torch.Generator(device="cuda").manual_seed(case)
+    q, do = (torch.randn(T, H, d, device="cuda", generator=g).bfloat16() for _ in range(2))
+    k, v = (torch.randn(T, Hkv, d, device="cuda", generator=g).bfloat16() for _ in range(2))
+    cu = plan.cu_seqlens
+    seg = packing.seg_src(plan)
+    gidx = torch.empty(T, dtype=torch.int32, device="cuda")
+    packing.token_ids_into(plan, T, gather_idx=gidx)
+    Lp = np.diff(cu.cpu().numpy())
+    prefix = torch.tensor(Lp // 3, dtype=torch.int32, device="cuda") if mask == 2 else None
+    # explicit path: gather → attention on the packed stream → scatter back (row_map)
+    qp, kp, vp, dop = (packing.gather_rows(x, plan) for x in (q, k, v, do))
+    o_p, lse_p = attention.varlen_attn_fwd(qp, kp, vp, cu, mask_mode=mask, prefix_len=prefix)
+    dq_p, dk_p, dv_p = attention.varlen_attn_bwd(dop, qp, kp, vp, o_p, lse_p, cu, mask_mode=mask,
+                                                 prefix_len=prefix, row_map=gidx)
+    # fused path: sample-major tensors + seg_src
+    o_s, lse_s = attention.varlen_attn_fwd(q, k, v, cu, mask_mode=mask, prefix_len=prefix, seg_src=seg)
+    dq_s, dk_s, dv_s = attention.varlen_attn_bwd(do, q, k, v, o_s, lse_s, cu, mask_mode=mask, prefix_len=prefix,
+                                                 seg_src=seg)
+    torch.cuda.synchronize()
+    gl = gidx.long()
+    assert torch.equal(o_s[gl], o_p)
+    assert torch.equal(lse_s[:, gl], lse_p)
+    assert torch.equal(dq_s, dq_p) and torch.equal(dk_s, dk_p) and torch.equal(dv_s, dv_p)
+
+
+def test_seg_src_fp8_within_tolerance(gpu, orc):
+    """FP8 Q/K forward on sample-major codes (scale blocks of source rows) vs the fp64 oracle."""
+    from paper_2603_11101_b200 import fp8, packing
+    rng = np.random.default_rng(9)
+    L = rng.integers(1, 400, 30).astype(np.int32)
+    plan = packing.pack_ffd(L, 1024)
+    T, H, d = int(L.sum()), 2, 128
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v = (torch.randn(T, H, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+    qc, qs = fp8.quant_block(q)
+    kc, ks = fp8.quant_block(k)
+    o8, _ = fp8.varlen_attn_fwd_fp8qk(qc, qs, kc, ks, v, plan.cu_seqlens, seg_src=packing.seg_src(plan))
+    gidx = torch.empty(T, dtype=torch.int32, device="cuda")
+    packing.token_ids_into(plan, T, gather_idx=gidx)
+    gl = gidx.long()
+    f = lambda t: t.float().cpu().numpy()
+    ro, _ = orc.mha_fwd(f(q[gl]), f(k[gl]), f(v[gl]), plan.cu_seqlens.cpu().numpy(), mask=0, prefix=None)
+    err = np.max(np.abs(f(o8[gl]) - ro)) / max(1.0, np.max(np.abs(ro)))
+    assert err < 6e-2, err
+
+
+def test_seg_src_and_row_map_exclusive(gpu):
+    from paper_2603_11101_b200 import attention, packing
+    from paper_2603_11101_b200.errors import ConfigError
+    L = np.array([5, 7], np.int32)
+    plan = packing.pack_ffd(L, 16)
+    q = torch.randn(12, 1, 64, device="cuda").bfloat16()
+    seg = packing.seg_src(plan)
+    o, lse = attention.varlen_attn_fwd(q, q, q, plan.cu_seqlens, seg_src=seg)
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_bwd(q, q, q, q, o, lse, plan.cu_seqlens, seg_src=seg,
+                                  row_map=torch.zeros(12, dtype=torch.int32, device="cuda"))

@@ -1,6 +1,6 @@
 # bench.py at N = 1, 2, 4 on one box (torchrun for N > 1), as the driver's scaling run does
 mkdir -p gpurun_out
-for N in 1 2 4; do
+for N in ${NS:-1 2 4}; do
   if [ $N -eq 1 ]; then
     timeout -s KILL 600 python bench.py --steps 10 --warmup 3 > gpurun_out/scale_n1.log 2>&1
   else

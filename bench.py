@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=48)
     ap.add_argument("--no-graph", action="store_true", help="launch the step's kernels directly (no CUDA graph)")
+    ap.add_argument("--pipeline", default="on", choices=["on", "off"],
+                    help="on: the GPU packer of batch i+1 runs on a side stream on one SM while batch i's attention "
+                         "takes the other SMs (sm_budget); off: pack and attention strictly in sequence")
     ap.add_argument("--layout", default="fused", choices=["fused", "packed"],
                     help="fused: attention reads / writes sample-major rows through seg_src; packed: explicit "
                          "gather into the packed stream + row_map scatter")
@@ -301,14 +304,51 @@ def main():
             g.replay()
         else:
             step(b=b)
+
+    # Pipelined steps (--pipeline on, fused layout): step i's graph runs batch i's attention on
+    # SMs − 1 CTAs (sm_budget) while a side stream packs batch i+1 into the other plan on the free
+    # SM — the data-loader overlap of a training loop.  Every timed step still packs one batch and
+    # runs one attention fwd + bwd; batch 0 is packed before the timed region.
+    pipelined = a.pipeline == "on" and a.layout == "fused" and not a.no_graph
+    if pipelined:
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        plans = [sub, packing.pack_ffd(d_len_mine, CAPACITY)]
+        segs = [seg, torch.empty_like(seg)]
+        side = torch.cuda.Stream(dev)
+
+        def pack_into(j, b=bufs):
+            packing.pack_ffd(b["len"], CAPACITY, plan=plans[j], sync_check=False)
+            packing.seg_src(plans[j], out=segs[j])
+
+        def pstep(j, b=bufs):
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                pack_into(1 - j, b)  # the next batch
+            cu = plans[j].cu_seqlens
+            attention.varlen_attn_fwd(b["q"], b["k"], b["v"], cu, out=b["o"], lse=b["lse"], seg_src=segs[j],
+                                      sm_budget=nsm - 1)
+            attention.varlen_attn_bwd(b["do"], b["q"], b["k"], b["v"], b["o"], b["lse"], cu, workspace=ws,
+                                      dq=b["dq"], dk=b["dk"], dv=b["dv"], seg_src=segs[j], sm_budget=nsm - 1)
+            torch.cuda.current_stream().wait_stream(side)
+
+        pgraphs = [capture(bufs, lambda j=j: pstep(j)) for j in range(2)]
+        pack_into(0)
+        for j in range(4):
+            pgraphs[j & 1].replay()
+        torch.cuda.synchronize()
+        pack_into(0)  # the timed loop starts on plan 0, packed here (outside the timed region)
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         t0.record(stream)
-        for _ in range(a.steps):
-            run_step()
+        for i in range(a.steps):
+            if pipelined:
+                pgraphs[i & 1].replay()
+            else:
+                run_step()
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / a.steps
@@ -426,6 +466,8 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB/GPU)" % (4 * T * H * D * 2 / 1e9),
                        "parallelism": f"packs sharded over {world} GPU(s) (LPT), no collective on attention",
                        "launch": "CUDA graph replay of the step" if not a.no_graph else "direct launches",
+                       "pipeline": "packer of batch i+1 on a side stream (1 SM) overlapping batch i's attention "
+                                   "(SMs-1 CTAs)" if pipelined else "pack then attention, in sequence",
                        "layout": "fused: gather / scatter folded into the attention kernels' TMA coordinates "
                                  "(seg_src)" if a.layout == "fused" else
                                  "packed: explicit row gather into the packed stream, row_map scatter"},

@@ -149,6 +149,10 @@ typedef struct vlasim_attn_args {
      packed stream and the scatter back are folded into the kernels' TMA coordinates.
      (ABI version 2; row_map must be NULL when it is set.)                                  */
   const int32_t* seg_src;
+  /* 0: the persistent attention kernels take every SM.  n > 0: at most n CTAs (one per SM), so
+     the remaining SMs stay free for a concurrent stream — e.g. the GPU packer of the next batch
+     overlapping this batch's attention.                                                       */
+  int32_t sm_budget;
 } vlasim_attn_args;
 
 typedef struct vlasim_attn_grads {

@@ -32,7 +32,7 @@ class AttnArgs(C.Structure):
         ("cu_seqlens", i32p), ("prefix_len", i32p), ("num_seqs", C.c_int32), ("total_tokens", C.c_int64),
         ("num_heads", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
         ("mask_mode", C.c_int32), ("softmax_scale", C.c_float), ("q_scale", f32p), ("k_scale", f32p),
-        ("seg_src", i32p)]
+        ("seg_src", i32p), ("sm_budget", C.c_int32)]
 
 
 class AttnGrads(C.Structure):

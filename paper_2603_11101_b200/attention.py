@@ -21,7 +21,7 @@ MASK_BIDIR, MASK_CAUSAL, MASK_PREFIX = 0, 1, 2
 
 
 def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_scale=None, k_scale=None,
-          seg_src=None):
+          seg_src=None, sm_budget=0):
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3:
         raise ConfigError("q, k, v must be [T, heads, d]")
     T, H, d = q.shape
@@ -45,7 +45,7 @@ def _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, q_s
         cu_seqlens.numel() - 1, T, H, k.shape[1], d, int(mask_mode), scale,
         _lib.ptr(q_scale, _lib.f32p) if q_scale is not None else None,
         _lib.ptr(k_scale, _lib.f32p) if k_scale is not None else None,
-        _lib.ptr(seg_src, _lib.i32p) if seg_src is not None else None)
+        _lib.ptr(seg_src, _lib.i32p) if seg_src is not None else None, int(sm_budget or 0))
     return a
 
 
@@ -66,12 +66,12 @@ _default_fwd_ws = BwdWorkspace()
 
 
 def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None, softmax_scale=None, out=None,
-                    lse=None, workspace: BwdWorkspace | None = None, seg_src=None, stream=None):
+                    lse=None, workspace: BwdWorkspace | None = None, seg_src=None, sm_budget=0, stream=None):
     """Block-diagonal attention forward. Returns (o [T,H,d] bf16, lse [H,T] fp32 natural-log)."""
     T, H, d = q.shape
     o = out if out is not None else torch.empty_like(q)
     lse = lse if lse is not None else torch.empty(H, T, dtype=torch.float32, device=q.device)
-    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, seg_src=seg_src)
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, seg_src=seg_src, sm_budget=sm_budget)
     L = _lib.lib()
     ws = (workspace or _default_fwd_ws).get(L.vlasim_varlen_attn_workspace_size(C.byref(a), 0), q.device)
     _lib.check(L.vlasim_varlen_attn_fwd_cuda(C.byref(a), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
@@ -81,7 +81,7 @@ def varlen_attn_fwd(q, k, v, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=Non
 
 def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, prefix_len=None,
                     softmax_scale=None, dq=None, dk=None, dv=None, workspace: BwdWorkspace | None = None,
-                    row_map=None, seg_src=None, stream=None):
+                    row_map=None, seg_src=None, sm_budget=0, stream=None):
     """Backward of varlen_attn_fwd. Returns (dq, dk, dv) bf16.  With row_map (int32 [T], e.g. the
     packer's gather index) gradient row t is written to row row_map[t] — the scatter back to sample
     order fused into the kernels."""
@@ -90,7 +90,7 @@ def varlen_attn_bwd(dout, q, k, v, o, lse, cu_seqlens, *, mask_mode=MASK_BIDIR, 
     dv = dv if dv is not None else torch.empty_like(v)
     if not dout.is_contiguous() or dout.shape != q.shape:
         raise ConfigError("dout must be contiguous with q's shape")
-    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, seg_src=seg_src)
+    a = _args(q, k, v, o, lse, cu_seqlens, mask_mode, prefix_len, softmax_scale, seg_src=seg_src, sm_budget=sm_budget)
     if row_map is not None and (row_map.dtype != torch.int32 or row_map.numel() != q.shape[0]):
         raise ConfigError("row_map must be int32 [T]")
     g = _lib.AttnGrads(_lib.ptr(dout).value, _lib.ptr(dq).value, _lib.ptr(dk).value, _lib.ptr(dv).value,

@@ -1099,7 +1099,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   const int skip = getenv("VLASIM_BWD_SKIP") ? atoi(getenv("VLASIM_BWD_SKIP")) : 0;  // debugging
   for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO && !(skip & 2); ++half) {
     using Cfg = DkvCfg<HD, UQ>;
-    const int grid = int(std::min<int64_t>(max_tiles * Hkv, num_sms()));
+    const int grid = persistent_grid(max_tiles * Hkv, a->sm_budget);
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
     p.ohalf = half;
     auto kern = p.prof ? k_bwd_dkdv<HD, UQ, true> : k_bwd_dkdv<HD, UQ, false>;
@@ -1120,7 +1120,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     auto kern = p.prof ? k_bwd_dq<HD, BN, KS, VS, true> : k_bwd_dq<HD, BN, KS, VS, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    const int grid = int(std::min<int64_t>(max_tiles * H, num_sms()));
+    const int grid = persistent_grid(max_tiles * H, a->sm_budget);
     kern<<<grid, kDqThreads, Cfg::SMEM, st>>>(tq, BN == 128 ? tk : tk64, BN == 128 ? tv : tv64, tdo, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});

@@ -605,7 +605,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, void* tiles_buf, cud
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
   // the tile count is known on the device only: one CTA per SM (bounded by the worst case)
   const int64_t max_items = (int64_t(T) / 128 + a->num_seqs) * a->num_heads;
-  const int grid = int(std::min<int64_t>(max_items, num_sms()));
+  const int grid = persistent_grid(max_items, a->sm_budget);
   if (prof_enabled()) {
     p.prof = prof_buffer();
     auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, true>;

@@ -45,6 +45,12 @@ int encode_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype
 inline cudaStream_t as_stream(vlasim_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int num_sms();
+// CTAs of a persistent attention kernel: min(work items, SMs, the caller's sm_budget when > 0)
+inline int persistent_grid(int64_t max_items, int sm_budget) {
+  int64_t g = max_items < num_sms() ? max_items : num_sms();
+  if (sm_budget > 0 && g > sm_budget) g = sm_budget;
+  return int(g < 1 ? 1 : g);
+}
 
 // Segment-aligned 128-row tiles of the packed stream, sorted by cost (attn_tiles.cu).  `buf` holds
 // tiles_bytes(T, nseq) bytes; *tiles / *ntiles point into it (the count is written on device).

@@ -222,11 +222,12 @@ __device__ __forceinline__ void kv_item_finish(const BwdParams& p, KvItem& it) {
 template <int UQ>
 struct UnitCursor {
   int i, it, k, u, n;
+  int iq, hq;  // unit = (q head hq of the group, query tile iq): it = hq·nq + iq, kept without division
   KvItem itm, nxt;
   __device__ __forceinline__ bool has_next() const { return sched_item(k + 1) < n; }
   __device__ __forceinline__ bool start(const BwdParams& p) {
     n = __ldg(p.ntiles) * p.Hkv;
-    it = k = u = 0;
+    it = k = u = iq = hq = 0;
     i = sched_item(0);
     if (i >= n) return false;
     itm = kv_item(p, i);
@@ -236,8 +237,12 @@ struct UnitCursor {
   }
   __device__ __forceinline__ bool next(const BwdParams& p) {
     ++u;
+    if (++iq == itm.nq) {
+      iq = 0;
+      ++hq;
+    }
     if (++it < itm.iters) return true;
-    it = 0;
+    it = iq = hq = 0;
     i = sched_item(++k);
     if (i >= n) return false;
     itm = nxt;
@@ -246,8 +251,8 @@ struct UnitCursor {
     return true;
   }
   __device__ __forceinline__ bool last() const { return it + 1 == itm.iters; }
-  __device__ __forceinline__ int head(int group) const { return itm.kh * group + it / itm.nq; }
-  __device__ __forceinline__ int qb() const { return itm.q_lo + (it % itm.nq) * UQ; }
+  __device__ __forceinline__ int head(int group) const { return itm.kh * group + hq; }
+  __device__ __forceinline__ int qb() const { return itm.q_lo + iq * UQ; }
 };
 
 // Warp roles (576 threads): warps 0-15 softmax — group g = w/8 takes the units with u%2 == g;

@@ -130,10 +130,10 @@ def bwd_traffic():
     import glob
     files = sorted(glob.glob(str(Path(__file__).parent / "profiles" / "*" / "ncu_traffic.json")))
     if not files:
-        return None
+        return None, None
     ks = json.load(open(files[-1]))["kernels"]
     tot = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in ks.items() if k.startswith("k_bwd"))
-    return {"bytes": tot, "src": str(Path(files[-1]).relative_to(Path(__file__).parent))}
+    return tot, str(Path(files[-1]).relative_to(Path(__file__).parent))
 
 
 def cpu_baseline(Ls, threads):
@@ -474,7 +474,10 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "backward: k_bwd_pre + k_bwd_dkdv + k_bwd_dq",
                          "achieved": bwd_flops / (kb / 1e3) / 1e12, "peak": PEAKS["bf16_tflops"],
                          "unit": "TFLOP/s", "frac": bwd_flops / (kb / 1e3) / 1e12 / PEAKS["bf16_tflops"],
-                         "traffic": bwd_traffic(), "peak_src": PEAKS["src"],
+                         "traffic": bwd_traffic()[0], "traffic_src": bwd_traffic()[1],
+                         "traffic_note": "dram read+write bytes of the 3 backward launches of one step (ncu --set "
+                                         "full); algorithmic minimum ≈ 4.5 GB (Q,K,V,O,dO in, dQ,dK,dV out)",
+                         "peak_src": PEAKS["src"],
                          "fwd": {"achieved": fl_fwd / (kf / 1e3) / 1e12, "ms": kf}, "bwd_ms": kb,
                          "pack_ms": statistics.mean(kpack)},
             "clocks": clk.summary(),

@@ -83,3 +83,24 @@ def test_seg_src_and_row_map_exclusive(gpu):
     with pytest.raises(ConfigError):
         attention.varlen_attn_bwd(q, q, q, q, o, lse, plan.cu_seqlens, seg_src=seg,
                                   row_map=torch.zeros(12, dtype=torch.int32, device="cuda"))
+
+
+def test_sm_budget_is_bit_identical(gpu):
+    """sm_budget only changes which CTA runs an item: outputs and gradients are bit-identical."""
+    from paper_2603_11101_b200 import attention, packing
+    rng = np.random.default_rng(3)
+    L = rng.integers(1, 300, 40).astype(np.int32)
+    plan = packing.pack_ffd(L, 1024)
+    T, H, d = int(L.sum()), 4, 128
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v, do = (torch.randn(T, H, d, device="cuda", generator=g).bfloat16() for _ in range(4))
+    seg = packing.seg_src(plan)
+    cu = plan.cu_seqlens
+    res = []
+    for budget in (0, 7, 147):
+        o, lse = attention.varlen_attn_fwd(q, k, v, cu, seg_src=seg, sm_budget=budget)
+        grads = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, seg_src=seg, sm_budget=budget)
+        res.append((o, lse) + tuple(grads))
+    torch.cuda.synchronize()
+    for other in res[1:]:
+        assert all(torch.equal(x, y) for x, y in zip(res[0], other))

@@ -66,14 +66,20 @@ struct Fwd2Cfg {
   static constexpr int Q_BYTES = BM * HD * QK_ELEM;
   static constexpr int K_BYTES = BN * HD * QK_ELEM;
   static constexpr int KV_BYTES = BN * HD * 2;          // one V tile (bf16)
-  static constexpr int OFF_Q = 0;                        // [2]
-  static constexpr int OFF_K = 2 * Q_BYTES;              // [KS] K ring
+  // Q ring of 3: an item's O is staged in its own (idle) Q buffer until the TMA store has read
+  // it, so the Q tile two items ahead no longer waits for that store (the MMA waited for Q at
+  // item boundaries ~16 % of the time with 2 buffers)
+  static constexpr int NQ = 3;
+  static constexpr int OFF_Q = 0;                        // [NQ]
+  static constexpr int OFF_K = NQ * Q_BYTES;             // [KS] K ring
   static constexpr int OFF_V = OFF_K + KS * K_BYTES;     // [VS] V ring
   // FP8: the E4M3 Q buffer is too small to stage the bf16 O tile, so O gets its own staging tile
   static constexpr int OFF_OST = OFF_V + VS * KV_BYTES;
-  static constexpr int OFF_XCH = OFF_OST + (FP8 ? BM * HD * 2 : 0);  // float [2 parity][4 quarter][128]
-  static constexpr int OFF_BAR = OFF_XCH + 2 * 4 * 128 * 4;
-  static constexpr int NUM_BARS = 4 + 2 * KS + 2 * VS + 4 + 5 + 2 + 1;
+  // row-max / row-sum exchange, 512 B per TMEM lane quadrant: bf16 maxima [2 parity][4 quarter][32
+  // rows] for the tiles, fp32 sums [4 quarter][32 rows] once per item over the same bytes
+  static constexpr int OFF_XCH = OFF_OST + (FP8 ? BM * HD * 2 : 0);
+  static constexpr int OFF_BAR = OFF_XCH + 4 * 512;
+  static constexpr int NUM_BARS = 2 * NQ + 2 * KS + 2 * VS + 9 + NQ + 1;
   // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
@@ -120,9 +126,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* bar_q_full = bars;                          // [2]
-  uint64_t* bar_q_empty = bars + 2;                     // [2]
-  uint64_t* bar_k_full = bars + 4;                      // [KS]
+  constexpr int NQ = Cfg::NQ;
+  uint64_t* bar_q_full = bars;                          // [NQ]
+  uint64_t* bar_q_empty = bars + NQ;                    // [NQ] FP8: the item's last S has read Q
+  uint64_t* bar_k_full = bars + 2 * NQ;                 // [KS]
   uint64_t* bar_k_empty = bar_k_full + KS;              // [KS]
   uint64_t* bar_v_full = bar_k_full + 2 * KS;           // [VS]
   uint64_t* bar_v_empty = bar_v_full + VS;              // [VS]
@@ -131,18 +138,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* bar_o_full = bar_s_full + 4;         // [2] per item: last PV landed in O[k%2]
   uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 16 warp arrivals: epilogue drained O[k%2]
   uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
-  uint64_t* bar_o_staged = bar_s_full + 9;       // [2] 16 warp arrivals: item's O staged in its Q buffer
-  uint64_t* bar_ost_free = bar_s_full + 11;      // FP8: the O staging tile has been read by its TMA store
+  uint64_t* bar_o_staged = bar_s_full + 9;       // [NQ] 16 warp arrivals: item's O staged in its Q buffer
+  uint64_t* bar_ost_free = bar_o_staged + NQ;    // FP8: the O staging tile has been read by its TMA store
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
-  float* xch = reinterpret_cast<float*>(smem + Cfg::OFF_XCH);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_items = __ldg(p.ntiles) * p.H;
   const int i0 = sched_item(0);
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NQ; ++s) {
       mbar_init(&bar_q_full[s], 1);
       mbar_init(&bar_q_empty[s], 1);
+      mbar_init(&bar_o_staged[s], 16);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&bar_s_full[s], 1);
       mbar_init(&bar_p_full[s], 16);
     }
@@ -160,7 +169,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bar_o_empty[s], 16);
     }
     mbar_init(bar_o_ready, 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&bar_o_staged[s], 16);
     mbar_init(bar_ost_free, 1);
     fence_barrier_init();
   }
@@ -189,13 +197,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) tma_load_2d(sv + c * BN * 128, &tmV, pv_kh * HD + c * 64, pv_kv0, &bar_v_full[vs]);
       };
-      // bf16: item k's O is staged in Q buffer k&1; write it out (two 128×64 TMA stores) and wait
-      // for the stores to read smem before that buffer takes item k+2's Q.  Every item has ≥ 1
-      // key tile (a query sees itself), so every item runs an epilogue.
-      int hq0[2] = {0, 0}, hh[2] = {0, 0}, hn[2] = {0, 0};
+      // bf16: item k's O is staged in Q buffer k % NQ; the producer writes it out (two 128×64 TMA
+      // stores, or 64/32/16/8-row boxes) as soon as it is staged, and waits for the stores to have
+      // read smem only when that buffer takes item k+NQ's Q.  Every item has ≥ 1 key tile (a query
+      // sees itself), so every item runs an epilogue.
+      int hq0[NQ] = {}, hh[NQ] = {}, hn[NQ] = {};
+      int st = 0;  // items < st have had their O stores issued
       auto store_o = [&](int kk) {
-        const int b = kk & 1;
-        wp.template wait<0>(&bar_o_staged[b], (kk >> 1) & 1);
+        const int b = kk % NQ;
+        wp.template wait<0>(&bar_o_staged[b], (kk / NQ) & 1);
         const uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + b * Cfg::Q_BYTES);
         if (hn[b] == 128) {
 #pragma unroll
@@ -212,18 +222,31 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
         bulk_commit();
-        bulk_wait_read0();
-        if constexpr (FP8) mbar_arrive(bar_ost_free);  // the next item's O may be staged
+        if constexpr (FP8) {
+          bulk_wait_read0();
+          mbar_arrive(bar_ost_free);  // the next item's O may be staged
+        }
+      };
+      auto try_stores = [&](int upto) {  // O stores of items < upto that are staged already (never blocks)
+        while (st < upto && mbar_test_wait(&bar_o_staged[st % NQ], (st / NQ) & 1)) store_o(st++);
       };
       FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
         if (sched_item(m + 1) < n_items) nxt = fwd_item(p, sched_item(m + 1), BN);  // prefetch
-        const int qs = k & 1;
-        if (k >= 2) {
-          if constexpr (FP8) wp.template wait<0>(&bar_q_empty[qs], ((k >> 1) - 1) & 1);
-          store_o(k - 2);
+        const int qs = k % NQ;
+        if (k >= NQ) {  // buffer qs held item k-NQ: its Q reads (FP8) / its O store's reads (bf16) done
+          if constexpr (FP8) {
+            wp.template wait<0>(&bar_q_empty[qs], ((k / NQ) - 1) & 1);
+          } else {
+            while (st <= k - NQ) store_o(st++);
+            bulk_wait_read0();
+          }
         }
+        // FP8: one O staging tile released through ost_free, whose parity waits stay exact only while
+        // the stores trail the epilogues by at most one item
+        if (FP8 && k >= 2)
+          while (st <= k - 2) store_o(st++);
         hq0[qs] = itm.q0 + itm.dl;  // data row of the tile (O stores)
         hh[qs] = itm.h;
         hn[qs] = itm.qe - itm.q0;
@@ -232,6 +255,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int c = 0; c < HD / Cfg::QK_BOX; ++c)
           tma_load_2d(sq + c * 128 * 128, &tmQ, itm.h * HD + c * Cfg::QK_BOX, itm.q0 + itm.dl, &bar_q_full[qs]);
+        try_stores(k);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           const int ks = g % KS;
           if (g >= KS) wp.template wait<1>(&bar_k_empty[ks], ((g / KS) - 1) & 1);
@@ -245,10 +269,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           pv_g = g;
           pv_kh = itm.kh;
           pv_kv0 = kv0;
+          try_stores(k);
         }
       }
       if (pv_g >= 0) load_v();
-      for (int kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) store_o(kk);
+      while (st < k) store_o(st++);
       bulk_wait_all();
       wp.flush(p.prof);
     }
@@ -293,9 +318,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
         if (sched_item(m + 1) < n_items) nxt = fwd_item(p, sched_item(m + 1), BN);  // prefetch
-        const int qs = k & 1;
+        const int qs = k % NQ;
         const uint64_t qd = dQ0 + qs * Q16;
-        wp.template wait<0>(&bar_q_full[qs], (k >> 1) & 1);
+        wp.template wait<0>(&bar_q_full[qs], (k / NQ) & 1);
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           wp.template wait<1>(&bar_k_full[ks], kph);
           tc_fence_after();
@@ -342,6 +367,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int r = quad * 32 + lane;
     const int c0 = qp * 32;
     constexpr int OC = HD / 4;  // O columns per quarter
+    __nv_bfloat16* xmax = reinterpret_cast<__nv_bfloat16*>(smem + Cfg::OFF_XCH + quad * 512);  // [2][4][32]
+    float* xsum = reinterpret_cast<float*>(smem + Cfg::OFF_XCH + quad * 512);                  // [4][32]
     float sl2 = p.scale_log2;
     // Epilogue of item `ek` is deferred until the first tile of the next item has been handed to
     // the MMA warp, so the tensor core never idles on it (O is double-buffered in TMEM).
@@ -356,7 +383,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + qp * OC;
       // staging tile: bf16 → this item's Q buffer; FP8 → the O tile, once item ek-1's store has read it
-      uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + (ek & 1) * Cfg::Q_BYTES);
+      uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + (ek % NQ) * Cfg::Q_BYTES);
       uint32_t o[32];
       tmem_ld32(o_tm, o);  // OC ≤ 32 columns (HD 64: the upper 16 belong to the next quarter, unused)
       tmem_wait_ld();
@@ -373,7 +400,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
         }
         fence_proxy_async_smem();
-        warp_arrive(&bar_o_staged[ek & 1]);  // the producer writes the tile out
+        warp_arrive(&bar_o_staged[ek % NQ]);  // the producer writes the tile out
         if (valid && r >= (e_n & ~7)) {       // the last n & 7 rows: no TMA box, stored here
           uint4* dst = reinterpret_cast<uint4*>(p.o + (int64_t(e_row) * p.H + e_h) * HD + qp * OC);
 #pragma unroll
@@ -416,10 +443,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           // them): this quarter has no S, exponentials or P.  It still takes part in the row-max
           // exchange and the lazy O rescale of its columns.
           wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
-          float* xs = xch + (g & 1) * 512;
-          xs[qp * 128 + r] = -INFINITY;
+          __nv_bfloat16* xb = xmax + (g & 1) * 128;
+          xb[qp * 32 + lane] = __float2bfloat16_ru(-INFINITY);
           named_bar_sync(1 + quad, 128);
-          float mt = fmaxf(fmaxf(xs[r], xs[128 + r]), fmaxf(xs[256 + r], xs[384 + r]));
+          float mt = fmaxf(fmaxf(__bfloat162float(xb[lane]), __bfloat162float(xb[32 + lane])),
+                           fmaxf(__bfloat162float(xb[64 + lane]), __bfloat162float(xb[96 + lane])));
           mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
           const bool grow = mt > m_run + kLazyRescale;
           const float alpha = grow ? exp2f(m_run - mt) : 1.f;
@@ -489,14 +517,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * ksc;  // scales are > 0
         // combine the four column quarters of this row
-        float* xs = xch + (g & 1) * 512;
-        xs[qp * 128 + r] = mt;
+        // rounded up to bf16: every quarter uses the same offset, ≥ the row max (P ≤ 1)
+        __nv_bfloat16* xb = xmax + (g & 1) * 128;
+        xb[qp * 32 + lane] = __float2bfloat16_ru(mt);
         {
           const long long tb = wp.now();
           named_bar_sync(1 + quad, 128);
           wp.template add_since<3>(tb);
         }
-        mt = fmaxf(fmaxf(xs[r], xs[128 + r]), fmaxf(xs[256 + r], xs[384 + r]));
+        mt = fmaxf(fmaxf(__bfloat162float(xb[lane]), __bfloat162float(xb[32 + lane])),
+                   fmaxf(__bfloat162float(xb[64 + lane]), __bfloat162float(xb[96 + lane])));
         mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
         const bool grow = mt > m_run + kLazyRescale;
         const float alpha = grow ? exp2f(m_run - mt) : 1.f;
@@ -543,11 +573,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (j == 0 && ek >= 0) epilogue();  // previous item, now that this tile is in flight
       }
       // combine the quarters' row sums and defer this item's epilogue
-      float* xs = xch + (g & 1) * 512;  // parity not used by any in-flight tile
-      xs[qp * 128 + r] = l_run;
+      // (over the quadrant's max bytes: every quarter has read the last tile's maxima first)
       named_bar_sync(1 + quad, 128);
-      const float l_tot = (xs[r] + xs[128 + r]) + (xs[256 + r] + xs[384 + r]);
-      named_bar_sync(1 + quad, 128);  // all quarters read before the slot is reused
+      xsum[qp * 32 + lane] = l_run;
+      named_bar_sync(1 + quad, 128);
+      const float l_tot = (xsum[lane] + xsum[32 + lane]) + (xsum[64 + lane] + xsum[96 + lane]);
+      named_bar_sync(1 + quad, 128);  // all quarters read before the bytes take the next maxima
       if (ek >= 0) epilogue();         // (only when this item had no tiles)
       if (itm.nkv > 0) {
         ek = k;

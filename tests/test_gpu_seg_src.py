@@ -104,3 +104,34 @@ def test_sm_budget_is_bit_identical(gpu):
     torch.cuda.synchronize()
     for other in res[1:]:
         assert all(torch.equal(x, y) for x, y in zip(res[0], other))
+
+
+def test_config2_scale_consistency(gpu):
+    """Race detector at the bench's scale (config 2: 512 samples U[16,512], 8192-token bins, H16
+    d128, ~140 items per CTA): the fused layout must equal the explicit gather bit for bit (fwd and
+    bwd), and the FP8 Q/K forward must stay within the FP8 tolerance of the bf16 one.  Pipelining
+    bugs (stale barriers, early buffer reuse) only show once items queue up per CTA."""
+    from paper_2603_11101_b200 import attention, fp8, packing, synthetic
+    L = synthetic.gen_lengths(512, 0, 16, 512)
+    plan = packing.pack_ffd(L, 8192)
+    T, H, d = int(L.sum()), 16, 128
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v, do = (torch.randn(T, H, d, device="cuda", generator=g).bfloat16() for _ in range(4))
+    cu, seg = plan.cu_seqlens, packing.seg_src(plan)
+    gidx = torch.empty(T, dtype=torch.int32, device="cuda")
+    packing.token_ids_into(plan, T, gather_idx=gidx)
+    gl = gidx.long()
+    o_s, lse_s = attention.varlen_attn_fwd(q, k, v, cu, seg_src=seg)
+    dq_s, dk_s, dv_s = attention.varlen_attn_bwd(do, q, k, v, o_s, lse_s, cu, seg_src=seg)
+    qp, kp, vp, dop = (x[gl].contiguous() for x in (q, k, v, do))
+    o_p, lse_p = attention.varlen_attn_fwd(qp, kp, vp, cu)
+    dq_p, dk_p, dv_p = attention.varlen_attn_bwd(dop, qp, kp, vp, o_p, lse_p, cu, row_map=gidx)
+    qc, qsc = fp8.quant_block(q)
+    kc, ksc = fp8.quant_block(k)
+    o8, _ = fp8.varlen_attn_fwd_fp8qk(qc, qsc, kc, ksc, v, cu, seg_src=seg)
+    torch.cuda.synchronize()
+    assert torch.equal(o_s[gl], o_p) and torch.equal(lse_s[:, gl], lse_p)
+    assert torch.equal(dq_s, dq_p) and torch.equal(dk_s, dk_p) and torch.equal(dv_s, dv_p)
+    # north_star FP8 tolerance, relative to max(1, max|o|) (the bf16 output stands in for the reference)
+    err = (o8.float() - o_s.float()).abs().max().item() / max(1.0, o_s.float().abs().max().item())
+    assert err < 6e-2, err

@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                            fmaxf(__bfloat162float(xb[64 + lane]), __bfloat162float(xb[96 + lane])));
           mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
           const bool grow = mt > m_run + kLazyRescale;
-          const float alpha = grow ? exp2f(m_run - mt) : 1.f;
+          const float alpha = grow ? ex2_approx(m_run - mt) : 1.f;  // same factor for l and O
           const bool rescale = __any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY);
           if (grow) {
             l_run *= alpha;
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                    fmaxf(__bfloat162float(xb[64 + lane]), __bfloat162float(xb[96 + lane])));
         mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
         const bool grow = mt > m_run + kLazyRescale;
-        const float alpha = grow ? exp2f(m_run - mt) : 1.f;
+        const float alpha = grow ? ex2_approx(m_run - mt) : 1.f;  // same factor for l and O
         const bool rescale = __any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY);
         if (grow) {
           l_run *= alpha;

@@ -1101,8 +1101,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.scale_log2 = a->softmax_scale * kLog2e;
   p.dbg = getenv("VLASIM_DBG") ? atoi(getenv("VLASIM_DBG")) : 0;
   p.ohalf = 0;
-  const int skip = getenv("VLASIM_BWD_SKIP") ? atoi(getenv("VLASIM_BWD_SKIP")) : 0;  // debugging
-  for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO && !(skip & 2); ++half) {
+  for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO; ++half) {
     using Cfg = DkvCfg<HD, UQ>;
     const int grid = persistent_grid(max_tiles * Hkv, a->sm_budget);
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
@@ -1118,7 +1117,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
                    "smx:s_full", "smx:dp_full", "", "smx:dkv_full", "smx:phaseA", "smx:phaseB", "smx:epilogue", "",
                    "", "", "", "smx:total"});
   }
-  if (!(skip & 1)) {
+  {
     constexpr int BN = HD == 256 ? 64 : 128;
     constexpr int KS = HD == 64 ? 5 : (HD == 128 ? 3 : 2), VS = HD == 64 ? 4 : (HD == 128 ? 2 : 1);
     using Cfg = DqCfg<HD, BN, KS, VS>;

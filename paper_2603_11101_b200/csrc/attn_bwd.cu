@@ -58,6 +58,12 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
   const int nt = min(kPreTokens, T - t0);
   const int tasks = nt * H * LPR;
   const int64_t base = int64_t(t0) * H * HD;
+  // r / H by multiply-high (r < 32·H ≤ 2^16: exact), one division per thread instead of per row
+  const unsigned long long mH = (1ull << 32) / unsigned(H) + 1ull;  // H = 1 needs the 33rd bit
+  auto slot = [&](int r) {
+    const int q = int((static_cast<unsigned long long>(r) * mH) >> 32);
+    return (r - q * H) * kPreTokens + q;
+  };
 #pragma unroll 4
   // Loop exits are warp-uniform (a warp's 32 tasks are consecutive) so that the shuffle reduction
   // always runs with the full warp; tasks past the end contribute zeros and are not written.
@@ -77,7 +83,7 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
     }
 #pragma unroll
     for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (act && sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
+    if (act && sub == 0) sh_d[slot(r)] = acc;
   }
   for (int task = kPreTokens * 16 * LPR + threadIdx.x; task - int(threadIdx.x & 31) < tasks; task += 256) {  // H > 16
     const bool act = task < tasks;
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
     }
 #pragma unroll
     for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (act && sub == 0) sh_d[(r % H) * kPreTokens + r / H] = acc;
+    if (act && sub == 0) sh_d[slot(r)] = acc;
   }
   __syncthreads();
   // 4 copies shifted by s = 0..3 elements: any 64/128-wide window [qb, qb+w) starts 16-B aligned

@@ -661,8 +661,12 @@ struct DqCfg {
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
   static constexpr int OFF_K = 2 * TILE;             // K ring [KS]: released after dQ
   static constexpr int OFF_V = OFF_K + KS * KTILE;   // V ring [VS]: released after dP
-  static constexpr int OFF_BAR = OFF_V + VS * KTILE;
-  static constexpr int NUM_BARS = 2 + 2 * KS + 2 * VS + 8;
+  // decoded item descriptors, written by the producer one item ahead: the softmax warps hold no
+  // next-item state in registers (at the 96-register cap it spilled and exposed the loads)
+  static constexpr int NDESC = 4;
+  static constexpr int OFF_DESC = OFF_V + VS * KTILE;    // int4 [NDESC][2]
+  static constexpr int OFF_BAR = OFF_DESC + NDESC * 32;
+  static constexpr int NUM_BARS = 2 + 2 * KS + 2 * VS + 8 + 2 * NDESC;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   // TMEM: BN 128 → S0 [0,128) · dP [128,256) · dQ [256,256+HD) · S1 [384,512)
   //       BN  64 → S0 [0,64) · S1 [64,128) · dP [128,192) · dQ [256,256+HD)   (HD up to 256)
@@ -721,6 +725,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   uint64_t* bar_dq_full = bar_s_full + 5;          // one per item
   uint64_t* bar_dq_empty = bar_s_full + 6;         // 16 warp arrivals
   uint64_t* bar_dp_free = bar_s_full + 7;          // 16 warp arrivals: phase B has loaded dP(g)
+  uint64_t* bar_desc_full = bar_s_full + 8;        // [NDESC] producer wrote item m's descriptor
+  uint64_t* bar_desc_empty = bar_desc_full + Cfg::NDESC;  // [NDESC] 16 warp arrivals: read
+  int4* descs = reinterpret_cast<int4*>(smem + Cfg::OFF_DESC);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -747,6 +754,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     mbar_init(bar_dq_full, 1);
     mbar_init(bar_dq_empty, 16);
     mbar_init(bar_dp_free, 16);
+    for (int d = 0; d < Cfg::NDESC; ++d) {
+      mbar_init(&bar_desc_full[d], 1);
+      mbar_init(&bar_desc_empty[d], 16);
+    }
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc<512>(tmem_slot);
@@ -761,9 +772,21 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       TraceCtr trace(trb);
       int g = 0, k = 0;
       QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
+      // descriptor of item ordinal mm (decoded) into the ring: {q0, qe, dl, h}, {kv_lo, kv_hi, nkv, kh}
+      auto put_desc = [&](int mm, const QItem& it) {
+        const int d = mm % Cfg::NDESC;
+        if (mm >= Cfg::NDESC) mbar_wait(&bar_desc_empty[d], ((mm / Cfg::NDESC) - 1) & 1);
+        descs[2 * d] = make_int4(it.q0, it.qe, it.dl, it.h);
+        descs[2 * d + 1] = make_int4(it.kv_lo, it.kv_hi, it.nkv, it.kh);
+        mbar_arrive(&bar_desc_full[d]);  // release semantics: the stores above are visible
+      };
+      if (i0 < n_items) put_desc(0, q_item_cur(nxt, BN));
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
         const QItem itm = q_item_cur(nxt, BN);
-        if (sched_item(m + 1) < n_items) nxt = q_item(p, sched_item(m + 1));
+        if (sched_item(m + 1) < n_items) {
+          nxt = q_item(p, sched_item(m + 1));
+          put_desc(m + 1, q_item_cur(nxt, BN));
+        }
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
         trace(1, g);  // P: Q/dO load issued
@@ -910,17 +933,40 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       l_ = v ? __ldg(p.lse2 + int64_t(it.h) * p.Tp + rw + it.dl) : 0.f;  // copy 0 (unshifted), data row
       d_ = v ? __ldg(p.dsum + int64_t(it.h) * p.Tp + rw + it.dl) : 0.f;
     };
-    QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
-    int2 rs_n;
-    float lse_n, dsum_n;
-    load_row(nxt, rs_n, lse_n, dsum_n);
+    auto get_desc = [&](int mm, QItem& it, bool full) {  // item ordinal mm from the producer's ring
+      const int d = mm % Cfg::NDESC;
+      mbar_wait(&bar_desc_full[d], (mm / Cfg::NDESC) & 1);
+      const int4 a = descs[2 * d];
+      it.q0 = a.x;
+      it.qe = a.y;
+      it.dl = a.z;
+      it.h = a.w;
+      if (full) {
+        const int4 b = descs[2 * d + 1];
+        it.kv_lo = b.x;
+        it.kv_hi = b.y;
+        it.nkv = b.z;
+        it.kh = b.w;
+      }
+    };
+    int2 rs_n = make_int2(0, 0);
+    float lse_n = 0.f, dsum_n = 0.f;
+    if (i0 < n_items) {
+      QItem f;
+      get_desc(0, f, false);
+      load_row(f, rs_n, lse_n, dsum_n);
+    }
     for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
-      const QItem itm = q_item_cur(nxt, BN);
+      QItem itm;
+      get_desc(m, itm, true);
+      __syncwarp();
+      warp_arrive(&bar_desc_empty[m % Cfg::NDESC]);  // (item m+1's row parameters read its slot below)
       const int2 rs = rs_n;
       const float lse2 = lse_n, dsum = dsum_n;
       if (sched_item(m + 1) < n_items) {
-        nxt = q_item(p, sched_item(m + 1));
-        load_row(nxt, rs_n, lse_n, dsum_n);
+        QItem f;
+        get_desc(m + 1, f, false);
+        load_row(f, rs_n, lse_n, dsum_n);
       }
       if (itm.nkv == 0) continue;
       const int row = itm.q0 + r;

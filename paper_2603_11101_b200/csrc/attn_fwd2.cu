@@ -78,8 +78,12 @@ struct Fwd2Cfg {
   // row-max / row-sum exchange, 512 B per TMEM lane quadrant: bf16 maxima [2 parity][4 quarter][32
   // rows] for the tiles, fp32 sums [4 quarter][32 rows] once per item over the same bytes
   static constexpr int OFF_XCH = OFF_OST + (FP8 ? BM * HD * 2 : 0);
-  static constexpr int OFF_BAR = OFF_XCH + 4 * 512;
-  static constexpr int NUM_BARS = 2 * NQ + 2 * KS + 2 * VS + 9 + NQ + 1;
+  // decoded item descriptors, written by the producer one item ahead (the softmax warps hold no
+  // next-item state in registers)
+  static constexpr int NDESC = 4;
+  static constexpr int OFF_DESC = OFF_XCH + 4 * 512;   // int4 [NDESC][2]
+  static constexpr int OFF_BAR = OFF_DESC + NDESC * 32;
+  static constexpr int NUM_BARS = 2 * NQ + 2 * KS + 2 * VS + 9 + NQ + 1 + 2 * NDESC;
   // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
@@ -140,6 +144,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
   uint64_t* bar_o_staged = bar_s_full + 9;       // [NQ] 16 warp arrivals: item's O staged in its Q buffer
   uint64_t* bar_ost_free = bar_o_staged + NQ;    // FP8: the O staging tile has been read by its TMA store
+  uint64_t* bar_desc_full = bar_ost_free + 1;    // [NDESC] producer wrote item m's descriptor
+  uint64_t* bar_desc_empty = bar_desc_full + Cfg::NDESC;  // [NDESC] 16 warp arrivals: read
+  int4* descs = reinterpret_cast<int4*>(smem + Cfg::OFF_DESC);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -170,6 +177,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     mbar_init(bar_o_ready, 1);
     mbar_init(bar_ost_free, 1);
+    for (int d = 0; d < Cfg::NDESC; ++d) {
+      mbar_init(&bar_desc_full[d], 1);
+      mbar_init(&bar_desc_empty[d], 16);
+    }
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc<512>(tmem_slot);
@@ -230,10 +241,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto try_stores = [&](int upto) {  // O stores of items < upto that are staged already (never blocks)
         while (st < upto && mbar_test_wait(&bar_o_staged[st % NQ], (st / NQ) & 1)) store_o(st++);
       };
+      // item ordinal mm's decoded descriptor into the ring: {q0, qe, dl, h}, {kv_lo, kv_hi, nkv, kh}
+      auto put_desc = [&](int mm, const FwdItem& it) {
+        const int d = mm % Cfg::NDESC;
+        if (mm >= Cfg::NDESC) mbar_wait(&bar_desc_empty[d], ((mm / Cfg::NDESC) - 1) & 1);
+        descs[2 * d] = make_int4(it.q0, it.qe, it.dl, it.h);
+        descs[2 * d + 1] = make_int4(it.kv_lo, it.kv_hi, it.nkv, it.kh);
+        mbar_arrive(&bar_desc_full[d]);
+      };
       FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
+      if (i0 < n_items) put_desc(0, fwd_item_cur(nxt, BN));
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
-        if (sched_item(m + 1) < n_items) nxt = fwd_item(p, sched_item(m + 1), BN);  // prefetch
+        if (sched_item(m + 1) < n_items) {  // prefetch
+          nxt = fwd_item(p, sched_item(m + 1), BN);
+          put_desc(m + 1, fwd_item_cur(nxt, BN));
+        }
         const int qs = k % NQ;
         if (k >= NQ) {  // buffer qs held item k-NQ: its Q reads (FP8) / its O store's reads (bf16) done
           if constexpr (FP8) {
@@ -415,14 +438,38 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       wp.template add_since<4>(te);
     };
     int g = 0, k = 0;
-    FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
-    int2 rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
+    auto get_desc = [&](int mm, FwdItem& it, bool full) {  // item ordinal mm from the producer's ring
+      const int d = mm % Cfg::NDESC;
+      mbar_wait(&bar_desc_full[d], (mm / Cfg::NDESC) & 1);
+      const int4 a = descs[2 * d];
+      it.q0 = a.x;
+      it.qe = a.y;
+      it.dl = a.z;
+      it.h = a.w;
+      if (full) {
+        const int4 b = descs[2 * d + 1];
+        it.kv_lo = b.x;
+        it.kv_hi = b.y;
+        it.nkv = b.z;
+        it.kh = b.w;
+      }
+    };
+    int2 rs_n = make_int2(0, 0);
+    if (i0 < n_items) {
+      FwdItem f;
+      get_desc(0, f, false);
+      rs_n = f.q0 + r < p.T ? __ldg(p.rows_span + f.q0 + r) : make_int2(0, 0);
+    }
     for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
-      const FwdItem itm = fwd_item_cur(nxt, BN);
+      FwdItem itm;
+      get_desc(m, itm, true);
+      __syncwarp();
+      warp_arrive(&bar_desc_empty[m % Cfg::NDESC]);
       const int2 rs = rs_n;
-      if (sched_item(m + 1) < n_items) {  // prefetch the next item's parameters
-        nxt = fwd_item(p, sched_item(m + 1), BN);
-        rs_n = nxt.q0 + r < p.T ? __ldg(p.rows_span + nxt.q0 + r) : make_int2(0, 0);
+      if (sched_item(m + 1) < n_items) {  // prefetch the next item's row span
+        FwdItem f;
+        get_desc(m + 1, f, false);
+        rs_n = f.q0 + r < p.T ? __ldg(p.rows_span + f.q0 + r) : make_int2(0, 0);
       }
       const int row = itm.q0 + r;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + qp * OC;

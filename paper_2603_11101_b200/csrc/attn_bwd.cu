@@ -542,13 +542,19 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           else tmem_ld16(tmem + lane_off + Cfg::s_col(g) + c0, sa);
           tmem_wait_ld();
 #pragma unroll
+          const float2 sl2v = make_float2(p.scale_log2, p.scale_log2);
           for (int j4 = 0; j4 < CW / 4; ++j4) {
             const float4 l = lse4[j4];  // 128-bit broadcast load
+            // packed FFMA2: s·scale·log2e − lse2, two columns per instruction (same rounding as FFMA)
+            const float2 a0 = f2_fma(make_float2(__uint_as_float(sa[4 * j4 + 0]), __uint_as_float(sa[4 * j4 + 1])), sl2v,
+                                     make_float2(-l.x, -l.y));
+            const float2 a1 = f2_fma(make_float2(__uint_as_float(sa[4 * j4 + 2]), __uint_as_float(sa[4 * j4 + 3])), sl2v,
+                                     make_float2(-l.z, -l.w));
             float e[4];
-            e[0] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 0]), p.scale_log2, -l.x));
-            e[1] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 1]), p.scale_log2, -l.y));
-            e[2] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 2]), p.scale_log2, -l.z));
-            e[3] = ex2_approx(fmaf(__uint_as_float(sa[4 * j4 + 3]), p.scale_log2, -l.w));
+            e[0] = ex2_approx(a0.x);
+            e[1] = ex2_approx(a0.y);
+            e[2] = ex2_approx(a1.x);
+            e[3] = ex2_approx(a1.y);
             if (!all_full) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) e[q] = (vis & (1u << (4 * j4 + q))) ? e[q] : 0.f;
@@ -581,9 +587,13 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             const int q = 4 * j4;
             const float p0 = __uint_as_float(pp[2 * j4] << 16), p1 = __uint_as_float(pp[2 * j4] & 0xFFFF0000u);
             const float p2 = __uint_as_float(pp[2 * j4 + 1] << 16), p3 = __uint_as_float(pp[2 * j4 + 1] & 0xFFFF0000u);
-            pk[2 * j4] = pack_bf16x2(p0 * (__uint_as_float(dr[q]) - dd.x), p1 * (__uint_as_float(dr[q + 1]) - dd.y));
-            pk[2 * j4 + 1] =
-                pack_bf16x2(p2 * (__uint_as_float(dr[q + 2]) - dd.z), p3 * (__uint_as_float(dr[q + 3]) - dd.w));
+            // packed FADD2 / FMUL2 (same rounding as the scalar forms)
+            const float2 d0 = f2_mul(make_float2(p0, p1), f2_add(make_float2(__uint_as_float(dr[q]), __uint_as_float(dr[q + 1])),
+                                                                 make_float2(-dd.x, -dd.y)));
+            const float2 d1 = f2_mul(make_float2(p2, p3), f2_add(make_float2(__uint_as_float(dr[q + 2]), __uint_as_float(dr[q + 3])),
+                                                                 make_float2(-dd.z, -dd.w)));
+            pk[2 * j4] = pack_bf16x2(d0.x, d0.y);
+            pk[2 * j4 + 1] = pack_bf16x2(d1.x, d1.y);
           }
         } else {
 #pragma unroll

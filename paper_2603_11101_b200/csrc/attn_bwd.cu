@@ -1011,15 +1011,16 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           if constexpr (W == 32) tmem_ld32(s_tm, sr);
           else tmem_ld16(s_tm, sr);
           tmem_wait_ld();
+          // masked columns → −∞ before the exponent (exp2 → 0) in a warp-uniform branch, so the
+          // common all-visible tile runs no per-element select (it was if-converted before)
+          if (!all_full) {
+#pragma unroll
+            for (int c = 0; c < W; ++c) sr[c] = ((vm >> c) & 1u) ? sr[c] : __float_as_uint(-INFINITY);
+          }
 #pragma unroll
           for (int t = 0; t < W / 2; ++t) {
             const float2 a = f2_fma(make_float2(__uint_as_float(sr[2 * t]), __uint_as_float(sr[2 * t + 1])), sl2v, nl2);
-            float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-            if (!all_full) {
-              e.x = (vm >> (2 * t)) & 1u ? e.x : 0.f;
-              e.y = (vm >> (2 * t + 1)) & 1u ? e.y : 0.f;
-            }
-            pr[t] = e;
+            pr[t] = make_float2(ex2_approx(a.x), ex2_approx(a.y));
           }
         }
         trace(21, g);  // S: phase A done

@@ -186,24 +186,22 @@ __global__ void __launch_bounds__(192, 1)
       tmem_wait_ld();
       const int kv0 = kv_lo + j * BN;
       const int c_lo = rs.lo - kv0, c_hi = rs.hi - kv0;
-      float mt = -INFINITY;
-      if (c_lo <= 0 && c_hi >= BN) {
+      // invisible columns → −∞ in a warp-uniform branch (exp2 → 0); the row max over raw S with 4
+      // independent FMNMX3 chains, scaled once (scale > 0)
+      if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= BN)) {
 #pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          const float x = __uint_as_float(r[c]) * sl2;
-          r[c] = __float_as_uint(x);
-          mt = fmaxf(mt, x);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          const float x = (c >= c_lo && c < c_hi) ? __uint_as_float(r[c]) * sl2 : -INFINITY;
-          r[c] = __float_as_uint(x);
-          mt = fmaxf(mt, x);
-        }
+        for (int c = 0; c < BN; ++c) r[c] = (c >= c_lo && c < c_hi) ? r[c] : __float_as_uint(-INFINITY);
       }
+      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < BN; c += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mq[u] = fmax3(mq[u], __uint_as_float(r[c + 2 * u]), __uint_as_float(r[c + 2 * u + 1]));
+      }
+      float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+      mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
       const bool grow = mt > m_run + kLazyRescale;
-      const float alpha = grow ? exp2f(m_run - mt) : 1.f;  // m_run = -inf → 0
+      const float alpha = grow ? ex2_approx(m_run - mt) : 1.f;  // m_run = -inf → 0
       if (__any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY)) {
         mbar_wait(&bar_o_ready, (j - 1) & 1);
         tc_fence_after();
@@ -222,20 +220,22 @@ __global__ void __launch_bounds__(192, 1)
         m_run = mt;
       }
       const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-      float ls = 0.f;
+      // P = exp2(S·scale·log2e − m): FFMA2 for the argument, 4 independent FADD2 sum chains
+      const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+      float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < BN; c += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2_approx(__uint_as_float(r[c + 2 * i]) - msub);
-          const float p1 = ex2_approx(__uint_as_float(r[c + 2 * i + 1]) - msub);
-          ls += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
+          const float2 a = f2_fma(make_float2(__uint_as_float(r[c + 2 * i]), __uint_as_float(r[c + 2 * i + 1])), sl2v, nmv);
+          const float2 pe = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+          lq[i & 1] = f2_add(lq[i & 1], pe);
+          pk[i] = pack_bf16x2(pe.x, pe.y);
         }
         tmem_st16(tmem + lane_off + Cfg::P_COL + sb * (BN / 2) + c / 2, pk);
       }
-      l_run += ls;
+      l_run += (lq[0].x + lq[1].x) + (lq[0].y + lq[1].y);
       tmem_wait_st();
       tc_fence_before();
       warp_arrive(&bar_p_full[sb]);

@@ -453,8 +453,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
-#pragma unroll
           const uint64_t om = opaque(dOm) + coff, qm = opaque(dQm) + coff;
+#pragma unroll
           for (int j = 0; j < UQ / 16; ++j)
             umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + Cfg::a_col(j),
                         sdesc_add(om, j * 2048), id_acc, j > 0 ? 1u : acc0);
@@ -541,8 +541,14 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           if constexpr (CW == 32) tmem_ld32(tmem + lane_off + Cfg::s_col(g) + c0, sa);
           else tmem_ld16(tmem + lane_off + Cfg::s_col(g) + c0, sa);
           tmem_wait_ld();
+          // invisible columns → −∞ before the exponent (exp2 → 0) in one warp-uniform branch, so the
+          // exponent loop below has no branch between its iterations
+          if (!all_full) {
 #pragma unroll
+            for (int q = 0; q < CW; ++q) sa[q] = ((vis >> q) & 1u) ? sa[q] : __float_as_uint(-INFINITY);
+          }
           const float2 sl2v = make_float2(p.scale_log2, p.scale_log2);
+#pragma unroll
           for (int j4 = 0; j4 < CW / 4; ++j4) {
             const float4 l = lse4[j4];  // 128-bit broadcast load
             // packed FFMA2: s·scale·log2e − lse2, two columns per instruction (same rounding as FFMA)
@@ -555,10 +561,6 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             e[1] = ex2_approx(a0.y);
             e[2] = ex2_approx(a1.x);
             e[3] = ex2_approx(a1.y);
-            if (!all_full) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) e[q] = (vis & (1u << (4 * j4 + q))) ? e[q] : 0.f;
-            }
             pp[2 * j4] = pack_bf16x2(e[0], e[1]);
             pp[2 * j4 + 1] = pack_bf16x2(e[2], e[3]);
           }

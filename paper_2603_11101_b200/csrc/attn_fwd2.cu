@@ -402,14 +402,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const long long te = wp.now();
       wp.template wait<2>(&bar_o_full[ek & 1], (ek >> 1) & 1);
       tc_fence_after();
+      uint32_t o[32];
+      // OC ≤ 32 columns (HD 64: the upper 16 belong to the next quarter, unused); the row's scalars
+      // and the LSE are computed while the TMEM load is in flight
+      tmem_ld32(tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + qp * OC, o);
       const bool valid = r < e_n;  // rows past the tile's end belong to the next segment
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
-      const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (ek & 1) * HD + qp * OC;
+      if (valid && qp == 0)
+        p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
       // staging tile: bf16 → this item's Q buffer; FP8 → the O tile, once item ek-1's store has read it
       uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + (ek % NQ) * Cfg::Q_BYTES);
-      uint32_t o[32];
-      tmem_ld32(o_tm, o);  // OC ≤ 32 columns (HD 64: the upper 16 belong to the next quarter, unused)
       tmem_wait_ld();
+      tc_fence_before();
+      warp_arrive(&bar_o_empty[ek & 1]);  // O is in registers: the buffer may take item ek+2
       uint32_t pk[16];
 #pragma unroll
       for (int t = 0; t < OC / 2; ++t)
@@ -430,10 +435,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int t = 0; t < OC / 8; ++t) dst[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
         }
       }
-      tc_fence_before();
-      warp_arrive(&bar_o_empty[ek & 1]);
-      if (valid && qp == 0)
-        p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
       ek = -1;
       wp.template add_since<4>(te);
     };

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define VLASIM_ABI_VERSION 2
+#define VLASIM_ABI_VERSION 3
 
 enum {
   VLASIM_OK = 0,
@@ -70,6 +70,10 @@ typedef struct vlasim_pack_out {
   int64_t* total_tokens;    /* [1]                                                           */
   int32_t* status;          /* [2]   {error code, offending sample id} written on device     */
 } vlasim_pack_out;
+
+/* flags of the calls that report input errors found on the device: synchronise `stream` and
+   return the device status (VLASIM_ECONFIG with the offending index in the message). */
+#define VLASIM_SYNC_CHECK 1u
 
 /* Maximum capacity accepted by the GPU packer (larger → VLASIM_ECONFIG). */
 #define VLASIM_PACK_MAX_CAPACITY 16384
@@ -165,6 +169,7 @@ typedef struct vlasim_attn_grads {
                                 gradients back to sample order into the kernels.         */
 } vlasim_attn_grads;
 
+/* backward: 0 forward, 1 backward, 2 FP8 Q/K backward */
 size_t vlasim_varlen_attn_workspace_size(const vlasim_attn_args* a, int backward);
 
 int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void* d_workspace, size_t workspace_bytes,
@@ -174,14 +179,24 @@ int vlasim_varlen_attn_bwd_cuda(const vlasim_attn_args* a, const vlasim_attn_gra
 /* FP8 Q/K forward: q/k are e4m3 codes with per-(head,128-token,128-d) block scales. */
 int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args* a, void* d_workspace, size_t workspace_bytes,
                                       vlasim_stream_t stream);
+/* Backward of the FP8 Q/K forward: gradients of attention(deq(q), deq(k), v) (straight-through for
+ * the quantiser) with the FP8 forward's o / lse.  q/k are the codes + scales of the forward; dq/dk
+ * are bf16 gradients with respect to the dequantised operands.  Workspace:
+ * vlasim_varlen_attn_workspace_size(a, 2). */
+int vlasim_varlen_attn_bwd_fp8qk_cuda(const vlasim_attn_args* a, const vlasim_attn_grads* g, void* d_workspace,
+                                      size_t workspace_bytes, vlasim_stream_t stream);
 
 /* ------------------------------------------------------------------ fp8
  * Replaces vlasim::quantize(t, PerBlock(128,128), E4M3) applied
- * per head to x [T, heads, d] bf16: scale = amax/448 (1 if the block is all zero),
- * codes = RNE(x / scale) saturated to ±448.  scales [heads, ceil(T/128), ceil(d/128)].
+ * per head to x [T, heads, d] bf16: scale = fp32(amax/448) (1 if the block is all zero),
+ * codes = the round-to-nearest-even E4M3 code of the REAL quotient x·448/amax (saturating
+ * to ±448).  scales [heads, ceil(T/128), ceil(d/128)].
+ * d_status ([2] int32 or NULL): {VLASIM_ECONFIG, flat index} when an element is non-finite
+ * ("non-finite input → error"; that block's codes are not written), else {0, 0}.
+ * flags VLASIM_SYNC_CHECK (needs d_status): synchronise and return the status.
  */
 int vlasim_fp8_quant_block_cuda(const void* d_x, int64_t T, int32_t heads, int32_t d, uint8_t* d_codes,
-                                float* d_scales, vlasim_stream_t stream);
+                                float* d_scales, int32_t* d_status, uint32_t flags, vlasim_stream_t stream);
 int vlasim_fp8_dequant_block_cuda(const uint8_t* d_codes, const float* d_scales, int64_t T, int32_t heads, int32_t d,
                                   float* d_out, vlasim_stream_t stream);
 /* quant_error(original, qt) per group (head, 128-token block, 128-d block),

@@ -303,6 +303,25 @@ std::uint8_t e4m3_encode(double x) {
 
 double e4m3_rne(double x) { return e4m3_decode(e4m3_encode(x)); }
 
+// SPEC.md:583 with the REAL quotient: code of RNE(num / den) for den > 0 without forming the quotient.
+// The exhaustive nearest-value search over the representable set ("oracle is exhaustive
+// nearest-value search") decided by exact comparisons: |num| against mid_i · den for the midpoints
+// mid_i = (v_i + v_{i+1}) / 2 of consecutive representable values.  Callers pass num = x · 448 and
+// den = amax with x, amax fp32: both products are exact in double (≤ 27 and ≤ 29 significant bits).
+std::uint8_t e4m3_encode_ratio(double num, double den) {
+  if (!std::isfinite(num) || !std::isfinite(den) || !(den > 0)) throw ConfigError("e4m3: non-finite input");
+  static const std::vector<double> vals = e4m3_values();
+  const std::uint8_t sign = std::signbit(num) ? 0x80 : 0x00;
+  const double a = std::fabs(num);
+  for (std::size_t i = 0; i + 1 < vals.size(); ++i) {
+    const double m = 0.5 * (vals[i] + vals[i + 1]);  // exact (≤ 5 significant bits)
+    const double b = m * den;                         // exact
+    if (a < b) return sign | static_cast<std::uint8_t>(i);
+    if (a == b) return sign | static_cast<std::uint8_t>(i % 2 == 0 ? i : i + 1);  // tie → even mantissa
+  }
+  return sign | 0x7E;  // above the last midpoint: 448 (saturating)
+}
+
 double e4m3_decode(std::uint8_t code) {
   static const std::vector<double> vals = e4m3_values();
   const std::uint8_t mag = code & 0x7F;
@@ -600,13 +619,18 @@ int oracle_fp8_quant_block(const float* x, std::int64_t T, std::int64_t heads, s
               amax = std::max(amax, a);
             }
           const float scale_f = amax == 0 ? 1.0f : static_cast<float>(amax) / 448.0f;
-          const double scale_d = amax == 0 ? 1.0 : amax / 448.0;
-          scales[(h * nbt + bt) * nbd + bd] = quotient_fp32 ? scale_f : static_cast<float>(scale_d);
+          // the stored scale is the fp32 rounding of amax / 448 in both modes (scale storage is
+          // 4-byte); the codes differ only in the quotient they round
+          scales[(h * nbt + bt) * nbd + bd] = scale_f;
           for (std::int64_t t = bt * 128; t < t1; ++t)
             for (std::int64_t c = bd * 128; c < d1; ++c) {
               const std::int64_t i = (t * heads + h) * d + c;
-              const double qv = quotient_fp32 ? static_cast<double>(x[i] / scale_f) : x[i] / scale_d;
-              codes[i] = vlasim::oracle::e4m3_encode(qv);
+              if (quotient_fp32)
+                codes[i] = vlasim::oracle::e4m3_encode(static_cast<double>(x[i] / scale_f));
+              else if (amax == 0)
+                codes[i] = vlasim::oracle::e4m3_encode(static_cast<double>(x[i]));  // ±0 at scale 1
+              else
+                codes[i] = vlasim::oracle::e4m3_encode_ratio(static_cast<double>(x[i]) * 448.0, amax);
             }
         }
   });

@@ -77,6 +77,7 @@ SmallTensor masked_attention(const SmallTensor& q, const SmallTensor& k, const S
 std::vector<double> e4m3_values();                // all finite non-negative representable values, ascending
 double e4m3_rne(double x);                        // RNE projection onto the set, saturating to ±448
 std::uint8_t e4m3_encode(double x);               // code byte of e4m3_rne(x)
+std::uint8_t e4m3_encode_ratio(double num, double den);  // code of RNE(num / den), exact (den > 0)
 double e4m3_decode(std::uint8_t code);
 
 }  // namespace vlasim::oracle

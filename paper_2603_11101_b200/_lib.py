@@ -60,8 +60,10 @@ _SIGS = {
     "vlasim_varlen_attn_bwd_cuda": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(AttnGrads), C.c_void_p, C.c_size_t,
                                               C.c_void_p]),
     "vlasim_varlen_attn_fwd_fp8qk_cuda": (C.c_int, [C.POINTER(AttnArgs), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vlasim_varlen_attn_bwd_fp8qk_cuda": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(AttnGrads), C.c_void_p,
+                                                    C.c_size_t, C.c_void_p]),
     "vlasim_fp8_quant_block_cuda": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, f32p,
-                                              C.c_void_p]),
+                                              i32p, C.c_uint32, C.c_void_p]),
     "vlasim_fp8_dequant_block_cuda": (C.c_int, [C.c_void_p, f32p, C.c_int64, C.c_int32, C.c_int32, f32p,
                                                 C.c_void_p]),
     "vlasim_fp8_quant_error_cuda": (C.c_int, [C.c_void_p, C.c_void_p, f32p, C.c_int64, C.c_int32, C.c_int32, f32p,

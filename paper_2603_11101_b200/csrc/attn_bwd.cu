@@ -31,6 +31,8 @@ using namespace vlasim_dev;
 
 namespace vlasim_host {
 int validate_attn_args(const vlasim_attn_args* a, bool fp8);
+int launch_fp8_dequant_bf16(const uint8_t* codes, const float* scales, int64_t T, int heads, int d, void* out,
+                            cudaStream_t st);
 }
 
 namespace {
@@ -116,6 +118,24 @@ __global__ void __launch_bounds__(256) k_bwd_pre(const __nv_bfloat16* __restrict
     for (int sh = 0; sh < 4; ++sh) {
       dsum[sh * cp + int64_t(h) * Tp + t + sh] = d;
       lse2[sh * cp + int64_t(h) * Tp + t + sh] = l2;
+    }
+  }
+  if (blockIdx.x == gridDim.x - 1) {
+    // Cells no token writes — [h·Tp + sh + T, (h+1)·Tp + sh) after every head (the next head's
+    // first sh slots included), [0, sh) and the +512 tail of each copy — are read by the dK/dV
+    // kernel's UQ-wide windows past the last token: give them finite neutral values (lse2 = 0,
+    // D = 0) so that a masked column computes exp2(−inf) = 0 and 0 · (dP − 0) = 0, never NaN.
+    const int gap = Tp - T;  // 0..3
+    for (int sh = 0; sh < 4; ++sh) {
+      float* l = lse2 + sh * cp;
+      float* dd = dsum + sh * cp;
+      for (int i = threadIdx.x; i < sh; i += 256) l[i] = dd[i] = 0.f;
+      for (int h = 0; h + 1 < H; ++h)
+        for (int i = threadIdx.x; i < gap; i += 256) {
+          const int64_t c = int64_t(h) * Tp + sh + T + i;
+          l[c] = dd[c] = 0.f;
+        }
+      for (int64_t c = int64_t(H - 1) * Tp + sh + T + threadIdx.x; c < cp; c += 256) l[c] = dd[c] = 0.f;
     }
   }
   if (threadIdx.x < nt) {
@@ -1199,11 +1219,19 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
 
 }  // namespace
 
+// FP8 backward: bf16 copies of the dequantised Q / K codes after the backward's own workspace
+size_t fp8_bwd_extra(const vlasim_attn_args* a) {
+  const size_t T = size_t(a->total_tokens), d = size_t(a->head_dim);
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return up(T * size_t(a->num_heads) * d * 2) + up(T * size_t(a->num_kv_heads) * d * 2);
+}
+
 extern "C" size_t vlasim_varlen_attn_workspace_size(const vlasim_attn_args* a, int backward) {
   if (!a) return 0;
   if (!backward) return vlasim_host::fwd_ws_bytes(a);  // forward: per-token visible spans + tiles
   BwdWs w;
-  return bwd_ws(&w, nullptr, a);
+  const size_t b = bwd_ws(&w, nullptr, a);
+  return backward == 2 ? b + fp8_bwd_extra(a) : b;
 }
 
 extern "C" int vlasim_varlen_attn_bwd_cuda(const vlasim_attn_args* a, const vlasim_attn_grads* g, void* ws,
@@ -1222,5 +1250,41 @@ extern "C" int vlasim_varlen_attn_bwd_cuda(const vlasim_attn_args* a, const vlas
     case 64: return launch_bwd<64>(a, g, w, st);
     case 128: return launch_bwd<128>(a, g, w, st);
     default: return launch_bwd<256>(a, g, w, st);
+  }
+}
+
+// Backward of the FP8 Q/K forward (config 4): the gradients of o = attention(deq(q), deq(k), v) with
+// deq(x) = value(code) · block scale (the straight-through gradient of the quantiser).  Q and K are
+// dequantised once to bf16 (an HBM pass over the codes) and the bf16 backward kernels run on them
+// with the FP8 forward's LSE; dQ / dK are with respect to the dequantised operands.
+extern "C" int vlasim_varlen_attn_bwd_fp8qk_cuda(const vlasim_attn_args* a, const vlasim_attn_grads* g, void* ws,
+                                                 size_t ws_bytes, vlasim_stream_t stream) {
+  using namespace vlasim_host;
+  if (int rc = validate_attn_args(a, true)) return rc;
+  if (!g || !g->dout || !g->dq || !g->dk || !g->dv) return set_error(VLASIM_ECONFIG, "attention bwd: grads required");
+  if (g->row_map && a->seg_src)
+    return set_error(VLASIM_ECONFIG, "attention bwd: row_map and seg_src are exclusive (seg_src keeps source order)");
+  BwdWs w;
+  const size_t base = bwd_ws(&w, nullptr, a), need = base + fp8_bwd_extra(a);
+  if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fp8 bwd: workspace %zu < %zu", ws_bytes, need);
+  bwd_ws(&w, ws, a);
+  cudaStream_t st = as_stream(stream);
+  const int64_t T = a->total_tokens;
+  uint8_t* wq = static_cast<uint8_t*>(ws) + base;
+  uint8_t* wk = wq + ((size_t(T) * a->num_heads * a->head_dim * 2 + 255) & ~size_t(255));
+  if (int rc = launch_fp8_dequant_bf16(static_cast<const uint8_t*>(a->q), a->q_scale, T, a->num_heads, a->head_dim,
+                                       wq, st))
+    return rc;
+  if (int rc = launch_fp8_dequant_bf16(static_cast<const uint8_t*>(a->k), a->k_scale, T, a->num_kv_heads,
+                                       a->head_dim, wk, st))
+    return rc;
+  vlasim_attn_args b = *a;
+  b.q = wq;
+  b.k = wk;
+  b.q_scale = b.k_scale = nullptr;
+  switch (a->head_dim) {
+    case 64: return launch_bwd<64>(&b, g, w, st);
+    case 128: return launch_bwd<128>(&b, g, w, st);
+    default: return launch_bwd<256>(&b, g, w, st);
   }
 }

@@ -4,8 +4,8 @@
 // dimensions" blocks, applied per head — DESIGN.md §2):
 //   scale = amax(block) / 448 (1 if the block is all zero)
 //   code  = RNE(x / scale) onto E4M3, saturating to ±448
-// Arithmetic is fp32 (scale = fp32(amax) / 448.f, quotient = correctly rounded fp32 division,
-// then cvt.rn.satfinite.e4m3x2.f32), which the oracle's quotient_fp32 mode restates bit-exactly.
+// scale = RN_fp32(amax / 448); codes = the RNE code of the REAL quotient x·448/amax (e4m3_fix below),
+// bit-exact with the oracle's exact mode; non-finite input → status VLASIM_ECONFIG.
 #include <cuda_bf16.h>
 
 #include "common.hpp"
@@ -31,9 +31,57 @@ __device__ __forceinline__ float e4m3_to_float(uint8_t c) {
   return (c & 0x80) ? -v : v;
 }
 
+// Exact RNE (the code of the REAL quotient x / scale, scale = amax / 448).  The fp32
+// quotient q = RN(x / RN(amax / 448)) is within a few fp32 ulps of the real quotient X = |x|·448/amax,
+// so cvt(q) is the right code unless X lies within those ulps of a midpoint between two E4M3 values
+// (or in the subnormal range, where the midpoint grid is finer): only then is the candidate code
+// re-decided, by exact fp64 comparisons of |x|·448 against midpoint · amax (both products exact:
+// ≤ 11 and ≤ 13 significant bits for bf16 inputs).  Midpoints have the fp32 pattern 1.xxx1 000…0,
+// i.e. low 20 mantissa bits 0x80000.
+__device__ __forceinline__ bool e4m3_suspect(float q) {
+  const float a = fabsf(q);
+  const int low = int(__float_as_uint(a) & 0xFFFFFu);
+  return a < 0.015625f || abs(low - 0x80000) <= 64;
+}
+
+__device__ __noinline__ uint32_t e4m3_fix(uint32_t c, float ax, float amax) {
+  const double A = double(ax) * 448.0, B = double(amax);
+  const int e = int(c >> 3), m = int(c & 7), ee = e == 0 ? 1 : e;
+  const int mant = e == 0 ? m : 8 + m;
+  if (c < 0x7E) {  // midpoint to the next code up: (2·mant + 1) · 2^(ee−11)
+    const double mu = ldexp(double(2 * mant + 1), ee - 11) * B;
+    if (A > mu || (A == mu && (c & 1))) return c + 1;
+  }
+  if (c > 0) {  // midpoint to the next code down (half the spacing across a binade edge)
+    const double md = (m == 0 && e >= 2) ? ldexp(double(4 * mant - 1), ee - 12) * B
+                                         : ldexp(double(2 * mant - 1), ee - 11) * B;
+    if (A < md || (A == md && (c & 1))) return c - 1;
+  }
+  return c;
+}
+
+// Non-finite bf16 in either half of a 32-bit word (exponent all ones).
+__device__ __forceinline__ bool bf16x2_nonfinite(uint32_t w) {
+  return ((w & 0x7F80u) == 0x7F80u) || ((w & 0x7F800000u) == 0x7F800000u);
+}
+
+__device__ __forceinline__ int first_nonfinite(uint4 q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  int k = 7;
+#pragma unroll
+  for (int j = 7; j >= 0; --j)
+    if (((w[j >> 1] >> (16 * (j & 1))) & 0x7F80u) == 0x7F80u) k = j;
+  return k;
+}
+
+__device__ __forceinline__ void report_nonfinite(int32_t* status, int64_t idx) {
+  if (status && atomicCAS(status, 0, VLASIM_ECONFIG) == 0) status[1] = int32_t(idx < INT32_MAX ? idx : INT32_MAX);
+}
+
 // One CTA (256 threads) per (head, 128-token block, 128-d block).
 __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __restrict__ x, int T, int heads, int d,
-                                                     uint8_t* __restrict__ codes, float* __restrict__ scales) {
+                                                     uint8_t* __restrict__ codes, float* __restrict__ scales,
+                                                     int32_t* __restrict__ status) {
   const int nbd = (d + 127) / 128, nbt = (T + 127) / 128;
   const int bd = blockIdx.x % nbd, bt = (blockIdx.x / nbd) % nbt, h = blockIdx.x / (nbd * nbt);
   const int t0 = bt * 128, c0 = bd * 128;
@@ -41,13 +89,24 @@ __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __rest
   __shared__ float red[8];
   // pass 1: amax (each thread: 2-element chunks of the block)
   float amax = 0.f;
+  int64_t bad = -1;
   for (int e = threadIdx.x * 2; e < rows * 128; e += 512) {
     const int r = e / 128, c = e % 128;
     if (c < cols) {
       const __nv_bfloat16* p = x + (int64_t(t0 + r) * heads + h) * d + c0 + c;
-      amax = fmaxf(amax, fabsf(__bfloat162float(p[0])));
-      if (c + 1 < cols) amax = fmaxf(amax, fabsf(__bfloat162float(p[1])));
+      const float a0 = __bfloat162float(p[0]);
+      if (!isfinite(a0)) bad = p - x;
+      amax = fmaxf(amax, fabsf(a0));
+      if (c + 1 < cols) {
+        const float a1 = __bfloat162float(p[1]);
+        if (!isfinite(a1)) bad = p + 1 - x;
+        amax = fmaxf(amax, fabsf(a1));
+      }
     }
+  }
+  if (__syncthreads_or(bad >= 0)) {
+    if (bad >= 0) report_nonfinite(status, bad);
+    return;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -68,14 +127,17 @@ __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __rest
     const int r = e / 128, c = e % 128;
     if (c < cols) {
       const int64_t off = (int64_t(t0 + r) * heads + h) * d + c0 + c;
-      const float a = __fdiv_rn(__bfloat162float(x[off]), scale);
+      const float xa = __bfloat162float(x[off]);
+      const float a = __fdiv_rn(xa, scale);
+      uint32_t ca = cvt_e4m3x2(a, 0.f) & 0xFF;
+      if (amax != 0.f && e4m3_suspect(a)) ca = (ca & 0x80) | e4m3_fix(ca & 0x7F, fabsf(xa), amax);
+      codes[off] = uint8_t(ca);
       if (c + 1 < cols) {
-        const float b = __fdiv_rn(__bfloat162float(x[off + 1]), scale);
-        const uint16_t pr = cvt_e4m3x2(a, b);
-        codes[off] = uint8_t(pr & 0xFF);
-        codes[off + 1] = uint8_t(pr >> 8);
-      } else {
-        codes[off] = uint8_t(cvt_e4m3x2(a, 0.f) & 0xFF);
+        const float xb = __bfloat162float(x[off + 1]);
+        const float b = __fdiv_rn(xb, scale);
+        uint32_t cb = cvt_e4m3x2(b, 0.f) & 0xFF;
+        if (amax != 0.f && e4m3_suspect(b)) cb = (cb & 0x80) | e4m3_fix(cb & 0x7F, fabsf(xb), amax);
+        codes[off + 1] = uint8_t(cb);
       }
     }
   }
@@ -87,7 +149,8 @@ __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __rest
 // 16 threads per 256-B row segment — reduced to amax, then written as 8-B code chunks.  One HBM
 // read of x and one write of the codes: the HBM roofline of the operation.
 __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __restrict__ x, int T, int heads, int d,
-                                                       uint8_t* __restrict__ codes, float* __restrict__ scales) {
+                                                       uint8_t* __restrict__ codes, float* __restrict__ scales,
+                                                       int32_t* __restrict__ status) {
   const int nbd = (d + 127) / 128, nbt = (T + 127) / 128;
   const int h = blockIdx.x % heads, rest = blockIdx.x / heads;
   const int bd = rest % nbd, bt = rest / nbd;
@@ -97,15 +160,22 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
   __shared__ float red[8];
   uint4 v[8];
   __nv_bfloat162 m2 = __floats2bfloat162_rn(0.f, 0.f);
+  int bad = -1;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int t = t0 + r0 + 16 * i;
     v[i] = make_uint4(0, 0, 0, 0);
     if (cv && t < T)
       v[i] = __ldcs(reinterpret_cast<const uint4*>(x + (int64_t(t) * heads + h) * d + c0 + ch * 8));
+    if (bf16x2_nonfinite(v[i].x) | bf16x2_nonfinite(v[i].y) | bf16x2_nonfinite(v[i].z) | bf16x2_nonfinite(v[i].w))
+      bad = 8 * i + first_nonfinite(v[i]);
     const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) m2 = __hmax2(m2, __habs2(b[j]));
+  }
+  if (__syncthreads_or(bad >= 0)) {  // non-finite input → error (no codes written)
+    if (bad >= 0) report_nonfinite(status, (int64_t(t0 + r0 + 16 * (bad >> 3)) * heads + h) * d + c0 + ch * 8 + (bad & 7));
+    return;
   }
   float amax = fmaxf(__bfloat162float(m2.x), __bfloat162float(m2.y));
 #pragma unroll
@@ -133,12 +203,27 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
     if (!cv || t >= T) continue;
     const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
     uint32_t w[2];
+    float qv[8];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const float2 q0 = quot(__bfloat1622float2(b[2 * j])), q1 = quot(__bfloat1622float2(b[2 * j + 1]));
+      qv[4 * j] = q0.x, qv[4 * j + 1] = q0.y, qv[4 * j + 2] = q1.x, qv[4 * j + 3] = q1.y;
       const uint32_t lo = cvt_e4m3x2(q0.x, q0.y);
       const uint32_t hi = cvt_e4m3x2(q1.x, q1.y);
       w[j] = lo | (hi << 16);
+    }
+    bool sus = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sus |= e4m3_suspect(qv[k]);
+    if (sus && amax != 0.f) {  // rare: re-decide the codes whose quotient sits at a midpoint
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (!e4m3_suspect(qv[k])) continue;
+        const uint32_t sh = 8 * (k & 3), c = (w[k >> 2] >> sh) & 0xFF;
+        const float ax = fabsf(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&v[i])[k]));
+        const uint32_t f = (c & 0x80) | e4m3_fix(c & 0x7F, ax, amax);
+        w[k >> 2] = (w[k >> 2] & ~(0xFFu << sh)) | (f << sh);
+      }
     }
     __stcs(reinterpret_cast<uint2*>(codes + (int64_t(t) * heads + h) * d + c0 + ch * 8), make_uint2(w[0], w[1]));
   }
@@ -208,7 +293,45 @@ __global__ void __launch_bounds__(256) k_quant_error(const __nv_bfloat16* __rest
   }
 }
 
+// codes → bf16(value(code) · scale) (fp32 product, one rounding): the Q/K operands of the FP8
+// path's backward.  8 codes per thread (8-B load, 16-B store); d % 8 == 0.
+__global__ void k_dequant_bf16(const uint8_t* __restrict__ codes, const float* __restrict__ scales, int64_t T,
+                               int heads, int d, __nv_bfloat16* __restrict__ out) {
+  const int64_t n8 = T * heads * d / 8;
+  const int nbd = (d + 127) / 128, nbt = int((T + 127) / 128);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = i * 8;
+    const int c = int(e % d);
+    const int64_t th = e / d;
+    const int h = int(th % heads);
+    const int64_t t = th / heads;
+    const float sc = scales[(int64_t(h) * nbt + t / 128) * nbd + c / 128];
+    const uint2 w = *reinterpret_cast<const uint2*>(codes + e);
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(&w);
+    uint4 r;
+    uint32_t* rr = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 v = __floats2bfloat162_rn(e4m3_to_float(b[2 * j]) * sc, e4m3_to_float(b[2 * j + 1]) * sc);
+      rr[j] = *reinterpret_cast<const uint32_t*>(&v);
+    }
+    *reinterpret_cast<uint4*>(out + e) = r;
+  }
+}
+
 }  // namespace
+
+namespace vlasim_host {
+int launch_fp8_dequant_bf16(const uint8_t* codes, const float* scales, int64_t T, int heads, int d, void* out,
+                            cudaStream_t st) {
+  if (d % 8) return set_error(VLASIM_ECONFIG, "fp8 dequant: head_dim %d not a multiple of 8", d);
+  const int64_t n8 = T * heads * d / 8;
+  const int64_t blocks = std::min<int64_t>((n8 + 255) / 256, int64_t(num_sms()) * 8);
+  k_dequant_bf16<<<blocks, 256, 0, st>>>(codes, scales, T, heads, d, static_cast<__nv_bfloat16*>(out));
+  VLASIM_LAUNCH_CHECK();
+  return VLASIM_OK;
+}
+}  // namespace vlasim_host
 
 extern "C" int vlasim_fp8_quant_error_cuda(const void* d_x, const uint8_t* d_codes, const float* d_scales, int64_t T,
                                            int32_t heads, int32_t d, float* d_group_maxrel, double* d_group_sse,
@@ -226,19 +349,30 @@ extern "C" int vlasim_fp8_quant_error_cuda(const void* d_x, const uint8_t* d_cod
 }
 
 extern "C" int vlasim_fp8_quant_block_cuda(const void* d_x, int64_t T, int32_t heads, int32_t d, uint8_t* d_codes,
-                                           float* d_scales, vlasim_stream_t stream) {
+                                           float* d_scales, int32_t* d_status, uint32_t flags,
+                                           vlasim_stream_t stream) {
   using namespace vlasim_host;
   if (!d_x || !d_codes || !d_scales) return set_error(VLASIM_ECONFIG, "fp8_quant_block: null buffer");
   if (T < 1 || heads < 1 || d < 1 || T >= (int64_t(1) << 31))
     return set_error(VLASIM_ECONFIG, "fp8_quant_block: bad shape T=%lld heads=%d d=%d", (long long)T, heads, d);
+  if ((flags & VLASIM_SYNC_CHECK) && !d_status)
+    return set_error(VLASIM_ECONFIG, "fp8_quant_block: VLASIM_SYNC_CHECK needs a status buffer");
+  cudaStream_t st = as_stream(stream);
+  if (d_status) VLASIM_CUDA_TRY(cudaMemsetAsync(d_status, 0, 2 * sizeof(int32_t), st));
   const int64_t blocks = int64_t(heads) * ((T + 127) / 128) * ((d + 127) / 128);
   if (d % 8 == 0 && (reinterpret_cast<uintptr_t>(d_x) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_codes) & 7) == 0)
-    k_quant_block_v<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(d_x), int(T), heads, d,
-                                                          d_codes, d_scales);
+    k_quant_block_v<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_x), int(T), heads, d, d_codes,
+                                            d_scales, d_status);
   else
-    k_quant_block<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(d_x), int(T), heads, d,
-                                                        d_codes, d_scales);
+    k_quant_block<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_x), int(T), heads, d, d_codes, d_scales,
+                                          d_status);
   VLASIM_LAUNCH_CHECK();
+  if (flags & VLASIM_SYNC_CHECK) {
+    int32_t h[2];
+    VLASIM_CUDA_TRY(cudaMemcpyAsync(h, d_status, sizeof(h), cudaMemcpyDeviceToHost, st));
+    VLASIM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h[0]) return set_error(VLASIM_ECONFIG, "quantize: non-finite input at element %d (SPEC.md:585)", h[1]);
+  }
   return VLASIM_OK;
 }
 

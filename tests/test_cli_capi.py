@@ -25,7 +25,7 @@ def test_capi_library_exports_every_declared_symbol():
     assert len(syms) >= 15
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.vlasim_version() == 2
+    assert lib.vlasim_version() == 3
     assert set(syms) <= set(_lib.EXPORTED)
 
 
@@ -73,6 +73,7 @@ def test_cli_pack_matches_oracle(gpu, orc, tmp_path):
         assert [slot[i] for i in mem] == list(range(len(mem)))
 
 
+@pytest.mark.gpu
 def test_cli_pack_greedy_matches_oracle(gpu, orc, tmp_path):
     rng = np.random.default_rng(5)
     L = rng.integers(1, 3000, 300).tolist()

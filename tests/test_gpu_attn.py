@@ -114,6 +114,71 @@ def test_bwd_row_map_fuses_scatter(gpu, d):
     dq2, dk2, dv2 = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, row_map=perm)
     torch.cuda.synchronize()
     pl = perm.long()
-    # dK/dV rows are produced by exactly one CTA (deterministic); dQ accumulates with fp32 atomics
-    assert torch.equal(dv2[pl], dv) and torch.equal(dk2[pl], dk)
-    assert (dq2[pl].float() - dq.float()).abs().max().item() <= 1e-2 * max(1.0, dq.float().abs().max().item())
+    # every gradient row is produced by exactly one CTA with a fixed reduction order (no atomics):
+    # the redirected rows are bit-identical
+    assert torch.equal(dv2[pl], dv) and torch.equal(dk2[pl], dk) and torch.equal(dq2[pl], dq)
+
+
+SHARP = [  # (case index into CASES, Q/K multiplier): very sharp softmax — the running max grows by
+    # more than the lazy-rescale threshold (2^8) inside a row, and the bf16 rounded-up row max matters
+    (0, 8.0), (0, 16.0), (3, 16.0), (4, 8.0), (7, 16.0), (9, 8.0), (12, 16.0), (13, 8.0), (14, 16.0), (6, 16.0)]
+
+
+@pytest.mark.parametrize("case", range(len(SHARP)))
+def test_sharp_softmax_fwd_bwd(gpu, orc, case):
+    from paper_2603_11101_b200 import attention
+    ci, mult = SHARP[case]
+    L, H, Hkv, d, mask = CASES[ci]
+    q, k, v, do, cu = _inputs(L, H, Hkv, d, 200 + case)
+    q, k = (q.float() * mult).bfloat16(), (k.float() * mult).bfloat16()
+    prefix = torch.tensor([max(0, l // 3) for l in L], dtype=torch.int32, device="cuda") if mask == 2 else None
+    o, lse = attention.varlen_attn_fwd(q, k, v, cu, mask_mode=mask, prefix_len=prefix)
+    dq, dk, dv = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, mask_mode=mask, prefix_len=prefix)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()
+    pre = None if prefix is None else prefix.cpu().numpy()
+    ro, rlse = orc.mha_fwd(f(q), f(k), f(v), cu.cpu().numpy(), mask=mask, prefix=pre)
+    rdq, rdk, rdv = orc.mha_bwd(f(q), f(k), f(v), ro, f(do), cu.cpu().numpy(), mask=mask, prefix=pre)
+    assert _err(o, ro) < TOL_BF16, "o"
+    assert np.max(np.abs(lse.cpu().numpy() - rlse)) / max(1.0, np.max(np.abs(rlse))) < 1e-3, "lse"
+    for name, x, r in (("dv", dv, rdv), ("dk", dk, rdk), ("dq", dq, rdq)):
+        assert _err(x, r) < TOL_BF16, name
+
+
+@pytest.mark.parametrize("d", [64, 128, 256])
+def test_bwd_workspace_garbage_is_harmless(gpu, orc, d):
+    """The backward must not read workspace cells it did not write: a workspace
+    pre-filled with NaN and -inf gives the same, finite gradients as a zeroed one."""
+    from paper_2603_11101_b200 import attention
+    L = [300, 45, 129, 2, 77]
+    q, k, v, do, cu = _inputs(L, 3, 1, d, 31)
+    o, lse = attention.varlen_attn_fwd(q, k, v, cu)
+    res = []
+    for fill in (0.0, float("nan"), float("-inf")):
+        ws = attention.BwdWorkspace()
+        ws.buf = torch.full((4 << 20,), fill, dtype=torch.float32, device="cuda").view(torch.uint8)  # 16 MB
+        res.append(attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, workspace=ws))
+    torch.cuda.synchronize()
+    for g in res[0]:
+        assert torch.isfinite(g.float()).all()
+    for other in res[1:]:
+        assert all(torch.equal(x, y) for x, y in zip(res[0], other))
+
+
+def test_api_rejects_wrong_dtypes_and_devices(gpu):
+    from paper_2603_11101_b200 import attention
+    from paper_2603_11101_b200.errors import ConfigError
+    q, k, v, do, cu = _inputs([10, 20], 2, 2, 64, 1)
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_fwd(q.half(), k, v, cu)
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_fwd(q.float(), k, v, cu)
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_fwd(q, k, v, cu, mask_mode=2, prefix_len=torch.zeros(2, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_fwd(q, k, v, cu, mask_mode=2, prefix_len=torch.zeros(2, dtype=torch.int32))
+    o, lse = attention.varlen_attn_fwd(q, k, v, cu)
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_bwd(do, q, k, v, o, lse.double(), cu)
+    with pytest.raises(ConfigError):
+        attention.varlen_attn_bwd(do.half(), q, k, v, o, lse, cu)

@@ -1,6 +1,7 @@
-"""FP8 E4M3 path (config 4): per-block quantisation bit-exact with the oracle's fp32-quotient
-restatement, and the FP8 Q/K attention forward within the north_star
-FP8 tolerance (6e-2 of the fp64 reference on the original bf16 inputs)."""
+"""FP8 E4M3 path (config 4): per-block quantisation bit-exact with the oracle's exact restatement of
+the SPEC (the RNE code of the REAL quotient x·448/amax; non-finite input →
+ConfigError), and the FP8 Q/K attention forward / backward within the north_star FP8
+tolerance (6e-2 of the fp64 reference on the original bf16 inputs)."""
 import numpy as np
 import pytest
 import torch
@@ -17,7 +18,7 @@ def test_quant_block_bit_exact(gpu, orc, T, H, d, scale):
     if H > 1:
         x[:, 0, :] = 0  # an all-zero head → scale 1, codes 0
     codes, scales = fp8.quant_block(x)
-    rc, rs = orc.fp8_quant_block(x.float().cpu().numpy(), quotient_fp32=True)
+    rc, rs = orc.fp8_quant_block(x.float().cpu().numpy(), quotient_fp32=False)
     assert np.array_equal(scales.cpu().numpy(), rs)
     assert np.array_equal(codes.cpu().numpy(), rc)
     deq = fp8.dequant_block(codes, scales).cpu().numpy()
@@ -28,15 +29,68 @@ def test_quant_block_bit_exact(gpu, orc, T, H, d, scale):
     assert np.array_equal(deq, (ref * sc).astype(np.float32))
 
 
-def test_quant_matches_high_precision_quotient_almost_everywhere(gpu, orc):
-    """fp32 quotient vs the SPEC's real-valued quotient: codes differ only at rare rounding ties."""
+def test_quant_matches_real_quotient_everywhere(gpu, orc):
+    """Random normal blocks at several magnitudes: every code byte equals the SPEC's (exact quotient)."""
     from paper_2603_11101_b200 import fp8
     g = torch.Generator(device="cuda").manual_seed(5)
-    x = torch.randn(1024, 4, 128, device="cuda", generator=g).bfloat16()
+    x = (torch.randn(4096, 4, 128, device="cuda", generator=g) *
+         torch.logspace(-4, 4, 4096, device="cuda")[:, None, None]).bfloat16()
     codes, _ = fp8.quant_block(x)
     rc, _ = orc.fp8_quant_block(x.float().cpu().numpy(), quotient_fp32=False)
-    diff = np.count_nonzero(codes.cpu().numpy() != rc)
-    assert diff <= 1e-3 * rc.size
+    assert np.array_equal(codes.cpu().numpy(), rc)
+
+
+def _tie_block(amax, rng):
+    """A 128×128 block whose amax is `amax` and whose other elements sit exactly on E4M3 midpoints of
+    the real quotient x·448/amax (x = m·amax/448 when that is a bf16), or one bf16 ulp either side."""
+    vals = []
+    for E in range(-9, 9):
+        for k in (17, 19, 21, 23, 25, 27, 29, 31):  # midpoints 2^(E-4)·k of the binade [2^E, 2^(E+1))
+            x = np.float64(k) * 2.0 ** (E - 4) * amax / 448.0
+            xb = torch.tensor([x], dtype=torch.float64).bfloat16()
+            if float(xb) == x and 0 < x < amax:
+                b = xb.view(torch.int16)
+                vals += [xb, (b + 1).view(torch.bfloat16), (b - 1).view(torch.bfloat16)]
+    v = torch.cat(vals).float().numpy() if vals else np.zeros(1, np.float32)
+    blk = rng.choice(v, size=128 * 128) * rng.choice([-1.0, 1.0], size=128 * 128)
+    blk[0] = amax
+    return blk.astype(np.float32).reshape(128, 128)
+
+
+def test_quant_exact_ties_and_neighbours(gpu, orc):
+    """Exact ties of the real quotient (decided to the even code) and their bf16 neighbours, for block
+    maxima whose scale amax/448 is not exact in fp32: the fp32 quotient alone gets some of these wrong."""
+    from paper_2603_11101_b200 import fp8
+    rng = np.random.default_rng(1)
+    # the two bf16 mantissas whose fp32 scale RN(amax / 448) moves some exact ties off their midpoint
+    amaxes = [1.78125, 1.9375, 1.78125 * 2 ** 10, 1.9375 * 2 ** -12, 1.78125 * 2 ** -30, 1.9375 * 2 ** 40, 5.0, 3.0]
+    x = np.concatenate([_tie_block(a, rng) for a in amaxes], 0)[:, None, :]
+    xt = torch.from_numpy(x).bfloat16()
+    assert torch.equal(xt.float(), torch.from_numpy(x))  # exactly representable
+    codes, scales = fp8.quant_block(xt.cuda())
+    rc, rs = orc.fp8_quant_block(x, quotient_fp32=False)
+    assert np.array_equal(scales.cpu().numpy(), rs)
+    assert np.array_equal(codes.cpu().numpy(), rc)
+    rc32, _ = orc.fp8_quant_block(x, quotient_fp32=True)
+    assert np.count_nonzero(rc32 != rc) > 0  # the case the exact decision exists for
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), float("-inf")])
+def test_quant_non_finite_is_config_error(gpu, bad):
+    """non-finite input → error (ConfigError naming the element)."""
+    from paper_2603_11101_b200 import fp8
+    from paper_2603_11101_b200.errors import ConfigError
+    x = torch.randn(300, 2, 128, device="cuda").bfloat16()
+    x[257, 1, 77] = bad
+    with pytest.raises(ConfigError, match=str((257 * 2 + 1) * 128 + 77)):
+        fp8.quant_block(x)
+    y = torch.randn(100, 1, 100, device="cuda").bfloat16()  # scalar (unaligned-d) kernel
+    y[5, 0, 3] = bad
+    with pytest.raises(ConfigError, match="non-finite"):
+        fp8.quant_block(y)
+    status = torch.zeros(2, dtype=torch.int32, device="cuda")
+    fp8.quant_block(x, check_finite=False, status=status)  # asynchronous: the error stays on device
+    assert status.tolist() == [2, (257 * 2 + 1) * 128 + 77]
 
 
 @pytest.mark.parametrize("L,H,Hkv,mask", [([100, 28, 300, 5, 1, 130], 2, 2, 0), ([600, 40, 260], 4, 2, 2),
@@ -52,7 +106,7 @@ def test_fp8qk_attention_within_tolerance(gpu, orc, L, H, Hkv, mask):
     prefix = torch.tensor([l // 3 for l in L], dtype=torch.int32, device="cuda") if mask == 2 else None
     qc, qs = fp8.quant_block(q)
     kc, ks = fp8.quant_block(k)
-    o8, _ = fp8.varlen_attn_fwd_fp8qk(qc, qs, kc, ks, v, cu, mask_mode=mask, prefix_len=prefix)
+    o8, lse8 = fp8.varlen_attn_fwd_fp8qk(qc, qs, kc, ks, v, cu, mask_mode=mask, prefix_len=prefix)
     o16, _ = attention.varlen_attn_fwd(q, k, v, cu, mask_mode=mask, prefix_len=prefix)
     torch.cuda.synchronize()
     pre = None if prefix is None else prefix.cpu().numpy()
@@ -62,6 +116,15 @@ def test_fp8qk_attention_within_tolerance(gpu, orc, L, H, Hkv, mask):
     err16 = np.max(np.abs(o16.float().cpu().numpy() - ro)) / max(1.0, np.max(np.abs(ro)))
     assert err8 < 6e-2, err8
     assert err16 < 2e-2, err16
+    # FP8 backward (gradients of the FP8 forward) within the FP8 tolerance of the fp64 reference
+    do = torch.randn(T, H, d, device="cuda", generator=g).bfloat16()
+    dq8, dk8, dv8 = fp8.varlen_attn_bwd_fp8qk(do, qc, qs, kc, ks, v, o8, lse8, cu, mask_mode=mask, prefix_len=prefix)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()
+    rdq, rdk, rdv = orc.mha_bwd(f(q), f(k), f(v), ro, f(do), cu.cpu().numpy(), mask=mask, prefix=pre)
+    for name, x, r in (("dq", dq8, rdq), ("dk", dk8, rdk), ("dv", dv8, rdv)):
+        e = np.max(np.abs(f(x) - r)) / max(1.0, np.max(np.abs(r)))
+        assert e < 6e-2, (name, e)
 
 
 # ---- quant_error
@@ -94,8 +157,8 @@ def test_quant_error_known_answers(gpu):
 
 
 def test_quant_block_quotient_stress(gpu, orc):
-    """The block quantiser's reciprocal + one-correction quotient against the oracle's correctly
-    rounded fp32 division: 64 blocks, each with its own amax (hence scale) and 16383 other
+    """The block quantiser (reciprocal + one-correction quotient, then the exact midpoint decision)
+    against the oracle's exact real quotient: 64 blocks, each with its own amax (hence scale) and 16383 other
     elements drawn uniformly over the bf16 bit patterns below it (every exponent range)."""
     from paper_2603_11101_b200 import fp8
     g = torch.Generator(device="cpu").manual_seed(7)
@@ -111,6 +174,6 @@ def test_quant_block_quotient_stress(gpu, orc):
         x[128 * b:128 * (b + 1), 0, :] = bits.to(torch.int16).view(torch.bfloat16).view(128, 128)
     xc = x.cuda()
     codes, scales = fp8.quant_block(xc)
-    rc, rs = orc.fp8_quant_block(x.float().numpy(), quotient_fp32=True)
+    rc, rs = orc.fp8_quant_block(x.float().numpy(), quotient_fp32=False)
     assert np.array_equal(scales.cpu().numpy(), rs)
     assert np.array_equal(codes.cpu().numpy(), rc)

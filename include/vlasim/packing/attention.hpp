@@ -23,6 +23,7 @@ struct SmallTensor {
 };
 
 // softmax(q·kᵀ/√d)·v, one head (= packed_attention with one segment).
+// model_dim (cols) 1..256: columns are zero-padded to the kernels' head_dim on the device.
 SmallTensor reference_attention(const SmallTensor& q, const SmallTensor& k, const SmallTensor& v);
 
 // per-segment attention over a packed stream; no cross-segment interaction.

@@ -55,6 +55,7 @@ def lib():
             "oracle_fp8_quant_block": [V, L, L, L, I, V, V],
             "oracle_e4m3_encode": [V, L, V],
             "oracle_e4m3_values": [V],
+            "oracle_gen_lengths": [C.c_uint64, C.c_char_p, I, L, D, D, D, V],
         }
         for name, args in sigs.items():
             fn = getattr(_lib, name)
@@ -277,3 +278,41 @@ def fp8_quant_error(x, codes, scales):
                 gsse[h, bt, bd] = sq[sl].sum()
                 gcnt[h, bt, bd] = sq[sl].size
     return gmax, gsse, gcnt, float(gmax.max()), float(gsse.sum() / gcnt.sum())
+
+
+# ------------------------------------------------------------------ synthetic inputs (CPU arms)
+def gen_lengths(n, dist=0, p1=16, p2=512, p3=0, seed=42, label="lengths"):
+    """Sample lengths on the reference's rng.hpp (make_rng(seed, label, 0)), same as the bench inputs."""
+    out = np.empty(n, np.int32)
+    _chk(lib().oracle_gen_lengths(seed, label.encode(), dist, n, p1, p2, p3, _p(out, i32p)))
+    return out
+
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(x):
+    z = (x + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _derive_seed(root, label, index=0):
+    h = (root ^ 0x8824A7155D1E9E31) & _M64
+    for ch in label.encode():
+        h = _splitmix64(h ^ ch)
+    return _splitmix64(h ^ _splitmix64(index))
+
+
+def synthetic_values(count, label, root=42, offset=0):
+    """Counter-based bench values: x[i] = (top8(splitmix64(seed ^ i)) − 128) / 128 with
+    seed = derive_seed(root, label, 0) (rng.hpp:9-24); float32, exactly bf16-representable."""
+    seed = np.uint64(_derive_seed(root, label))
+    i = np.arange(offset, offset + count, dtype=np.uint64) ^ seed
+    with np.errstate(over="ignore"):
+        z = i + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return ((z >> np.uint64(56)).astype(np.int32) - 128).astype(np.float32) / 128.0

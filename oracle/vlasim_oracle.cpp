@@ -14,6 +14,7 @@
 #include <thread>
 
 #include "vlasim/util/errors.hpp"
+#include "vlasim/util/rng.hpp"
 
 namespace vlasim::oracle {
 
@@ -640,6 +641,35 @@ int oracle_e4m3_encode(const double* x, std::int64_t n, std::uint8_t* codes) {
     for (std::int64_t i = 0; i < n; ++i) codes[i] = vlasim::oracle::e4m3_encode(x[i]);
   });
 }
+// Sample lengths on the reference's seeding API (rng.hpp:28-49), the same conventions as the bench
+// inputs: dist 0 uniform_int(p1, p2); 1 truncated geometric(p1, max p2) by inverse
+// CDF on uniform01; 2 GR00T-like 64·uniform_int(1,2) + uniform_int(16,64); 3 π0.5 512 +
+// uniform_int(p1, p2) + p3.  Lets the CPU arms generate their inputs without the product library.
+int oracle_gen_lengths(std::uint64_t root_seed, const char* label, int dist, std::int64_t n, double p1, double p2,
+                       double p3, std::int32_t* out) {
+  return guarded([&] {
+    auto rng = vlasim::make_rng(root_seed, std::string_view(label), 0);
+    for (std::int64_t i = 0; i < n; ++i) {
+      std::int64_t l = 0;
+      if (dist == 0) {
+        l = vlasim::uniform_int(rng, std::int64_t(p1), std::int64_t(p2));
+      } else if (dist == 1) {
+        const double tail = 1.0 - std::pow(1.0 - p1, p2);
+        double k = std::ceil(std::log1p(-vlasim::uniform01(rng) * tail) / std::log1p(-p1));
+        l = std::int64_t(std::min(std::max(k, 1.0), p2));
+      } else if (dist == 2) {
+        const std::int64_t views = vlasim::uniform_int(rng, 1, 2);
+        l = 64 * views + vlasim::uniform_int(rng, 16, 64);
+      } else if (dist == 3) {
+        l = 512 + vlasim::uniform_int(rng, std::int64_t(p1), std::int64_t(p2)) + std::int64_t(p3);
+      } else {
+        throw vlasim::ConfigError("gen_lengths: unknown distribution");
+      }
+      out[i] = std::int32_t(l);
+    }
+  });
+}
+
 int oracle_e4m3_values(double* out /* [127] */) {
   return guarded([&] {
     auto v = vlasim::oracle::e4m3_values();

@@ -249,15 +249,25 @@ SmallTensor packed_attention(const SmallTensor& q, const SmallTensor& k, const S
   for (std::size_t i = 1; i < cu.size(); ++i)
     if (cu[i] <= cu[i - 1]) throw ConfigError("packed_attention: cu_seqlens not strictly increasing");
   const std::int64_t T = q.rows, d = q.cols;
-  if (d != 64 && d != 128 && d != 256) throw ConfigError("packed_attention: model_dim must be 64, 128 or 256");
-  std::vector<std::uint16_t> hq(T * d), hk(T * d), hv(T * d), ho(T * d);
-  for (std::int64_t i = 0; i < T * d; ++i) {
-    hq[i] = to_bf16(q.data[i]);
-    hk[i] = to_bf16(k.data[i]);
-    hv[i] = to_bf16(v.data[i]);
-  }
+  if (d < 1 || T < 1) throw ConfigError("packed_attention: empty tensors");
+  if (std::int64_t(q.data.size()) != T * d || std::int64_t(k.data.size()) != T * d ||
+      std::int64_t(v.data.size()) != T * d)
+    throw ConfigError("packed_attention: data size does not match rows x cols");
+  // Any model_dim up to 256: the columns are zero-padded to the kernels' head_dim (64 / 128 / 256),
+  // which leaves q·kᵀ unchanged and adds zero columns to p·v that are sliced off; the softmax
+  // scale stays 1/sqrt(model_dim).
+  if (d > 256) throw ConfigError("packed_attention: model_dim " + std::to_string(d) + " > 256 (one head of the "
+                                 "sm_100a kernels; split heads instead)");
+  const std::int64_t D = d <= 64 ? 64 : (d <= 128 ? 128 : 256);
+  std::vector<std::uint16_t> hq(T * D, 0), hk(T * D, 0), hv(T * D, 0), ho(T * D);
+  for (std::int64_t r = 0; r < T; ++r)
+    for (std::int64_t c = 0; c < d; ++c) {
+      hq[r * D + c] = to_bf16(q.data[r * d + c]);
+      hk[r * D + c] = to_bf16(k.data[r * d + c]);
+      hv[r * D + c] = to_bf16(v.data[r * d + c]);
+    }
   std::vector<std::int32_t> hcu(cu.begin(), cu.end());
-  DevBuf<std::uint16_t> dq(T * d), dk(T * d), dv(T * d), dout(T * d);
+  DevBuf<std::uint16_t> dq(T * D), dk(T * D), dv(T * D), dout(T * D);
   DevBuf<float> dlse(T);
   DevBuf<std::int32_t> dcu(hcu.size());
   cuda_check(cudaMemcpy(dq.p, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice), "cudaMemcpy");
@@ -275,14 +285,15 @@ SmallTensor packed_attention(const SmallTensor& q, const SmallTensor& k, const S
   a.total_tokens = T;
   a.num_heads = 1;
   a.num_kv_heads = 1;
-  a.head_dim = std::int32_t(d);
+  a.head_dim = std::int32_t(D);
   a.mask_mode = VLASIM_MASK_BIDIR;
   a.softmax_scale = float(1.0 / std::sqrt(double(d)));
   VarlenAttention attn;
   attn.forward(a, nullptr);
   cuda_check(cudaMemcpy(ho.data(), dout.p, ho.size() * 2, cudaMemcpyDeviceToHost), "cudaMemcpy");
   SmallTensor o{T, d, std::vector<double>(std::size_t(T * d))};
-  for (std::int64_t i = 0; i < T * d; ++i) o.data[i] = from_bf16(ho[i]);
+  for (std::int64_t r = 0; r < T; ++r)
+    for (std::int64_t c = 0; c < d; ++c) o.data[r * d + c] = from_bf16(ho[r * D + c]);
   return o;
 }
 

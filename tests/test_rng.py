@@ -46,3 +46,13 @@ def test_product_length_generator_matches_reference_stream():
     from paper_2603_11101_b200.synthetic import gen_lengths
     assert gen_lengths(64, 0, 16, 512).tolist() == GOLD["uniform_int_42_lengths_16_512"]
     assert gen_lengths(16, 0, 16, 512, seed=7).tolist() == GOLD["uniform_int_7_lengths_16_512"]
+
+
+def test_oracle_and_product_generate_identical_inputs():
+    """The CPU arms (oracle) and the GPU bench (product C-ABI) draw identical lengths and values."""
+    import numpy as np
+    from oracle import oracle as orc
+    from paper_2603_11101_b200 import synthetic
+    for dist, p in ((0, (16, 512, 0)), (1, (0.02, 500, 0)), (2, (0, 0, 0)), (3, (16, 200, 50))):
+        assert np.array_equal(orc.gen_lengths(2000, dist, *p), synthetic.gen_lengths(2000, dist, *p))
+    assert np.array_equal(orc.synthetic_values(4096, "k", offset=12345), synthetic.values_np(4096, "k", offset=12345))

@@ -2,28 +2,34 @@
 """bench.py — effective (non-pad) tokens/s and TFLOPS of the packing + varlen attention fwd+bwd step.
 
 Workload (BASELINE.json configs[1], "GR00T-N1.5 Eagle-backbone shape"): per GPU, 512 samples with
-lengths uniform_int(16, 512) from make_rng(42, "lengths", rank) (rng.hpp), packed to 8192-token bins
-by the GPU FFD packer; 16 heads × d = 128, bf16, bidirectional block-diagonal attention, fwd + bwd.
-One step = GPU pack → per-segment source offsets (seg_src) → attention fwd → attention bwd.  The
-gather of Q/K/V into the packed stream and the scatter of O/dQ/dK/dV back to sample order are
-folded into the attention kernels' TMA coordinates (--layout fused, default); --layout packed runs
-the explicit 16-B row-gather kernels + a materialised packed stream instead (identical results,
-tests/test_gpu_seg_src.py).  Inputs (≈2.3 GB per GPU) are larger than L2 (126 MB).
+lengths uniform_int(16, 512) from make_rng(42 + 1000·rank, "lengths", 0) (rng.hpp), packed to
+8192-token bins by the GPU FFD packer; 16 heads × d = 128, bf16, bidirectional block-diagonal
+attention, fwd + bwd.  One step, identical at every N:
+
+    [N > 1: NCCL all-gather of the per-rank lengths — the path's only collective]
+    GPU FFD over the global lengths → device LPT shard plan (this rank's bins, cu_seqlens, seg_src)
+    → attention fwd → attention bwd over this rank's sample-major rows (gather / scatter folded into
+    the kernels' TMA coordinates through seg_src).
+
+Everything is stream-ordered with no host round trip; at N = 1 the step is replayed as a CUDA graph
+and the packing of batch i+1 runs on a side stream (one SM) beside batch i's attention.  Inputs
+(≈2.2 GB per GPU) are larger than L2 (126 MB).
+
+The default run prints ONE JSON line (config 2).  It also measures, in the same run on rank 0 at
+N = 1, the other BASELINE configs under "configs": config 1 (64 × U[16,512], 2048-token bins, H8
+d64), config 3 (π0.5: H8 Hkv1 d256, prefix mask), config 4 (E4M3 Q/K: quantiser + FP8 forward /
+backward vs bf16; FP8 dense peak measured with torch._scaled_mm) and config 5 (the 1M-sample
+packer: samples/s and HBM GB/s; LPT shard balance at 1/2/4/8 ranks).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dist uniform|groot]
-
-N > 1 (torchrun): the global batch is N × 512 samples; every rank receives the global lengths by
-one NCCL all-gather (the only collective), packs them identically, and takes its share of the bins
-from the length-balanced LPT assignment (weak scaling; no collective on the attention path).
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
-import math
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -46,6 +52,9 @@ H, HKV, D = 16, 16, 128
 SAMPLES_PER_GPU = 512
 CAPACITY = 8192
 METRIC = "effective tokens/sec & TFLOPS (non-pad) varlen attn fwd+bwd, 1/2/4/8 B200"
+# our kernel launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
+# shard plan 1, fwd 3 (spans, tiles, attention), bwd 4 (pre, tiles, dK/dV, dQ)
+LAUNCHES_PER_STEP = 22
 
 
 def parse():
@@ -58,31 +67,68 @@ def parse():
     ap.add_argument("--samples", type=int, default=SAMPLES_PER_GPU)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 1/3/4/5 measurements")
     ap.add_argument("--cpu-samples", type=int, default=48)
     ap.add_argument("--no-graph", action="store_true", help="launch the step's kernels directly (no CUDA graph)")
     ap.add_argument("--pipeline", default="on", choices=["on", "off"],
-                    help="on: the GPU packer of batch i+1 runs on a side stream on one SM while batch i's attention "
-                         "takes the other SMs (sm_budget); off: pack and attention strictly in sequence")
-    ap.add_argument("--layout", default="fused", choices=["fused", "packed"],
-                    help="fused: attention reads / writes sample-major rows through seg_src; packed: explicit "
-                         "gather into the packed stream + row_map scatter")
+                    help="on (N = 1): the packing of batch i+1 runs on a side stream on one SM while batch i's "
+                         "attention takes the other SMs (sm_budget); off: pack and attention in sequence")
     return ap.parse_args()
 
 
-def lengths_for(rank, n, dist):
-    from paper_2603_11101_b200.synthetic import DIST_GR00T, DIST_UNIFORM, gen_lengths
+def lengths_for(rank, n, dist, gen):
+    """gen = synthetic.gen_lengths (product C-ABI) or oracle.gen_lengths (CPU arms): identical draws."""
     if dist == "groot":
-        return gen_lengths(n, DIST_GR00T, label="lengths", seed=42 + 1000 * rank)
-    return gen_lengths(n, DIST_UNIFORM, 16, 512, label="lengths", seed=42 + 1000 * rank)
+        return gen(n, 2, 0, 0, 0, seed=42 + 1000 * rank)
+    return gen(n, 0, 16, 512, 0, seed=42 + 1000 * rank)
+
+
+# ---------------------------------------------------------------------------- algorithmic work
+def visible_pairs(L, mask=0, prefix=None):
+    L = np.asarray(L, np.float64)
+    if mask == 0:
+        return float(np.sum(L * L))
+    if mask == 1:
+        return float(np.sum(L * (L + 1) / 2))
+    P = np.asarray(prefix, np.float64)
+    S = L - P
+    return float(np.sum(P * P + S * P + S * (S + 1) / 2))
+
+
+def attn_bytes(T, H_, Hkv_, d, qk_bytes=2):
+    """Algorithmic HBM bytes: every tensor read or written once (fwd: Q,K,V in, O + LSE out; bwd: Q,K,V,
+    O,dO + LSE in, dQ,dK,dV out)."""
+    row_q, row_kv = H_ * d * 2, Hkv_ * d * 2
+    fwd = T * (H_ * d * qk_bytes + Hkv_ * d * qk_bytes + row_kv + row_q + 4 * H_)
+    bwd = T * (2 * row_q + 2 * row_kv + 2 * row_q + 4 * H_) + T * (row_q + 2 * row_kv)
+    return fwd, bwd
+
+
+def roofline(flops, nbytes, ms, tensor_peak, label):
+    """min(tensor, HBM × intensity) roofline of one launch (or pass): the bound is whichever floor is
+    higher; `frac` = achieved / the peak of that bound; both fractions are reported."""
+    t_tensor = flops / (tensor_peak * 1e12)
+    t_hbm = nbytes / (PEAKS["hbm_gbs"] * 1e9)
+    tf = flops / (ms / 1e3) / 1e12
+    gbs = nbytes / (ms / 1e3) / 1e9
+    hbm_bound = t_hbm > t_tensor
+    return {"kernel": label, "bound": "hbm" if hbm_bound else "tensor",
+            "achieved": gbs if hbm_bound else tf, "peak": PEAKS["hbm_gbs"] if hbm_bound else tensor_peak,
+            "unit": "GB/s" if hbm_bound else "TFLOP/s",
+            "frac": (gbs / PEAKS["hbm_gbs"]) if hbm_bound else (tf / tensor_peak),
+            "tflops": tf, "frac_of_tensor_peak": tf / tensor_peak, "gbs": gbs,
+            "frac_of_hbm_peak": gbs / PEAKS["hbm_gbs"], "algorithmic_flops": flops, "algorithmic_bytes": nbytes,
+            "intensity_flop_per_byte": flops / nbytes,
+            "attainable_tflops": min(tensor_peak, PEAKS["hbm_gbs"] * flops / nbytes / 1e3),
+            "frac_of_attainable": tf / min(tensor_peak, PEAKS["hbm_gbs"] * flops / nbytes / 1e3), "ms": ms}
 
 
 class Clocks:
-    """NVML sampler running during the timed region (the B200_PROFILING.md clocks line):
-    SM clock, max SM clock and the active clock-event (throttle) reasons."""
+    """NVML sampler running during the timed region (the B200_PROFILING.md clocks line)."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
-    def __init__(self, index, period=0.05):
+    def __init__(self, index, period=0.02):
         self.index, self.period, self.rows, self.stop = index, period, [], threading.Event()
 
     def __enter__(self):
@@ -102,9 +148,8 @@ class Clocks:
         nv = self.nv
         while not self.stop.is_set():
             try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append((sm, rs))
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
             except Exception:
                 pass
             time.sleep(self.period)
@@ -124,58 +169,58 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
-def bwd_traffic():
-    """DRAM bytes (read + write) per backward step (3 launches) from the committed ncu --set full
-    capture (profiles/*/ncu_traffic.json); None when no capture is present."""
+def ncu_traffic():
+    """DRAM bytes (read + write) per launch of the backward / forward kernels from the newest committed
+    ncu --set full capture (profiles/rNN/ncu_traffic.json); (None, None) when absent."""
     import glob
-    files = sorted(glob.glob(str(Path(__file__).parent / "profiles" / "*" / "ncu_traffic.json")))
+    files = sorted(glob.glob(str(ROOT / "profiles" / "*" / "ncu_traffic.json")))
     if not files:
         return None, None
     ks = json.load(open(files[-1]))["kernels"]
-    tot = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in ks.items() if k.startswith("k_bwd"))
-    return tot, str(Path(files[-1]).relative_to(Path(__file__).parent))
+    return ks, str(Path(files[-1]).relative_to(ROOT))
 
 
+# ---------------------------------------------------------------------------- CPU arms (oracle)
 def cpu_baseline(Ls, threads):
-    """The reference's CPU path (oracle restatement of SPEC.md:502-509 + closed-form bwd), fp32,
-    on a bounded sample of the step's samples; returns (tokens/s, seconds, sample description)."""
+    """The reference's CPU path (oracle restatement of SPEC.md:437-445 + 502-509 + the closed-form
+    backward), fp32, on a bounded sample of the step's samples; returns (tokens/s, seconds, sample)."""
     from oracle import oracle as orc
-    from paper_2603_11101_b200.synthetic import values_np
     T = int(np.sum(Ls))
     cu = np.concatenate([[0], np.cumsum(Ls)]).astype(np.int32)
-    q = values_np(T * H * D, "q").reshape(T, H, D)
-    k = values_np(T * HKV * D, "k").reshape(T, HKV, D)
-    v = values_np(T * HKV * D, "v").reshape(T, HKV, D)
-    do = values_np(T * H * D, "do").reshape(T, H, D)
-    bins, *_ = orc.pack(np.asarray(Ls, np.int64), CAPACITY, 0)
+    q = orc.synthetic_values(T * H * D, "q").reshape(T, H, D)
+    k = orc.synthetic_values(T * HKV * D, "k").reshape(T, HKV, D)
+    v = orc.synthetic_values(T * HKV * D, "v").reshape(T, HKV, D)
+    do = orc.synthetic_values(T * H * D, "do").reshape(T, H, D)
     t0 = time.perf_counter()
-    orc.pack(np.asarray(Ls, np.int64), CAPACITY, 0)
+    orc.pack(np.asarray(Ls, np.int64), CAPACITY, 1)
     o, lse = orc.mha_fwd(q, k, v, cu, dtype=np.float32, threads=threads)
     orc.mha_bwd(q, k, v, o, do, cu, dtype=np.float32, threads=threads)
     dt = time.perf_counter() - t0
-    return T / dt, dt, f"{len(Ls)} samples ({T} tokens) of the step's batch, fp32 fwd+bwd, {threads} threads"
+    return T / dt, dt, f"{len(Ls)} samples ({T} tokens) of the step's batch, FFD + fp32 fwd+bwd, {threads} threads"
 
 
 def run_reference(a, rank, world):
-    """--impl reference: the reference's CPU implementation (oracle port; the reference ships no code)."""
+    """--impl reference: the reference's CPU implementation of the path (the oracle port: the reference
+    ships no code), all host threads, bounded sample; no product code is loaded."""
     if rank != 0:
         return
+    from oracle import oracle as orc
     threads = len(os.sched_getaffinity(0))
-    Ls = lengths_for(0, a.samples, a.dist)[: a.cpu_samples]
+    Ls = lengths_for(0, a.samples, a.dist, orc.gen_lengths)[: a.cpu_samples]
     vals = []
     for i in range(a.warmup + a.steps):
         tps, dt, desc = cpu_baseline(Ls, threads)
         if i >= a.warmup:
             vals.append(tps)
-        if sum(vals) and len(vals) >= 1 and dt * (a.steps - len(vals)) > 240:
+        if vals and dt * (a.steps - len(vals)) > 240:
             break  # keep the whole run within a few minutes
     v = statistics.mean(vals)
-    pairs = float(np.sum(np.asarray(Ls, np.float64) ** 2))
+    pairs = visible_pairs(Ls)
     toks = float(np.sum(Ls))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
             "steps": len(vals), "warmup": a.warmup, "ms_per_step": 1e3 * toks / v, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config2 GR00T-N1.5 shape: U[16,512] lengths, 8192-token bins, H16 d128 bf16 "
+            "config": {"workload": "config2 GR00T-N1.5 shape: U[16,512] lengths, 8192-token bins, H16 d128 "
                                    "bidirectional fwd+bwd (CPU: bounded sample)", "samples": len(Ls),
                        "tflops": 3.5 * 4 * D * H * pairs * v / toks / 1e12},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc},
@@ -183,6 +228,189 @@ def run_reference(a, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------- GPU timing helpers
+def event_ms(fn, iters, stream, warm=3):
+    import torch
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def boundary_ms(fn, nev, iters, stream, warm=2):
+    """Per-kernel device times of one attention call from the C-ABI's kernel-boundary events
+    (vlasim_set_boundary_events), median over iters: [t(e1) − t(e0), t(e2) − t(e1), …]."""
+    import torch
+    from paper_2603_11101_b200 import _lib
+    L = _lib.lib()
+    for _ in range(warm):
+        fn()
+    rows = []
+    for _ in range(iters):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        arr = (C.c_void_p * nev)(*[e.cuda_event for e in evs])
+        _lib.check(L.vlasim_set_boundary_events(arr, nev), "boundary events")
+        fn()
+        got = L.vlasim_boundary_count()
+        _lib.check(L.vlasim_set_boundary_events(None, 0), "boundary events")
+        torch.cuda.synchronize()
+        assert got == nev, f"expected {nev} kernel-boundary events, got {got}"
+        rows.append([evs[i].elapsed_time(evs[i + 1]) for i in range(nev - 1)])
+    return [statistics.median(r[i] for r in rows) for i in range(nev - 1)]
+
+
+def fp8_dense_peak(dev):
+    """FP8 (e4m3) dense tensor peak on this GPU: torch._scaled_mm 8192³, best of 10 (burst)."""
+    import torch
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev).to(torch.float8_e4m3fn)
+        b = torch.randn(n, n, device=dev).to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device=dev)
+        for _ in range(3):
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        st = torch.cuda.current_stream()
+        best = min(event_ms(lambda: torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16),
+                            1, st, warm=0) for _ in range(10))
+        return 2 * n ** 3 / (best / 1e3) / 1e12
+    except Exception as e:  # pragma: no cover
+        return None
+
+
+# ---------------------------------------------------------------------------- configs 1 / 3 / 4 / 5
+def measure_configs(dev, iters=10):
+    import torch
+    from paper_2603_11101_b200 import attention, dist as vdist, fp8, packing, synthetic
+    st = torch.cuda.current_stream()
+    out = {}
+
+    def attn_case(n, dist, p, cap, H_, Hkv_, d, mask):
+        L = synthetic.gen_lengths(n, dist, *p)
+        plan = packing.pack_ffd(L, cap)
+        T = int(L.sum())
+        Lp = L[plan.member_ids[:n].cpu().numpy()]
+        prefix_h = (Lp - 50).astype(np.int32) if mask == 2 else None
+        prefix = torch.from_numpy(prefix_h).to(dev) if mask == 2 else None
+        seg = packing.seg_src(plan)
+        q = synthetic.fill_bf16(torch.empty(T, H_, d, dtype=torch.bfloat16, device=dev), "q")
+        k = synthetic.fill_bf16(torch.empty(T, Hkv_, d, dtype=torch.bfloat16, device=dev), "k")
+        v = synthetic.fill_bf16(torch.empty(T, Hkv_, d, dtype=torch.bfloat16, device=dev), "v")
+        do = synthetic.fill_bf16(torch.empty(T, H_, d, dtype=torch.bfloat16, device=dev), "do")
+        o, lse = torch.empty_like(q), torch.empty(H_, T, dtype=torch.float32, device=dev)
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        ws, fws = attention.BwdWorkspace(), attention.BwdWorkspace()
+        cu = plan.cu_seqlens
+        pairs = visible_pairs(Lp, mask, prefix_h)
+        fl = 4.0 * d * H_ * pairs
+
+        def fwd():
+            attention.varlen_attn_fwd(q, k, v, cu, mask_mode=mask, prefix_len=prefix, out=o, lse=lse, seg_src=seg,
+                                      workspace=fws)
+
+        def bwd():
+            attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, mask_mode=mask, prefix_len=prefix, dq=dq, dk=dk, dv=dv,
+                                      seg_src=seg, workspace=ws)
+
+        tf, tb = event_ms(fwd, iters, st), event_ms(bwd, iters, st)
+        kf = boundary_ms(fwd, 3, iters, st)
+        kb = boundary_ms(bwd, 5, iters, st)
+        fb, bb = attn_bytes(T, H_, Hkv_, d)
+        res = {"samples": n, "tokens": T, "bins": plan.num_bins(), "heads": H_, "kv_heads": Hkv_, "head_dim": d,
+               "mask": ["bidirectional", "causal", "prefix"][mask], "pairs": pairs, "fwd_ms": tf, "bwd_ms": tb,
+               "fwd_tflops": fl / tf / 1e9, "bwd_tflops": 2.5 * fl / tb / 1e9,
+               "fwd_bwd_tflops": 3.5 * fl / (tf + tb) / 1e9,
+               "fwd_bwd_frac_of_tensor_peak": 3.5 * fl / (tf + tb) / 1e9 / PEAKS["bf16_tflops"],
+               "kernel_ms": {"fwd_prep": kf[0], "fwd_attention": kf[1], "bwd_pre": kb[0], "bwd_tiles": kb[1],
+                             "bwd_dkdv": kb[2], "bwd_dq": kb[3]},
+               "roofline_fwd": roofline(fl, fb, tf, PEAKS["bf16_tflops"], "forward"),
+               "roofline_bwd": roofline(2.5 * fl, bb, tb, PEAKS["bf16_tflops"], "backward"),
+               "l2": "inputs larger than L2" if 4 * T * H_ * d * 2 > 126e6 else "inputs fit in L2 (toy size)"}
+        return res, (q, k, v, do, o, lse, cu, seg, fl, T)
+
+    out["config1"], _ = attn_case(64, synthetic.DIST_UNIFORM, (16, 512), 2048, 8, 8, 64, 0)
+    out["config1"]["workload"] = "64 x U[16,512], 2048-token bins, H8 d64, bf16 fwd+bwd (BASELINE: fp32 fwd on CPU)"
+    out["config3"], _ = attn_case(256, synthetic.DIST_PI05, (16, 200, 50), 8192, 8, 1, 256, 2)
+    out["config3"]["workload"] = ("pi0.5: 256 x (2x256 views + U[16,200] text + 50 action), prefix mask, H8 Hkv1 "
+                                  "d256 bf16 fwd+bwd")
+    # config 4: E4M3 Q/K on the config-2 inputs
+    c2, (q, k, v, do, o, lse, cu, seg, fl, T) = attn_case(512, synthetic.DIST_UNIFORM, (16, 512), 8192, 16, 16, 128, 0)
+    qc, kc = torch.empty(q.shape, dtype=torch.uint8, device=dev), torch.empty(k.shape, dtype=torch.uint8, device=dev)
+    qs = torch.empty(16, (T + 127) // 128, 1, dtype=torch.float32, device=dev)
+    ks = torch.empty_like(qs)
+
+    def quant():
+        fp8.quant_block(q, codes=qc, scales=qs, check_finite=False)
+        fp8.quant_block(k, codes=kc, scales=ks, check_finite=False)
+
+    o8, l8 = torch.empty_like(o), torch.empty_like(lse)
+    dq8, dk8, dv8 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ws8, fws8 = attention.BwdWorkspace(), attention.BwdWorkspace()
+
+    def f8():
+        fp8.varlen_attn_fwd_fp8qk(qc, qs, kc, ks, v, cu, out=o8, lse=l8, seg_src=seg)
+
+    def b8():
+        fp8.varlen_attn_bwd_fp8qk(do, qc, qs, kc, ks, v, o8, l8, cu, dq=dq8, dk=dk8, dv=dv8, seg_src=seg,
+                                  workspace=ws8)
+
+    fp8.quant_block(q)  # finiteness checked once, outside the timing
+    tq, t8, tb8 = event_ms(quant, iters, st), event_ms(f8, iters, st), event_ms(b8, iters, st)
+    quant()
+    f8()
+    torch.cuda.synchronize()
+    peak8 = fp8_dense_peak(dev)
+    qbytes = 2 * (q.numel() + k.numel()) + (q.numel() + k.numel()) + 8 * qs.numel()
+    out["config4"] = {
+        "workload": "config-2 inputs, Q/K as E4M3 PerBlock(128x128 per head) codes; P.V and the backward in bf16",
+        "quant_qk_ms": tq, "quant_gbs": qbytes / (tq / 1e3) / 1e9, "quant_frac_of_hbm": qbytes / (tq / 1e3) / 1e9 /
+        PEAKS["hbm_gbs"], "fp8_fwd_ms": t8, "fp8_fwd_tflops": fl / t8 / 1e9, "bf16_fwd_ms": c2["fwd_ms"],
+        "fp8_bwd_ms": tb8, "fp8_fwd_vs_bf16_fwd": c2["fwd_ms"] / t8,
+        "fp8_vs_bf16_max_abs": float((o8.float() - o.float()).abs().max()),
+        "fp8_dense_peak_tflops_measured": peak8,
+        "fp8_fwd_frac_of_fp8_peak": (fl / t8 / 1e9 / peak8) if peak8 else None}
+    out["config2_kernels"] = {"kernel_ms": c2["kernel_ms"], "roofline_fwd": c2["roofline_fwd"],
+                              "roofline_bwd": c2["roofline_bwd"]}
+    del q, k, v, do, o, lse, qc, kc, o8, dq8, dk8, dv8
+    torch.cuda.empty_cache()
+    # config 5: the 1M-sample packer (truncated geometric p = 0.02, max 500; SURVEY §8(d))
+    n5 = 1 << 20
+    L5 = synthetic.gen_lengths(n5, synthetic.DIST_GEOMETRIC, 0.02, 500)
+    d_len = torch.from_numpy(L5).to(dev)
+    plan5 = packing.pack_ffd(d_len, CAPACITY)
+    tp = event_ms(lambda: packing.pack_ffd(d_len, CAPACITY, plan=plan5, sync_check=False), iters, st)
+    nb5 = plan5.num_bins()
+    tok5 = int(L5.sum())
+    # algorithmic bytes (SURVEY §8(d) row 5): 4 B/sample read + (bin_of, slot, tok_off) 12 B/sample +
+    # member_ids + cu_seqlens + per-bin cu_seqlens + src_off 16 B/sample + per-bin count/fill/offsets 16 B/bin
+    pbytes = 4 * n5 + 12 * n5 + 16 * n5 + 16 * nb5
+    pos, segi, gat = (torch.empty(tok5, dtype=torch.int32, device=dev) for _ in range(3))
+    tid = event_ms(lambda: packing.token_ids_into(plan5, tok5, pos, segi, gat), iters, st)
+    del pos, segi, gat
+    balance = {}
+    for w in (1, 2, 4, 8):
+        sp = vdist.shard_lpt(plan5, w, 0)
+        loads = sp.rank_load.cpu().numpy().astype(np.float64)
+        balance[str(w)] = float(loads.max() / loads.mean())
+    tsh = event_ms(lambda: vdist.shard_lpt(plan5, 8, 0, out=sp, sync_check=False), iters, st)
+    out["config5"] = {"workload": "1M samples, truncated geometric(p=0.02, max 500) lengths, 8192-token bins (GPU "
+                                  "FFD, 14 launches)", "samples": n5, "tokens": tok5, "bins": nb5,
+                      "pack_ms": tp, "samples_per_s": n5 / (tp / 1e3), "algorithmic_bytes": pbytes,
+                      "pack_gbs": pbytes / (tp / 1e3) / 1e9, "pack_frac_of_hbm": pbytes / (tp / 1e3) / 1e9 /
+                      PEAKS["hbm_gbs"], "token_ids_ms": tid,
+                      "token_ids_gbs": (12 * tok5 + 8 * n5) / (tid / 1e3) / 1e9,
+                      "shard_lpt_ms_8_ranks": tsh, "lpt_balance_max_over_mean": balance,
+                      "l2": "packer metadata (4 MB lengths) fits in L2; token ids (600 MB) do not"}
+    return out
+
+
+# ---------------------------------------------------------------------------- main (our arm)
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -194,150 +422,125 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2603_11101_b200 import attention, packing, synthetic
-    from paper_2603_11101_b200.dist import lpt_assign, shard_plan
+    from paper_2603_11101_b200 import dist as vdist
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    # ---------------------------------------------------------------- inputs (sample-major, resident)
-    L_local = lengths_for(rank, a.samples, a.dist)
-    n_local = L_local.size
-    d_len_local = torch.from_numpy(L_local).to(dev)
-    if world > 1:
-        gathered = torch.empty(world * n_local, dtype=torch.int32, device=dev)
-        dist.all_gather_into_tensor(gathered, d_len_local)
-        L_global = gathered.cpu().numpy()
-    else:
-        L_global = L_local
-    plan = packing.pack_ffd(L_global, CAPACITY)  # warm + host view for sizing
-    assign = lpt_assign(plan, L_global, world)
-    my = shard_plan(plan, L_global, assign, rank)  # this rank's bins: sample ids + packed layout
-    T = my["tokens"]
-    Ls = L_global[my["sample_ids"]]
-    pairs = float(np.sum(Ls.astype(np.float64) ** 2))
-    fl_fwd = 4.0 * D * H * pairs
-    fl_total = 3.5 * fl_fwd
-
-    q_src = synthetic.fill_bf16(torch.empty(T, H, D, dtype=torch.bfloat16, device=dev), "q")
-    k_src = synthetic.fill_bf16(torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev), "k")
-    v_src = synthetic.fill_bf16(torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev), "v")
-    do_p = synthetic.fill_bf16(torch.empty(T, H, D, dtype=torch.bfloat16, device=dev), "do")
-    qp, kp, vp = torch.empty_like(q_src), torch.empty_like(k_src), torch.empty_like(v_src)
-    dq_s, dk_s, dv_s = torch.empty_like(q_src), torch.empty_like(k_src), torch.empty_like(v_src)
-    d_len_mine = torch.from_numpy(np.ascontiguousarray(Ls)).to(dev)
-    sub = packing.pack_ffd(d_len_mine, CAPACITY)  # this rank's packs (same FFD on its samples)
-    ws = attention.BwdWorkspace()
     stream = torch.cuda.current_stream()
 
-    gidx = torch.empty(T, dtype=torch.int32, device=dev)
-    seg = torch.empty(sub.n, dtype=torch.int32, device=dev)
+    # ---------------------------------------------------------------- inputs
+    L_local = lengths_for(rank, a.samples, a.dist, synthetic.gen_lengths)
+    n_local = L_local.size
+    n_glob = n_local * world
+    d_len_local = torch.from_numpy(L_local).to(dev)
+    d_len_glob = torch.empty(n_glob, dtype=torch.int32, device=dev)
 
-    bufs = {"q": q_src, "k": k_src, "v": v_src, "do": do_p, "len": d_len_mine, "o": None, "lse": None,
-            "dq": dq_s, "dk": dk_s, "dv": dv_s}
+    def gather_lengths(dst, src):
+        if world > 1:
+            dist.all_gather_into_tensor(dst, src)  # the path's only collective: the pack metadata
+        else:
+            dst.copy_(src)
 
-    bufs["o"] = torch.empty_like(q_src)
-    bufs["lse"] = torch.empty(H, T, dtype=torch.float32, device=dev)
+    gather_lengths(d_len_glob, d_len_local)
+    L_glob = d_len_glob.cpu().numpy()
+    plans = [packing.pack_ffd(d_len_glob, CAPACITY) for _ in range(2)]
+    shards = [vdist.shard_lpt(plans[j], world, rank) for j in range(2)]
+    sp = shards[0]
+    nseg, T = sp.nseg(), sp.tokens()
+    my_ids = sp.local_ids[:nseg].cpu().numpy()
+    Ls = L_glob[my_ids]
+    pairs = visible_pairs(Ls)
+    fl_fwd = 4.0 * D * H * pairs
+    fl_total = 3.5 * fl_fwd
+    loads = sp.rank_load.cpu().numpy().astype(np.float64)
 
-    def phases(b):
-        """The step as three stream-ordered phases: pack, attention fwd, attention bwd."""
-        cu = sub.cu_seqlens
+    def tensors():
+        return {"q": synthetic.fill_bf16(torch.empty(T, H, D, dtype=torch.bfloat16, device=dev), "q"),
+                "k": synthetic.fill_bf16(torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev), "k"),
+                "v": synthetic.fill_bf16(torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev), "v"),
+                "do": synthetic.fill_bf16(torch.empty(T, H, D, dtype=torch.bfloat16, device=dev), "do"),
+                "o": torch.empty(T, H, D, dtype=torch.bfloat16, device=dev),
+                "lse": torch.empty(H, T, dtype=torch.float32, device=dev),
+                "dq": torch.empty(T, H, D, dtype=torch.bfloat16, device=dev),
+                "dk": torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev),
+                "dv": torch.empty(T, HKV, D, dtype=torch.bfloat16, device=dev),
+                "len": d_len_local, "ws": attention.BwdWorkspace(), "fws": attention.BwdWorkspace()}
 
-        def p_pack():
-            packing.pack_ffd(b["len"], CAPACITY, plan=sub, sync_check=False)
-            if a.layout == "fused":  # segment source offsets: the packed stream stays virtual
-                packing.seg_src(sub, out=seg)
-            else:  # gather index + explicit gather of Q/K/V rows into the packed stream
-                packing.token_ids_into(sub, T, gather_idx=gidx)
-                packing.gather_rows(b["q"], sub, out=qp)
-                packing.gather_rows(b["k"], sub, out=kp)
-                packing.gather_rows(b["v"], sub, out=vp)
+    bufs = tensors()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    pipelined = a.pipeline == "on" and not a.no_graph and world == 1
+    budget = nsm - 1 if pipelined else 0
 
-        if a.layout == "fused":  # attention over the sample-major rows (TMA coordinates = seg_src + offset)
-            def p_fwd():
-                attention.varlen_attn_fwd(b["q"], b["k"], b["v"], cu, out=b["o"], lse=b["lse"], seg_src=seg)
+    def pack_phase(j, b):
+        """all-gather (N > 1) → global FFD → device LPT shard plan, into plan / shard set j."""
+        gather_lengths(d_len_glob, b["len"])
+        packing.pack_ffd(d_len_glob, CAPACITY, plan=plans[j], sync_check=False)
+        vdist.shard_lpt(plans[j], world, rank, out=shards[j], sync_check=False)
 
-            def p_bwd():
-                attention.varlen_attn_bwd(b["do"], b["q"], b["k"], b["v"], b["o"], b["lse"], cu, workspace=ws,
-                                          dq=b["dq"], dk=b["dk"], dv=b["dv"], seg_src=seg)
-        else:  # packed stream; dQ/dK/dV scattered back to sample order in the epilogues (row_map)
-            def p_fwd():
-                attention.varlen_attn_fwd(qp, kp, vp, cu, out=b["o"], lse=b["lse"])
+    def fwd_phase(j, b):
+        s = shards[j]
+        attention.varlen_attn_fwd(b["q"], b["k"], b["v"], s.local_cu[: nseg + 1], out=b["o"], lse=b["lse"],
+                                  seg_src=s.local_seg_src[:nseg], sm_budget=budget, workspace=b["fws"])
 
-            def p_bwd():
-                attention.varlen_attn_bwd(b["do"], qp, kp, vp, b["o"], b["lse"], cu, workspace=ws, dq=b["dq"],
-                                          dk=b["dk"], dv=b["dv"], row_map=gidx)
-        return [p_pack, p_fwd, p_bwd]
+    def bwd_phase(j, b):
+        s = shards[j]
+        attention.varlen_attn_bwd(b["do"], b["q"], b["k"], b["v"], b["o"], b["lse"], s.local_cu[: nseg + 1],
+                                  dq=b["dq"], dk=b["dk"], dv=b["dv"], seg_src=s.local_seg_src[:nseg],
+                                  sm_budget=budget, workspace=b["ws"])
 
-    def step(b=bufs):
-        for f in phases(b):
-            f()
+    side = torch.cuda.Stream(dev)
 
-    for _ in range(max(3, a.warmup)):
-        step()
+    def step(i, b=bufs):
+        if pipelined:  # batch i+1's packing on a side stream (1 SM) beside batch i's attention
+            j = i & 1
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                pack_phase(1 - j, b)
+            fwd_phase(j, b)
+            bwd_phase(j, b)
+            torch.cuda.current_stream().wait_stream(side)
+        else:
+            pack_phase(0, b)
+            fwd_phase(0, b)
+            bwd_phase(0, b)
+
+    for i in range(max(3, a.warmup)):
+        step(i)
     torch.cuda.synchronize()
-    # The step's 23 launches are captured once into a CUDA graph and replayed (same kernels, same
-    # data dependencies, every step recomputed): no per-launch host / driver gaps between the
-    # dependent small packer kernels and the attention kernels.
-    graphs = {}
 
-    def capture(b, fn=None):
-        fn = fn or (lambda: step(b=b))
+    def capture(fn):
         g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            fn()  # warm-up on the capture stream
-        torch.cuda.current_stream().wait_stream(side)
+        s2 = torch.cuda.Stream(dev)
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s2):
+            fn()
+        torch.cuda.current_stream().wait_stream(s2)
         with torch.cuda.graph(g):
             fn()
         torch.cuda.synchronize()
         return g
 
-    if not a.no_graph:
-        graphs[id(bufs)] = capture(bufs)
+    graphs = {}
+    use_graph = not a.no_graph and world == 1  # N > 1: eager (NCCL collective in the step)
+    if use_graph:
+        graphs[(id(bufs), 0)] = capture(lambda: step(0))
+        graphs[(id(bufs), 1)] = capture(lambda: step(1))
 
-    def run_step(b=bufs):
-        g = graphs.get(id(b))
+    def run_step(i, b=bufs):
+        g = graphs.get((id(b), i & 1))
         if g is not None:
             g.replay()
         else:
-            step(b=b)
+            step(i, b)
 
-    # Pipelined steps (--pipeline on, fused layout): step i's graph runs batch i's attention on
-    # SMs − 1 CTAs (sm_budget) while a side stream packs batch i+1 into the other plan on the free
-    # SM — the data-loader overlap of a training loop.  Every timed step still packs one batch and
-    # runs one attention fwd + bwd; batch 0 is packed before the timed region.
-    pipelined = a.pipeline == "on" and a.layout == "fused" and not a.no_graph
     if pipelined:
-        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-        plans = [sub, packing.pack_ffd(d_len_mine, CAPACITY)]
-        segs = [seg, torch.empty_like(seg)]
-        side = torch.cuda.Stream(dev)
-
-        def pack_into(j, b=bufs):
-            packing.pack_ffd(b["len"], CAPACITY, plan=plans[j], sync_check=False)
-            packing.seg_src(plans[j], out=segs[j])
-
-        def pstep(j, b=bufs):
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                pack_into(1 - j, b)  # the next batch
-            cu = plans[j].cu_seqlens
-            attention.varlen_attn_fwd(b["q"], b["k"], b["v"], cu, out=b["o"], lse=b["lse"], seg_src=segs[j],
-                                      sm_budget=nsm - 1)
-            attention.varlen_attn_bwd(b["do"], b["q"], b["k"], b["v"], b["o"], b["lse"], cu, workspace=ws,
-                                      dq=b["dq"], dk=b["dk"], dv=b["dv"], seg_src=segs[j], sm_budget=nsm - 1)
-            torch.cuda.current_stream().wait_stream(side)
-
-        pgraphs = [capture(bufs, lambda j=j: pstep(j)) for j in range(2)]
-        pack_into(0)
-        for j in range(4):
-            pgraphs[j & 1].replay()
-        torch.cuda.synchronize()
-        pack_into(0)  # the timed loop starts on plan 0, packed here (outside the timed region)
-        torch.cuda.synchronize()
+        pack_phase(0, bufs)
+        for i in range(4):
+            run_step(i)
+        pack_phase(0, bufs)  # the timed loop starts on plan 0, packed here (outside the timed region)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -345,27 +548,10 @@ def main():
         torch.cuda.synchronize()
         t0.record(stream)
         for i in range(a.steps):
-            if pipelined:
-                pgraphs[i & 1].replay()
-            else:
-                run_step()
+            run_step(i)
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / a.steps
-    # per-phase device time: the three phases captured as separate graphs and replayed back to back
-    # with events between them on the launching stream (no host gaps inside a phase)
-    ph_graphs = [capture(bufs, f) for f in phases(bufs)] if not a.no_graph else None
-    nrep = min(a.steps, 10)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nrep)]
-    for r in range(nrep):
-        evs[r][0].record(stream)
-        for i, f in enumerate(phases(bufs)):
-            ph_graphs[i].replay() if ph_graphs else f()
-            evs[r][i + 1].record(stream)
-    torch.cuda.synchronize()
-    kpack = [e[0].elapsed_time(e[1]) for e in evs]
-    kfwd = [e[1].elapsed_time(e[2]) for e in evs]
-    kbwd = [e[2].elapsed_time(e[3]) for e in evs]
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -373,57 +559,72 @@ def main():
     fl_all = torch.tensor([fl_total], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(fl_all)
-    toks_all = T * world if world == 1 else float(np.sum(L_global))
+    toks_all = float(np.sum(L_glob))
+
+    # per-phase device times (eager, events between the phases on the launching stream)
+    nrep = min(a.steps, 10)
+    ph = []
+    for _ in range(nrep):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        pack_phase(0, bufs)
+        ev[1].record(stream)
+        fwd_phase(0, bufs)
+        ev[2].record(stream)
+        bwd_phase(0, bufs)
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(3)])
+    kpack, kfwd, kbwd = (statistics.median(r[i] for r in ph) for i in range(3))
+    kf = boundary_ms(lambda: fwd_phase(0, bufs), 3, nrep, stream)
+    kb = boundary_ms(lambda: bwd_phase(0, bufs), 5, nrep, stream)
 
     # ---------------------------------------------------------------- e2e through host buffers
-    # Every step copies its inputs (lengths, Q, K, V, dO) from pinned host memory and reads its
-    # results (O, dQ, dK, dV) back.  Steps are pipelined like a data loader: H2D of step i+1 and
-    # D2H of step i-1 run on their own copy streams (PCIe is full duplex) while step i computes;
-    # device input/output sets are double-buffered.
+    # Every step copies its inputs (this rank's lengths, Q, K, V, dO) from pinned host memory and reads
+    # its results (O, dQ, dK, dV) back; H2D of step i+1 and D2H of step i-1 run on their own copy
+    # streams (PCIe is full duplex) while step i computes; device input/output sets are double-buffered.
     e2e = None
     if not a.no_e2e:
-        hq = q_src.cpu().pin_memory()
-        hk = k_src.cpu().pin_memory()
-        hv = v_src.cpu().pin_memory()
-        hdo = do_p.cpu().pin_memory()
-        hL = torch.from_numpy(np.ascontiguousarray(Ls)).pin_memory()
-        outs = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q_src, q_src, k_src, v_src)]
-        sets = [bufs if j == 0 else {"q": torch.empty_like(q_src), "k": torch.empty_like(k_src),
-                                      "v": torch.empty_like(v_src), "do": torch.empty_like(do_p),
-                                      "len": torch.empty_like(d_len_mine), "dq": torch.empty_like(dq_s),
-                                      "dk": torch.empty_like(dk_s), "dv": torch.empty_like(dv_s)} for j in range(2)]
-        for b in sets:
-            b["o"] = torch.empty_like(q_src)
-            b["lse"] = torch.empty(H, T, dtype=torch.float32, device=dev)
-            if not a.no_graph:
-                graphs[id(b)] = capture(b)
+        hin = {k_: bufs[k_].cpu().pin_memory() for k_ in ("q", "k", "v", "do")}
+        hin["len"] = torch.from_numpy(L_local).pin_memory()
+        hout = [torch.empty(bufs[k_].shape, dtype=bufs[k_].dtype).pin_memory() for k_ in ("o", "dq", "dk", "dv")]
+        sets = [bufs, tensors()]
+        sets[1]["len"] = torch.empty_like(d_len_local)
+        if use_graph:
+            graphs[(id(sets[1]), 0)] = capture(lambda: step(0, sets[1]))
+            graphs[(id(sets[1]), 1)] = capture(lambda: step(1, sets[1]))
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_cp = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_in, ev_cp, ev_out = ([torch.cuda.Event() for _ in range(2)] for _ in range(3))
 
         def e2e_step(i):
             b, j = sets[i & 1], i & 1
             with torch.cuda.stream(s_in):
                 if i >= 2:
                     s_in.wait_event(ev_cp[j])  # compute of step i-2 has read this input set
-                for d_, h_ in ((b["len"], hL), (b["q"], hq), (b["k"], hk), (b["v"], hv), (b["do"], hdo)):
-                    d_.copy_(h_, non_blocking=True)
+                for k_ in ("len", "q", "k", "v", "do"):
+                    b[k_].copy_(hin[k_], non_blocking=True)
                 ev_in[j].record(s_in)
             stream.wait_event(ev_in[j])
             if i >= 2:
                 stream.wait_event(ev_out[j])  # D2H of step i-2 has read this output set
-            run_step(b=b)
+            run_step(i, b)
             ev_cp[j].record(stream)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cp[j])
-                for h_, d_ in zip(outs, (b["o"], b["dq"], b["dk"], b["dv"])):
-                    h_.copy_(d_, non_blocking=True)
+                for h_, k_ in zip(hout, ("o", "dq", "dk", "dv")):
+                    h_.copy_(b[k_], non_blocking=True)
                 ev_out[j].record(s_out)
 
+        if pipelined:
+            pack_phase(0, sets[0])
         for i in range(2):
             e2e_step(i)
         torch.cuda.synchronize()
+        if pipelined:
+            pack_phase(0, sets[0])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         n_e2e = max(4, min(a.steps, 8))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -436,24 +637,35 @@ def main():
         ems = torch.tensor([e0.elapsed_time(e1) / n_e2e], device=dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo, hL))
-        d2h = sum(x.numel() * x.element_size() for x in outs)
+        h2d = sum(x.numel() * x.element_size() for x in hin.values())
+        d2h = sum(x.numel() * x.element_size() for x in hout)
         e2e = {"value": toks_all / (float(ems.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item()),
                "pipelining": "H2D / compute / D2H on separate streams, double-buffered device sets"}
+        del sets, hin, hout
 
-    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
+    # ---------------------------------------------------------------- CPU baseline, other configs (rank 0, N = 1)
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu:
-        threads = len(os.sched_getaffinity(0))
-        tps, dt, desc = cpu_baseline(Ls[: a.cpu_samples], threads)
-        cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc,
-               "seconds": dt}
+    configs = None
+    if rank == 0 and world == 1:
+        if not a.no_cpu:
+            threads = len(os.sched_getaffinity(0))
+            tps, dt, desc = cpu_baseline(Ls[: a.cpu_samples], threads)
+            cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc, "seconds": dt}
+        if not a.no_configs:
+            del bufs
+            torch.cuda.empty_cache()
+            configs = measure_configs(dev)
 
     if rank == 0:
-        kb = statistics.mean(kbwd)
-        kf = statistics.mean(kfwd)
-        bwd_flops = 2.5 * fl_fwd
+        fb, bb = attn_bytes(T, H, HKV, D)
+        rf_bwd = roofline(2.5 * fl_fwd, bb, kbwd, PEAKS["bf16_tflops"], "backward pass: k_bwd_pre + k_bwd_dkdv + k_bwd_dq")
+        rf_step = roofline(fl_total, fb + bb, kfwd + kbwd, PEAKS["bf16_tflops"], "attention fwd + bwd")
+        traffic, tsrc = ncu_traffic()
+        bwd_traffic = None
+        if traffic:
+            bwd_traffic = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for k_, v in traffic.items()
+                              if k_.startswith("k_bwd"))
         line = {
             "metric": METRIC, "value": toks_all / (ms_max / 1e3), "unit": "tokens/s", "n_gpus": world,
             "steps": a.steps, "warmup": max(3, a.warmup), "ms_per_step": ms_max, "higher_is_better": True,
@@ -461,32 +673,30 @@ def main():
             "config": {"workload": f"config2 GR00T-N1.5 shape: {n_local} samples/GPU, "
                                    f"{'U[16,512]' if a.dist == 'uniform' else 'GR00T-like 64*U{1,2}+U[16,64]'} "
                                    f"lengths, {CAPACITY}-token bins, H{H} d{D} bf16 bidirectional fwd+bwd",
-                       "tokens_per_gpu": T, "bins_per_gpu": sub.num_bins(), "tflops_effective":
-                           float(fl_all.item()) / (ms_max / 1e3) / 1e12,
+                       "global_samples": n_glob, "tokens_rank0": T, "bins_global": plans[0].num_bins(),
+                       "segments_rank0": nseg, "tflops_effective": float(fl_all.item()) / (ms_max / 1e3) / 1e12,
+                       "lpt_balance_max_over_mean": float(loads.max() / loads.mean()),
                        "l2": "inputs larger than L2 (%.1f GB/GPU)" % (4 * T * H * D * 2 / 1e9),
-                       "parallelism": f"packs sharded over {world} GPU(s) (LPT), no collective on attention",
-                       "launch": "CUDA graph replay of the step" if not a.no_graph else "direct launches",
-                       "pipeline": "packer of batch i+1 on a side stream (1 SM) overlapping batch i's attention "
+                       "parallelism": f"packs sharded over {world} GPU(s): all-gather of lengths (NCCL) + GPU FFD + "
+                                      "device LPT inside every step; no collective on attention",
+                       "launch": "CUDA graph replay of the step" if use_graph else "direct launches",
+                       "pipeline": "packing of batch i+1 on a side stream (1 SM) beside batch i's attention "
                                    "(SMs-1 CTAs)" if pipelined else "pack then attention, in sequence",
-                       "layout": "fused: gather / scatter folded into the attention kernels' TMA coordinates "
-                                 "(seg_src)" if a.layout == "fused" else
-                                 "packed: explicit row gather into the packed stream, row_map scatter"},
-            "roofline": {"bound": "tensor", "kernel": "backward: k_bwd_pre + k_bwd_dkdv + k_bwd_dq",
-                         "achieved": bwd_flops / (kb / 1e3) / 1e12, "peak": PEAKS["bf16_tflops"],
-                         "unit": "TFLOP/s", "frac": bwd_flops / (kb / 1e3) / 1e12 / PEAKS["bf16_tflops"],
-                         "traffic": bwd_traffic()[0], "traffic_src": bwd_traffic()[1],
-                         "traffic_note": "dram read+write bytes of the 3 backward launches of one step (ncu --set "
-                                         "full); algorithmic minimum ≈ 4.5 GB (Q,K,V,O,dO in, dQ,dK,dV out)",
-                         "peak_src": PEAKS["src"],
-                         "fwd": {"achieved": fl_fwd / (kf / 1e3) / 1e12, "ms": kf}, "bwd_ms": kb,
-                         "pack_ms": statistics.mean(kpack)},
+                       "layout": "sample-major rows; gather / scatter folded into the attention kernels' TMA "
+                                 "coordinates (seg_src from the shard plan)"},
+            "roofline": dict(rf_bwd, traffic=bwd_traffic, traffic_src=tsrc,
+                             traffic_note="dram read+write bytes of the 3 backward launches of one step (ncu --set "
+                                          "full) vs algorithmic_bytes", peak_src=PEAKS["src"]),
+            "step_roofline": rf_step,
+            "phase_ms": {"pack_allgather_ffd_lpt": kpack, "fwd": kfwd, "bwd": kbwd},
+            "kernel_ms": {"fwd_prep": kf[0], "fwd_attention": kf[1], "bwd_pre": kb[0], "bwd_tiles": kb[1],
+                          "bwd_dkdv": kb[2], "bwd_dq": kb[3]},
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
-            # our launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
-            # fused: seg_src 1; packed: token ids 1 + gather 3; fwd 3 (spans, tiles, attention),
-            # bwd 4 (pre, tiles, dK/dV, dQ)
-            "gpu_launches": (22 if a.layout == "fused" else 25) * a.steps,
+            "gpu_launches": LAUNCHES_PER_STEP * a.steps,
         }
+        if configs is not None:
+            line["configs"] = configs
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -111,6 +111,31 @@ int vlasim_scatter_rows_cuda(const void* d_packed, void* d_dst, int64_t row_byte
  * segment's first token (vlasim_attn_args.seg_src — the gather folded into attention). */
 int vlasim_pack_seg_src_cuda(const vlasim_pack_out* out, int64_t n, int32_t* d_seg_src, vlasim_stream_t stream);
 
+/* ------------------------------------------------------------------ sharding (multi-GPU)
+ * Length-balanced assignment of the packs to `world` ranks, computed identically on every rank
+ * after the all-gather of the lengths (host restatement dist.py:lpt):
+ * cost(bin) = Σ l² of its members; bins in (cost desc, index asc) order each go to the least-loaded
+ * rank (ties: lowest rank).  Then this rank's share: its bins in index order, members in order,
+ * as a packed stream (local_cu) over the rank's sample-major layout (its samples in id order:
+ * local_src_off), with local_seg_src = the attention's seg_src.  Segments past *local_nseg have
+ * zero length (local_cu[j] = *local_tokens).  world <= 16, bins <= 16384 (else status
+ * VLASIM_ECONFIG; flags VLASIM_SYNC_CHECK synchronises and returns it).  One CTA, stream-ordered.
+ */
+typedef struct vlasim_shard_out {
+  int32_t* bin_rank;       /* [n]    rank of bin b (first num_bins valid)                    */
+  int64_t* rank_load;      /* [world] Σ l² of each rank's bins                                */
+  int32_t* local_ids;      /* [n]    sample id of local segment j                             */
+  int32_t* local_cu;       /* [n+1]  cu_seqlens of the rank's packed stream                   */
+  int32_t* local_seg_src;  /* [n]    row of local segment j's sample in the local layout      */
+  int32_t* local_src_off;  /* [n]    row of sample i in the local layout, -1 if not this rank's */
+  int32_t* local_nseg;     /* [1]                                                             */
+  int64_t* local_tokens;   /* [1]                                                             */
+  int32_t* status;         /* [2]                                                             */
+} vlasim_shard_out;
+
+int vlasim_shard_lpt_cuda(const int32_t* d_len, const vlasim_pack_out* plan, int64_t n, int32_t world, int32_t rank,
+                          const vlasim_shard_out* out, uint32_t flags, vlasim_stream_t stream);
+
 /* ------------------------------------------------------------------ attention
  * Replaces vlasim::packed_attention(q, k, v, cu_seqlens),
  * multi-head as the reference's looped single-head op.
@@ -219,6 +244,16 @@ int vlasim_fill_synthetic_bf16(void* d_x, int64_t count, uint64_t seed, vlasim_s
  * (prefix = length − p3).  h_out is a HOST buffer of n int32. */
 int vlasim_gen_lengths(uint64_t root_seed, const char* label, int dist, int64_t n, double p1, double p2, double p3,
                        int32_t* h_out);
+
+/* ------------------------------------------------------------------ measurement hook
+ * Per calling thread: the attention entry points record the registered cudaEvent_t handles, in
+ * order, on their stream at every kernel boundary — forward (head_dim 64/128): start, after the
+ * span + tile-table kernels, after the attention kernel; forward (256): start, after the tile
+ * table, after the attention kernel; backward: start, after k_bwd_pre, after the tile table,
+ * after dK/dV, after dQ.  n ≤ 16; n = 0 disables.  vlasim_boundary_count() = events recorded since
+ * the last registration.  Used by bench.py for per-kernel CUDA-event times. */
+int vlasim_set_boundary_events(void* const* events, int n);
+int vlasim_boundary_count(void);
 
 /* ------------------------------------------------------------------ self-test
  * Single-CTA tcgen05 GEMM used to validate the UMMA/TMA descriptor layouts the

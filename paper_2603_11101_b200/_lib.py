@@ -26,6 +26,12 @@ class PackOut(C.Structure):
         ("total_tokens", i64p), ("status", i32p)]
 
 
+class ShardOut(C.Structure):
+    _fields_ = [("bin_rank", i32p), ("rank_load", i64p), ("local_ids", i32p), ("local_cu", i32p),
+                ("local_seg_src", i32p), ("local_src_off", i32p), ("local_nseg", i32p), ("local_tokens", i64p),
+                ("status", i32p)]
+
+
 class AttnArgs(C.Structure):
     _fields_ = [
         ("q", C.c_void_p), ("k", C.c_void_p), ("v", C.c_void_p), ("o", C.c_void_p), ("lse", f32p),
@@ -52,6 +58,8 @@ _SIGS = {
                                              C.c_void_p]),
     "vlasim_gather_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, C.POINTER(PackOut), C.c_int64,
                                           C.c_void_p]),
+    "vlasim_shard_lpt_cuda": (C.c_int, [i32p, C.POINTER(PackOut), C.c_int64, C.c_int32, C.c_int32,
+                                         C.POINTER(ShardOut), C.c_uint32, C.c_void_p]),
     "vlasim_pack_seg_src_cuda": (C.c_int, [C.POINTER(PackOut), C.c_int64, i32p, C.c_void_p]),
     "vlasim_scatter_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, C.POINTER(PackOut), C.c_int64,
                                            C.c_void_p]),
@@ -71,6 +79,8 @@ _SIGS = {
     "vlasim_fill_synthetic_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p]),
     "vlasim_gen_lengths": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, i32p]),
+    "vlasim_set_boundary_events": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+    "vlasim_boundary_count": (C.c_int, []),
     "vlasim_selftest_umma": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, f32p, C.c_int32, C.c_int32, C.c_void_p]),
 }
 

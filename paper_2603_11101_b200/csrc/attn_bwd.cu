@@ -1139,13 +1139,16 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   using namespace vlasim_host;
   const int T = int(a->total_tokens), H = a->num_heads, Hkv = a->num_kv_heads;
   const int Tp = (T + 3) & ~3;
+  mark_boundary(st);
   k_bwd_pre<HD><<<(T + kPreTokens - 1) / kPreTokens, 256, H * kPreTokens * sizeof(float), st>>>(
       static_cast<const __nv_bfloat16*>(a->o), static_cast<const __nv_bfloat16*>(g->dout), a->lse, w.lse2, w.dsum,
       w.rows_span, w.cols_span, a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, Tp, H);
   VLASIM_LAUNCH_CHECK();
+  mark_boundary(st);
   int4* tiles;
   int* ntiles;
   if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, T, w.tiles, st, &tiles, &ntiles)) return rc;
+  mark_boundary(st);
   const int64_t max_tiles = int64_t(T) / 128 + a->num_seqs;
   CUtensorMap tq, tk, tv, tdo;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -1202,6 +1205,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
                    "smx:s_full", "smx:dp_full", "", "smx:dkv_full", "smx:phaseA", "smx:phaseB", "smx:epilogue", "",
                    "", "", "", "smx:total"});
   }
+  mark_boundary(st);
   {
     constexpr int BN = HD == 256 ? 64 : 128;
     constexpr int KS = HD == 64 ? 5 : (HD == 128 ? 3 : 2), VS = HD == 64 ? 4 : (HD == 128 ? 2 : 1);
@@ -1214,6 +1218,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     VLASIM_LAUNCH_CHECK();
     if (p.prof) prof_report("k_bwd_dq", grid, st, {});
   }
+  mark_boundary(st);
   return VLASIM_OK;
 }
 

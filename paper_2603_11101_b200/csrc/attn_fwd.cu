@@ -293,9 +293,11 @@ int launch_fwd(const vlasim_attn_args* a, void* tiles_buf, cudaStream_t st) {
   p.lse = a->lse;
   p.cu = a->cu_seqlens;
   p.prefix = a->prefix_len;
+  mark_boundary(st);
   if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, int64_t(T), tiles_buf, st,
                                   const_cast<int4**>(&p.tiles), const_cast<int**>(&p.ntiles)))
     return rc;
+  mark_boundary(st);
   p.nseq = a->num_seqs;
   p.T = static_cast<int>(T);
   p.H = a->num_heads;
@@ -307,6 +309,7 @@ int launch_fwd(const vlasim_attn_args* a, void* tiles_buf, cudaStream_t st) {
   const int64_t max_tiles = int64_t(T) / 128 + a->num_seqs;
   kern<<<max_tiles * a->num_heads, 192, Cfg::SMEM, st>>>(tq, tk, tv, p);
   VLASIM_LAUNCH_CHECK();
+  mark_boundary(st);
   return VLASIM_OK;
 }
 

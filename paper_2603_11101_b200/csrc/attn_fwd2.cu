@@ -650,11 +650,13 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, void* tiles_buf, cud
   using namespace vlasim_host;
   using Cfg = Fwd2Cfg<HD, KS, VS, FP8>;
   const int T = int(a->total_tokens);
+  mark_boundary(st);
   k_fwd_spans<<<(T + 255) / 256, 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, T, rows_span);
   VLASIM_LAUNCH_CHECK();
   int4* tiles;
   int* ntiles;
   if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, T, tiles_buf, st, &tiles, &ntiles)) return rc;
+  mark_boundary(st);
   CUtensorMap tq, tk, tv;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto QK = FP8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : BF;
@@ -701,6 +703,7 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, void* tiles_buf, cud
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, to64, to32, to16, to8, p);
   VLASIM_LAUNCH_CHECK();
+  mark_boundary(st);
   return VLASIM_OK;
 }
 

@@ -116,9 +116,32 @@ int prof_report(const char* kernel, int grid, cudaStream_t st, std::initializer_
   return VLASIM_OK;
 }
 
+namespace {
+struct BoundaryEvents {
+  cudaEvent_t ev[16];
+  int n = 0, next = 0;
+};
+thread_local BoundaryEvents g_bev;
+}  // namespace
+
+void mark_boundary(cudaStream_t st) {
+  if (g_bev.next < g_bev.n) cudaEventRecord(g_bev.ev[g_bev.next++], st);
+}
+
 }  // namespace vlasim_host
 
 extern "C" {
+
+int vlasim_set_boundary_events(void* const* events, int n) {
+  using namespace vlasim_host;
+  if (n < 0 || n > 16 || (n > 0 && !events)) return set_error(VLASIM_ECONFIG, "boundary events: 0..16 events");
+  for (int i = 0; i < n; ++i) g_bev.ev[i] = static_cast<cudaEvent_t>(events[i]);
+  g_bev.n = n;
+  g_bev.next = 0;
+  return VLASIM_OK;
+}
+
+int vlasim_boundary_count(void) { return vlasim_host::g_bev.next; }
 
 const char* vlasim_last_error_message(void) { return vlasim_host::last_error().c_str(); }
 

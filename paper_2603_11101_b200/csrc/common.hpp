@@ -59,6 +59,10 @@ size_t fwd_ws_bytes(const vlasim_attn_args* a);  // forward workspace: spans + t
 int launch_build_tiles(const int32_t* cu, const int32_t* seg_src, int nseq, int64_t T, void* buf, cudaStream_t st,
                        int4** tiles, int** ntiles);
 
+// Kernel-boundary events (vlasim_set_boundary_events): records the calling thread's next event on
+// `st`; a no-op unless events were registered.
+void mark_boundary(cudaStream_t st);
+
 // VLASIM_PROF=1: kernels with wait-time accounting are launched instead and each launch prints
 // (stderr) the average cycles per CTA spent in every named wait category.
 bool prof_enabled();

@@ -15,6 +15,8 @@ from typing import List, Sequence
 
 import numpy as np
 
+from . import _lib
+
 
 def bin_costs(bins_members: Sequence[Sequence[int]], lengths) -> np.ndarray:
     L = np.asarray(lengths, np.float64)
@@ -46,6 +48,49 @@ def shard_plan(plan, lengths, assign, rank: int) -> dict:
     L = np.asarray(lengths)
     return {"sample_ids": np.array(ids, dtype=np.int64), "tokens": int(L[ids].sum()) if ids else 0,
             "bins": list(assign[rank])}
+
+
+class ShardPlan:
+    """Device-resident result of vlasim_shard_lpt_cuda: the LPT assignment and this rank's packed stream."""
+
+    def __init__(self, n: int, world: int, device):
+        import torch
+        i32 = dict(dtype=torch.int32, device=device)
+        self.n, self.world = n, world
+        self.bin_rank = torch.empty(n, **i32)
+        self.rank_load = torch.empty(world, dtype=torch.int64, device=device)
+        self.local_ids = torch.empty(n, **i32)
+        self.local_cu = torch.empty(n + 1, **i32)
+        self.local_seg_src = torch.empty(n, **i32)
+        self.local_src_off = torch.empty(n, **i32)
+        self.local_nseg = torch.empty(1, **i32)
+        self.local_tokens = torch.empty(1, dtype=torch.int64, device=device)
+        self.status = torch.empty(2, **i32)
+        P = _lib.ptr
+        self._struct = _lib.ShardOut(P(self.bin_rank, _lib.i32p), P(self.rank_load, _lib.i64p),
+                                     P(self.local_ids, _lib.i32p), P(self.local_cu, _lib.i32p),
+                                     P(self.local_seg_src, _lib.i32p), P(self.local_src_off, _lib.i32p),
+                                     P(self.local_nseg, _lib.i32p), P(self.local_tokens, _lib.i64p),
+                                     P(self.status, _lib.i32p))
+
+    def nseg(self) -> int:
+        return int(self.local_nseg.item())
+
+    def tokens(self) -> int:
+        return int(self.local_tokens.item())
+
+
+def shard_lpt(plan, world: int, rank: int, *, out: ShardPlan | None = None, sync_check: bool = True, stream=None):
+    """Device LPT over the bins of a GPU PackPlan (identical on every rank) + this rank's packed stream,
+    stream-ordered with no host round trip (vlasim_shard_lpt_cuda)."""
+    import ctypes as C
+    if out is None or out.n != plan.n or out.world != world:
+        out = ShardPlan(plan.n, world, plan.bin_of.device)
+    rc = _lib.lib().vlasim_shard_lpt_cuda(_lib.ptr(plan.lengths, _lib.i32p), plan.c_struct, plan.n, int(world),
+                                          int(rank), C.byref(out._struct), 1 if sync_check else 0,
+                                          _lib.stream_ptr(stream))
+    _lib.check(rc, "shard_lpt")
+    return out
 
 
 def balance(assign, costs) -> float:

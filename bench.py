@@ -255,6 +255,8 @@ def boundary_ms(fn, nev, iters, stream, warm=2):
     rows = []
     for _ in range(iters):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        for e in evs:  # torch creates the underlying cudaEvent_t lazily, on the first record
+            e.record(stream)
         arr = (C.c_void_p * nev)(*[e.cuda_event for e in evs])
         _lib.check(L.vlasim_set_boundary_events(arr, nev), "boundary events")
         fn()

@@ -125,7 +125,8 @@ thread_local BoundaryEvents g_bev;
 }  // namespace
 
 void mark_boundary(cudaStream_t st) {
-  if (g_bev.next < g_bev.n) cudaEventRecord(g_bev.ev[g_bev.next++], st);
+  // a bad handle must not surface as the next kernel's launch error: the hook is measurement only
+  if (g_bev.next < g_bev.n && cudaEventRecord(g_bev.ev[g_bev.next++], st) != cudaSuccess) (void)cudaGetLastError();
 }
 
 }  // namespace vlasim_host

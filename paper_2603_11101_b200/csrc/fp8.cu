@@ -60,6 +60,30 @@ __device__ __noinline__ uint32_t e4m3_fix(uint32_t c, float ax, float amax) {
   return c;
 }
 
+// The same decision in fp32, exact once both sides are scaled by p2 = 2^-E(amax): A = |x|·p2·448
+// (≤ 11 significant bits, ≤ 896) and B = amax·p2 ∈ [1, 2) (8 bits); midpoint · B has ≤ 13 bits.
+// Valid for normal amax below 2^127 (p2 normal); e4m3_fix (fp64) covers the two degenerate cases.
+__device__ __forceinline__ uint32_t e4m3_fix_f32(uint32_t c, float A, float B) {
+  const int e = int(c >> 3), m = int(c & 7), ee = e == 0 ? 1 : e;
+  const int mant = e == 0 ? m : 8 + m;
+  const float u = __int_as_float((ee - 11 + 127) << 23);  // 2^(ee−11)
+  const float mu = float(2 * mant + 1) * u * B;
+  const float md = (m == 0 && e >= 2) ? float(4 * mant - 1) * (0.5f * u) * B : float(2 * mant - 1) * u * B;
+  if (c < 0x7E && (A > mu || (A == mu && (c & 1)))) return c + 1;
+  if (c > 0 && (A < md || (A == md && (c & 1)))) return c - 1;
+  return c;
+}
+
+// Per-block constants of the fp32 decision: p2 = 2^-E(amax) (0 → use the fp64 path).
+__device__ __forceinline__ float e4m3_fix_scale(float amax) {
+  const int ef = int((__float_as_uint(amax) >> 23) & 0xFF);
+  return (ef == 0 || ef >= 254) ? 0.f : __int_as_float((254 - ef) << 23);
+}
+
+__device__ __forceinline__ uint32_t e4m3_decide(uint32_t c, float ax, float amax, float p2) {
+  return p2 != 0.f ? e4m3_fix_f32(c, ax * p2 * 448.f, amax * p2) : e4m3_fix(c, ax, amax);
+}
+
 // Non-finite bf16 in either half of a 32-bit word (exponent all ones).
 __device__ __forceinline__ bool bf16x2_nonfinite(uint32_t w) {
   return ((w & 0x7F80u) == 0x7F80u) || ((w & 0x7F800000u) == 0x7F800000u);
@@ -121,6 +145,7 @@ __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __rest
   __syncthreads();
   amax = red[0];
   const float scale = amax == 0.f ? 1.f : __fdiv_rn(amax, 448.f);
+  const float p2 = e4m3_fix_scale(amax);
   if (threadIdx.x == 0) scales[(int64_t(h) * nbt + bt) * nbd + bd] = scale;
   // pass 2: codes
   for (int e = threadIdx.x * 2; e < rows * 128; e += 512) {
@@ -130,13 +155,13 @@ __global__ void __launch_bounds__(256) k_quant_block(const __nv_bfloat16* __rest
       const float xa = __bfloat162float(x[off]);
       const float a = __fdiv_rn(xa, scale);
       uint32_t ca = cvt_e4m3x2(a, 0.f) & 0xFF;
-      if (amax != 0.f && e4m3_suspect(a)) ca = (ca & 0x80) | e4m3_fix(ca & 0x7F, fabsf(xa), amax);
+      if (amax != 0.f && e4m3_suspect(a)) ca = (ca & 0x80) | e4m3_decide(ca & 0x7F, fabsf(xa), amax, p2);
       codes[off] = uint8_t(ca);
       if (c + 1 < cols) {
         const float xb = __bfloat162float(x[off + 1]);
         const float b = __fdiv_rn(xb, scale);
         uint32_t cb = cvt_e4m3x2(b, 0.f) & 0xFF;
-        if (amax != 0.f && e4m3_suspect(b)) cb = (cb & 0x80) | e4m3_fix(cb & 0x7F, fabsf(xb), amax);
+        if (amax != 0.f && e4m3_suspect(b)) cb = (cb & 0x80) | e4m3_decide(cb & 0x7F, fabsf(xb), amax, p2);
         codes[off + 1] = uint8_t(cb);
       }
     }
@@ -184,6 +209,7 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
   __syncthreads();
   amax = fmaxf(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])), fmaxf(fmaxf(red[4], red[5]), fmaxf(red[6], red[7])));
   const float scale = amax == 0.f ? 1.f : __fdiv_rn(amax, 448.f);
+  const float p2 = e4m3_fix_scale(amax);
   if (threadIdx.x == 0) scales[(int64_t(h) * nbt + bt) * nbd + bd] = scale;
   // x / scale correctly rounded without a division per element (IEEE div.rn is ~10 dependent
   // instructions and made this kernel ALU-bound): q0 = RN(x·r) with r = RN(1/scale), then one
@@ -221,7 +247,7 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
         if (!e4m3_suspect(qv[k])) continue;
         const uint32_t sh = 8 * (k & 3), c = (w[k >> 2] >> sh) & 0xFF;
         const float ax = fabsf(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&v[i])[k]));
-        const uint32_t f = (c & 0x80) | e4m3_fix(c & 0x7F, ax, amax);
+        const uint32_t f = (c & 0x80) | e4m3_decide(c & 0x7F, ax, amax, p2);
         w[k >> 2] = (w[k >> 2] & ~(0xFFu << sh)) | (f << sh);
       }
     }

@@ -27,9 +27,11 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_default_arm_line(gpu):
-    d = _run(["--steps", "3", "--warmup", "3", "--samples", "64", "--no-cpu"], 600)
+    d = _run(["--steps", "3", "--warmup", "3", "--samples", "64", "--no-cpu", "--no-configs"], 600)
     assert KEYS <= set(d) and d["value"] > 0 and d["n_gpus"] == 1 and d["warmup"] >= 3
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r) and 0 < r["frac"] < 1
+    assert r["bound"] in ("hbm", "tensor") and r["unit"] == ("GB/s" if r["bound"] == "hbm" else "TFLOP/s")
+    assert set(d["kernel_ms"]) == {"fwd_prep", "fwd_attention", "bwd_pre", "bwd_tiles", "bwd_dkdv", "bwd_dq"}
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 22 * d["steps"] and "sm_mhz" in d["clocks"]

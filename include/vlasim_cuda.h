@@ -75,8 +75,10 @@ typedef struct vlasim_pack_out {
    return the device status (VLASIM_ECONFIG with the offending index in the message). */
 #define VLASIM_SYNC_CHECK 1u
 
-/* Maximum capacity accepted by the GPU packer (larger → VLASIM_ECONFIG). */
-#define VLASIM_PACK_MAX_CAPACITY 16384
+/* Maximum capacity accepted by the GPU packer (larger → VLASIM_ECONFIG).  Bin room is held in
+   16-bit counters by the greedy variant's room tree; FFD has no open-bin limit (the open-bin
+   list spills from shared memory to the workspace), greedy supports up to 2^20 bins. */
+#define VLASIM_PACK_MAX_CAPACITY 65535
 
 size_t vlasim_pack_workspace_size(int64_t n, int32_t capacity);
 

@@ -211,16 +211,25 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
   const float scale = amax == 0.f ? 1.f : __fdiv_rn(amax, 448.f);
   const float p2 = e4m3_fix_scale(amax);
   if (threadIdx.x == 0) scales[(int64_t(h) * nbt + bt) * nbd + bd] = scale;
-  // x / scale correctly rounded without a division per element (IEEE div.rn is ~10 dependent
-  // instructions and made this kernel ALU-bound): q0 = RN(x·r) with r = RN(1/scale), then one
-  // Markstein correction q = RN(q0 + RN(x − q0·scale)·r) (the residual is exact by FMA), which is
-  // the correctly rounded quotient for normal operands; quotients below 2^-10 map to code 0
-  // either way.  Packed f32x2 FMUL / FFMA.
-  const float rs = __frcp_rn(scale);
-  const float2 r2 = make_float2(rs, rs), ns2 = make_float2(-scale, -scale);
+  // Codes = RNE of the REAL quotient X = |x|·448/amax, computed as A / B with both operands
+  // scaled by p2 = 2^-E(amax) so that they are exact in fp32: A = x·(448·p2) (≤ 11 significant
+  // bits) and B = amax·p2 ∈ [1, 2) (8 bits).  A midpoint M between two E4M3 codes has ≤ 5
+  // significant bits, so when X ≠ M, |A − M·B| is a nonzero multiple of a grid ≥ 2^-13·M·B: X sits
+  // at relative distance ≥ 2^-14 from every midpoint, far beyond the few fp32 ulps of error of the
+  // quotient below — cvt.rn of the fp32 quotient is then the RNE code of X, and when X = M exactly
+  // the quotient is exactly M and cvt's ties-to-even decides as the SPEC does.  No per-element
+  // re-decision: the kernel stays a single HBM pass.  The quotient avoids a division per element
+  // (IEEE div.rn is ~10 dependent instructions and made this kernel ALU-bound): q0 = RN(A·r) with
+  // r = RN(1/B), corrected once, q = RN(q0 + RN(A − q0·B)·r) (the residual is exact by FMA).
+  // Degenerate block maxima (bf16 subnormal or ≥ 2^127, p2 = 0) take the fp64 decision instead.
+  const bool fast = p2 != 0.f;
+  const float Bs = fast ? amax * p2 : scale, As = fast ? 448.f * p2 : 1.f;
+  const float rs = __frcp_rn(Bs);
+  const float2 r2 = make_float2(rs, rs), ns2 = make_float2(-Bs, -Bs), a2 = make_float2(As, As);
   auto quot = [&](float2 f) {  // (the correction turns −0 into +0: the sign is restored)
-    const float2 q0 = f2_mul(f, r2);
-    const float2 q = f2_fma(f2_fma(q0, ns2, f), r2, q0);
+    const float2 fa = f2_mul(f, a2);
+    const float2 q0 = f2_mul(fa, r2);
+    const float2 q = f2_fma(f2_fma(q0, ns2, fa), r2, q0);
     return make_float2(copysignf(q.x, f.x), copysignf(q.y, f.y));
   };
 #pragma unroll
@@ -238,16 +247,13 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
       const uint32_t hi = cvt_e4m3x2(q1.x, q1.y);
       w[j] = lo | (hi << 16);
     }
-    bool sus = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) sus |= e4m3_suspect(qv[k]);
-    if (sus && amax != 0.f) {  // rare: re-decide the codes whose quotient sits at a midpoint
+    if (!fast && amax != 0.f) {  // degenerate block maximum (block-uniform): fp64 re-decision
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (!e4m3_suspect(qv[k])) continue;
         const uint32_t sh = 8 * (k & 3), c = (w[k >> 2] >> sh) & 0xFF;
         const float ax = fabsf(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&v[i])[k]));
-        const uint32_t f = (c & 0x80) | e4m3_decide(c & 0x7F, ax, amax, p2);
+        const uint32_t f = (c & 0x80) | e4m3_fix(c & 0x7F, ax, amax);
         w[k >> 2] = (w[k >> 2] & ~(0xFFu << sh)) | (f << sh);
       }
     }

@@ -17,6 +17,7 @@
 //   k_assign      stable rank inside class → run → (bin, slot, token offset)
 //   k_scan_*      exclusive scans: bin member/token offsets, source offsets
 //   k_layout      member order, global + per-bin cu_seqlens
+#include <algorithm>
 #include <climits>
 
 #include "common.hpp"
@@ -29,7 +30,9 @@ namespace {
 constexpr int kChunk = 4096;         // items per histogram / rank chunk
 constexpr int kRankThreads = 1024;   // k_assign block (4 rounds of 1024 items)
 constexpr int kScanItems = 4096;     // items per scan block (1024 threads × 4)
-constexpr int kMaxActiveBins = 16384;  // open bins kept in k_ffd shared memory
+constexpr int kMaxActiveBins = 16384;  // open bins kept in k_ffd shared memory (then spilled to HBM)
+constexpr int kSmemHistMaxCap = 40959;  // (cap + 1) int32 counters in smem; larger caps count in HBM
+constexpr int kGreedyDeepMaxBins = 1 << 20;  // 4-level 32-ary room tree, level 0 in HBM
 
 struct PackWs {
   int32_t* chunk_hist;       // [C][cap+1]   → exclusive per-class base after k_class_scan
@@ -41,6 +44,8 @@ struct PackWs {
   int32_t* run_tok;          // [n]  bin fill (tokens) before this run
   int32_t* run_mem;          // [n]  bin member count before this run
   int64_t* scan_part;        // [3][num_scan_blocks + 1]
+  int32_t* spill;            // [3][n]  k_ffd open-bin list once it outgrows shared memory;
+                             //         k_greedy level-0 room / count ([2][min(n, 2^20)])
 };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -66,6 +71,7 @@ size_t carve(PackWs* w, void* base, int64_t n, int cap) {
   w->run_tok = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
   w->run_mem = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
   w->scan_part = reinterpret_cast<int64_t*>(take(size_t(3) * (num_scan_blocks(n) + 1) * 8));
+  w->spill = reinterpret_cast<int32_t*>(take(size_t(3) * ((n + 31) & ~int64_t(31)) * 4));
   return off;
 }
 
@@ -83,11 +89,17 @@ __global__ void k_init(vlasim_pack_out out, int64_t n) {
   }
 }
 
+// kGlobal (cap > kSmemHistMaxCap): the chunk's counters live in its chunk_hist row (zeroed by
+// the host-side memset) and are incremented with HBM atomics.
+template <bool kGlobal>
 __global__ void k_hist(const int32_t* __restrict__ len, int64_t n, int cap, int32_t* __restrict__ chunk_hist,
                        int32_t* status) {
-  extern __shared__ int32_t sh[];
-  for (int i = threadIdx.x; i <= cap; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
+  extern __shared__ int32_t sh_[];
+  int32_t* sh = kGlobal ? chunk_hist + size_t(blockIdx.x) * (cap + 1) : sh_;
+  if (!kGlobal) {
+    for (int i = threadIdx.x; i <= cap; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
   const int64_t base = int64_t(blockIdx.x) * kChunk;
   for (int j = threadIdx.x; j < kChunk; j += blockDim.x) {
     const int64_t i = base + j;
@@ -100,6 +112,7 @@ __global__ void k_hist(const int32_t* __restrict__ len, int64_t n, int cap, int3
     }
     atomicAdd(&sh[L], 1);
   }
+  if (kGlobal) return;
   __syncthreads();
   int32_t* o = chunk_hist + size_t(blockIdx.x) * (cap + 1);
   for (int i = threadIdx.x; i <= cap; i += blockDim.x) o[i] = sh[i];
@@ -124,13 +137,17 @@ __global__ void k_class_scan(int32_t* __restrict__ chunk_hist, int64_t nchunks, 
 // Single CTA.  Open ("active") bins are kept in shared memory sorted by bin id:
 // act_id / act_rem / act_cnt.  A bin whose remaining room is below the smallest length
 // still to come can never receive an item again; it is retired (final count/fill written)
-// during compaction, which preserves the id order of the survivors.
-__global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack_out out) {
+// during compaction, which preserves the id order of the survivors.  When more than
+// kMaxActiveBins bins stay open even after retirement, the list moves to the workspace
+// (`spill`, n entries per array — FFD never opens more bins than items) and the kernel carries
+// on there: any input the reference packs, the GPU packs (no open-bin limit).
+__global__ void __launch_bounds__(1024, 1) k_ffd(int n, int cap, PackWs ws, vlasim_pack_out out) {
   extern __shared__ int32_t sm[];
   int32_t* act_id = sm;
   int32_t* act_rem = sm + kMaxActiveBins;
   int32_t* act_cnt = sm + 2 * kMaxActiveBins;
   int32_t* cls = sm + 3 * kMaxActiveBins;  // [1024] compacted class list of the current L-chunk
+  int act_cap = kMaxActiveBins;            // uniform: capacity of the current open-bin arrays
   __shared__ int32_t scratch[33];
   __shared__ int32_t s_ncls, s_lmin;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -208,15 +225,9 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack
       if (r > 0) {
         const int k = cap / L;
         const int nnew = (r + k - 1) / k;
-        if (nact + nnew > kMaxActiveBins) {
-          // retire bins that can never be used again, then re-check
-          if (per > 32) {  // per-thread staging below holds 32 bins (1024-thread mode: per <= 16)
-            if (tid == 0) {
-              out.status[0] = VLASIM_ECONFIG;
-              out.status[1] = -2;
-            }
-            return;
-          }
+        if (nact + nnew > act_cap) {
+          // (smem mode only: in the spilled arrays nact + nnew <= bins opened <= n = act_cap)
+          // retire bins that can never be used again, then re-check; per <= 16 here
           __syncthreads();
           int keep = 0;
           for (int b = b0; b < b1; ++b) keep += act_rem[b] >= lmin;
@@ -243,12 +254,21 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack
           }
           nact = kept;
           __syncthreads();
-          if (nact + nnew > kMaxActiveBins) {
-            if (tid == 0) {
-              out.status[0] = VLASIM_ECONFIG;
-              out.status[1] = -2;  // open-bin limit
+          if (nact + nnew > act_cap) {  // spill the open-bin list to the workspace, id order kept
+            const int64_t stride = (int64_t(n) + 31) & ~int64_t(31);
+            int32_t* g_id = ws.spill;
+            int32_t* g_rem = ws.spill + stride;
+            int32_t* g_cnt = ws.spill + 2 * stride;
+            for (int b = tid; b < nact; b += nt) {
+              g_id[b] = act_id[b];
+              g_rem[b] = act_rem[b];
+              g_cnt[b] = act_cnt[b];
             }
-            return;
+            __syncthreads();
+            act_id = g_id;
+            act_rem = g_rem;
+            act_cnt = g_cnt;
+            act_cap = n;
           }
         }
         for (int j = tid; j < nnew; j += nt) {
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int cap, PackWs ws, vlasim_pack
 // class counts staged in smem, bins visited 32 at a time with early exit once the class is
 // placed (no block barriers on the per-class critical path).
 constexpr int kWarpMaxBins = 16384;
+constexpr int kWarpCntMaxCap = 24575;  // 2 × 64 KB of bins + (cap + 1) counters within 227 KB
 // floor(a / b) for 0 <= a, 1 <= b <= 2^15 via the fp32 reciprocal, corrected to the exact quotient
 // (the estimate is off by at most one either way at these magnitudes).
 __device__ __forceinline__ int udiv_small(int a, int b, float inv_b) {
@@ -296,7 +317,9 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
   extern __shared__ int32_t sm[];
   int32_t* act_rem = sm;                    // bins are never retired here: id == index
   int32_t* act_cnt = sm + kWarpMaxBins;
-  int32_t* cnt = sm + 2 * kWarpMaxBins;     // [cap + 1] class counts
+  // [cap + 1] class counts: staged in smem up to kWarpCntMaxCap, read from the workspace beyond
+  const bool cnt_smem = cap <= kWarpCntMaxCap;
+  int32_t* cnt = cnt_smem ? sm + 2 * kWarpMaxBins : ws.class_count;
   const int lane = threadIdx.x;
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   if (out.status[0] != 0) return;
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
 #pragma unroll 32
   for (int L = lane; L <= cap; L += 32) {
     const int c = __ldg(ws.class_count + L);
-    cnt[L] = c;
+    if (cnt_smem) cnt[L] = c;
     tok += static_cast<long long>(c) * L;
   }
 #pragma unroll
@@ -472,14 +495,20 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
 }
 
 // ------------------------------------------------------------------ stable ranks → bins
+// kGlobal (cap > kSmemHistMaxCap): the running ranks advance in the chunk's own chunk_hist row
+// (the exclusive class base; nothing reads it afterwards).
+template <bool kGlobal>
 __global__ void __launch_bounds__(kRankThreads) k_assign(const int32_t* __restrict__ len, int64_t n, int cap,
                                                           PackWs ws, vlasim_pack_out out) {
-  extern __shared__ int32_t cnt[];  // [cap+1] running per-class rank inside this chunk
+  extern __shared__ int32_t cnt_[];  // [cap+1] running per-class rank inside this chunk
   if (out.status[0] != 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int32_t* base = ws.chunk_hist + size_t(blockIdx.x) * (cap + 1);
-  for (int i = tid; i <= cap; i += blockDim.x) cnt[i] = base[i];
-  __syncthreads();
+  int32_t* base = ws.chunk_hist + size_t(blockIdx.x) * (cap + 1);
+  int32_t* cnt = kGlobal ? base : cnt_;
+  if (!kGlobal) {
+    for (int i = tid; i <= cap; i += blockDim.x) cnt[i] = base[i];
+    __syncthreads();
+  }
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int round = 0; round < kChunk / kRankThreads; ++round) {
     if (int64_t(blockIdx.x) * kChunk + round * kRankThreads >= n) break;  // uniform
@@ -516,32 +545,51 @@ __global__ void __launch_bounds__(kRankThreads) k_assign(const int32_t* __restri
 // ------------------------------------------------------------------ greedy (arrival order)
 // Streaming first-fit in id order: sample i goes to the lowest-index bin whose
 // remaining room is >= len[i] (a fresh bin has room cap, so the first unopened bin always
-// qualifies).  Inherently sequential; one warp walks a 32-ary max-tree of remaining room held
-// in shared memory (3 levels, 32768 bins): 3 ballots down, 2 warp max-reductions up per sample.
+// qualifies).  Inherently sequential; one warp walks a 32-ary max-tree of remaining room:
+//   n <= 32768 : 3 levels in shared memory (bins = level 0, 32768 of them);
+//   n >  32768 : 4 levels (2^20 bins) — level 0 (room, count) in the workspace (L2-resident),
+//                levels 1-3 in shared memory; one coalesced 128-B load per sample.
+// Each descent step is one ballot; the update walks back up with warp max-reductions over the
+// 32 values each lane already holds in registers (no re-read after the owner's store).
 constexpr int kGreedyMaxBins = 32768;
 constexpr size_t kGreedySmem = (2 * kGreedyMaxBins + 1024 + 32) * sizeof(uint16_t);
+constexpr size_t kGreedyDeepSmem = (kGreedyMaxBins + 1024 + 32) * sizeof(uint16_t);
 
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void k_greedy_fill(int32_t* __restrict__ rem0, int32_t* __restrict__ cnt0, int64_t nb, int cap) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < nb) {
+    rem0[i] = cap;
+    cnt0[i] = 0;
+  }
+}
+
+template <bool kDeep>
 __global__ void __launch_bounds__(32, 1) k_greedy(const int32_t* __restrict__ len, int64_t n, int cap,
-                                                  vlasim_pack_out out) {
+                                                  PackWs ws, vlasim_pack_out out) {
   extern __shared__ uint16_t gsm[];
-  uint16_t* rem0 = gsm;                   // [32768] remaining room of bin b
-  uint16_t* cnt = rem0 + kGreedyMaxBins;  // [32768] members of bin b
-  uint16_t* rem1 = cnt + kGreedyMaxBins;  // [1024] max over 32 bins
-  uint16_t* rem2 = rem1 + 1024;           // [32]   max over 32 level-1 nodes
+  // shallow: rem0/cnt = bins in smem; deep: g_rem/g_cnt = bins in HBM, rem0 = level-1 maxima
+  uint16_t* rem0 = gsm;                                      // [32768]
+  uint16_t* cnt = kDeep ? nullptr : rem0 + kGreedyMaxBins;   // [32768] (shallow)
+  uint16_t* rem1 = rem0 + (kDeep ? 1 : 2) * kGreedyMaxBins;  // [1024]
+  uint16_t* rem2 = rem1 + 1024;                              // [32]
+  const int64_t gstride = (n + 31) & ~int64_t(31);
+  int32_t* g_rem = ws.spill;
+  int32_t* g_cnt = ws.spill + gstride;
   const int lane = threadIdx.x;
   if (out.status[0] != 0) return;  // invalid lengths (k_hist)
   for (int i = lane; i < kGreedyMaxBins; i += 32) {
     rem0[i] = uint16_t(cap);
-    cnt[i] = 0;
+    if (!kDeep) cnt[i] = 0;
   }
   for (int i = lane; i < 1024; i += 32) rem1[i] = uint16_t(cap);
   rem2[lane] = uint16_t(cap);
   __syncwarp();
-  auto wmax = [](int v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-  };
   int nb = 0;
   for (int64_t base = 0; base < n; base += 32) {
     const int64_t my = base + lane;
@@ -551,7 +599,7 @@ __global__ void __launch_bounds__(32, 1) k_greedy(const int32_t* __restrict__ le
     for (int j = 0; j < cntv; ++j) {
       const int L = __shfl_sync(0xffffffffu, lm, j);
       const unsigned m2 = __ballot_sync(0xffffffffu, rem2[lane] >= L);
-      if (m2 == 0) {  // every one of the 32768 bins is too full: out of tree capacity
+      if (m2 == 0) {  // every bin of the tree is too full: out of tree capacity
         if (lane == 0) {
           out.status[1] = -4;
           out.status[0] = VLASIM_ECONFIG;
@@ -560,18 +608,40 @@ __global__ void __launch_bounds__(32, 1) k_greedy(const int32_t* __restrict__ le
       }
       const int j2 = __ffs(m2) - 1;
       const int j1 = j2 * 32 + __ffs(__ballot_sync(0xffffffffu, rem1[j2 * 32 + lane] >= L)) - 1;
-      const int b = j1 * 32 + __ffs(__ballot_sync(0xffffffffu, rem0[j1 * 32 + lane] >= L)) - 1;
-      const int r = rem0[b], c = cnt[b];
-      __syncwarp();
-      if (lane == 0) {
-        rem0[b] = uint16_t(r - L);
-        cnt[b] = uint16_t(c + 1);
+      int v0 = rem0[j1 * 32 + lane];
+      int b = j1 * 32 + __ffs(__ballot_sync(0xffffffffu, v0 >= L)) - 1;
+      int r, c;
+      if (kDeep) {  // one more level: the 32 bins under node b live in HBM
+        const int64_t g = int64_t(b) * 32 + lane;
+        const int vg = g < gstride ? g_rem[g] : 0;
+        const unsigned mg = __ballot_sync(0xffffffffu, vg >= L);
+        const int jg = __ffs(mg) - 1;  // node b has max >= L, so some bin under it qualifies
+        const int64_t bb = int64_t(b) * 32 + jg;
+        r = __shfl_sync(0xffffffffu, vg, jg);
+        c = lane == 0 ? g_cnt[bb] : 0;
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const int vg2 = lane == jg ? vg - L : vg;
+        if (lane == jg) g_rem[bb] = vg2;
+        if (lane == 0) g_cnt[bb] = c + 1;
+        const int mx = warp_max(vg2);  // new maximum of node b
+        if (lane == (b & 31)) v0 = mx;
+        if (lane == 0) rem0[b] = uint16_t(mx);
+        b = int(bb);
+      } else {
+        r = __shfl_sync(0xffffffffu, v0, b & 31);
+        c = cnt[b];
+        if (lane == (b & 31)) v0 -= L;
+        __syncwarp();
+        if (lane == 0) {
+          rem0[b] = uint16_t(r - L);
+          cnt[b] = uint16_t(c + 1);
+        }
       }
+      const int v1 = warp_max(v0);
       __syncwarp();
-      const int v1 = wmax(rem0[j1 * 32 + lane]);
       if (lane == 0) rem1[j1] = uint16_t(v1);
       __syncwarp();
-      const int v2 = wmax(rem1[j2 * 32 + lane]);
+      const int v2 = warp_max(rem1[j2 * 32 + lane]);
       if (lane == 0) rem2[j2] = uint16_t(v2);
       __syncwarp();
       if (lane == j) {
@@ -588,8 +658,8 @@ __global__ void __launch_bounds__(32, 1) k_greedy(const int32_t* __restrict__ le
     }
   }
   for (int b = lane; b < nb; b += 32) {
-    out.bin_count[b] = cnt[b];
-    out.bin_fill[b] = cap - rem0[b];
+    out.bin_count[b] = kDeep ? g_cnt[b] : cnt[b];
+    out.bin_fill[b] = cap - (kDeep ? g_rem[b] : rem0[b]);
   }
   if (lane == 0) *out.num_bins = nb;
 }
@@ -717,6 +787,21 @@ int run_scan(const int32_t* in, int64_t n, int32_t* out, int64_t* part, int64_t*
   return 0;
 }
 
+// validation + per-chunk length histogram (smem counters up to kSmemHistMaxCap, HBM beyond)
+int launch_hist(const int32_t* d_len, int64_t n, int cap, const PackWs& w, const vlasim_pack_out* out,
+                cudaStream_t st) {
+  const int64_t nchunks = num_chunks(n);
+  if (cap <= kSmemHistMaxCap) {
+    if ((cap + 1) * 4 > 48 * 1024)
+      VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + 1) * 4));
+    k_hist<false><<<nchunks, 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);
+  } else {
+    VLASIM_CUDA_TRY(cudaMemsetAsync(w.chunk_hist, 0, size_t(nchunks) * (cap + 1) * 4, st));
+    k_hist<true><<<nchunks, 512, 0, st>>>(d_len, n, cap, w.chunk_hist, out->status);
+  }
+  return VLASIM_OK;
+}
+
 int check_out(const vlasim_pack_out* o) {
   if (!o || !o->bin_of || !o->slot || !o->tok_off || !o->bin_count || !o->bin_fill || !o->bin_member_off ||
       !o->bin_token_off || !o->member_ids || !o->cu_seqlens || !o->cu_seqlens_bins || !o->src_off || !o->num_bins ||
@@ -732,9 +817,8 @@ int finish(const vlasim_pack_out* out, int64_t n, uint32_t flags, cudaStream_t s
   VLASIM_CUDA_TRY(cudaMemcpyAsync(h, out->status, sizeof(h), cudaMemcpyDeviceToHost, st));
   VLASIM_CUDA_TRY(cudaStreamSynchronize(st));
   if (h[0] == 0) return VLASIM_OK;
-  if (h[1] == -2) return set_error(VLASIM_ECONFIG, "GPU packer: more than %d simultaneously open bins", kMaxActiveBins);
   if (h[1] == -3) return set_error(VLASIM_ECONFIG, "GPU packer: total tokens exceed int32 cu_seqlens range");
-  if (h[1] == -4) return set_error(VLASIM_ECONFIG, "greedy packer: more than %d bins", kGreedyMaxBins);
+  if (h[1] == -4) return set_error(VLASIM_ECONFIG, "greedy packer: more than %d bins", kGreedyDeepMaxBins);
   return set_error(VLASIM_ECONFIG, "oversize or empty sample: id %d (length must be in [1, capacity])", h[1]);
 }
 
@@ -762,23 +846,25 @@ extern "C" int vlasim_pack_ffd_cuda(const int32_t* d_len, int64_t n, int32_t cap
   const int64_t nchunks = num_chunks(n);
 
   k_init<<<(n + 255) / 256, 256, 0, st>>>(*out, n);
-  if ((cap + 1) * 4 > 48 * 1024)
-    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + 1) * 4));
-  k_hist<<<nchunks, 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);
+  if (int rc = launch_hist(d_len, n, cap, w, out, st)) return rc;
   k_class_scan<<<(cap + 1 + 255) / 256, 256, 0, st>>>(w.chunk_hist, nchunks, cap, w.class_count);
   if (n <= kWarpMaxBins) {  // at most n bins: the warp-synchronous packer holds them all in smem
-    const size_t wsm = (2 * kWarpMaxBins + cap + 1) * 4;
+    const size_t wsm = (2 * kWarpMaxBins + (cap <= kWarpCntMaxCap ? cap + 1 : 0)) * 4;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
     k_ffd_warp<<<1, 32, wsm, st>>>(cap, w, *out);
   } else {
     const size_t ffd_smem = (3 * kMaxActiveBins + 1024) * 4;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffd_smem));
-    k_ffd<<<1, 1024, ffd_smem, st>>>(cap, w, *out);
+    k_ffd<<<1, 1024, ffd_smem, st>>>(int(n), cap, w, *out);
   }
-  const size_t as_smem = (cap + 1) * 4;
-  if (as_smem > 48 * 1024)
-    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as_smem));
-  k_assign<<<nchunks, kRankThreads, as_smem, st>>>(d_len, n, cap, w, *out);
+  if (cap <= kSmemHistMaxCap) {
+    const size_t as_smem = (cap + 1) * 4;
+    if (as_smem > 48 * 1024)
+      VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_assign<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as_smem));
+    k_assign<false><<<nchunks, kRankThreads, as_smem, st>>>(d_len, n, cap, w, *out);
+  } else {
+    k_assign<true><<<nchunks, kRankThreads, 0, st>>>(d_len, n, cap, w, *out);
+  }
   const int64_t nsb = num_scan_blocks(n) + 1;
   run_scan(out->bin_count, n, out->bin_member_off, w.scan_part, nullptr, nullptr, st);
   run_scan(out->bin_fill, n, out->bin_token_off, w.scan_part + nsb, nullptr, out->status, st);
@@ -858,11 +944,17 @@ extern "C" int vlasim_pack_greedy_cuda(const int32_t* d_len, int64_t n, int32_t 
   carve(&w, d_ws, n, cap);
   cudaStream_t st = as_stream(stream);
   k_init<<<(n + 255) / 256, 256, 0, st>>>(*out, n);
-  if ((cap + 1) * 4 > 48 * 1024)
-    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (cap + 1) * 4));
-  k_hist<<<num_chunks(n), 512, (cap + 1) * 4, st>>>(d_len, n, cap, w.chunk_hist, out->status);  // validation
-  VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGreedySmem));
-  k_greedy<<<1, 32, kGreedySmem, st>>>(d_len, n, cap, *out);
+  if (int rc = launch_hist(d_len, n, cap, w, out, st)) return rc;  // validation
+  if (n <= kGreedyMaxBins) {  // at most n bins: the 3-level smem tree holds them all
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_greedy<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGreedySmem));
+    k_greedy<false><<<1, 32, kGreedySmem, st>>>(d_len, n, cap, w, *out);
+  } else {
+    const int64_t gstride = (n + 31) & ~int64_t(31);
+    const int64_t nfill = std::min<int64_t>(gstride, kGreedyDeepMaxBins);
+    k_greedy_fill<<<(nfill + 255) / 256, 256, 0, st>>>(w.spill, w.spill + gstride, nfill, cap);
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_greedy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGreedyDeepSmem));
+    k_greedy<true><<<1, 32, kGreedyDeepSmem, st>>>(d_len, n, cap, w, *out);
+  }
   const int64_t nsb = num_scan_blocks(n) + 1;
   run_scan(out->bin_count, n, out->bin_member_off, w.scan_part, nullptr, nullptr, st);
   run_scan(out->bin_fill, n, out->bin_token_off, w.scan_part + nsb, nullptr, out->status, st);

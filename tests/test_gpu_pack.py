@@ -76,7 +76,8 @@ def test_random_instances(gpu, orc, seed):
 
 def test_equal_lengths_and_edge_caps(gpu, orc):
     from paper_2603_11101_b200 import packing
-    for L, cap in [([8] * 100, 8), ([1] * 5000, 7), ([4] * 33, 8), ([16384] * 3, 16384), ([1], 1)]:
+    for L, cap in [([8] * 100, 8), ([1] * 5000, 7), ([4] * 33, 8), ([16384] * 3, 16384), ([1], 1),
+                   ([65535] * 2 + [1] * 3, 65535), ([40000, 30000, 25000, 1, 2, 3] * 50, 65535)]:
         L = np.array(L, np.int32)
         _check_plan(orc, L, cap, packing.pack_ffd(L, cap))
 
@@ -138,4 +139,46 @@ def test_greedy_config1_and_long_tail(gpu, orc):
     L = np.asarray(gen_lengths(64, 0, 16, 512), np.int32)
     _check_plan(orc, L, 2048, packing.pack_greedy(L, 2048), mode=2)
     L = np.asarray(gen_lengths(200000, DIST_GEOMETRIC, 0.02, 500, label="lengths", seed=42), np.int32)
+    _check_plan(orc, L, 8192, packing.pack_greedy(L, 8192), mode=2)
+
+
+# ---- inputs beyond the shared-memory working sets (ADVICE r1 pack.cu:211):
+# the reference packs any list of lengths in [1, capacity]; so must the GPU.
+@pytest.mark.parametrize("case", ["5000_then_1", "many_open_bins", "u1000_6000", "5000_3000"])
+def test_ffd_open_bin_spill(gpu, orc, case):
+    from paper_2603_11101_b200 import packing
+    rng = np.random.default_rng(7)
+    if case == "5000_then_1":      # 20k bins stay open (room 3192 >= every later length 1)
+        L = np.array([5000] * 20000 + [1] * 20000, np.int32)
+    elif case == "many_open_bins":  # 60k bins with room 1 left, then a class of length 1
+        L = np.array([8191] * 60000 + [1] * 70000, np.int32)
+    elif case == "u1000_6000":
+        L = rng.integers(1000, 6001, 100_000).astype(np.int32)
+    else:
+        L = np.array([5000] * 20000 + [3000] * 20000, np.int32)
+    _check_plan(orc, L, 8192, packing.pack_ffd(L, 8192), mode=1)
+
+
+@pytest.mark.parametrize("cap", [32768, 65535])
+def test_large_capacity(gpu, orc, cap):
+    """cap > 40959: histogram / rank counters in HBM; cap up to VLASIM_PACK_MAX_CAPACITY."""
+    from paper_2603_11101_b200 import packing
+    rng = np.random.default_rng(cap)
+    for n, hi in [(500, cap), (20_000, cap // 8), (3000, cap)]:
+        L = rng.integers(1, hi + 1, n).astype(np.int32)
+        _check_plan(orc, L, cap, packing.pack_ffd(L, cap), mode=1)
+        _check_plan(orc, L, cap, packing.pack_greedy(L, cap), mode=2)
+
+
+@pytest.mark.parametrize("case", ["40k_full_bins", "alternating", "long_tail_100k"])
+def test_greedy_deep_tree(gpu, orc, case):
+    """More than 32768 bins: the greedy room tree's level 0 lives in HBM (up to 2^20 bins)."""
+    from paper_2603_11101_b200 import packing
+    rng = np.random.default_rng(11)
+    if case == "40k_full_bins":
+        L = np.array([8192] * 40000 + [1] * 100, np.int32)
+    elif case == "alternating":      # 5000, 1, 5000, 1 ...: 40k bins, ones fill the earliest
+        L = np.array([5000, 1] * 40000, np.int32)
+    else:
+        L = rng.integers(1, 8193, 100_000).astype(np.int32)
     _check_plan(orc, L, 8192, packing.pack_greedy(L, 8192), mode=2)

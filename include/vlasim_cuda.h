@@ -234,6 +234,39 @@ int vlasim_fp8_quant_error_cuda(const void* d_x, const uint8_t* d_codes, const f
                                 int32_t heads, int32_t d, float* d_group_maxrel, double* d_group_sse,
                                 int32_t* d_group_count, vlasim_stream_t stream);
 
+/* ------------------------------------------------------------------ general quantizer
+ * Replaces vlasim::quantize / dequantize / quant_error of the reference's quantizer module
+ * (proj/CMakeLists.txt:18-21 src/quant/{fp8,tensor,quantize,compression}.cpp; contract
+ * SPEC.md:539-627) on the GPU: Granularity PerTensor | PerChannel(axis) | PerBlock(128, 128 over
+ * the last two dims) over an fp32 or bf16 row-major tensor of 1-8 dims.
+ * Scales (fp32, RN(amax / 448), 1 for an all-zero group) are laid out per granularity:
+ *   PerTensor [1];  PerChannel [shape[axis]];  PerBlock [Π shape[:-2], ⌈rows/128⌉, ⌈cols/128⌉].
+ * Codes are the exact RNE E4M3 code of |x|·448/amax, one byte per element
+ * in the input's layout.  Non-finite input → VLASIM_ECONFIG naming the flat index:
+ * with VLASIM_SYNC_CHECK the call synchronises and returns it; otherwise d_status ({code, index},
+ * optional) holds it and no codes are written. */
+enum { VLASIM_GRAN_TENSOR = 0, VLASIM_GRAN_CHANNEL = 1, VLASIM_GRAN_BLOCK = 2 };
+enum { VLASIM_DTYPE_F32 = 0, VLASIM_DTYPE_BF16 = 1 };
+
+int64_t vlasim_fp8_groups(const int64_t* shape, int32_t ndim, int32_t granularity, int32_t axis);
+size_t vlasim_fp8_quantize_workspace_size(const int64_t* shape, int32_t ndim, int32_t granularity, int32_t axis);
+int vlasim_fp8_quantize_cuda(const void* d_x, int32_t dtype, const int64_t* shape, int32_t ndim, int32_t granularity,
+                             int32_t axis, uint8_t* d_codes, float* d_scales, int32_t* d_status, void* d_workspace,
+                             size_t workspace_bytes, uint32_t flags, vlasim_stream_t stream);
+/* out = fp32(value(code) · scale of its group) */
+int vlasim_fp8_dequantize_cuda(const uint8_t* d_codes, const float* d_scales, const int64_t* shape, int32_t ndim,
+                               int32_t granularity, int32_t axis, float* d_out, vlasim_stream_t stream);
+/* quant_error(original, qt) per group, reduced in a fixed order (bit-identical run
+ * to run): max relative error over elements in E4M3's normal range, Σ squared error
+ * (fp64), element count.  Output arrays hold vlasim_fp8_error_groups(...) entries: the groups of the
+ * granularity, except PerTensor, which uses ⌈n / 65536⌉ entries of scratch and leaves the result in
+ * entry 0. */
+int64_t vlasim_fp8_error_groups(const int64_t* shape, int32_t ndim, int32_t granularity, int32_t axis);
+int vlasim_fp8_quant_error_general_cuda(const void* d_x, int32_t dtype, const uint8_t* d_codes, const float* d_scales,
+                                        const int64_t* shape, int32_t ndim, int32_t granularity, int32_t axis,
+                                        float* d_group_maxrel, double* d_group_sse, int64_t* d_group_count,
+                                        vlasim_stream_t stream);
+
 /* ------------------------------------------------------------------ synthetic inputs
  * Counter-based values shared with the CPU oracle:
  * x[i] = (top8(splitmix64(seed ^ i)) - 128) / 128, exactly representable in bf16. */

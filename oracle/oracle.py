@@ -53,6 +53,7 @@ def lib():
             "oracle_mha_bwd_f64": [V] * 9 + [L, V, L, L, L, L, I, D, I],
             "oracle_mha_bwd_f32": [V] * 9 + [L, V, L, L, L, L, I, D, I],
             "oracle_fp8_quant_block": [V, L, L, L, I, V, V],
+            "oracle_fp8_quantize": [V, V, I, I, I, V, V],
             "oracle_e4m3_encode": [V, L, V],
             "oracle_e4m3_values": [V],
             "oracle_gen_lengths": [C.c_uint64, C.c_char_p, I, L, D, D, D, V],
@@ -243,6 +244,71 @@ def fp8_quant_block(x, quotient_fp32=True):
     _chk(lib().oracle_fp8_quant_block(_p(x, f32p), T, Hh, d, 1 if quotient_fp32 else 0, _p(codes, u8p),
                                       _p(scales, f32p)))
     return codes, scales
+
+
+GRAN = {"tensor": 0, "channel": 1, "block": 2}
+
+
+def fp8_groups(shape, gran, axis=0):
+    """Group count and flat index → group map of a granularity."""
+    shape = tuple(int(s) for s in shape)
+    n = int(np.prod(shape))
+    i = np.arange(n, dtype=np.int64)
+    if gran == "tensor":
+        return 1, np.zeros(n, np.int64)
+    if gran == "channel":
+        axis = axis % len(shape)
+        inner = int(np.prod(shape[axis + 1:])) if axis + 1 < len(shape) else 1
+        return shape[axis], (i // inner) % shape[axis]
+    rows, cols = shape[-2], shape[-1]
+    nbr, nbc = (rows + 127) // 128, (cols + 127) // 128
+    c, r, b = i % cols, (i // cols) % rows, i // (rows * cols)
+    return (n // (rows * cols)) * nbr * nbc, (b * nbr + r // 128) * nbc + c // 128
+
+
+def fp8_quantize(x, gran="block", axis=0):
+    """SPEC quantize at any granularity: (codes uint8 like x, scales f32 [groups])."""
+    x = np.ascontiguousarray(x, np.float32)
+    shape = np.asarray(x.shape, np.int64)
+    ngroups, _ = fp8_groups(x.shape, gran, axis)
+    codes = np.empty(x.shape, np.uint8)
+    scales = np.empty(ngroups, np.float32)
+    _chk(lib().oracle_fp8_quantize(_p(x, f32p), _p(shape, i64p), x.ndim, GRAN[gran], axis, _p(codes, u8p),
+                                   _p(scales, f32p)))
+    return codes, scales
+
+
+def e4m3_decode_table():
+    vals = np.zeros(256, np.float32)
+    for c in range(256):  # E4M3 decode (SPEC.md:544-562): bias 7, subnormals, 0x7f/0xff NaN
+        e, m = (c >> 3) & 0xF, c & 7
+        v = (m / 8.0) * 2.0 ** -6 if e == 0 else ((1 + m / 8.0) * 2.0 ** (e - 7) if not (e == 15 and m == 7) else np.nan)
+        vals[c] = -v if c & 0x80 else v
+    return vals
+
+
+def fp8_dequantize(codes, scales, gran="block", axis=0):
+    """codes × group scale in fp32, original shape restored."""
+    _, grp = fp8_groups(codes.shape, gran, axis)
+    return (e4m3_decode_table()[codes.reshape(-1)] * np.asarray(scales, np.float32)[grp]).astype(np.float32).reshape(
+        codes.shape)
+
+
+def fp8_quant_error_general(x, codes, scales, gran="block", axis=0):
+    """quant_error per group, the arithmetic of fp8_quant_error below:
+    (group max_rel f32, group sse f64, group count, max_rel, mse)."""
+    x = np.asarray(x, np.float32).reshape(-1)
+    ngroups, grp = fp8_groups(codes.shape, gran, axis)
+    sc = np.asarray(scales, np.float32)[grp]
+    deq = (e4m3_decode_table()[codes.reshape(-1)] * sc).astype(np.float32)
+    diff = (deq - x).astype(np.float32)
+    normal = np.abs((x / sc).astype(np.float32)) >= np.float32(2.0 ** -6)
+    rel = np.where(normal, np.abs(diff) / np.where(x != 0, np.abs(x), np.float32(1)), np.float32(0)).astype(np.float32)
+    gmax = np.zeros(ngroups, np.float32)
+    np.maximum.at(gmax, grp, rel)
+    gsse = np.bincount(grp, weights=diff.astype(np.float64) ** 2, minlength=ngroups)
+    gcnt = np.bincount(grp, minlength=ngroups)
+    return gmax, gsse, gcnt, float(gmax.max()), float(gsse.sum() / gcnt.sum())
 
 
 def fp8_quant_error(x, codes, scales):

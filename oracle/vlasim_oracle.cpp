@@ -636,6 +636,52 @@ int oracle_fp8_quant_block(const float* x, std::int64_t T, std::int64_t heads, s
         }
   });
 }
+// The SPEC's quantize for every Granularity: groups are
+// PerTensor (one), PerChannel(axis) (index along `axis`), PerBlock (128×128 tiles of the last two
+// dims, per leading index; block_partition SPEC.md:566-572).  scale_g = fp32(amax_g / 448) (1 if
+// the group is all zero); codes by the exhaustive midpoint search on the REAL quotient
+// x·448 / amax_g (e4m3_encode_ratio).  Non-finite input → ConfigError.
+// gran: 0 tensor, 1 channel, 2 block.  Scales laid out like vlasim_fp8_quantize_cuda's.
+int oracle_fp8_quantize(const float* x, const std::int64_t* shape, int ndim, int gran, int axis,
+                        std::uint8_t* codes, float* scales) {
+  return guarded([&] {
+    std::int64_t n = 1;
+    for (int i = 0; i < ndim; ++i) n *= shape[i];
+    std::vector<std::int64_t> grp(static_cast<std::size_t>(n));
+    std::int64_t groups = 1;
+    if (gran == 1) {
+      if (axis < 0) axis += ndim;
+      std::int64_t inner = 1;
+      for (int i = axis + 1; i < ndim; ++i) inner *= shape[i];
+      groups = shape[axis];
+      for (std::int64_t i = 0; i < n; ++i) grp[i] = (i / inner) % groups;
+    } else if (gran == 2) {
+      if (ndim < 2) throw vlasim::ConfigError("block_partition: shape needs >= 2 dims");
+      const std::int64_t rows = shape[ndim - 2], cols = shape[ndim - 1];
+      const std::int64_t nbr = (rows + 127) / 128, nbc = (cols + 127) / 128;
+      groups = (n / (rows * cols)) * nbr * nbc;
+      for (std::int64_t i = 0; i < n; ++i) {
+        const std::int64_t c = i % cols, r = (i / cols) % rows, b = i / (rows * cols);
+        grp[i] = (b * nbr + r / 128) * nbc + c / 128;
+      }
+    } else {
+      std::fill(grp.begin(), grp.end(), 0);
+    }
+    std::vector<double> amax(static_cast<std::size_t>(groups), 0.0);
+    for (std::int64_t i = 0; i < n; ++i) {
+      const double a = std::fabs(static_cast<double>(x[i]));
+      if (!std::isfinite(a)) throw vlasim::ConfigError("quantize: non-finite input");
+      amax[grp[i]] = std::max(amax[grp[i]], a);
+    }
+    for (std::int64_t g = 0; g < groups; ++g)
+      scales[g] = amax[g] == 0 ? 1.0f : static_cast<float>(amax[g]) / 448.0f;
+    for (std::int64_t i = 0; i < n; ++i) {
+      const double a = amax[grp[i]];
+      codes[i] = a == 0 ? vlasim::oracle::e4m3_encode(static_cast<double>(x[i]))
+                        : vlasim::oracle::e4m3_encode_ratio(static_cast<double>(x[i]) * 448.0, a);
+    }
+  });
+}
 int oracle_e4m3_encode(const double* x, std::int64_t n, std::uint8_t* codes) {
   return guarded([&] {
     for (std::int64_t i = 0; i < n; ++i) codes[i] = vlasim::oracle::e4m3_encode(x[i]);

@@ -76,6 +76,15 @@ _SIGS = {
                                                 C.c_void_p]),
     "vlasim_fp8_quant_error_cuda": (C.c_int, [C.c_void_p, C.c_void_p, f32p, C.c_int64, C.c_int32, C.c_int32, f32p,
                                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vlasim_fp8_groups": (C.c_int64, [i64p, C.c_int32, C.c_int32, C.c_int32]),
+    "vlasim_fp8_quantize_workspace_size": (C.c_size_t, [i64p, C.c_int32, C.c_int32, C.c_int32]),
+    "vlasim_fp8_quantize_cuda": (C.c_int, [C.c_void_p, C.c_int32, i64p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                           f32p, i32p, C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]),
+    "vlasim_fp8_dequantize_cuda": (C.c_int, [C.c_void_p, f32p, i64p, C.c_int32, C.c_int32, C.c_int32, f32p,
+                                             C.c_void_p]),
+    "vlasim_fp8_error_groups": (C.c_int64, [i64p, C.c_int32, C.c_int32, C.c_int32]),
+    "vlasim_fp8_quant_error_general_cuda": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, f32p, i64p, C.c_int32,
+                                                      C.c_int32, C.c_int32, f32p, C.c_void_p, i64p, C.c_void_p]),
     "vlasim_fill_synthetic_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p]),
     "vlasim_gen_lengths": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, i32p]),

@@ -720,9 +720,19 @@ __global__ void k_scan_apply(const int32_t* __restrict__ in, int64_t n, const in
 }
 
 // ------------------------------------------------------------------ layout
+// On a device-side input error (status set upstream; the caller may not synchronise — the CUDA
+// graph path) the plan is left DEFINED and empty: every cu_seqlens entry 0 and num_bins 0, so
+// kernels stream-ordered after the packer see zero-length segments and do no work.
 __global__ void k_layout(const int32_t* __restrict__ len, int64_t n, vlasim_pack_out out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (out.status[0] != 0) return;
+  if (out.status[0] != 0) {
+    if (i < n) out.cu_seqlens[i] = 0;
+    if (i == 0) {
+      out.cu_seqlens[n] = 0;
+      *out.num_bins = 0;
+    }
+    return;
+  }
   if (i >= n) return;
   const int b = out.bin_of[i], s = out.slot[i], t = out.tok_off[i];
   const int mo = out.bin_member_off[b];

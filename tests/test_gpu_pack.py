@@ -182,3 +182,16 @@ def test_greedy_deep_tree(gpu, orc, case):
     else:
         L = rng.integers(1, 8193, 100_000).astype(np.int32)
     _check_plan(orc, L, 8192, packing.pack_greedy(L, 8192), mode=2)
+
+
+def test_unsynchronised_error_leaves_defined_empty_plan(gpu):
+    """sync_check=False (the CUDA-graph path): a bad length leaves the status on the device and a
+    defined, empty plan (cu_seqlens all 0, num_bins 0) that downstream kernels treat as no work."""
+    from paper_2603_11101_b200 import packing
+    good = packing.pack_ffd([5, 3, 7, 2], 8)
+    assert good.num_bins() > 0
+    bad = packing.pack_ffd([5, 3, 9, 2], 8, plan=good, sync_check=False)
+    torch.cuda.synchronize()
+    assert bad.status.cpu().tolist() == [2, 2]  # VLASIM_ECONFIG, offending id
+    assert bad.num_bins() == 0
+    assert int(bad.cu_seqlens.abs().sum()) == 0

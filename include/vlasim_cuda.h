@@ -162,7 +162,8 @@ typedef struct vlasim_attn_args {
   const int32_t* cu_seqlens;  /* [num_seqs + 1]                                      */
   const int32_t* prefix_len;  /* [num_seqs]  (mask_mode == PREFIX only)              */
   int32_t num_seqs;
-  int64_t total_tokens;       /* T                                                   */
+  int64_t total_tokens;       /* T: rows of the tensors (>= cu_seqlens[num_seqs]; rows past
+                                 the last segment belong to none — the padded layout below)  */
   int32_t num_heads;          /* H                                                   */
   int32_t num_kv_heads;       /* Hkv (divides H)                                     */
   int32_t head_dim;           /* d                                                   */
@@ -266,6 +267,22 @@ int vlasim_fp8_quant_error_general_cuda(const void* d_x, int32_t dtype, const ui
                                         const int64_t* shape, int32_t ndim, int32_t granularity, int32_t axis,
                                         float* d_group_maxrel, double* d_group_sse, int64_t* d_group_count,
                                         vlasim_stream_t stream);
+
+/* ------------------------------------------------------------------ dynamic padding (π0.5)
+ * dynamic_pad_length (PAPER.md:166-176 π0.5's per-batch max_length) on the device:
+ * *d_pad_to = max(len), d_cu_seqlens [n+1] = exclusive scan of len (the valid tokens as segments),
+ * d_seg_src [n] = i·pad_to.  With these, vlasim_varlen_attn_*_cuda run directly on padded
+ * [n, pad_to, heads, d] storage (total_tokens = n·pad_to, seg_src set): each sample is one
+ * segment, pad keys are never visible and pad queries never computed.  In that layout the
+ * caller zero-initialises o and lse (their pad rows are never written and the backward reads
+ * them).  A length < 1 → VLASIM_ECONFIG naming the id.
+ * pad: sample-major rows (sample i at d_src_off[i]) → [n, pad_to] rows, zero fill; unpad: inverse. */
+int vlasim_dynamic_pad_cuda(const int32_t* d_len, int64_t n, int32_t* d_pad_to, int32_t* d_cu_seqlens,
+                            int32_t* d_seg_src, int32_t* d_status, uint32_t flags, vlasim_stream_t stream);
+int vlasim_pad_rows_cuda(const void* d_src, void* d_padded, int64_t row_bytes, const int32_t* d_len,
+                         const int32_t* d_src_off, const int32_t* d_pad_to, int64_t n, vlasim_stream_t stream);
+int vlasim_unpad_rows_cuda(const void* d_padded, void* d_dst, int64_t row_bytes, const int32_t* d_len,
+                           const int32_t* d_src_off, const int32_t* d_pad_to, int64_t n, vlasim_stream_t stream);
 
 /* ------------------------------------------------------------------ synthetic inputs
  * Counter-based values shared with the CPU oracle:

@@ -85,6 +85,10 @@ _SIGS = {
     "vlasim_fp8_error_groups": (C.c_int64, [i64p, C.c_int32, C.c_int32, C.c_int32]),
     "vlasim_fp8_quant_error_general_cuda": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, f32p, i64p, C.c_int32,
                                                       C.c_int32, C.c_int32, f32p, C.c_void_p, i64p, C.c_void_p]),
+    "vlasim_dynamic_pad_cuda": (C.c_int, [i32p, C.c_int64, i32p, i32p, i32p, i32p, C.c_uint32, C.c_void_p]),
+    "vlasim_pad_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, i32p, i32p, C.c_int64, C.c_void_p]),
+    "vlasim_unpad_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, i32p, i32p, C.c_int64,
+                                         C.c_void_p]),
     "vlasim_fill_synthetic_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p]),
     "vlasim_gen_lengths": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, i32p]),

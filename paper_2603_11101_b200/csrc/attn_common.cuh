@@ -15,7 +15,9 @@ struct RowSpan {
   int seg;
 };
 
-// Largest s with cu[s] <= t (cu strictly increasing, cu[0] = 0, cu[nseq] = T).
+// Largest s with cu[s] <= t (cu strictly increasing, cu[0] = 0, cu[nseq] <= T: rows of the tensors
+// past cu[nseq] — e.g. the pad rows of a dynamically padded batch read through seg_src — belong to
+// no segment).
 __device__ __forceinline__ int find_segment(const int32_t* __restrict__ cu, int nseq, int t) {
   int lo = 0, hi = nseq - 1;
   while (lo < hi) {
@@ -28,7 +30,7 @@ __device__ __forceinline__ int find_segment(const int32_t* __restrict__ cu, int 
 __device__ __forceinline__ RowSpan row_span(const int32_t* __restrict__ cu, const int32_t* __restrict__ prefix,
                                             int nseq, int mask_mode, int t, int T) {
   RowSpan r{0, 0, -1};
-  if (t < 0 || t >= T) return r;
+  if (t < 0 || t >= T || t >= __ldg(cu + nseq)) return r;  // rows past the last segment: none
   const int s = find_segment(cu, nseq, t);
   const int b = __ldg(cu + s), e = __ldg(cu + s + 1);
   int P = e - b;
@@ -44,7 +46,7 @@ __device__ __forceinline__ RowSpan row_span(const int32_t* __restrict__ cu, cons
 __device__ __forceinline__ RowSpan key_span(const int32_t* __restrict__ cu, const int32_t* __restrict__ prefix,
                                             int nseq, int mask_mode, int j, int T) {
   RowSpan r{0, 0, -1};
-  if (j < 0 || j >= T) return r;
+  if (j < 0 || j >= T || j >= __ldg(cu + nseq)) return r;
   const int s = find_segment(cu, nseq, j);
   const int b = __ldg(cu + s), e = __ldg(cu + s + 1);
   int P = e - b;

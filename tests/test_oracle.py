@@ -370,3 +370,20 @@ def test_fp8_quant_error_known_answers(orc):
     xs[:128] = x[:128]
     one = np.concatenate([x[:128], x[128:]], 0)
     assert s[0, 0, 0] < 1e-3 * s[0, 1, 0]
+
+
+def test_prune_corpus_spec_examples():
+    """SPEC.md:487-491 through the product's host helpers: prune 'right' → 304; prune twice → error;
+    pruning across a corpus strictly lowers attention_flops."""
+    from paper_2603_11101_b200 import ConfigError
+    from paper_2603_11101_b200.packing import SampleLen, attention_flops
+    from paper_2603_11101_b200.padding import prune_corpus
+    s = SampleLen(0, {"left": 256, "right": 256}, 48)
+    (p,) = prune_corpus([s], "right")
+    assert p.total_len == 304
+    with pytest.raises(ConfigError):
+        prune_corpus([p], "right")
+    corpus = [SampleLen(i, {"left": 256, "right": 256}, 16 + 7 * i) for i in range(10)]
+    before = attention_flops([c.total_len for c in corpus], 64)
+    after = attention_flops([c.total_len for c in prune_corpus(corpus, "right")], 64)
+    assert after < before

@@ -646,6 +646,38 @@ def main():
                "pipelining": "H2D / compute / D2H on separate streams, double-buffered device sets"}
         del sets, hin, hout
 
+    # ---------------------------------------------------------------- DDP gradient all-reduce (N > 1)
+    # The step after the path in training: measured outside the attention step, which
+    # has no collective.  NCCL all-reduce times per bucket size (CUDA events, max over ranks), the
+    # least-squares (latency, bandwidth) fit replacing the SPEC's ring-model constants, and the
+    # bucketed, stream-overlapped all-reduce of one Eagle-LM layer's projection gradients.
+    ddp = None
+    if world > 1:
+        from paper_2603_11101_b200 import ddp as vddp
+        sizes = [1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20]
+        ts = vddp.measure_allreduce(sizes, iters=10)
+        lat, bw, resid = vddp.fit_alpha_beta(sizes, ts, world)
+        layer = [H * D * H * D] * 4  # Wq, Wk, Wv, Wo of the H16 d128 (2048-wide) attention layer
+        gb = vddp.GradientBuckets(layer, bucket_bytes=32 << 20, dtype=torch.bfloat16, device=dev)
+        red = vddp.BucketAllReducer(gb)
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for it in range(4):
+            dist.barrier()
+            s_ev.record()
+            for i in reversed(range(len(layer))):
+                red.mark_ready(i)
+            red.finish()
+            e_ev.record()
+            torch.cuda.synchronize()
+        lt = torch.tensor([s_ev.elapsed_time(e_ev)], dtype=torch.float64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+        ddp = {"allreduce_bytes": sizes, "allreduce_ms": [t * 1e3 for t in ts],
+               "busbw_gbs": [2 * (world - 1) / world * b / t / 1e9 for b, t in zip(sizes, ts)],
+               "fit_link_latency_us": lat * 1e6, "fit_bandwidth_gbs": bw / 1e9, "fit_max_rel_residual": resid,
+               "ring_formula_ms_nvlink5_900gbs_2us": [vddp.allreduce_time(b, world, 900e9, 2e-6) * 1e3 for b in sizes],
+               "layer_grad_bytes": gb.total * 2, "layer_buckets": len(gb.buckets), "layer_allreduce_ms": float(lt.item()),
+               "note": "NCCL over NVLink/NVSwitch, bf16 gradients, outside the attention step (no collective there)"}
+
     # ---------------------------------------------------------------- CPU baseline, other configs (rank 0, N = 1)
     cpu = None
     configs = None
@@ -694,7 +726,7 @@ def main():
             "kernel_ms": {"fwd_prep": kf[0], "fwd_attention": kf[1], "bwd_pre": kb[0], "bwd_tiles": kb[1],
                           "bwd_dkdv": kb[2], "bwd_dq": kb[3]},
             "clocks": clk.summary(),
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "ddp_allreduce": ddp,
             "gpu_launches": LAUNCHES_PER_STEP * a.steps,
         }
         if configs is not None:

@@ -472,7 +472,7 @@ def main():
 
     bufs = tensors()
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    pipelined = a.pipeline == "on" and not a.no_graph and world == 1
+    pipelined = a.pipeline == "on" and not a.no_graph
     budget = nsm - 1 if pipelined else 0
 
     def pack_phase(j, b):
@@ -525,10 +525,17 @@ def main():
         return g
 
     graphs = {}
-    use_graph = not a.no_graph and world == 1  # N > 1: eager (NCCL collective in the step)
+    use_graph = not a.no_graph  # N > 1: the NCCL all-gather of the lengths is captured with the step
+    graph_note = None
     if use_graph:
-        graphs[(id(bufs), 0)] = capture(lambda: step(0))
-        graphs[(id(bufs), 1)] = capture(lambda: step(1))
+        try:
+            graphs[(id(bufs), 0)] = capture(lambda: step(0))
+            graphs[(id(bufs), 1)] = capture(lambda: step(1))
+        except RuntimeError as e:  # (NCCL capture unsupported on this stack: fall back to direct launches)
+            graphs.clear()
+            use_graph = False
+            graph_note = f"graph capture failed ({str(e)[:80]}); direct launches"
+            torch.cuda.synchronize()
 
     def run_step(i, b=bufs):
         g = graphs.get((id(b), i & 1))
@@ -713,7 +720,7 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB/GPU)" % (4 * T * H * D * 2 / 1e9),
                        "parallelism": f"packs sharded over {world} GPU(s): all-gather of lengths (NCCL) + GPU FFD + "
                                       "device LPT inside every step; no collective on attention",
-                       "launch": "CUDA graph replay of the step" if use_graph else "direct launches",
+                       "launch": "CUDA graph replay of the step" if use_graph else (graph_note or "direct launches"),
                        "pipeline": "packing of batch i+1 on a side stream (1 SM) beside batch i's attention "
                                    "(SMs-1 CTAs)" if pipelined else "pack then attention, in sequence",
                        "layout": "sample-major rows; gather / scatter folded into the attention kernels' TMA "
@@ -733,7 +740,13 @@ def main():
             line["configs"] = configs
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        # Captured CUDA graphs hold the NCCL communicator; tearing the process group down under them
+        # can block in ncclCommDestroy.  Synchronise every rank, then leave without destructors.
+        torch.cuda.synchronize()
+        dist.barrier()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 if __name__ == "__main__":

@@ -26,6 +26,10 @@
 
 using namespace vlasim_dev;
 
+namespace vlasim_host {
+void* fwd_ws_tiles(const vlasim_attn_args* a, void* ws);
+}
+
 namespace {
 
 struct FwdParams {
@@ -313,6 +317,359 @@ int launch_fwd(const vlasim_attn_args* a, void* tiles_buf, cudaStream_t st) {
   return VLASIM_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent variant (head_dim 256, config 3): grid = min(#SMs, items, sm_budget); each CTA walks
+// the cost-sorted items (segment-aligned Q tile, head) on the boustrophedon schedule with the same
+// three roles.  Every pipeline runs on CONTINUOUS counters across items, so an item boundary costs
+// no prologue: the next item's Q tile loads as soon as the current item's last S MMA has read the
+// Q buffer (bar_q_empty), its K/V tiles stream through the same ring, its first S MMA issues while
+// the softmax warps drain the current O, and only its first P·V waits for that drain (bar_o_free):
+// O (256 columns) is single-buffered — S[2] (2·BN) + O (HD) + P[2] (BN) = 448 of 512 columns.
+// Visible-key spans per token come from k_spans_p (the forward workspace's span table).
+__global__ void k_spans_p(const int32_t* __restrict__ cu, const int32_t* __restrict__ prefix, int nseq, int mask,
+                          int T, int2* __restrict__ rows_span) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const RowSpan r = row_span(cu, prefix, nseq, mask, t, T);
+  rows_span[t] = make_int2(r.lo, r.hi);
+}
+
+// Persistent layout: Q | K ring (KS) | V ring (VS).  K and V have separate rings: a K stage is
+// released as soon as its S MMA has read it and a V stage after its P·V, so the K/V streaming from
+// L2 — the limiter of this kernel (128 flop per K/V byte at d = 256, BN = 64) — is not held up by
+// the softmax of the tile.  The producer issues V one tile behind K.
+template <int HD, int BN, int KS, int VS>
+struct FwdPCfg {
+  static constexpr int BM = 128;
+  static constexpr int Q_BYTES = BM * HD * 2;
+  static constexpr int KV_BYTES = BN * HD * 2;
+  static constexpr int OFF_K = Q_BYTES, OFF_V = OFF_K + KS * KV_BYTES;
+  static constexpr int SMEM = OFF_V + VS * KV_BYTES + 1024;
+  static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, P_COL = 2 * BN + HD;
+  static_assert(P_COL + BN <= 512, "TMEM budget");
+  static_assert(SMEM <= 232448 - 1024, "smem budget");
+};
+
+struct FwdPParams {
+  __nv_bfloat16* o;
+  float* lse;
+  const int2* rows_span;
+  const int4* tiles;
+  const int* ntiles;
+  int T, H, Hkv;
+  float scale_log2;
+};
+
+struct FwdPItem {
+  int q0, qe, dl, h, kh, kv_lo, nkv;
+};
+template <int BN>
+__device__ __forceinline__ FwdPItem fwdp_item(const FwdPParams& p, int i) {
+  FwdPItem it;
+  const int4 t = __ldg(&p.tiles[i / p.H]);
+  it.h = i % p.H;
+  it.q0 = t.x;
+  it.qe = t.y;
+  it.dl = t.z;
+  it.kh = it.h / (p.H / p.Hkv);
+  it.kv_lo = __ldg(&p.rows_span[t.x].x);  // spans are monotone inside a segment
+  const int kv_hi = __ldg(&p.rows_span[t.y - 1].y);
+  it.nkv = max(0, (kv_hi - it.kv_lo + BN - 1) / BN);
+  return it;
+}
+
+template <int HD, int BN, int KS, int VS>
+__global__ void __launch_bounds__(192, 1)
+    attn_fwd_p_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const FwdPParams p) {
+  using Cfg = FwdPCfg<HD, BN, KS, VS>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+
+  __shared__ uint64_t bar_q_full, bar_q_empty, bar_k_full[KS], bar_k_empty[KS], bar_v_full[VS], bar_v_empty[VS],
+      bar_s_full[2], bar_p_full[2], bar_o_ready, bar_o_done, bar_o_free;
+  __shared__ uint32_t tmem_base_s;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nitems = __ldg(p.ntiles) * p.H;
+  if (tid == 0) {
+    mbar_init(&bar_q_full, 1);
+    mbar_init(&bar_q_empty, 1);
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(&bar_k_full[s], 1);
+      mbar_init(&bar_k_empty[s], 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(&bar_v_full[s], 1);
+      mbar_init(&bar_v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_s_full[b], 1);
+      mbar_init(&bar_p_full[b], 4);
+    }
+    mbar_init(&bar_o_ready, 1);
+    mbar_init(&bar_o_done, 1);
+    mbar_init(&bar_o_free, 4);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 4) {
+    // ------------------------------------------------ TMA producer (V one tile behind K)
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      int gk = 0, gv = 0, k = 0;
+      int pv_row = -1, pv_kh = 0;  // the V tile still to load (data row, kv head)
+      auto load_v = [&]() {
+        const int st = gv % VS;
+        if (gv >= VS) mbar_wait(&bar_v_empty[st], ((gv / VS) - 1) & 1);
+        mbar_expect_tx(&bar_v_full[st], Cfg::KV_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_2d(sV + st * Cfg::KV_BYTES + c * BN * 128, &tmV, pv_kh * HD + c * 64, pv_row, &bar_v_full[st]);
+        ++gv;
+        pv_row = -1;
+      };
+      for (int m = 0;; ++m) {
+        const int i = sched_item(m);
+        if (i >= nitems) break;
+        const FwdPItem it = fwdp_item<BN>(p, i);
+        if (k > 0) mbar_wait(&bar_q_empty, (k - 1) & 1);  // the previous item's last S has read Q
+        mbar_expect_tx(&bar_q_full, Cfg::Q_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_2d(sQ + c * Cfg::BM * 128, &tmQ, it.h * HD + c * 64, it.q0 + it.dl, &bar_q_full);
+        for (int j = 0; j < it.nkv; ++j, ++gk) {
+          const int st = gk % KS;
+          if (gk >= KS) mbar_wait(&bar_k_empty[st], ((gk / KS) - 1) & 1);
+          const int kv0 = it.kv_lo + j * BN + it.dl;  // data row
+          mbar_expect_tx(&bar_k_full[st], Cfg::KV_BYTES);
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_2d(sK + st * Cfg::KV_BYTES + c * BN * 128, &tmK, it.kh * HD + c * 64, kv0, &bar_k_full[st]);
+          if (pv_row >= 0) load_v();
+          pv_row = kv0;
+          pv_kh = it.kh;
+        }
+        ++k;
+      }
+      if (pv_row >= 0) load_v();
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, BN, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      int g = 0, k = 0;
+      for (int m = 0;; ++m) {
+        const int i = sched_item(m);
+        if (i >= nitems) break;
+        const int nkv = fwdp_item<BN>(p, i).nkv;
+        mbar_wait(&bar_q_full, k & 1);
+        tc_fence_after();
+        if (nkv == 0) {  // (no visible key: cannot happen for a non-empty tile) keep the phases aligned
+          umma_commit(&bar_q_empty);
+          umma_commit(&bar_o_done);
+        }
+        for (int j = 0; j <= nkv; ++j) {
+          if (j < nkv) {
+            const int gj = g + j, st = gj % KS;
+            mbar_wait(&bar_k_full[st], (gj / KS) & 1);
+            tc_fence_after();
+            const uint32_t k_addr = smem_u32(sK + st * Cfg::KV_BYTES);
+            const uint32_t d_s = tmem + Cfg::S_COL + (gj & 1) * BN;
+#pragma unroll
+            for (int s = 0; s < HD / 16; ++s) {
+              const uint64_t a = make_sdesc_sw128(q_addr + (s / 4) * Cfg::BM * 128 + (s % 4) * 32, 16, 1024);
+              const uint64_t b = make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024);
+              umma_f16_ss(d_s, a, b, idesc_s, s > 0);
+            }
+            umma_commit(&bar_s_full[gj & 1]);
+            umma_commit(&bar_k_empty[st]);
+            if (j == nkv - 1) umma_commit(&bar_q_empty);  // Q free for the next item's tile
+          }
+          if (j > 0) {
+            const int gj = g + j - 1, st = gj % VS;
+            mbar_wait(&bar_p_full[gj & 1], (gj >> 1) & 1);
+            if (j == 1 && k > 0) mbar_wait(&bar_o_free, (k - 1) & 1);  // previous item's O drained
+            mbar_wait(&bar_v_full[st], (gj / VS) & 1);
+            tc_fence_after();
+            const uint32_t v_addr = smem_u32(sV + st * Cfg::KV_BYTES);
+            const uint32_t a_tm = tmem + Cfg::P_COL + (gj & 1) * (BN / 2);
+#pragma unroll
+            for (int s = 0; s < BN / 16; ++s) {
+              const uint64_t b = make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024);
+              umma_f16_ts(tmem + Cfg::O_COL, a_tm + s * 8, b, idesc_o, (j > 1 || s > 0) ? 1u : 0u);
+            }
+            umma_commit(&bar_v_empty[st]);
+            umma_commit(&bar_o_ready);
+            if (j == nkv) umma_commit(&bar_o_done);
+          }
+        }
+        g += nkv;
+        ++k;
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax + epilogue (warps 0-3, thread = row)
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const float sl2 = p.scale_log2;
+    int g = 0, k = 0;
+    for (int m = 0;; ++m) {
+      const int i = sched_item(m);
+      if (i >= nitems) break;
+      const FwdPItem it = fwdp_item<BN>(p, i);
+      const int row = it.q0 + tid;
+      const int2 rs = row < it.qe ? __ldg(&p.rows_span[row]) : make_int2(0, 0);  // rows past the tile: none
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < it.nkv; ++j) {
+        const int gj = g + j, sb = gj & 1;
+        mbar_wait(&bar_s_full[sb], (gj >> 1) & 1);
+        tc_fence_after();
+        uint32_t r[BN];
+#pragma unroll
+        for (int c = 0; c < BN; c += 32)
+          tmem_ld32(tmem + lane_off + Cfg::S_COL + sb * BN + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+        tmem_wait_ld();
+        const int kv0 = it.kv_lo + j * BN;
+        const int c_lo = rs.x - kv0, c_hi = rs.y - kv0;
+        if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= BN)) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) r[c] = (c >= c_lo && c < c_hi) ? r[c] : __float_as_uint(-INFINITY);
+        }
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            mq[u] = fmax3(mq[u], __uint_as_float(r[c + 2 * u]), __uint_as_float(r[c + 2 * u + 1]));
+        }
+        float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
+        const bool grow = mt > m_run + kLazyRescale;
+        const float alpha = grow ? ex2_approx(m_run - mt) : 1.f;
+        if (__any_sync(0xffffffffu, grow && j > 0 && m_run != -INFINITY)) {
+          mbar_wait(&bar_o_ready, (gj - 1) & 1);  // P·V of the previous tile has landed in O
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_off + Cfg::O_COL + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+            tmem_st32(tmem + lane_off + Cfg::O_COL + c, o);
+          }
+        }
+        if (grow) {
+          l_run *= alpha;
+          m_run = mt;
+        }
+        const float msub = (m_run == -INFINITY) ? 0.f : m_run;
+        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-msub, -msub);
+        float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float2 a2 = f2_fma(make_float2(__uint_as_float(r[c + 2 * q]), __uint_as_float(r[c + 2 * q + 1])),
+                                     sl2v, nmv);
+            const float2 pe = make_float2(ex2_approx(a2.x), ex2_approx(a2.y));
+            lq[q & 1] = f2_add(lq[q & 1], pe);
+            pk[q] = pack_bf16x2(pe.x, pe.y);
+          }
+          tmem_st16(tmem + lane_off + Cfg::P_COL + sb * (BN / 2) + c / 2, pk);
+        }
+        l_run += (lq[0].x + lq[1].x) + (lq[0].y + lq[1].y);
+        tmem_wait_st();
+        tc_fence_before();
+        warp_arrive(&bar_p_full[sb]);
+      }
+      // epilogue: O / l → bf16 (direct row stores), LSE; then hand O back to the MMA warp
+      mbar_wait(&bar_o_done, k & 1);
+      tc_fence_after();
+      const bool valid = row < it.qe && rs.x < rs.y;
+      const float inv_l = (valid && l_run > 0.f) ? 1.f / l_run : 0.f;
+      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(row + it.dl) * p.H + it.h) * HD;
+#pragma unroll
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + Cfg::O_COL + c, o);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            pk[q] = pack_bf16x2(__uint_as_float(o[2 * q]) * inv_l, __uint_as_float(o[2 * q + 1]) * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      warp_arrive(&bar_o_free);
+      if (valid)
+        p.lse[static_cast<int64_t>(it.h) * p.T + row + it.dl] = (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+      g += it.nkv;
+      ++k;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+template <int HD, int BN, int KS, int VS>
+int launch_fwd_p(const vlasim_attn_args* a, void* ws, cudaStream_t st) {
+  using namespace vlasim_host;
+  using Cfg = FwdPCfg<HD, BN, KS, VS>;
+  CUtensorMap tq, tk, tv;
+  const uint64_t T = a->total_tokens;
+  if (int rc = encode_tmap_2d(&tq, a->q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, uint64_t(a->num_heads) * HD,
+                              uint64_t(a->num_heads) * HD * 2, 128, 64, true))
+    return rc;
+  if (int rc = encode_tmap_2d(&tk, a->k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, uint64_t(a->num_kv_heads) * HD,
+                              uint64_t(a->num_kv_heads) * HD * 2, BN, 64, true))
+    return rc;
+  if (int rc = encode_tmap_2d(&tv, a->v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, uint64_t(a->num_kv_heads) * HD,
+                              uint64_t(a->num_kv_heads) * HD * 2, BN, 64, true))
+    return rc;
+  FwdPParams p;
+  p.o = static_cast<__nv_bfloat16*>(a->o);
+  p.lse = a->lse;
+  int2* spans = static_cast<int2*>(ws);
+  p.rows_span = spans;
+  mark_boundary(st);
+  k_spans_p<<<int((T + 255) / 256), 256, 0, st>>>(a->cu_seqlens, a->prefix_len, a->num_seqs, a->mask_mode, int(T),
+                                                  spans);
+  if (int rc = launch_build_tiles(a->cu_seqlens, a->seg_src, a->num_seqs, int64_t(T), fwd_ws_tiles(a, ws), st,
+                                  const_cast<int4**>(&p.tiles), const_cast<int**>(&p.ntiles)))
+    return rc;
+  mark_boundary(st);
+  p.T = static_cast<int>(T);
+  p.H = a->num_heads;
+  p.Hkv = a->num_kv_heads;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  auto kern = attn_fwd_p_kernel<HD, BN, KS, VS>;
+  VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int64_t max_tiles = int64_t(T) / 128 + a->num_seqs;
+  kern<<<persistent_grid(max_tiles * a->num_heads, a->sm_budget), 192, Cfg::SMEM, st>>>(tq, tk, tv, p);
+  VLASIM_LAUNCH_CHECK();
+  mark_boundary(st);
+  return VLASIM_OK;
+}
+
 }  // namespace
 
 namespace vlasim_host {
@@ -345,7 +702,8 @@ void* fwd_ws_tiles(const vlasim_attn_args* a, void* ws);
 }
 
 // head_dim 64/128: persistent kernel (attn_fwd2.cu, needs the span workspace);
-// head_dim 256: the one-tile-per-CTA kernel above (O is too wide to double-buffer in TMEM).
+// head_dim 256: the persistent single-O kernel above (attn_fwd_p_kernel; VLASIM_FWD_V1 selects the
+// one-tile-per-CTA kernel for comparison).
 extern "C" int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void* ws, size_t ws_bytes,
                                            vlasim_stream_t stream) {
   using namespace vlasim_host;
@@ -353,7 +711,9 @@ extern "C" int vlasim_varlen_attn_fwd_cuda(const vlasim_attn_args* a, void* ws, 
   cudaStream_t st = as_stream(stream);
   const size_t need = fwd_ws_bytes(a);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
-  if (a->head_dim == 256) return launch_fwd<256, 64, 2>(a, fwd_ws_tiles(a, ws), st);
+  if (a->head_dim == 256)
+    return getenv("VLASIM_FWD_V1") ? launch_fwd<256, 64, 2>(a, fwd_ws_tiles(a, ws), st)
+                                   : launch_fwd_p<256, 64, 3, 2>(a, ws, st);
   if (getenv("VLASIM_FWD_V1"))
     return a->head_dim == 64 ? launch_fwd<64, 128, 4>(a, fwd_ws_tiles(a, ws), st)
                              : launch_fwd<128, 128, 3>(a, fwd_ws_tiles(a, ws), st);

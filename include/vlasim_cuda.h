@@ -133,8 +133,10 @@ typedef struct vlasim_shard_out {
   int32_t* local_nseg;     /* [1]                                                             */
   int64_t* local_tokens;   /* [1]                                                             */
   int32_t* status;         /* [2]                                                             */
+  int32_t* scratch;        /* vlasim_shard_scratch_size(n) bytes of device workspace          */
 } vlasim_shard_out;
 
+size_t vlasim_shard_scratch_size(int64_t n);
 int vlasim_shard_lpt_cuda(const int32_t* d_len, const vlasim_pack_out* plan, int64_t n, int32_t world, int32_t rank,
                           const vlasim_shard_out* out, uint32_t flags, vlasim_stream_t stream);
 

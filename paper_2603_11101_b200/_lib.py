@@ -29,7 +29,7 @@ class PackOut(C.Structure):
 class ShardOut(C.Structure):
     _fields_ = [("bin_rank", i32p), ("rank_load", i64p), ("local_ids", i32p), ("local_cu", i32p),
                 ("local_seg_src", i32p), ("local_src_off", i32p), ("local_nseg", i32p), ("local_tokens", i64p),
-                ("status", i32p)]
+                ("status", i32p), ("scratch", i32p)]
 
 
 class AttnArgs(C.Structure):
@@ -60,6 +60,7 @@ _SIGS = {
                                           C.c_void_p]),
     "vlasim_shard_lpt_cuda": (C.c_int, [i32p, C.POINTER(PackOut), C.c_int64, C.c_int32, C.c_int32,
                                          C.POINTER(ShardOut), C.c_uint32, C.c_void_p]),
+    "vlasim_shard_scratch_size": (C.c_size_t, [C.c_int64]),
     "vlasim_pack_seg_src_cuda": (C.c_int, [C.POINTER(PackOut), C.c_int64, i32p, C.c_void_p]),
     "vlasim_scatter_rows_cuda": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, i32p, C.POINTER(PackOut), C.c_int64,
                                            C.c_void_p]),

@@ -44,6 +44,7 @@ struct PackWs {
   int32_t* run_tok;          // [n]  bin fill (tokens) before this run
   int32_t* run_mem;          // [n]  bin member count before this run
   int64_t* scan_part;        // [3][num_scan_blocks + 1]
+  int32_t* mode;             // [1]     1: k_ffd_warp placed the batch (k_ffd returns at once)
   int32_t* spill;            // [3][n]  k_ffd open-bin list once it outgrows shared memory;
                              //         k_greedy level-0 room / count ([2][min(n, 2^20)])
 };
@@ -71,6 +72,7 @@ size_t carve(PackWs* w, void* base, int64_t n, int cap) {
   w->run_tok = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
   w->run_mem = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
   w->scan_part = reinterpret_cast<int64_t*>(take(size_t(3) * (num_scan_blocks(n) + 1) * 8));
+  w->mode = reinterpret_cast<int32_t*>(take(4));
   w->spill = reinterpret_cast<int32_t*>(take(size_t(3) * ((n + 31) & ~int64_t(31)) * 4));
   return off;
 }
@@ -124,7 +126,18 @@ __global__ void k_class_scan(int32_t* __restrict__ chunk_hist, int64_t nchunks, 
   const int L = blockIdx.x * blockDim.x + threadIdx.x;
   if (L > cap) return;
   int32_t run = 0;
-  for (int64_t c = 0; c < nchunks; ++c) {
+  int64_t c = 0;
+  for (; c + 8 <= nchunks; c += 8) {  // 8 independent loads in flight, then the running sums
+    int32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = chunk_hist[size_t(c + u) * (cap + 1) + L];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      chunk_hist[size_t(c + u) * (cap + 1) + L] = run;
+      run += v[u];
+    }
+  }
+  for (; c < nchunks; ++c) {
     int32_t* p = chunk_hist + size_t(c) * (cap + 1) + L;
     const int32_t v = *p;
     *p = run;
@@ -153,6 +166,7 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int n, int cap, PackWs ws, vlas
   const int tid = threadIdx.x, nt = blockDim.x;
 
   if (out.status[0] != 0) return;  // validation failed upstream
+  if (*ws.mode == 1) return;       // k_ffd_warp placed this batch (at most kWarpMaxBins bins)
 
   // smallest present length (retirement threshold)
   int lmin_local = INT_MAX;
@@ -304,7 +318,7 @@ __global__ void __launch_bounds__(1024, 1) k_ffd(int n, int cap, PackWs ws, vlas
 // class counts staged in smem, bins visited 32 at a time with early exit once the class is
 // placed (no block barriers on the per-class critical path).
 constexpr int kWarpMaxBins = 16384;
-constexpr int kWarpCntMaxCap = 24575;  // 2 × 64 KB of bins + (cap + 1) counters within 227 KB
+constexpr int kWarpCntMaxCap = 24575;  // 2 × 64 KB of bins + (cap + 1) counters + 2 KB within 227 KB
 // floor(a / b) for 0 <= a, 1 <= b <= 2^15 via the fp32 reciprocal, corrected to the exact quotient
 // (the estimate is off by at most one either way at these magnitudes).
 __device__ __forceinline__ int udiv_small(int a, int b, float inv_b) {
@@ -313,7 +327,7 @@ __device__ __forceinline__ int udiv_small(int a, int b, float inv_b) {
   q += (q + 1) * b <= a;
   return q;
 }
-__global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_pack_out out) {
+__global__ void __launch_bounds__(32, 1) k_ffd_warp(int64_t n, int cap, PackWs ws, vlasim_pack_out out) {
   extern __shared__ int32_t sm[];
   int32_t* act_rem = sm;                    // bins are never retired here: id == index
   int32_t* act_cnt = sm + kWarpMaxBins;
@@ -334,6 +348,15 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(full, tok, o);
   __syncwarp();
+  // Any first-fit packing keeps every bin but one more than half full, so it opens fewer than
+  // 2·Σl/cap + 1 bins (and never more than n): when that bound fits the smem bin arrays this warp
+  // places the batch (config 5: 1M samples, ≈ 6.4k bins); otherwise the 1024-thread k_ffd does.
+  const long long bound = min(static_cast<long long>(n), 2 * tok / cap + 1);
+  if (bound > kWarpMaxBins) {
+    if (lane == 0) *ws.mode = 0;
+    return;
+  }
+  if (lane == 0) *ws.mode = 1;
   // Register-resident fast path: FFD never opens more than 2·Σl/cap + 1 bins (every pair of
   // consecutive bins holds more than cap tokens), so when that bound is ≤ 64 the open bins live
   // in registers, two per lane (bins lane and 32 + lane).  Each run of a class is one first-fit
@@ -418,6 +441,17 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
     if (lane == 0) *out.num_bins = nb;
     return;
   }
+  // General path: the open bins in smem with a per-32-bin maximum of the room (cmax), so a class
+  // visits only the chunks that have room for it — 32 chunk maxima per ballot — instead of every
+  // bin from the first (1M long-tailed samples: ~487 classes over ~6.4k bins).
+  int32_t* cmax = sm + 2 * kWarpMaxBins + (cnt_smem ? cap + 1 : 0);  // [kWarpMaxBins / 32]
+  auto chunk_max = [&](int ch, int nbins) {  // recompute cmax[ch] from the bins themselves
+    const int b = ch * 32 + lane;
+    int v = b < nbins ? act_rem[b] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(full, v, o));
+    if (lane == 0) cmax[ch] = v;
+  };
   int nb = 0, nruns = 0;
   for (int hi = cap; hi >= 1; hi -= 32) {
     const int myL = hi - lane;
@@ -430,38 +464,51 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
       const float invL = __frcp_rn(float(L));
       const int runs_before = nruns;
       int running = 0;  // items of class L accounted for by bins visited so far (Σq)
-      for (int b0 = 0; b0 < nb && running < c; b0 += 32) {
-        const int b = b0 + lane;
-        const int rem = b < nb ? act_rem[b] : 0;
-        const int q = udiv_small(rem, L, invL);
-        int inc = q;
+      const int nch = (nb + 31) >> 5;
+      for (int g0 = 0; g0 < nch && running < c; g0 += 32) {
+        unsigned cm = __ballot_sync(full, g0 + lane < nch && cmax[g0 + lane] >= L);
+        while (cm && running < c) {
+          const int ch = g0 + __ffs(cm) - 1;
+          cm &= cm - 1;
+          const int b = ch * 32 + lane;
+          const int rem = b < nb ? act_rem[b] : 0;
+          const int q = udiv_small(rem, L, invL);
+          int inc = q;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(full, inc, o);
-          if (lane >= o) inc += t;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(full, inc, o);
+            if (lane >= o) inc += t;
+          }
+          const int before = running + inc - q;
+          const bool takes = q > 0 && before < c;
+          const unsigned tm = __ballot_sync(full, takes);
+          int nrem = rem;
+          if (takes) {
+            const int take = min(q, c - before);
+            const int r = nruns + __popc(tm & lt);
+            ws.run_bin[r] = b;
+            ws.run_cum[r] = before;
+            ws.run_tok[r] = cap - rem;
+            ws.run_mem[r] = act_cnt[b];
+            nrem = rem - take * L;
+            act_rem[b] = nrem;
+            act_cnt[b] += take;
+          }
+          nruns += __popc(tm);
+          running += __shfl_sync(full, inc, 31);
+          int mx = nrem;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(full, mx, o));
+          if (lane == 0) cmax[ch] = mx;
+          __syncwarp();
         }
-        const int before = running + inc - q;
-        const bool takes = q > 0 && before < c;
-        const unsigned tm = __ballot_sync(full, takes);
-        if (takes) {
-          const int take = min(q, c - before);
-          const int r = nruns + __popc(tm & lt);
-          ws.run_bin[r] = b;
-          ws.run_cum[r] = before;
-          ws.run_tok[r] = cap - rem;
-          ws.run_mem[r] = act_cnt[b];
-          act_rem[b] = rem - take * L;
-          act_cnt[b] += take;
-        }
-        nruns += __popc(tm);
-        running += __shfl_sync(full, inc, 31);
       }
       const int placed = min(c, running);
       const int r = c - placed;
       if (r > 0) {
         const int kk = udiv_small(cap, L, invL);
         const int nnew = udiv_small(r + kk - 1, kk, __frcp_rn(float(kk)));
-        if (nb + nnew > kWarpMaxBins) {
+        if (nb + nnew > kWarpMaxBins) {  // (unreachable: nb stays below the bound checked above)
           if (lane == 0) {
             out.status[0] = VLASIM_ECONFIG;
             out.status[1] = -2;
@@ -477,6 +524,9 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int cap, PackWs ws, vlasim_p
           act_rem[nb + j] = cap - take * L;
           act_cnt[nb + j] = take;
         }
+        __syncwarp();
+        for (int ch = nb >> 5; ch <= (nb + nnew - 1) >> 5; ++ch) chunk_max(ch, nb + nnew);
+        __syncwarp();
         nb += nnew;
         nruns += nnew;
       }
@@ -858,11 +908,12 @@ extern "C" int vlasim_pack_ffd_cuda(const int32_t* d_len, int64_t n, int32_t cap
   k_init<<<(n + 255) / 256, 256, 0, st>>>(*out, n);
   if (int rc = launch_hist(d_len, n, cap, w, out, st)) return rc;
   k_class_scan<<<(cap + 1 + 255) / 256, 256, 0, st>>>(w.chunk_hist, nchunks, cap, w.class_count);
-  if (n <= kWarpMaxBins) {  // at most n bins: the warp-synchronous packer holds them all in smem
-    const size_t wsm = (2 * kWarpMaxBins + (cap <= kWarpCntMaxCap ? cap + 1 : 0)) * 4;
+  {  // the warp packer takes every batch whose bin count is bounded by its smem bin arrays
+    const size_t wsm = (2 * kWarpMaxBins + (cap <= kWarpCntMaxCap ? cap + 1 : 0) + kWarpMaxBins / 32) * 4;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-    k_ffd_warp<<<1, 32, wsm, st>>>(cap, w, *out);
-  } else {
+    k_ffd_warp<<<1, 32, wsm, st>>>(n, cap, w, *out);
+  }
+  if (n > kWarpMaxBins) {  // the 1024-thread packer (returns at once when the warp placed the batch)
     const size_t ffd_smem = (3 * kMaxActiveBins + 1024) * 4;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_ffd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffd_smem));
     k_ffd<<<1, 1024, ffd_smem, st>>>(int(n), cap, w, *out);

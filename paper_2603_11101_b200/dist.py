@@ -66,12 +66,13 @@ class ShardPlan:
         self.local_nseg = torch.empty(1, **i32)
         self.local_tokens = torch.empty(1, dtype=torch.int64, device=device)
         self.status = torch.empty(2, **i32)
+        self.scratch = torch.empty(max(1, _lib.lib().vlasim_shard_scratch_size(n)), dtype=torch.uint8, device=device)
         P = _lib.ptr
         self._struct = _lib.ShardOut(P(self.bin_rank, _lib.i32p), P(self.rank_load, _lib.i64p),
                                      P(self.local_ids, _lib.i32p), P(self.local_cu, _lib.i32p),
                                      P(self.local_seg_src, _lib.i32p), P(self.local_src_off, _lib.i32p),
                                      P(self.local_nseg, _lib.i32p), P(self.local_tokens, _lib.i64p),
-                                     P(self.status, _lib.i32p))
+                                     P(self.status, _lib.i32p), P(self.scratch, _lib.i32p))
 
     def nseg(self) -> int:
         return int(self.local_nseg.item())

@@ -36,6 +36,7 @@ int validate_attn_args(const vlasim_attn_args* a, bool fp8);
 namespace {
 
 constexpr float kLazyRescale = 8.0f;  // log2-domain row-max growth tolerated before rescaling O
+constexpr int kDefaultPoly = 0;       // pairs of 16 per quarter tile exponentiated on the FMA pipe
 
 __global__ void k_fwd_spans(const int32_t* __restrict__ cu, const int32_t* __restrict__ prefix, int nseq, int mask,
                             int T, int2* __restrict__ rows_span) {
@@ -118,7 +119,16 @@ __device__ __forceinline__ FwdItem fwd_item_cur(FwdItem it, int BN) {
 
 constexpr int kFwdThreads = 576;
 
-template <int HD, int KS, int VS, bool FP8, bool PROF>
+// The four column quarters' (bf16, rounded-up) maxima of a row, stored row-major [32 rows][4], read
+// back as one 8-byte word: one LDS.64 per row instead of four LDS.U16.
+__device__ __forceinline__ float xmax4(const __nv_bfloat16* xb, int lane) {
+  const uint2 w = *reinterpret_cast<const uint2*>(xb + lane * 4);
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&w.x), b = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+  const __nv_bfloat162 m = __hmax2(a, b);
+  return fmaxf(__bfloat162float(m.x), __bfloat162float(m.y));
+}
+
+template <int HD, int KS, int VS, bool FP8, bool PROF, int NPOLY = 0>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -492,10 +502,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           // exchange and the lazy O rescale of its columns.
           wp.template wait<0>(&bar_s_full[g & 1], (g >> 1) & 1);
           __nv_bfloat16* xb = xmax + (g & 1) * 128;
-          xb[qp * 32 + lane] = __float2bfloat16_ru(-INFINITY);
+          xb[lane * 4 + qp] = __float2bfloat16_ru(-INFINITY);
           named_bar_sync(1 + quad, 128);
-          float mt = fmaxf(fmaxf(__bfloat162float(xb[lane]), __bfloat162float(xb[32 + lane])),
-                           fmaxf(__bfloat162float(xb[64 + lane]), __bfloat162float(xb[96 + lane])));
+          float mt = xmax4(xb, lane);
           mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
           const bool grow = mt > m_run + kLazyRescale;
           const float alpha = grow ? ex2_approx(m_run - mt) : 1.f;  // same factor for l and O
@@ -567,14 +576,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // combine the four column quarters of this row
         // rounded up to bf16: every quarter uses the same offset, ≥ the row max (P ≤ 1)
         __nv_bfloat16* xb = xmax + (g & 1) * 128;
-        xb[qp * 32 + lane] = __float2bfloat16_ru(mt);
+        xb[lane * 4 + qp] = __float2bfloat16_ru(mt);
         {
           const long long tb = wp.now();
           named_bar_sync(1 + quad, 128);
           wp.template add_since<3>(tb);
         }
-        mt = fmaxf(fmaxf(__bfloat162float(xb[lane]), __bfloat162float(xb[32 + lane])),
-                   fmaxf(__bfloat162float(xb[64 + lane]), __bfloat162float(xb[96 + lane])));
+        mt = xmax4(xb, lane);
         mt = (mt == -INFINITY) ? -INFINITY : mt * sl2;
         const bool grow = mt > m_run + kLazyRescale;
         const float alpha = grow ? ex2_approx(m_run - mt) : 1.f;  // same factor for l and O
@@ -587,10 +595,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 independent sum chains (FADD2)
         const float2 sl2v = make_float2(sl2 * ksc, sl2 * ksc), nmv = make_float2(-msub, -msub);
         uint32_t pk[16];
+        // NPOLY of the 16 pairs take 2^x on the FMA pipe (f2_ex2_poly) when no column of this warp's
+        // quarter is masked (warp-uniform): MUFU.EX2 throughput bounds this loop, the FMA pipe has room
+        const bool poly_ok = NPOLY > 0 && __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32);
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           const float2 a = f2_fma(make_float2(__uint_as_float(x[2 * t]), __uint_as_float(x[2 * t + 1])), sl2v, nmv);
-          const float2 pe = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+          float2 pe;
+          if (NPOLY > 0 && (t % (16 / (NPOLY > 0 ? NPOLY : 1))) == 16 / (NPOLY > 0 ? NPOLY : 1) - 1 && poly_ok)
+            pe = f2_ex2_poly(a);
+          else
+            pe = make_float2(ex2_approx(a.x), ex2_approx(a.y));
           lq[t & 1] = f2_add(lq[t & 1], pe);
           pk[t] = pack_bf16x2(pe.x, pe.y);
         }
@@ -699,7 +714,13 @@ int launch_fwd2(const vlasim_attn_args* a, int2* rows_span, void* tiles_buf, cud
                         "smx:o_full", "smx:xchg_bar", "smx:epilogue", "", "", "smx:total"});
   }
   p.prof = nullptr;
-  auto kern = attn_fwd2_kernel<HD, KS, VS, FP8, false>;
+  // MUFU offload (f2_ex2_poly pairs of 16 per quarter tile): VLASIM_POLY = 0 / 2 / 4 / 8
+  const char* pe = getenv("VLASIM_POLY");
+  const int npoly = pe ? atoi(pe) : kDefaultPoly;
+  auto kern = npoly == 8 ? attn_fwd2_kernel<HD, KS, VS, FP8, false, 8>
+            : npoly == 4 ? attn_fwd2_kernel<HD, KS, VS, FP8, false, 4>
+            : npoly == 2 ? attn_fwd2_kernel<HD, KS, VS, FP8, false, 2>
+                         : attn_fwd2_kernel<HD, KS, VS, FP8, false, 0>;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   kern<<<grid, kFwdThreads, Cfg::SMEM, st>>>(tq, tk, tv, to, to64, to32, to16, to8, p);
   VLASIM_LAUNCH_CHECK();

@@ -315,6 +315,25 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for a pair of finite x on the FMA pipe (offloads MUFU.EX2, the softmax's binding unit):
+// x = n + f with n = rint(x) by the 1.5·2^23 magic add, f ∈ [-0.5, 0.5]; 2^f by a degree-3
+// polynomial fitted for relative error (max 1.0e-4, below bf16's 2^-9 rounding of P); 2^n added to
+// the exponent field — t's low bits hold n, so (bits(t) << 23) ≡ n << 23 (mod 2^32): one LEA.  x is
+// clamped at −126 (callers use it only where no column is masked: such results are ≤ 2^-126 of
+// the row maximum, i.e. nothing after the bf16 P·V).
+__device__ __forceinline__ float2 f2_ex2_poly(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 M = make_float2(12582912.f, 12582912.f), nM = make_float2(-12582912.f, -12582912.f);
+  const float2 t = f2_add(x, M);
+  const float2 f = f2_fma(f2_add(t, nM), make_float2(-1.f, -1.f), x);  // x − rint(x), exact
+  const float2 c3 = make_float2(0.05500893f, 0.05500893f), c2 = make_float2(0.24221098f, 0.24221098f);
+  const float2 c1 = make_float2(0.69328293f, 0.69328293f), one = make_float2(1.f, 1.f);
+  const float2 p = f2_fma(f2_fma(f2_fma(c3, f, c2), f, c1), f, one);
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -188,16 +188,22 @@ struct BwdParams {
 // head_dim 256: dV and dK of the full head dim (2 × 256 fp32 columns) do not fit next to S / dP,
 // so two launches each accumulate one 128-column half (p.ohalf; S / dP recomputed), and the
 // unit is 32 queries (UQ) so that 3 Q/dO stages fit beside the 64 KB K and V tiles.
-template <int HD, int UQ = 64>
+// MODE (head_dim 256): 0 = dV and dK together (head_dim ≤ 128: HO = HD); 1 = dV only, 2 = dK only,
+// each over the full head dim (HO = 256) in its own launch.  The dV pass needs neither dP nor dS
+// (Sᵀ → Pᵀ → dV) and loads no V; the dK pass skips the dV GEMM — 5 GEMMs per (key, query) pair over
+// the two launches against the 6 of two head-dim halves that each recompute S and dP.
+template <int HD, int UQ = 64, int MODE = 0>
 struct DkvCfg {
-  static constexpr int HO = HD < 128 ? HD : 128;  // dK / dV head-dim columns per launch
+  static constexpr int HO = MODE ? HD : (HD < 128 ? HD : 128);  // dK / dV head-dim columns per launch
   static constexpr int CW = UQ / 2;               // query columns per softmax warp
   static constexpr int QBOX = UQ * 128;           // one 64-column TMA box of a Q / dO stage
   static constexpr int KT = 128 * HD * 2;  // K or V tile (128 keys)
   static constexpr int QT = UQ * HD * 2;   // Q or dO tile (UQ queries)
-  static constexpr int NS = HD == 256 ? 3 : 5;  // Q / dO stages
+  // Q / dO stages: 5, except head_dim 256 with K and V resident (3); the dV pass loads no V, and its
+  // 64 KB hold two more stages — with S look-ahead of 2 units, 3 stages leave no load in flight
+  static constexpr int NS = HD == 256 && MODE != 1 ? 3 : 5;
   static constexpr int OFF_K = 0, OFF_V = KT;
-  static constexpr int OFF_Q = 2 * KT;              // [NS]
+  static constexpr int OFF_Q = (MODE == 1 ? 1 : 2) * KT;  // [NS]
   static constexpr int OFF_DO = OFF_Q + NS * QT;    // [NS]
   static constexpr int VEC = UQ * 4;                // UQ floats of lse2 / D (16-B aligned window)
   static constexpr int OFF_LSE = OFF_DO + NS * QT;  // [NS][VEC]
@@ -205,14 +211,14 @@ struct DkvCfg {
   static constexpr int OFF_BAR = OFF_DSUM + NS * VEC;
   static constexpr int NUM_BARS = 12 + 2 * NS;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
-  static constexpr uint32_t DV_COL = 256, DK_COL = 256 + HO;
+  static constexpr uint32_t DV_COL = 256, DK_COL = MODE ? 256 : 256 + HO;
   __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? uint32_t(UQ) : 0u; }
   __host__ __device__ static constexpr uint32_t dp_col(int b) { return 128u + (b ? uint32_t(UQ) : 0u); }
   // TMEM column of K-step j (16 queries) of Pᵀ / dSᵀ: warp chunks of CW queries sit at column
   // offsets part·CW, each packed into CW/2 columns as bf16 pairs
   __host__ __device__ static constexpr uint32_t a_col(int j) { return (j / (CW / 16)) * CW + (j % (CW / 16)) * 8; }
   static_assert(UQ == 64 || UQ == 32, "unit width");
-  static_assert(DK_COL + HO <= 512, "TMEM budget");
+  static_assert(DK_COL + HO <= 512 && DV_COL + HO <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
   static_assert(4 * 2001 * 8 <= 2 * NS * QT, "PROF trace fits the Q/dO stages");
 };
@@ -288,12 +294,13 @@ struct UnitCursor {
 // Warp 16 TMA producer, warp 17 TMEM allocator + MMA issuer.
 constexpr int kDkvThreads = 576;
 
-template <int HD, int UQ, bool PROF>
+template <int HD, int UQ, bool PROF, int MODE = 0>
 __global__ void __launch_bounds__(kDkvThreads, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const BwdParams p) {
-  using Cfg = DkvCfg<HD, UQ>;
+  using Cfg = DkvCfg<HD, UQ, MODE>;
+  constexpr bool kDV = MODE != 2, kDK = MODE != 1;  // accumulators of this launch (dK needs dP / dS)
   constexpr int NS = Cfg::NS, HO = Cfg::HO, CW = Cfg::CW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
@@ -349,11 +356,12 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (c.it == 0) {
           if (c.k > 0) wp.template wait<1>(bar_kv_empty, (c.k - 1) & 1);
           trace(2, c.u);  // P: K/V load issued
-          mbar_expect_tx(bar_kv_full, 2 * Cfg::KT);
+          mbar_expect_tx(bar_kv_full, (kDK ? 2 : 1) * Cfg::KT);
 #pragma unroll
           for (int j = 0; j < HD / 64; ++j) {
             tma_load_2d(smem + Cfg::OFF_K + j * 16384, &tmK, c.itm.kh * HD + j * 64, c.itm.k0 + c.itm.dl, bar_kv_full);
-            tma_load_2d(smem + Cfg::OFF_V + j * 16384, &tmV, c.itm.kh * HD + j * 64, c.itm.k0 + c.itm.dl, bar_kv_full);
+            if (kDK)  // V only for dP (the dV pass has no dP)
+              tma_load_2d(smem + Cfg::OFF_V + j * 16384, &tmV, c.itm.kh * HD + j * 64, c.itm.k0 + c.itm.dl, bar_kv_full);
           }
           // the next item's K/V into L2 now: its load (single K/V buffer, issued only once this
           // item's last dP has run) then hits L2 at the item boundary
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
 #pragma unroll
             for (int j = 0; j < HD / 64; ++j) {
               tma_prefetch_2d(&tmK, c.nxt.kh * HD + j * 64, c.nxt.k0 + c.nxt.dl);
-              tma_prefetch_2d(&tmV, c.nxt.kh * HD + j * 64, c.nxt.k0 + c.nxt.dl);
+              if (kDK) tma_prefetch_2d(&tmV, c.nxt.kh * HD + j * 64, c.nxt.k0 + c.nxt.dl);
             }
           }
         }
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (PROF && (p.dbg & 2)) {  // timing experiment: no Q/dO traffic (the trace lives in the Q stages)
           mbar_arrive(&bar_qd_full[s]);
         } else {
-          mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + 2 * Cfg::VEC);
+          mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + (kDK ? 2 : 1) * Cfg::VEC);
 #pragma unroll
           for (int j = 0; j < HD / 64; ++j) {
             tma_load_2d(smem + Cfg::OFF_Q + s * Cfg::QT + j * Cfg::QBOX, &tmQ, h * HD + j * 64, qb, &bar_qd_full[s]);
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
                         &bar_qd_full[s]);
           }
           bulk_load(smem + Cfg::OFF_LSE + s * Cfg::VEC, p.lse2 + vo, Cfg::VEC, &bar_qd_full[s]);
-          bulk_load(smem + Cfg::OFF_DSUM + s * Cfg::VEC, p.dsum + vo, Cfg::VEC, &bar_qd_full[s]);
+          if (kDK) bulk_load(smem + Cfg::OFF_DSUM + s * Cfg::VEC, p.dsum + vo, Cfg::VEC, &bar_qd_full[s]);
         }
         if (++s == NS) {
           s = 0;
@@ -450,8 +458,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (elect_one()) {
           mma_S(Cfg::s_col(bb), as * QT16);
           umma_commit(&bar_s_full[bb]);
-          mma_dP(Cfg::dp_col(bb), as * QT16);
-          umma_commit(&bar_dp_full[bb]);
+          if (kDK) {
+            mma_dP(Cfg::dp_col(bb), as * QT16);
+            umma_commit(&bar_dp_full[bb]);
+          }
           if (ca.last()) umma_commit(bar_kv_empty);  // the item's last readers of K and V
         }
         __syncwarp();
@@ -474,22 +484,27 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         if (elect_one()) {
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
           const uint64_t om = opaque(dOm) + coff, qm = opaque(dQm) + coff;
+          if (kDV) {
 #pragma unroll
-          for (int j = 0; j < UQ / 16; ++j)
-            umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + Cfg::a_col(j),
-                        sdesc_add(om, j * 2048), id_acc, j > 0 ? 1u : acc0);
+            for (int j = 0; j < UQ / 16; ++j)
+              umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + Cfg::a_col(j),
+                          sdesc_add(om, j * 2048), id_acc, j > 0 ? 1u : acc0);
+          }
           if (early) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
             mma_S(Cfg::s_col(b), aoff);
             umma_commit(&bar_s_full[b]);
+            if (!kDK && a_last) umma_commit(bar_kv_empty);
           }
-          // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
+          if (kDK) {
+            // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns
 #pragma unroll
-          for (int j = 0; j < UQ / 16; ++j)
-            umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + Cfg::a_col(j),
-                        sdesc_add(qm, j * 2048), id_acc, j > 0 ? 1u : acc0);
+            for (int j = 0; j < UQ / 16; ++j)
+              umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + Cfg::a_col(j),
+                          sdesc_add(qm, j * 2048), id_acc, j > 0 ? 1u : acc0);
+          }
           umma_commit(&bar_qd_empty[cs]);
           if (c_last) umma_commit(bar_dkv_full);
-          if (early) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
+          if (early && kDK) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
             mma_dP(Cfg::dp_col(b), aoff);
             umma_commit(&bar_dp_full[b]);
             if (a_last) umma_commit(bar_kv_empty);
@@ -592,6 +607,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         else tmem_st8(tmem + lane_off + Cfg::s_col(g) + c0, pp);  // completion awaited with dS's (phase B)
         trace(22 + g, c.u);  // S: P written
         wp.template add_since<4>(ta);
+        if constexpr (!kDK) {  // dV pass: Pᵀ is all the MMA needs (released on the dS barrier)
+          tmem_wait_st();
+          tc_fence_before();
+          warp_arrive(&bar_ds_full[g]);
+        } else {
         // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over the dP columns (P as the dV GEMM saw it)
         wp.template wait<1>(&bar_dp_full[g], ph);
         trace(24 + g, c.u);  // S: dp_full seen
@@ -628,6 +648,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         warp_arrive(&bar_ds_full[g]);
         trace(26 + g, c.u);  // S: ds arrived
         wp.template add_since<5>(tb);
+        }  // phase B (dK)
       }
       if (c.last() && (c.u & 1) == g) {
         // ---- item epilogue, by the group that ran the item's last unit (the other group goes
@@ -641,27 +662,31 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_after();
         const int hh = (warp >> 2) & 1;
         const int64_t stride = int64_t(p.Hkv) * HD;
-        const int col0 = c.itm.kh * HD + p.ohalf * HO + hh * (HO / 2);
-        uint32_t pw[HO / 4];
+        constexpr int HW = HO / 2 < 64 ? HO / 2 : 64;  // columns per transposed store pass
+        uint32_t pw[HW / 2];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {  // t = 0: dV, 1: dK (· scale)
-          const uint32_t col = (t ? Cfg::DK_COL : Cfg::DV_COL) + hh * (HO / 2);
+        for (int t = kDV ? 0 : 1; t < (kDK ? 2 : 1); ++t) {  // t = 0: dV, 1: dK (· scale)
           const float sc = t ? p.scale : 1.f;
 #pragma unroll
-          for (int cc = 0; cc < HO / 2; cc += 32) {
-            uint32_t v[32];
-            tmem_ld32(tmem + lane_off + col + cc, v);
-            tmem_wait_ld();
+          for (int h0 = 0; h0 < HO / 2; h0 += HW) {  // this warp's HO/2 columns, HW at a time
+            const uint32_t col = (t ? Cfg::DK_COL : Cfg::DV_COL) + hh * (HO / 2) + h0;
+            const int col0 = c.itm.kh * HD + p.ohalf * HO + hh * (HO / 2) + h0;
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              pw[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]) * sc, __uint_as_float(v[2 * j + 1]) * sc);
+            for (int cc = 0; cc < HW; cc += 32) {
+              uint32_t v[32];
+              tmem_ld32(tmem + lane_off + col + cc, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                pw[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]) * sc, __uint_as_float(v[2 * j + 1]) * sc);
+            }
+            if (t == (kDK ? 1 : 0) && h0 + HW == HO / 2) {
+              tc_fence_before();
+              warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
+              trace(50, c.u);  // E: TMEM drained
+            }
+            store_rows_xpose<HW / 8>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
           }
-          if (t == 1) {
-            tc_fence_before();
-            warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
-            trace(50, c.u);  // E: TMEM drained
-          }
-          store_rows_xpose<HO / 16>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
         }
         trace(51, c.u);  // E: stored
         trace(34 + (warp >> 3), c.u);  // E: epilogue done
@@ -1189,14 +1214,22 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   p.scale_log2 = a->softmax_scale * kLog2e;
   p.dbg = getenv("VLASIM_DBG") ? atoi(getenv("VLASIM_DBG")) : 0;
   p.ohalf = 0;
-  for (int half = 0; half < HD / DkvCfg<HD, UQ>::HO; ++half) {
-    using Cfg = DkvCfg<HD, UQ>;
+  // head_dim 256: a dV pass (MODE 1) and a dK pass (MODE 2) over the full head dim (VLASIM_DKV_HALVES
+  // selects the previous two head-dim halves, for comparison); head_dim ≤ 128: one launch (MODE 0)
+  const bool halves = HD == 256 && getenv("VLASIM_DKV_HALVES");
+  const int nlaunch = HD == 256 ? 2 : 1;
+  for (int half = 0; half < nlaunch; ++half) {
     const int grid = persistent_grid(max_tiles * Hkv, a->sm_budget);
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
-    p.ohalf = half;
-    auto kern = p.prof ? k_bwd_dkdv<HD, UQ, true> : k_bwd_dkdv<HD, UQ, false>;
-    VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<grid, kDkvThreads, Cfg::SMEM, st>>>(tqu, tk, tv, tdou, p);
+    p.ohalf = halves ? half : 0;
+    auto kern = HD != 256 || halves ? (p.prof ? k_bwd_dkdv<HD, UQ, true, 0> : k_bwd_dkdv<HD, UQ, false, 0>)
+              : half == 0           ? (p.prof ? k_bwd_dkdv<HD, UQ, true, 1> : k_bwd_dkdv<HD, UQ, false, 1>)
+                                    : (p.prof ? k_bwd_dkdv<HD, UQ, true, 2> : k_bwd_dkdv<HD, UQ, false, 2>);
+    const int smem = HD != 256 || halves ? DkvCfg<HD, UQ, 0>::SMEM
+                     : half == 0         ? DkvCfg<HD, UQ, 1>::SMEM
+                                         : DkvCfg<HD, UQ, 2>::SMEM;
+    VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kDkvThreads, smem, st>>>(tqu, tk, tv, tdou, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,

@@ -180,7 +180,7 @@ struct BwdParams {
 // column aliasing — S(u+2) over Pᵀ(u), dP(u+2) over dSᵀ(u) — relies on tcgen05.mma executing in
 // issue order).  One wait and one issue block per unit keep the MMA warp's serial overhead
 // (≈ 6 cycles per instruction) from draining the shallow MMA queue between blocks.  Q/dO stream through
-// NS = 5 stages (the look-ahead of 2 units plus ~2 units of HBM latency); every role prefetches
+// NS = 5 stages (the look-ahead of 2 units plus ~2 units of HBM latency; per ring, see DkvCfg); every role prefetches
 // the next item's descriptor so item boundaries do not expose a global-load round trip.  The
 // item epilogue writes dK/dV from TMEM-loaded registers through row_map after a 4-lane chunk
 // transpose (store_rows_xpose: 8 rows × 64 B per warp store; no smem staging, barrier or TMA).
@@ -202,14 +202,19 @@ struct DkvCfg {
   // Q / dO stages: 5, except head_dim 256 with K and V resident (3); the dV pass loads no V, and its
   // 64 KB hold two more stages — with S look-ahead of 2 units, 3 stages leave no load in flight
   static constexpr int NS = HD == 256 && MODE != 1 ? 3 : 5;
+  // Q (+ lse2 / D windows) and dO have separate rings: NQ / ND stages.  Where dO is read only by
+  // dP (the dK pass) its stage is released right after dP — 4 Q + 2 dO stages in the smem of 3 pairs,
+  // so one more unit's loads are in flight; elsewhere dV reads dO at the end of the unit (NQ = ND).
+  static constexpr int NQ = MODE == 2 && HD == 256 ? 4 : NS, ND = MODE == 2 && HD == 256 ? 2 : NS;
+  static constexpr bool kEarlyDO = MODE == 2;  // dO stage released after dP
   static constexpr int OFF_K = 0, OFF_V = KT;
-  static constexpr int OFF_Q = (MODE == 1 ? 1 : 2) * KT;  // [NS]
-  static constexpr int OFF_DO = OFF_Q + NS * QT;    // [NS]
+  static constexpr int OFF_Q = (MODE == 1 ? 1 : 2) * KT;  // [NQ]
+  static constexpr int OFF_DO = OFF_Q + NQ * QT;    // [ND]
   static constexpr int VEC = UQ * 4;                // UQ floats of lse2 / D (16-B aligned window)
-  static constexpr int OFF_LSE = OFF_DO + NS * QT;  // [NS][VEC]
-  static constexpr int OFF_DSUM = OFF_LSE + NS * VEC;
-  static constexpr int OFF_BAR = OFF_DSUM + NS * VEC;
-  static constexpr int NUM_BARS = 12 + 2 * NS;
+  static constexpr int OFF_LSE = OFF_DO + ND * QT;  // [NQ][VEC]
+  static constexpr int OFF_DSUM = OFF_LSE + NQ * VEC;
+  static constexpr int OFF_BAR = OFF_DSUM + NQ * VEC;
+  static constexpr int NUM_BARS = 12 + 2 * NQ + 2 * ND;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t DV_COL = 256, DK_COL = MODE ? 256 : 256 + HO;
   __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? uint32_t(UQ) : 0u; }
@@ -220,7 +225,7 @@ struct DkvCfg {
   static_assert(UQ == 64 || UQ == 32, "unit width");
   static_assert(DK_COL + HO <= 512 && DV_COL + HO <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "smem budget");
-  static_assert(4 * 2001 * 8 <= 2 * NS * QT, "PROF trace fits the Q/dO stages");
+  static_assert(4 * 2001 * 8 <= (NQ + ND) * QT, "PROF trace fits the Q/dO stages");
 };
 
 // Item descriptors are loaded one item ahead; only the raw span loads are issued then and the
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
                const BwdParams p) {
   using Cfg = DkvCfg<HD, UQ, MODE>;
   constexpr bool kDV = MODE != 2, kDK = MODE != 1;  // accumulators of this launch (dK needs dP / dS)
-  constexpr int NS = Cfg::NS, HO = Cfg::HO, CW = Cfg::CW;
+  constexpr int NQ = Cfg::NQ, ND = Cfg::ND, HO = Cfg::HO, CW = Cfg::CW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* bar_kv_full = bars + 0;
@@ -312,8 +317,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   uint64_t* bar_dp_full = bars + 6;    // [2]
   // bars + 8, + 9: spare (Pᵀ completion rides on the dSᵀ barrier: one MMA wait per unit)
   uint64_t* bar_ds_full = bars + 10;   // [2] 8 warp arrivals: dSᵀ written over dP
-  uint64_t* bar_qd_full = bars + 12;        // [NS] Q + dO (+ lse2 / D windows) of a unit
-  uint64_t* bar_qd_empty = bars + 12 + NS;  // [NS] committed after the unit's dK
+  uint64_t* bar_qd_full = bars + 12;        // [NQ] Q (+ lse2 / D windows) of a unit
+  uint64_t* bar_qd_empty = bars + 12 + NQ;  // [NQ] committed after the unit's dK (dV pass: dV)
+  uint64_t* bar_do_full = bars + 12 + 2 * NQ;       // [ND] dO of a unit
+  uint64_t* bar_do_empty = bars + 12 + 2 * NQ + ND;  // [ND] after its last reader (dV, or dP)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -332,9 +339,13 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       mbar_init(&bar_dp_full[b], 1);
       mbar_init(&bar_ds_full[b], 8);
     }
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NQ; ++s) {
       mbar_init(&bar_qd_full[s], 1);
       mbar_init(&bar_qd_empty[s], 1);
+    }
+    for (int s = 0; s < ND; ++s) {
+      mbar_init(&bar_do_full[s], 1);
+      mbar_init(&bar_do_empty[s], 1);
     }
     fence_barrier_init();
   }
@@ -350,8 +361,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       WaitProf<PROF> wp;
       TraceCtr trace(trb);
       UnitCursor<UQ> c;
-      int s = 0;          // stage of unit c.u (= c.u % NS)
-      uint32_t ph = 0;    // parity of that stage's current use
+      int s = 0, sd = 0;        // Q / dO stages of unit c.u
+      uint32_t ph = 0, phd = 0;  // parities of those stages' current use
       for (bool v = c.start(p); v; v = c.next(p)) {
         if (c.it == 0) {
           if (c.k > 0) wp.template wait<1>(bar_kv_empty, (c.k - 1) & 1);
@@ -376,24 +387,33 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const int h = c.head(group), qb = c.qb() + c.itm.dl;  // data row of the unit's first query
         const int sh = (-qb) & 3;  // 16-B aligned window in shifted copy sh (k_bwd_pre)
         const int64_t vo = sh * p.vec_copy + int64_t(h) * p.Tp + qb + sh;
-        if (c.u >= NS) wp.template wait<0>(&bar_qd_empty[s], ph ^ 1);
+        if (c.u >= NQ) wp.template wait<0>(&bar_qd_empty[s], ph ^ 1);
         trace(1, c.u);  // P: Q/dO load issued
         if (PROF && (p.dbg & 2)) {  // timing experiment: no Q/dO traffic (the trace lives in the Q stages)
           mbar_arrive(&bar_qd_full[s]);
+          if (c.u >= ND) wp.template wait<0>(&bar_do_empty[sd], phd ^ 1);
+          mbar_arrive(&bar_do_full[sd]);
         } else {
-          mbar_expect_tx(&bar_qd_full[s], 2 * Cfg::QT + (kDK ? 2 : 1) * Cfg::VEC);
+          mbar_expect_tx(&bar_qd_full[s], Cfg::QT + (kDK ? 2 : 1) * Cfg::VEC);
 #pragma unroll
-          for (int j = 0; j < HD / 64; ++j) {
+          for (int j = 0; j < HD / 64; ++j)
             tma_load_2d(smem + Cfg::OFF_Q + s * Cfg::QT + j * Cfg::QBOX, &tmQ, h * HD + j * 64, qb, &bar_qd_full[s]);
-            tma_load_2d(smem + Cfg::OFF_DO + s * Cfg::QT + j * Cfg::QBOX, &tmdO, h * HD + j * 64, qb,
-                        &bar_qd_full[s]);
-          }
           bulk_load(smem + Cfg::OFF_LSE + s * Cfg::VEC, p.lse2 + vo, Cfg::VEC, &bar_qd_full[s]);
           if (kDK) bulk_load(smem + Cfg::OFF_DSUM + s * Cfg::VEC, p.dsum + vo, Cfg::VEC, &bar_qd_full[s]);
+          if (c.u >= ND) wp.template wait<0>(&bar_do_empty[sd], phd ^ 1);
+          mbar_expect_tx(&bar_do_full[sd], Cfg::QT);
+#pragma unroll
+          for (int j = 0; j < HD / 64; ++j)
+            tma_load_2d(smem + Cfg::OFF_DO + sd * Cfg::QT + j * Cfg::QBOX, &tmdO, h * HD + j * 64, qb,
+                        &bar_do_full[sd]);
         }
-        if (++s == NS) {
+        if (++s == NQ) {
           s = 0;
           ph ^= 1;
+        }
+        if (++sd == ND) {
+          sd = 0;
+          phd ^= 1;
         }
       }
       wp.flush(p.prof);
@@ -442,16 +462,19 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
                       sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
       };
       UnitCursor<UQ> ca, cc;
-      uint32_t as = 0, aph = 0;  // stage / parity of the look-ahead unit ca.u
+      uint32_t as = 0, aph = 0;    // Q stage / parity of the look-ahead unit ca.u
+      uint32_t ads = 0, adph = 0;  // its dO stage / parity
       bool va = false;
       auto adv_a = [&] {
         va = ca.next(p);
-        if (++as == NS) { as = 0; aph ^= 1; }
+        if (++as == NQ) { as = 0; aph ^= 1; }
+        if (++ads == ND) { ads = 0; adph ^= 1; }
       };
       auto issue_SdP = [&] {  // S and dP of unit ca.u (both buffers of its parity are free)
         trace(14, ca.u);  // M: boundary S/dP issue entered
         if (ca.it == 0) wp.template wait<0>(bar_kv_full, ca.k & 1);
         wp.template wait<1>(&bar_qd_full[as], aph);
+        wp.template wait<1>(&bar_do_full[ads], adph);  // (dV pass: for dV(u), issued later)
         trace(15, ca.u);  // M: K/V + Q/dO ready
         tc_fence_after();
         const uint32_t bb = ca.u & 1;
@@ -459,8 +482,9 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           mma_S(Cfg::s_col(bb), as * QT16);
           umma_commit(&bar_s_full[bb]);
           if (kDK) {
-            mma_dP(Cfg::dp_col(bb), as * QT16);
+            mma_dP(Cfg::dp_col(bb), ads * QT16);
             umma_commit(&bar_dp_full[bb]);
+            if (Cfg::kEarlyDO) umma_commit(&bar_do_empty[ads]);  // dP is dO's only reader here
           }
           if (ca.last()) umma_commit(bar_kv_empty);  // the item's last readers of K and V
         }
@@ -469,13 +493,16 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       };
       va = ca.start(p);
       while (va && ca.k == 0 && ca.u < 2) issue_SdP();  // prologue: first item only
-      uint32_t cs = 0, b = 0, ph = 0;  // stage of cc.u; TMEM buffer cc.u & 1; its use parity
+      uint32_t cs = 0, cds = 0, b = 0, ph = 0;  // Q / dO stages of cc.u; TMEM buffer cc.u & 1; its use parity
       for (bool vc = cc.start(p); vc; vc = cc.next(p)) {
-        const uint32_t coff = cs * QT16, aoff = as * QT16;
+        const uint32_t coff = cs * QT16, aoff = as * QT16, cdoff = cds * QT16, adoff = ads * QT16;
         const bool early = va && ca.u == cc.u + 2 && ca.k == cc.k;  // S/dP(u+2) in this unit's block
         const bool a_last = ca.last(), c_last = cc.last();
         const uint32_t acc0 = cc.it > 0 ? 1u : 0u;
-        if (early) wp.template wait<1>(&bar_qd_full[as], aph);
+        if (early) {
+          wp.template wait<1>(&bar_qd_full[as], aph);
+          wp.template wait<1>(&bar_do_full[ads], adph);
+        }
         // dSᵀ(u) written ⇒ Pᵀ(u) written (each softmax warp stores P before dS): one wait per unit
         wp.template wait<5>(&bar_ds_full[b], ph);
         trace(12, cc.u);  // M: ds_full seen
@@ -483,7 +510,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           // dV += Pᵀ·dO: A = Pᵀ in TMEM (queries 32j'..32j'+31 packed at S cols 32j'.. 32j'+15)
-          const uint64_t om = opaque(dOm) + coff, qm = opaque(dQm) + coff;
+          const uint64_t om = opaque(dOm) + cdoff, qm = opaque(dQm) + coff;
           if (kDV) {
 #pragma unroll
             for (int j = 0; j < UQ / 16; ++j)
@@ -503,10 +530,12 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
                           sdesc_add(qm, j * 2048), id_acc, j > 0 ? 1u : acc0);
           }
           umma_commit(&bar_qd_empty[cs]);
+          if (!Cfg::kEarlyDO) umma_commit(&bar_do_empty[cds]);  // dV(u) was dO's last reader
           if (c_last) umma_commit(bar_dkv_full);
           if (early && kDK) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
-            mma_dP(Cfg::dp_col(b), aoff);
+            mma_dP(Cfg::dp_col(b), adoff);
             umma_commit(&bar_dp_full[b]);
+            if (Cfg::kEarlyDO) umma_commit(&bar_do_empty[ads]);
             if (a_last) umma_commit(bar_kv_empty);
           }
         }
@@ -516,7 +545,8 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         // item boundary: the next item's first units (their buffers' previous readers, the dV /
         // dK of units ≤ u, are issued)
         while (va && ca.u <= cc.u + 2 && (ca.k == cc.k || (c_last && ca.k == cc.k + 1))) issue_SdP();
-        if (++cs == NS) cs = 0;
+        if (++cs == NQ) cs = 0;
+        if (++cds == ND) cds = 0;
         b ^= 1;
         ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
       }
@@ -552,7 +582,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         }
       }
       const int s = ss;
-      if (++ss == NS) ss = 0;
+      if (++ss == NQ) ss = 0;
       if ((c.u & 1) == g) {
         const uint32_t ph = (c.u >> 1) & 1;
         const int qb = c.qb();

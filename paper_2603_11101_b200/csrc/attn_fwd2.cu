@@ -466,10 +466,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     };
     int2 rs_n = make_int2(0, 0);
+    float qs_n = 1.f;  // FP8: the next item's row Q block scale (prefetched with its span)
+    auto q_scale_of = [&](const FwdItem& f) {
+      return __ldg(p.q_scale + int64_t(f.h) * p.nbt + min(f.q0 + r + f.dl, p.T - 1) / 128);
+    };
     if (i0 < n_items) {
       FwdItem f;
       get_desc(0, f, false);
       rs_n = f.q0 + r < p.T ? __ldg(p.rows_span + f.q0 + r) : make_int2(0, 0);
+      if constexpr (FP8) qs_n = q_scale_of(f);
     }
     for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
       FwdItem itm;
@@ -477,25 +482,34 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       __syncwarp();
       warp_arrive(&bar_desc_empty[m % Cfg::NDESC]);
       const int2 rs = rs_n;
-      if (sched_item(m + 1) < n_items) {  // prefetch the next item's row span
+      const float qs = qs_n;
+      if (sched_item(m + 1) < n_items) {  // prefetch the next item's row span (and FP8 row scale)
         FwdItem f;
         get_desc(m + 1, f, false);
         rs_n = f.q0 + r < p.T ? __ldg(p.rows_span + f.q0 + r) : make_int2(0, 0);
+        if constexpr (FP8) qs_n = q_scale_of(f);
       }
       const int row = itm.q0 + r;
       const uint32_t o_tm = tmem + lane_off + Cfg::O_COL + (k & 1) * HD + qp * OC;
       // FP8: the row's Q block scale (a segment-aligned tile may straddle two 128-token blocks)
-      if constexpr (FP8) sl2 = p.scale_log2 * __ldg(p.q_scale + int64_t(itm.h) * p.nbt + min(row + itm.dl, p.T - 1) / 128);
+      if constexpr (FP8) sl2 = p.scale_log2 * qs;
+      (void)qs;
       float m_run = -INFINITY, l_run = 0.f;
+      // FP8: this quarter's K block scales, one tile ahead in registers (data-row blocks)
+      const float* ksc = FP8 ? p.k_scale + int64_t(itm.kh) * p.nbt : nullptr;
+      auto kscale = [&](int jj, float& a, float& b) {
+        const int kb = (itm.kv_lo + jj * BN + c0 + itm.dl) / 128;
+        a = __ldg(ksc + min(kb, p.nbt - 1));
+        b = __ldg(ksc + min(kb + 1, p.nbt - 1));
+      };
+      float k0n = 1.f, k1n = 1.f;
+      if constexpr (FP8) kscale(0, k0n, k1n);
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
         const int kv0 = itm.kv_lo + j * BN + c0;
-        float k0s = 1.f, k1s = 1.f;  // FP8: this quarter's K block scales, loaded before the S wait
-        if constexpr (FP8) {  // scale blocks of data rows
-          const float* ksc = p.k_scale + int64_t(itm.kh) * p.nbt;
-          k0s = __ldg(ksc + min((kv0 + itm.dl) / 128, p.nbt - 1));
-          k1s = __ldg(ksc + min((kv0 + itm.dl) / 128 + 1, p.nbt - 1));
-        }
+        const float k0s = k0n, k1s = k1n;
+        if constexpr (FP8)
+          if (j + 1 < itm.nkv) kscale(j + 1, k0n, k1n);
         if (j + 1 == itm.nkv && qp >= ((itm.kv_hi - kv0 + c0 + 31) >> 5)) {
           // The item's last key tile covers only ⌈valid/32⌉ quarters (its S MMA ran with N = 32 of
           // them): this quarter has no S, exponentials or P.  It still takes part in the row-max

@@ -52,9 +52,10 @@ H, HKV, D = 16, 16, 128
 SAMPLES_PER_GPU = 512
 CAPACITY = 8192
 METRIC = "effective tokens/sec & TFLOPS (non-pad) varlen attn fwd+bwd, 1/2/4/8 B200"
-# our kernel launches per step: pack 14 (init, hist, class_scan, ffd, assign, 3 scans x 3, layout),
-# shard plan 1, fwd 3 (spans, tiles, attention), bwd 4 (pre, tiles, dK/dV, dQ)
-LAUNCHES_PER_STEP = 22
+# our kernel launches per step (profiles/r02/step_breakdown.txt): pack 14 (init, hist, class_scan,
+# ffd_warp, assign, 3 scans x 3, layout), shard plan 8 (cost, bins, lpt, binscan, 3 sample scans,
+# tail), fwd 3 (spans, tiles, attention), bwd 4 (pre, tiles, dK/dV, dQ)
+LAUNCHES_PER_STEP = 29
 
 
 def parse():

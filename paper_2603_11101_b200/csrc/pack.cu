@@ -447,9 +447,7 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int64_t n, int cap, PackWs w
   int32_t* cmax = sm + 2 * kWarpMaxBins + (cnt_smem ? cap + 1 : 0);  // [kWarpMaxBins / 32]
   auto chunk_max = [&](int ch, int nbins) {  // recompute cmax[ch] from the bins themselves
     const int b = ch * 32 + lane;
-    int v = b < nbins ? act_rem[b] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(full, v, o));
+    const int v = __reduce_max_sync(full, unsigned(b < nbins ? act_rem[b] : 0));  // REDUX: one instruction
     if (lane == 0) cmax[ch] = v;
   };
   int nb = 0, nruns = 0;
@@ -496,9 +494,7 @@ __global__ void __launch_bounds__(32, 1) k_ffd_warp(int64_t n, int cap, PackWs w
           }
           nruns += __popc(tm);
           running += __shfl_sync(full, inc, 31);
-          int mx = nrem;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(full, mx, o));
+          const int mx = __reduce_max_sync(full, unsigned(nrem));
           if (lane == 0) cmax[ch] = mx;
           __syncwarp();
         }

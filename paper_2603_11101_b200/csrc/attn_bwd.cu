@@ -217,6 +217,13 @@ struct DkvCfg {
   static constexpr int NUM_BARS = 12 + 2 * NQ + 2 * ND;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t DV_COL = 256, DK_COL = MODE ? 256 : 256 + HO;
+  // head_dim-256 passes: the item's K tile lives in TMEM (tcgen05.cp from the TMA-loaded smem tile at
+  // the item's first unit), so Sᵀ = K·Qᵀ takes A from TMEM instead of re-reading 64 KB of smem per
+  // 32-query unit: 16 K-steps × 8 columns in the columns S / dP leave free
+  static constexpr bool kKTmem = HD == 256 && MODE != 0;
+  __host__ __device__ static constexpr uint32_t k_col(int s) {
+    return MODE == 1 ? 128u + 8u * s : (s < 8 ? 64u + 8u * s : 192u + 8u * (s - 8));
+  }
   __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? uint32_t(UQ) : 0u; }
   __host__ __device__ static constexpr uint32_t dp_col(int b) { return 128u + (b ? uint32_t(UQ) : 0u); }
   // TMEM column of K-step j (16 queries) of Pᵀ / dSᵀ: warp chunks of CW queries sit at column
@@ -450,9 +457,14 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       auto mma_S = [&](uint32_t col, uint32_t soff) {
         const uint64_t a0 = opaque(dK0), b0 = opaque(dQk) + soff;
 #pragma unroll
-        for (int j = 0; j < HD / 16; ++j)
-          umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
-                      sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
+        for (int j = 0; j < HD / 16; ++j) {
+          if constexpr (Cfg::kKTmem)
+            umma_f16_ts(tmem + col, tmem + Cfg::k_col(j), sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s,
+                        j > 0 ? 1u : 0u);
+          else
+            umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
+                        sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
+        }
       };
       auto mma_dP = [&](uint32_t col, uint32_t soff) {
         const uint64_t a0 = opaque(dV0), b0 = opaque(dOk) + soff;
@@ -479,6 +491,13 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_after();
         const uint32_t bb = ca.u & 1;
         if (elect_one()) {
+          if (Cfg::kKTmem && ca.it == 0) {  // the item's K tile → TMEM (in order after the previous
+            const uint64_t a0 = opaque(dK0);  // item's last Sᵀ, before this item's first)
+#pragma unroll
+            for (int j = 0; j < HD / 16; ++j)
+              tmem_cp_128x256b(tmem + Cfg::k_col(j), sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32));
+            if (!kDK) umma_commit(bar_kv_empty);  // dV pass: K's smem tile is free once copied
+          }
           mma_S(Cfg::s_col(bb), as * QT16);
           umma_commit(&bar_s_full[bb]);
           if (kDK) {
@@ -486,7 +505,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             umma_commit(&bar_dp_full[bb]);
             if (Cfg::kEarlyDO) umma_commit(&bar_do_empty[ads]);  // dP is dO's only reader here
           }
-          if (ca.last()) umma_commit(bar_kv_empty);  // the item's last readers of K and V
+          if (ca.last() && !(Cfg::kKTmem && !kDK)) umma_commit(bar_kv_empty);  // the item's last readers of K and V
         }
         __syncwarp();
         adv_a();
@@ -520,7 +539,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           if (early) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
             mma_S(Cfg::s_col(b), aoff);
             umma_commit(&bar_s_full[b]);
-            if (!kDK && a_last) umma_commit(bar_kv_empty);
+            if (!kDK && a_last && !Cfg::kKTmem) umma_commit(bar_kv_empty);
           }
           if (kDK) {
             // dK += dSᵀ·Q: A = dSᵀ in TMEM over the dP columns

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- loads
   if (tid == 0) {
     uint32_t bytes = 0;
-    if (mode == 0 || mode == 1 || mode == 2) {
+    if (mode == 0 || mode == 1 || mode == 2 || mode == 4) {
       if (mode != 2) {
         for (int i = 0; i < K / 64; ++i) tma_load_2d(sA + i * 128 * 128, &tmA, i * 64, 0, &bar_load);
         bytes += 128 * K * 2;
@@ -77,13 +77,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool a_mn = (mode == 3), b_mn = (mode != 0);
     const uint32_t idesc = make_idesc_bf16(128, N, a_mn, b_mn);
     const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
+    if (mode == 4)  // A: TMA (K-major SW128) → smem → tcgen05.cp per 16-element K-step → TMEM [256, 256 + K/2)
+      for (int s = 0; s < K / 16; ++s)
+        tmem_cp_128x256b(tmem + 256 + s * 8, make_sdesc_sw128(sa + (s / 4) * 128 * 128 + (s % 4) * 32, 16, 1024));
     for (int s = 0; s < K / 16; ++s) {
       uint64_t bdesc;
       if (!b_mn)
         bdesc = make_sdesc_sw128(sb + (s / 4) * N * 128 + (s % 4) * 32, 16, 1024);
       else
         bdesc = make_sdesc_sw128(sb + s * 2048, K * 128, 1024);
-      if (mode == 2) {
+      if (mode == 2 || mode == 4) {
         umma_f16_ts(tmem, tmem + 256 + s * 8, bdesc, idesc, s > 0);
       } else {
         uint64_t adesc;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 extern "C" int vlasim_selftest_umma(int mode, const void* d_a, const void* d_b, float* d_c, int32_t N, int32_t K,
                                     vlasim_stream_t stream) {
   using namespace vlasim_host;
-  if (mode < 0 || mode > 3) return set_error(VLASIM_ECONFIG, "selftest: bad mode %d", mode);
+  if (mode < 0 || mode > 4) return set_error(VLASIM_ECONFIG, "selftest: bad mode %d", mode);
   if (N < 64 || N > 256 || N % 64 || K < 64 || K > 256 || K % 64)
     return set_error(VLASIM_ECONFIG, "selftest: N,K must be multiples of 64 in [64,256] (N=%d K=%d)", N, K);
   CUtensorMap tA{}, tB{};

@@ -334,6 +334,12 @@ __device__ __forceinline__ float2 f2_ex2_poly(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// smem → TMEM copy of a 128-row × 256-bit tile described by a UMMA smem descriptor (one A-operand
+// K-step of 16 bf16): lane r ← row r, 8 columns.  Executes in issue order with tcgen05.mma.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

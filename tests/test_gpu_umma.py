@@ -17,7 +17,7 @@ def _run(mode, a, b, N):
 
 
 @pytest.mark.parametrize("N,K", [(128, 128), (64, 64), (256, 128), (128, 256), (64, 256)])
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 def test_umma_layouts(gpu, mode, N, K):
     g = torch.Generator(device="cuda").manual_seed(mode * 1000 + N + K)
     if mode == 3:

@@ -345,8 +345,12 @@ struct FwdPCfg {
   static constexpr int KV_BYTES = BN * HD * 2;
   static constexpr int OFF_K = Q_BYTES, OFF_V = OFF_K + KS * KV_BYTES;
   static constexpr int SMEM = OFF_V + VS * KV_BYTES + 1024;
-  static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, P_COL = 2 * BN + HD;
-  static_assert(P_COL + BN <= 512, "TMEM budget");
+  // TMEM: S[2] [0, 2·BN) with P (bf16) written over its S buffer, O [2·BN, 2·BN + HD), and the item's
+  // Q tile [Q_COL, +HD/2): copied from smem by tcgen05.cp at the item start, so S = Q·Kᵀ takes A
+  // from TMEM — the 64 KB Q tile is not re-read from smem for every key tile, and its smem buffer is
+  // released as soon as it is copied (the next item's Q loads during this item)
+  static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, Q_COL = 2 * BN + HD;
+  static_assert(Q_COL + HD / 2 <= 512, "TMEM budget");
   static_assert(SMEM <= 232448 - 1024, "smem budget");
 };
 
@@ -477,10 +481,14 @@ __global__ void __launch_bounds__(192, 1)
         const int nkv = fwdp_item<BN>(p, i).nkv;
         mbar_wait(&bar_q_full, k & 1);
         tc_fence_after();
-        if (nkv == 0) {  // (no visible key: cannot happen for a non-empty tile) keep the phases aligned
-          umma_commit(&bar_q_empty);
-          umma_commit(&bar_o_done);
-        }
+        // Q → TMEM (one tcgen05.cp per 16-element K-step; in issue order after the previous item's
+        // last S MMA), then Q's smem buffer is free
+#pragma unroll
+        for (int s = 0; s < HD / 16; ++s)
+          tmem_cp_128x256b(tmem + Cfg::Q_COL + 8 * s,
+                           make_sdesc_sw128(q_addr + (s / 4) * Cfg::BM * 128 + (s % 4) * 32, 16, 1024));
+        umma_commit(&bar_q_empty);
+        if (nkv == 0) umma_commit(&bar_o_done);  // (no visible key: cannot happen) keep the phases aligned
         for (int j = 0; j <= nkv; ++j) {
           if (j < nkv) {
             const int gj = g + j, st = gj % KS;
@@ -490,13 +498,11 @@ __global__ void __launch_bounds__(192, 1)
             const uint32_t d_s = tmem + Cfg::S_COL + (gj & 1) * BN;
 #pragma unroll
             for (int s = 0; s < HD / 16; ++s) {
-              const uint64_t a = make_sdesc_sw128(q_addr + (s / 4) * Cfg::BM * 128 + (s % 4) * 32, 16, 1024);
               const uint64_t b = make_sdesc_sw128(k_addr + (s / 4) * BN * 128 + (s % 4) * 32, 16, 1024);
-              umma_f16_ss(d_s, a, b, idesc_s, s > 0);
+              umma_f16_ts(d_s, tmem + Cfg::Q_COL + 8 * s, b, idesc_s, s > 0 ? 1u : 0u);
             }
             umma_commit(&bar_s_full[gj & 1]);
             umma_commit(&bar_k_empty[st]);
-            if (j == nkv - 1) umma_commit(&bar_q_empty);  // Q free for the next item's tile
           }
           if (j > 0) {
             const int gj = g + j - 1, st = gj % VS;
@@ -505,7 +511,7 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&bar_v_full[st], (gj / VS) & 1);
             tc_fence_after();
             const uint32_t v_addr = smem_u32(sV + st * Cfg::KV_BYTES);
-            const uint32_t a_tm = tmem + Cfg::P_COL + (gj & 1) * (BN / 2);
+            const uint32_t a_tm = tmem + Cfg::S_COL + (gj & 1) * BN;  // P over its S buffer
 #pragma unroll
             for (int s = 0; s < BN / 16; ++s) {
               const uint64_t b = make_sdesc_sw128(v_addr + s * 2048, BN * 128, 1024);
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(192, 1)
             lq[q & 1] = f2_add(lq[q & 1], pe);
             pk[q] = pack_bf16x2(pe.x, pe.y);
           }
-          tmem_st16(tmem + lane_off + Cfg::P_COL + sb * (BN / 2) + c / 2, pk);
+          tmem_st16(tmem + lane_off + Cfg::S_COL + sb * BN + c / 2, pk);  // P over the S it was read from
         }
         l_run += (lq[0].x + lq[1].x) + (lq[0].y + lq[1].y);
         tmem_wait_st();

@@ -410,6 +410,31 @@ def measure_configs(dev, iters=10):
                       "token_ids_gbs": (12 * tok5 + 8 * n5) / (tid / 1e3) / 1e9,
                       "shard_lpt_ms_8_ranks": tsh, "lpt_balance_max_over_mean": balance,
                       "l2": "packer metadata (4 MB lengths) fits in L2; token ids (600 MB) do not"}
+    del plan5
+    # ---- §8(f) next rows: the general quantizer on one weight-sized tensor, and π0.5 dynamic padding
+    from paper_2603_11101_b200 import padding, quant
+    w = torch.randn(8192, 8192, device=dev)  # 256 MB fp32 (> L2)
+    qrows = {}
+    wsq = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+    for gname, ax in (("tensor", 0), ("channel", 0), ("channel", 1), ("block", 0)):
+        qo = quant.quantize(w, gname, ax, workspace=wsq)
+        tq = event_ms(lambda: quant.quantize(w, gname, ax, check_finite=False, out=qo, workspace=wsq), iters, st)
+        qrows[f"{gname}:{ax}" if gname == "channel" else gname] = {
+            "ms": tq, "gbs_algorithmic": 5 * w.numel() / (tq / 1e3) / 1e9,
+            "frac_of_hbm": 5 * w.numel() / (tq / 1e3) / 1e9 / PEAKS["hbm_gbs"]}
+    out["quantizer"] = {"workload": "8192 x 8192 fp32 -> E4M3 codes + scales (amax pass + code pass)",
+                        "algorithmic_bytes": 5 * w.numel(), "granularities": qrows,
+                        "note": "PerTensor and last-axis PerChannel read x twice (9 B/element of HBM traffic, the scale needs the maximum first); PerBlock and axis-0 PerChannel are one fused pass (5 B/element)"}
+    del w
+    Lp = synthetic.gen_lengths(256, synthetic.DIST_PI05, 16, 200, 50)
+    dp = padding.dynamic_pad(Lp)
+    xs = torch.randn(int(Lp.sum()), 8, 256, device=dev).bfloat16()
+    xp = padding.pad_rows(xs, dp)
+    tpad = event_ms(lambda: padding.pad_rows(xs, dp), iters, st)
+    out["dynamic_padding"] = {"workload": "pi0.5 batch of 256 samples (config-3 lengths), rows 8 x 256 bf16",
+                              "pad_to": dp.pad_to, "padding_rate": dp.padding_rate(), "pad_rows_ms": tpad,
+                              "pad_rows_gbs": (xs.numel() * 2 + xp.numel() * 2) / (tpad / 1e3) / 1e9}
+    del xs, xp
     return out
 
 

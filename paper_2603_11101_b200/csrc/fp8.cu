@@ -9,18 +9,17 @@
 #include <cuda_bf16.h>
 
 #include "common.hpp"
+#include "e4m3.cuh"
 #include "sm100.cuh"
 
+using vlasim_dev::cvt_e4m3x2;
+using vlasim_dev::e4m3_fix;
+using vlasim_dev::e4m3_suspect;
 using vlasim_dev::f2_fma;
 using vlasim_dev::f2_mul;
 
 namespace {
 
-__device__ __forceinline__ uint16_t cvt_e4m3x2(float lo, float hi) {
-  uint16_t r;
-  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
-  return r;
-}
 
 __device__ __forceinline__ float e4m3_to_float(uint8_t c) {
   const int e = (c >> 3) & 0xF, m = c & 7;
@@ -29,35 +28,6 @@ __device__ __forceinline__ float e4m3_to_float(uint8_t c) {
   else if (e == 15 && m == 7) v = __int_as_float(0x7fc00000);
   else v = ldexpf(1.f + float(m) / 8.f, e - 7);
   return (c & 0x80) ? -v : v;
-}
-
-// Exact RNE (the code of the REAL quotient x / scale, scale = amax / 448).  The fp32
-// quotient q = RN(x / RN(amax / 448)) is within a few fp32 ulps of the real quotient X = |x|·448/amax,
-// so cvt(q) is the right code unless X lies within those ulps of a midpoint between two E4M3 values
-// (or in the subnormal range, where the midpoint grid is finer): only then is the candidate code
-// re-decided, by exact fp64 comparisons of |x|·448 against midpoint · amax (both products exact:
-// ≤ 11 and ≤ 13 significant bits for bf16 inputs).  Midpoints have the fp32 pattern 1.xxx1 000…0,
-// i.e. low 20 mantissa bits 0x80000.
-__device__ __forceinline__ bool e4m3_suspect(float q) {
-  const float a = fabsf(q);
-  const int low = int(__float_as_uint(a) & 0xFFFFFu);
-  return a < 0.015625f || abs(low - 0x80000) <= 64;
-}
-
-__device__ __noinline__ uint32_t e4m3_fix(uint32_t c, float ax, float amax) {
-  const double A = double(ax) * 448.0, B = double(amax);
-  const int e = int(c >> 3), m = int(c & 7), ee = e == 0 ? 1 : e;
-  const int mant = e == 0 ? m : 8 + m;
-  if (c < 0x7E) {  // midpoint to the next code up: (2·mant + 1) · 2^(ee−11)
-    const double mu = ldexp(double(2 * mant + 1), ee - 11) * B;
-    if (A > mu || (A == mu && (c & 1))) return c + 1;
-  }
-  if (c > 0) {  // midpoint to the next code down (half the spacing across a binade edge)
-    const double md = (m == 0 && e >= 2) ? ldexp(double(4 * mant - 1), ee - 12) * B
-                                         : ldexp(double(2 * mant - 1), ee - 11) * B;
-    if (A < md || (A == md && (c & 1))) return c - 1;
-  }
-  return c;
 }
 
 // The same decision in fp32, exact once both sides are scaled by p2 = 2^-E(amax): A = |x|·p2·448

@@ -101,9 +101,10 @@ def block_partition(shape: Sequence[int], block: Tuple[int, int] = (128, 128)) -
 
 
 def quantize(x: torch.Tensor, granularity: str = "block", axis: int = 0, *, check_finite: bool = True,
-             stream=None) -> QuantizedTensor:
+             out: QuantizedTensor | None = None, workspace: torch.Tensor | None = None, stream=None) -> QuantizedTensor:
     """SPEC.md:580-588 on the GPU.  Non-finite input → ConfigError naming the flat index (synchronising;
-    check_finite=False keeps the call asynchronous and leaves codes unwritten on error)."""
+    check_finite=False keeps the call asynchronous and leaves codes unwritten on error).  `out` (a
+    QuantizedTensor of this shape and granularity) and `workspace` are reused when given."""
     if not torch.is_tensor(x) or not x.is_cuda or x.dtype not in _DTYPES or not x.is_contiguous():
         raise ConfigError("quantize expects a contiguous CUDA fp32 or bf16 tensor")
     if x.dim() < 1 or x.dim() > 8 or x.numel() < 1:
@@ -112,14 +113,19 @@ def quantize(x: torch.Tensor, granularity: str = "block", axis: int = 0, *, chec
     sshape = scales_shape(tuple(x.shape), granularity, axis)
     shp, keep = _shape_arr(x.shape)
     L = _lib.lib()
-    ws = torch.empty(max(1, L.vlasim_fp8_quantize_workspace_size(shp, x.dim(), g, axis)), dtype=torch.uint8,
-                     device=x.device)
-    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
-    scales = torch.empty(sshape, dtype=torch.float32, device=x.device)
-    status = torch.empty(2, dtype=torch.int32, device=x.device)
+    nws = max(1, L.vlasim_fp8_quantize_workspace_size(shp, x.dim(), g, axis))
+    nws = (nws + 15) // 16 * 16  # the 8-byte status word sits after the aligned workspace
+    ws = workspace if workspace is not None and workspace.numel() >= nws + 8 else \
+        torch.empty(nws + 8, dtype=torch.uint8, device=x.device)
+    if out is not None and tuple(out.codes.shape) == tuple(x.shape) and tuple(out.scales.shape) == sshape:
+        codes, scales = out.codes, out.scales
+    else:
+        codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+        scales = torch.empty(sshape, dtype=torch.float32, device=x.device)
+    status = ws[nws:nws + 8].view(torch.int32)
     _lib.check(L.vlasim_fp8_quantize_cuda(_lib.ptr(x), _DTYPES[x.dtype], shp, x.dim(), g, axis, _lib.ptr(codes),
                                           _lib.ptr(scales, _lib.f32p), _lib.ptr(status, _lib.i32p), _lib.ptr(ws),
-                                          ws.numel(), 1 if check_finite else 0, _lib.stream_ptr(stream)), "quantize")
+                                          nws, 1 if check_finite else 0, _lib.stream_ptr(stream)), "quantize")
     del keep
     return QuantizedTensor(codes, scales, tuple(x.shape), granularity, axis % x.dim() if g == 1 else 0)
 

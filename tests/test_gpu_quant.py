@@ -10,7 +10,11 @@ pytestmark = pytest.mark.gpu
 CASES = [((300, 260), "tensor", 0), ((300, 260), "channel", 0), ((300, 260), "channel", 1),
          ((300, 260), "block", 0), ((3, 129, 257), "block", 0), ((5, 7, 11), "channel", 1),
          ((4, 6, 130, 33), "block", 0), ((1000,), "tensor", 0), ((1000,), "channel", 0),
-         ((2, 3000, 64), "channel", -1), ((257, 4100), "channel", 1), ((1, 1), "block", 0)]
+         ((2, 3000, 64), "channel", -1), ((257, 4100), "channel", 1), ((1, 1), "block", 0),
+         # one case per kernel route: PerTensor with a scalar tail, fused PerChannel (vector and
+         # scalar), generic PerChannel (middle axis / a group above 16 K elements), a column slab split
+         ((7, 333), "tensor", 0), ((2, 9000), "channel", 0), ((3, 5001), "channel", 0),
+         ((3, 40, 6000), "channel", 1), ((2, 20000), "channel", 0), ((5000, 12), "channel", 1)]
 
 
 def _inputs(shape, seed, kind):
@@ -81,3 +85,36 @@ def test_bad_arguments(gpu):
         quant.quantize(torch.ones(4, 4, device="cuda"), "channel", 2)
     with pytest.raises(ConfigError):
         quant.quantize(torch.ones(4, 4, device="cuda", dtype=torch.float16), "tensor")
+
+
+def test_unaligned_input_view(gpu, orc):
+    """An input that starts off a 16-byte boundary (a contiguous view into a larger buffer) takes the
+    scalar-load path and gives the same codes."""
+    from paper_2603_11101_b200 import quant
+    buf = torch.randn(1 + 300 * 260, device="cuda")
+    x = buf[1:].view(300, 260)
+    assert x.data_ptr() % 16 != 0
+    for g, ax in (("tensor", 0), ("channel", 0), ("channel", 1), ("block", 0)):
+        qt = quant.quantize(x, g, ax)
+        codes, scales = orc.fp8_quantize(x.cpu().numpy(), g, ax)
+        assert np.array_equal(qt.codes.cpu().numpy(), codes)
+
+
+@pytest.mark.parametrize("shape,g,axis", [((300, 260), "tensor", 0), ((300, 260), "channel", 0),
+                                          ((300, 260), "channel", 1), ((300, 260), "block", 0),
+                                          ((3, 40, 6000), "channel", 1)])
+def test_extreme_magnitudes(gpu, orc, shape, g, axis):
+    """Group maxima from fp32 subnormals to 1e38 (the degenerate-maximum fp64 path and the
+    subnormal-range midpoint test), small elements in wide-range groups, and exact E4M3 midpoints."""
+    from paper_2603_11101_b200 import quant
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(shape).astype(np.float32)
+    mag = rng.choice(np.array([1e-40, 1e-38, 1e-31, 1e-3, 1.0, 1e31, 3e37], np.float32), shape[:-1] + (1,))
+    x = (x * mag).astype(np.float32)
+    x.reshape(-1)[::17] *= np.float32(1e-6)  # tiny elements inside large groups
+    mid = (rng.integers(-512, 512, shape) / 1024.0).astype(np.float32)  # subnormal-range midpoints
+    x.reshape(-1)[::5] = mid.reshape(-1)[::5]
+    qt = quant.quantize(torch.from_numpy(x).cuda(), g, axis)
+    codes, scales = orc.fp8_quantize(x, g, axis)
+    assert np.array_equal(qt.scales.cpu().numpy().reshape(-1), scales)
+    assert np.array_equal(qt.codes.cpu().numpy(), codes)

@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--cfg", type=int, default=2, choices=[2, 3, 4])
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--samples", type=int, default=0)
+    ap.add_argument("--seg-src", action="store_true", help="sample-major inputs through seg_src (as bench.py)")
     a = ap.parse_args()
     dev = torch.device("cuda")
     if a.cfg == 3:
@@ -65,20 +66,21 @@ def main():
     v = synthetic.fill_bf16(torch.empty(T, Hkv, d, dtype=torch.bfloat16, device=dev), "v")
     do = synthetic.fill_bf16(torch.empty(T, H, d, dtype=torch.bfloat16, device=dev), "do")
     cu = plan.cu_seqlens[: n + 1]
+    seg = packing.seg_src(plan) if a.seg_src else None
     o = torch.empty_like(q)
     lse = torch.empty(H, T, dtype=torch.float32, device=dev)
     ws = attention.BwdWorkspace()
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     fl = 4.0 * d * H * pairs
-    out = {"cfg": a.cfg, "samples": n, "tokens": T, "bins": plan.num_bins(), "H": H, "Hkv": Hkv, "d": d,
+    out = {"cfg": a.cfg, "seg_src": a.seg_src, "samples": n, "tokens": T, "bins": plan.num_bins(), "H": H, "Hkv": Hkv, "d": d,
            "mask": mask, "pairs": pairs}
 
     def fwd():
-        attention.varlen_attn_fwd(q, k, v, cu, mask_mode=mask, prefix_len=prefix, out=o, lse=lse)
+        attention.varlen_attn_fwd(q, k, v, cu, mask_mode=mask, prefix_len=prefix, out=o, lse=lse, seg_src=seg)
 
     def bwd():
         attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, mask_mode=mask, prefix_len=prefix, workspace=ws,
-                                  dq=dq, dk=dk, dv=dv)
+                                  dq=dq, dk=dk, dv=dv, seg_src=seg)
 
     tf = timed(fwd, a.iters)
     out["fwd_ms"], out["fwd_tflops"] = tf, fl / tf / 1e9
@@ -89,7 +91,7 @@ def main():
         l8 = torch.empty_like(lse)
 
         def f8():
-            fp8.varlen_attn_fwd_fp8qk(qc, qs, kc, ks, v, cu, out=o8, lse=l8)
+            fp8.varlen_attn_fwd_fp8qk(qc, qs, kc, ks, v, cu, out=o8, lse=l8, seg_src=seg)
 
         def quant():
             fp8.quant_block(q)

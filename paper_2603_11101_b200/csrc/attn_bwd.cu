@@ -22,6 +22,7 @@
 // through the optional row_map (scatter back to sample order fused into the epilogues).
 #include <cfloat>
 #include <climits>
+#include <cstring>
 
 #include "attn_common.cuh"
 #include "common.hpp"
@@ -201,7 +202,8 @@ struct DkvCfg {
   static constexpr int QT = UQ * HD * 2;   // Q or dO tile (UQ queries)
   // Q / dO stages: 5, except head_dim 256 with K and V resident (3); the dV pass loads no V, and its
   // 64 KB hold two more stages — with S look-ahead of 2 units, 3 stages leave no load in flight
-  static constexpr int NS = HD == 256 && MODE != 1 ? 3 : 5;
+  // head_dim 128 (one pass): 4, so that the dK / dV staging tile of the TMA-store epilogue fits
+  static constexpr int NS = HD == 256 && MODE != 1 ? 3 : (HD == 128 && MODE == 0 ? 4 : 5);
   // Q (+ lse2 / D windows) and dO have separate rings: NQ / ND stages.  Where dO is read only by
   // dP (the dK pass) its stage is released right after dP — 4 Q + 2 dO stages in the smem of 3 pairs,
   // so one more unit's loads are in flight; elsewhere dV reads dO at the end of the unit (NQ = ND).
@@ -213,8 +215,14 @@ struct DkvCfg {
   static constexpr int VEC = UQ * 4;                // UQ floats of lse2 / D (16-B aligned window)
   static constexpr int OFF_LSE = OFF_DO + ND * QT;  // [NQ][VEC]
   static constexpr int OFF_DSUM = OFF_LSE + NQ * VEC;
-  static constexpr int OFF_BAR = OFF_DSUM + NQ * VEC;
-  static constexpr int NUM_BARS = 12 + 2 * NQ + 2 * ND;
+  // single-pass launches (head_dim ≤ 128) write dK / dV through an SW128 staging tile and TMA stores
+  // (128 rows × HO bf16, 64-column boxes of 16 KB); the head-dim-256 passes store rows directly
+  static constexpr bool kTmaEpi = MODE == 0 && HD <= 128;
+  static constexpr int THREADS = 576;
+  static constexpr int OFF_STG = kTmaEpi ? (OFF_DSUM + NQ * VEC + 1023) & ~1023 : OFF_DSUM + NQ * VEC;
+  static constexpr int STG = kTmaEpi ? 128 * HO * 2 : 0;
+  static constexpr int OFF_BAR = OFF_STG + STG;
+  static constexpr int NUM_BARS = 12 + 2 * NQ + 2 * ND + 1;  // + epi_done
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
   static constexpr uint32_t DV_COL = 256, DK_COL = MODE ? 256 : 256 + HO;
   // head_dim-256 passes: the item's K tile lives in TMEM (tcgen05.cp from the TMA-loaded smem tile at
@@ -242,9 +250,8 @@ struct DkvCfg {
 struct KvItem {
   int k0, ke, dl, kh, q_lo, q_hi, nq, iters;
 };
-__device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
+__device__ __forceinline__ KvItem kv_item_t(const BwdParams& p, int i, int4 t) {
   KvItem it;
-  const int4 t = __ldg(&p.tiles[i / p.Hkv]);
   it.kh = i % p.Hkv;
   it.k0 = t.x;
   it.ke = t.y;
@@ -253,6 +260,8 @@ __device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) {
   it.q_hi = __ldg(&p.cols_span[t.y - 1].y);
   return it;
 }
+__device__ __forceinline__ int4 kv_tile(const BwdParams& p, int i) { return __ldg(&p.tiles[i / p.Hkv]); }
+__device__ __forceinline__ KvItem kv_item(const BwdParams& p, int i) { return kv_item_t(p, i, kv_tile(p, i)); }
 template <int UQ>
 __device__ __forceinline__ void kv_item_finish(const BwdParams& p, KvItem& it) {
   it.nq = max(0, (it.q_hi - it.q_lo + UQ - 1) / UQ);
@@ -268,6 +277,9 @@ struct UnitCursor {
   int i, it, k, u, n;
   int iq, hq;  // unit = (q head hq of the group, query tile iq): it = hq·nq + iq, kept without division
   KvItem itm, nxt;
+  // The tile record of item k+2 is loaded one boundary before its spans (which index by it): no
+  // role stalls on the dependent tiles → cols_span load chain at an item boundary.
+  int4 tnn;
   __device__ __forceinline__ bool has_next() const { return sched_item(k + 1) < n; }
   __device__ __forceinline__ bool start(const BwdParams& p) {
     n = __ldg(p.ntiles) * p.Hkv;
@@ -277,6 +289,7 @@ struct UnitCursor {
     itm = kv_item(p, i);
     kv_item_finish<UQ>(p, itm);
     if (has_next()) nxt = kv_item(p, sched_item(1));
+    if (sched_item(2) < n) tnn = kv_tile(p, sched_item(2));
     return true;
   }
   __device__ __forceinline__ bool next(const BwdParams& p) {
@@ -291,7 +304,10 @@ struct UnitCursor {
     if (i >= n) return false;
     itm = nxt;
     kv_item_finish<UQ>(p, itm);
-    if (has_next()) nxt = kv_item(p, sched_item(k + 1));
+    if (has_next()) {
+      nxt = kv_item_t(p, sched_item(k + 1), tnn);
+      if (sched_item(k + 2) < n) tnn = kv_tile(p, sched_item(k + 2));
+    }
     return true;
   }
   __device__ __forceinline__ bool last() const { return it + 1 == itm.iters; }
@@ -306,11 +322,18 @@ struct UnitCursor {
 // Warp 16 TMA producer, warp 17 TMEM allocator + MMA issuer.
 constexpr int kDkvThreads = 576;
 
+// dK / dV output tensor maps of the TMA-store epilogue: boxes of 128 / 64 / 32 / 16 / 8 rows × 64
+// columns (a partial tile's rows [0, n & ~7) go out as the binary digits of n; its last n & 7 rows
+// are stored directly)
+struct DkvOutMaps {
+  CUtensorMap dv[5], dk[5];
+};
+
 template <int HD, int UQ, bool PROF, int MODE = 0>
-__global__ void __launch_bounds__(kDkvThreads, 1)
+__global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
     k_bwd_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-               const BwdParams p) {
+               const __grid_constant__ DkvOutMaps om, const BwdParams p) {
   using Cfg = DkvCfg<HD, UQ, MODE>;
   constexpr bool kDV = MODE != 2, kDK = MODE != 1;  // accumulators of this launch (dK needs dP / dS)
   constexpr int NQ = Cfg::NQ, ND = Cfg::ND, HO = Cfg::HO, CW = Cfg::CW;
@@ -328,6 +351,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   uint64_t* bar_qd_empty = bars + 12 + NQ;  // [NQ] committed after the unit's dK (dV pass: dV)
   uint64_t* bar_do_full = bars + 12 + 2 * NQ;       // [ND] dO of a unit
   uint64_t* bar_do_empty = bars + 12 + 2 * NQ + ND;  // [ND] after its last reader (dV, or dP)
+  uint64_t* bar_epi_done = bars + 12 + 2 * NQ + 2 * ND;  // the item's dK store has read the staging tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -341,6 +365,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     mbar_init(bar_kv_empty, 1);
     mbar_init(bar_dkv_full, 1);
     mbar_init(bar_dkv_empty, 8);
+    mbar_init(bar_epi_done, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
       mbar_init(&bar_dp_full[b], 1);
@@ -711,6 +736,92 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         tc_fence_after();
         const int hh = (warp >> 2) & 1;
         const int64_t stride = int64_t(p.Hkv) * HD;
+        bool done = false;
+        if (PROF && (p.dbg & 8)) {  // ablation: no epilogue work (TMEM released at once)
+          tc_fence_before();
+          warp_arrive(bar_dkv_empty);
+          if (Cfg::kTmaEpi && (warp & 7) == 0 && lane == 0) mbar_arrive(bar_epi_done);
+          done = true;
+        }
+        if constexpr (Cfg::kTmaEpi) {
+          if (!done && p.row_map == nullptr) {
+            // Each thread's key row r (its TMEM lane) goes into the SW128 staging tile as 16-B chunks
+            // (no transposes); the group's elected thread writes the tile with TMA stores.  dV first;
+            // dK is loaded from TMEM (TMEM drained) while dV's stores read the tile, then staged over it.
+            constexpr int HC = HO / 2;  // columns of this warp half
+            uint8_t* stg = smem + Cfg::OFF_STG;
+            const int n = c.itm.ke - c.itm.k0, r = krow;
+            const int row0 = c.itm.k0 + c.itm.dl;  // data row of the tile's first key
+            const bool tail = r >= (n & ~7) && r < n;
+            const bool elected = (warp & 7) == 0 && lane == 0;
+            auto ld_pack = [&](uint32_t col, float sc, uint32_t (&w)[HC / 2]) {
+#pragma unroll
+              for (int cc = 0; cc < HC; cc += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_off + col + cc, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  w[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]) * sc, __uint_as_float(v[2 * j + 1]) * sc);
+              }
+            };
+            auto stage = [&](const uint32_t (&w)[HC / 2]) {
+#pragma unroll
+              for (int t = 0; t < HC / 8; ++t) {
+                const int col = hh * HC + 8 * t;
+                *reinterpret_cast<uint4*>(stg + (col >> 6) * 16384 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4)) =
+                    make_uint4(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3]);
+              }
+            };
+            auto direct = [&](const uint32_t (&w)[HC / 2], __nv_bfloat16* base) {
+              uint4* dst = reinterpret_cast<uint4*>(base + int64_t(row0 + r) * stride + c.itm.kh * HD + hh * HC);
+#pragma unroll
+              for (int t = 0; t < HC / 8; ++t) dst[t] = make_uint4(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3]);
+            };
+            auto issue = [&](const CUtensorMap* maps) {  // the group's elected thread
+              if (n == 128) {
+#pragma unroll
+                for (int b = 0; b < HO / 64; ++b) tma_store_2d(&maps[0], c.itm.kh * HD + b * 64, row0, stg + b * 16384);
+              } else {
+                int r0 = 0;
+#pragma unroll
+                for (int bi = 1; bi <= 4; ++bi) {
+                  const int bh = 128 >> bi;
+                  if (!(n & bh)) continue;
+#pragma unroll
+                  for (int b = 0; b < HO / 64; ++b)
+                    tma_store_2d(&maps[bi], c.itm.kh * HD + b * 64, row0 + r0, stg + b * 16384 + r0 * 128);
+                  r0 += bh;
+                }
+              }
+              bulk_commit();
+              bulk_wait_read0();
+            };
+            if (c.k > 0) wp.template wait<3>(bar_epi_done, (c.k - 1) & 1);  // previous item's dK store read the tile
+            uint32_t w[HC / 2];
+            ld_pack(Cfg::DV_COL + hh * HC, 1.f, w);
+            stage(w);
+            if (tail) direct(w, p.dv);
+            ld_pack(Cfg::DK_COL + hh * HC, p.scale, w);
+            tc_fence_before();
+            warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
+            trace(50, c.u);  // E: TMEM drained
+            fence_proxy_async_smem();
+            named_bar_sync(1 + g, 256);  // dV staged
+            if (elected) issue(om.dv);
+            named_bar_sync(1 + g, 256);  // dV's stores have read the tile
+            stage(w);
+            if (tail) direct(w, p.dk);
+            fence_proxy_async_smem();
+            named_bar_sync(1 + g, 256);  // dK staged
+            if (elected) {
+              issue(om.dk);
+              mbar_arrive(bar_epi_done);
+            }
+            done = true;
+          }
+        }
+        if (!done) {
         constexpr int HW = HO / 2 < 64 ? HO / 2 : 64;  // columns per transposed store pass
         uint32_t pw[HW / 2];
 #pragma unroll
@@ -734,9 +845,11 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
               warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV/dK may start
               trace(50, c.u);  // E: TMEM drained
             }
-            store_rows_xpose<HW / 8>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
+            if (!(PROF && (p.dbg & 4)))  // ablation: no dK / dV stores
+              store_rows_xpose<HW / 8>(pw, dst_key, t ? p.dk : p.dv, stride, col0);
           }
         }
+        }  // direct-store epilogue
         trace(51, c.u);  // E: stored
         trace(34 + (warp >> 3), c.u);  // E: epilogue done
         wp.template add_since<6>(te);
@@ -748,7 +861,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (trb)  // copy CTA 0's event trace out
-    for (int i = tid; i < 4 * 2001; i += kDkvThreads) p.prof[64 + i] = trb[i];
+    for (int i = tid; i < 4 * 2001; i += int(blockDim.x)) p.prof[64 + i] = trb[i];
   if (warp == 17) tmem_dealloc<512>(tmem);
 }
 
@@ -787,9 +900,9 @@ struct DqCfg {
 struct QItem {
   int q0, qe, dl, h, kh, kv_lo, kv_hi, nkv;
 };
-__device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {  // raw loads (see KvItem)
+__device__ __forceinline__ int4 q_tile(const BwdParams& p, int i) { return __ldg(&p.tiles[i / p.H]); }
+__device__ __forceinline__ QItem q_item_t(const BwdParams& p, int i, int4 t) {  // raw loads (see KvItem)
   QItem it;
-  const int4 t = __ldg(&p.tiles[i / p.H]);
   it.h = i % p.H;
   it.q0 = t.x;
   it.qe = t.y;
@@ -800,6 +913,7 @@ __device__ __forceinline__ QItem q_item(const BwdParams& p, int i) {  // raw loa
   it.nkv = -1;
   return it;
 }
+__device__ __forceinline__ QItem q_item(const BwdParams& p, int i) { return q_item_t(p, i, q_tile(p, i)); }
 __device__ __forceinline__ QItem q_item_cur(QItem it, int BN) {  // derived count, when the item is current
   it.nkv = max(0, (it.kv_hi - it.kv_lo + BN - 1) / BN);
   return it;
@@ -887,11 +1001,19 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         mbar_arrive(&bar_desc_full[d]);  // release semantics: the stores above are visible
       };
       if (i0 < n_items) put_desc(0, q_item_cur(nxt, BN));
+      // descriptor m+1 published at the start of item m from span loads issued one item earlier,
+      // whose tile record was fetched one item before that (no dependent-load stall)
+      QItem n1 = q_item(p, sched_item(1) < n_items ? sched_item(1) : 0);
+      int4 t2 = q_tile(p, sched_item(2) < n_items ? sched_item(2) : 0);
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
         const QItem itm = q_item_cur(nxt, BN);
         if (sched_item(m + 1) < n_items) {
-          nxt = q_item(p, sched_item(m + 1));
-          put_desc(m + 1, q_item_cur(nxt, BN));
+          put_desc(m + 1, q_item_cur(n1, BN));
+          nxt = n1;
+          if (sched_item(m + 2) < n_items) {
+            n1 = q_item_t(p, sched_item(m + 2), t2);
+            if (sched_item(m + 3) < n_items) t2 = q_tile(p, sched_item(m + 3));
+          }
         }
         if (itm.nkv == 0) continue;
         if (k > 0) mbar_wait(bar_qdo_empty, (k - 1) & 1);
@@ -971,9 +1093,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         pend = false;
       };
       QItem nxt = q_item(p, i0 < n_items ? i0 : 0);
+      int4 tn = q_tile(p, sched_item(1) < n_items ? sched_item(1) : 0);  // tile record one item ahead
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m)) {
         const QItem itm = q_item_cur(nxt, BN);
-        if (sched_item(m + 1) < n_items) nxt = q_item(p, sched_item(m + 1));
+        if (sched_item(m + 1) < n_items) {
+          nxt = q_item_t(p, sched_item(m + 1), tn);
+          if (sched_item(m + 2) < n_items) tn = q_tile(p, sched_item(m + 2));
+        }
         if (itm.nkv == 0) continue;
         if (pend) do_dq();  // previous item's last dQ before this item's Q/dO wait
         mbar_wait(bar_qdo_full, k & 1);
@@ -1238,6 +1364,18 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     tk64 = tk;
     tv64 = tv;
   }
+  DkvOutMaps om;  // TMA-store epilogue (single-pass launches, head_dim ≤ 128)
+  if (HD <= 128) {
+    const uint32_t bh[5] = {128, 64, 32, 16, 8};
+    for (int i = 0; i < 5; ++i) {
+      if (int rc = encode_tmap_2d(&om.dv[i], g->dv, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, bh[i], 64, true))
+        return rc;
+      if (int rc = encode_tmap_2d(&om.dk[i], g->dk, BF, T, uint64_t(Hkv) * HD, uint64_t(Hkv) * HD * 2, bh[i], 64, true))
+        return rc;
+    }
+  } else {
+    memset(&om, 0, sizeof(om));
+  }
   constexpr int UQ = HD == 256 ? 32 : 64;  // query unit of the dK/dV kernel
   CUtensorMap tqu, tdou;                    // UQ-row Q / dO boxes of the dK/dV kernel
   if (int rc = encode_tmap_2d(&tqu, a->q, BF, T, uint64_t(H) * HD, uint64_t(H) * HD * 2, UQ, 64, true)) return rc;
@@ -1277,8 +1415,11 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
     const int smem = HD != 256 || halves ? DkvCfg<HD, UQ, 0>::SMEM
                      : half == 0         ? DkvCfg<HD, UQ, 1>::SMEM
                                          : DkvCfg<HD, UQ, 2>::SMEM;
+    const int threads = HD != 256 || halves ? DkvCfg<HD, UQ, 0>::THREADS
+                        : half == 0         ? DkvCfg<HD, UQ, 1>::THREADS
+                                            : DkvCfg<HD, UQ, 2>::THREADS;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, kDkvThreads, smem, st>>>(tqu, tk, tv, tdou, p);
+    kern<<<grid, threads, smem, st>>>(tqu, tk, tv, tdou, om, p);
     VLASIM_LAUNCH_CHECK();
     if (p.prof)
       prof_report("k_bwd_dkdv", grid, st,

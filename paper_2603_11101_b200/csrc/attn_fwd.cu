@@ -365,22 +365,52 @@ struct FwdPParams {
 };
 
 struct FwdPItem {
-  int q0, qe, dl, h, kh, kv_lo, nkv;
+  int q0, qe, dl, h, kh, kv_lo, kv_hi, nkv;
 };
-template <int BN>
-__device__ __forceinline__ FwdPItem fwdp_item(const FwdPParams& p, int i) {
-  FwdPItem it;
-  const int4 t = __ldg(&p.tiles[i / p.H]);
-  it.h = i % p.H;
-  it.q0 = t.x;
-  it.qe = t.y;
-  it.dl = t.z;
-  it.kh = it.h / (p.H / p.Hkv);
-  it.kv_lo = __ldg(&p.rows_span[t.x].x);  // spans are monotone inside a segment
-  const int kv_hi = __ldg(&p.rows_span[t.y - 1].y);
-  it.nkv = max(0, (kv_hi - it.kv_lo + BN - 1) / BN);
-  return it;
-}
+// Every role walks the items with a look-ahead: the tile record (tiles[i / H]) two items ahead, the
+// span loads that index by it one item ahead, and the derived count when the item becomes current —
+// no load result is consumed at the boundary where it is issued (no dependent-load stall per item).
+struct FwdPCursor {
+  int m = 0, i = 0, n = 0;
+  FwdPItem nx;
+  int4 tn;
+  __device__ __forceinline__ int4 tile(const FwdPParams& p, int mm) const {
+    const int ii = sched_item(mm);
+    return ii < n ? __ldg(&p.tiles[ii / p.H]) : make_int4(0, 1, 0, 0);
+  }
+  __device__ __forceinline__ FwdPItem raw(const FwdPParams& p, int ii, int4 t) const {
+    FwdPItem it;
+    it.h = ii % p.H;
+    it.q0 = t.x;
+    it.qe = t.y;
+    it.dl = t.z;
+    it.kh = it.h / (p.H / p.Hkv);
+    it.kv_lo = __ldg(&p.rows_span[t.x].x);  // spans are monotone inside a segment
+    it.kv_hi = __ldg(&p.rows_span[t.y - 1].y);
+    it.nkv = -1;
+    return it;
+  }
+  __device__ __forceinline__ void start(const FwdPParams& p, int nitems) {
+    n = nitems;
+    m = 0;
+    i = sched_item(0);
+    if (i < n) nx = raw(p, i, tile(p, 0));
+    tn = tile(p, 1);
+  }
+  // the current item (m), then the look-ahead advances; false past the last item
+  template <int BN>
+  __device__ __forceinline__ bool take(const FwdPParams& p, FwdPItem& it) {
+    if (i >= n) return false;
+    it = nx;
+    it.nkv = max(0, (it.kv_hi - it.kv_lo + BN - 1) / BN);
+    i = sched_item(++m);
+    if (i < n) {
+      nx = raw(p, i, tn);
+      tn = tile(p, m + 1);
+    }
+    return true;
+  }
+};
 
 template <int HD, int BN, int KS, int VS>
 __global__ void __launch_bounds__(192, 1)
@@ -443,10 +473,9 @@ __global__ void __launch_bounds__(192, 1)
         ++gv;
         pv_row = -1;
       };
-      for (int m = 0;; ++m) {
-        const int i = sched_item(m);
-        if (i >= nitems) break;
-        const FwdPItem it = fwdp_item<BN>(p, i);
+      FwdPCursor cur;
+      cur.start(p, nitems);
+      for (FwdPItem it; cur.take<BN>(p, it);) {
         if (k > 0) mbar_wait(&bar_q_empty, (k - 1) & 1);  // the previous item's last S has read Q
         mbar_expect_tx(&bar_q_full, Cfg::Q_BYTES);
 #pragma unroll
@@ -475,10 +504,10 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, HD, false, true);
       const uint32_t q_addr = smem_u32(sQ);
       int g = 0, k = 0;
-      for (int m = 0;; ++m) {
-        const int i = sched_item(m);
-        if (i >= nitems) break;
-        const int nkv = fwdp_item<BN>(p, i).nkv;
+      FwdPCursor cur;
+      cur.start(p, nitems);
+      for (FwdPItem itc; cur.take<BN>(p, itc);) {
+        const int nkv = itc.nkv;
         mbar_wait(&bar_q_full, k & 1);
         tc_fence_after();
         // Q → TMEM (one tcgen05.cp per 16-element K-step; in issue order after the previous item's
@@ -531,12 +560,16 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const float sl2 = p.scale_log2;
     int g = 0, k = 0;
-    for (int m = 0;; ++m) {
-      const int i = sched_item(m);
-      if (i >= nitems) break;
-      const FwdPItem it = fwdp_item<BN>(p, i);
+    FwdPCursor cur;
+    cur.start(p, nitems);
+    auto row_span_of = [&](const FwdPItem& f) {  // rows past the tile: none
+      return f.q0 + tid < f.qe ? __ldg(&p.rows_span[f.q0 + tid]) : make_int2(0, 0);
+    };
+    int2 rs_n = cur.i < cur.n ? row_span_of(cur.nx) : make_int2(0, 0);
+    for (FwdPItem it; cur.take<BN>(p, it);) {
       const int row = it.q0 + tid;
-      const int2 rs = row < it.qe ? __ldg(&p.rows_span[row]) : make_int2(0, 0);  // rows past the tile: none
+      const int2 rs = rs_n;  // loaded one item ahead
+      if (cur.i < cur.n) rs_n = row_span_of(cur.nx);
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < it.nkv; ++j) {
         const int gj = g + j, sb = gj & 1;

@@ -98,9 +98,12 @@ struct Fwd2Cfg {
 struct FwdItem {
   int q0, qe, dl, h, kh, kv_lo, kv_hi, nkv;
 };
-__device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) {
+// Item descriptors are built from the tile record (tiles[i / H]) and two span loads indexed by it.
+// Roles look ahead so that no load result is consumed within the same item boundary: the tile
+// record is fetched one boundary before the span loads that index by it (no dependent-load stall).
+__device__ __forceinline__ int4 fwd_tile(const Fwd2Params& p, int i) { return __ldg(&p.tiles[i / p.H]); }
+__device__ __forceinline__ FwdItem fwd_item_t(const Fwd2Params& p, int i, int4 t) {
   FwdItem it;
-  const int4 t = __ldg(&p.tiles[i / p.H]);
   it.h = i % p.H;
   it.q0 = t.x;
   it.qe = t.y;
@@ -109,8 +112,11 @@ __device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) 
   it.kv_lo = __ldg(&p.rows_span[t.x].x);      // spans are monotone inside a segment
   it.kv_hi = __ldg(&p.rows_span[t.y - 1].y);
   it.nkv = -1;
-  (void)BN;
   return it;
+}
+__device__ __forceinline__ FwdItem fwd_item(const Fwd2Params& p, int i, int BN) {
+  (void)BN;
+  return fwd_item_t(p, i, fwd_tile(p, i));
 }
 __device__ __forceinline__ FwdItem fwd_item_cur(FwdItem it, int BN) {
   it.nkv = max(0, (it.kv_hi - it.kv_lo + BN - 1) / BN);
@@ -259,13 +265,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         descs[2 * d + 1] = make_int4(it.kv_lo, it.kv_hi, it.nkv, it.kh);
         mbar_arrive(&bar_desc_full[d]);
       };
+      // descriptor m+1 is published at the start of item m (the softmax warps prefetch its row span
+      // then), from span loads issued one item earlier; tile records are fetched one item before those
       FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
       if (i0 < n_items) put_desc(0, fwd_item_cur(nxt, BN));
+      FwdItem n1 = fwd_item(p, sched_item(1) < n_items ? sched_item(1) : 0, BN);
+      int4 t2 = fwd_tile(p, sched_item(2) < n_items ? sched_item(2) : 0);
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
-        if (sched_item(m + 1) < n_items) {  // prefetch
-          nxt = fwd_item(p, sched_item(m + 1), BN);
-          put_desc(m + 1, fwd_item_cur(nxt, BN));
+        if (sched_item(m + 1) < n_items) {
+          put_desc(m + 1, fwd_item_cur(n1, BN));
+          nxt = n1;
+          if (sched_item(m + 2) < n_items) {
+            n1 = fwd_item_t(p, sched_item(m + 2), t2);
+            if (sched_item(m + 3) < n_items) t2 = fwd_tile(p, sched_item(m + 3));
+          }
         }
         const int qs = k % NQ;
         if (k >= NQ) {  // buffer qs held item k-NQ: its Q reads (FP8) / its O store's reads (bf16) done
@@ -348,9 +362,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         pend = false;
       };
       FwdItem nxt = fwd_item(p, i0 < n_items ? i0 : 0, BN);
+      int4 tn = fwd_tile(p, sched_item(1) < n_items ? sched_item(1) : 0);  // tile record one item ahead
       for (int m = 0, i = i0; i < n_items; i = sched_item(++m), ++k) {
         const FwdItem itm = fwd_item_cur(nxt, BN);
-        if (sched_item(m + 1) < n_items) nxt = fwd_item(p, sched_item(m + 1), BN);  // prefetch
+        if (sched_item(m + 1) < n_items) {  // prefetch (no load result used before the next boundary)
+          nxt = fwd_item_t(p, sched_item(m + 1), tn);
+          if (sched_item(m + 2) < n_items) tn = fwd_tile(p, sched_item(m + 2));
+        }
         const int qs = k % NQ;
         const uint64_t qd = dQ0 + qs * Q16;
         wp.template wait<0>(&bar_q_full[qs], (k / NQ) & 1);

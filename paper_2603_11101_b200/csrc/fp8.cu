@@ -296,28 +296,34 @@ __global__ void __launch_bounds__(256) k_quant_error(const __nv_bfloat16* __rest
 }
 
 // codes → bf16(value(code) · scale) (fp32 product, one rounding): the Q/K operands of the FP8
-// path's backward.  8 codes per thread (8-B load, 16-B store); d % 8 == 0.
-__global__ void k_dequant_bf16(const uint8_t* __restrict__ codes, const float* __restrict__ scales, int64_t T,
-                               int heads, int d, __nv_bfloat16* __restrict__ out) {
-  const int64_t n8 = T * heads * d / 8;
-  const int nbd = (d + 127) / 128, nbt = int((T + 127) / 128);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t e = i * 8;
-    const int c = int(e % d);
-    const int64_t th = e / d;
-    const int h = int(th % heads);
-    const int64_t t = th / heads;
-    const float sc = scales[(int64_t(h) * nbt + t / 128) * nbd + c / 128];
-    const uint2 w = *reinterpret_cast<const uint2*>(codes + e);
-    const uint8_t* b = reinterpret_cast<const uint8_t*>(&w);
-    uint4 r;
-    uint32_t* rr = reinterpret_cast<uint32_t*>(&r);
+// path's backward.  A thread converts 8 codes of one (token, head) row (8-B load, 16-B store) with
+// the hardware E4M3 → f16 conversion (exact: every E4M3 value is an f16), indexing rows with 32-bit
+// arithmetic (T · heads · d / 8 < 2^31, host-checked); d % 8 == 0.
+__device__ __forceinline__ float2 e4m3x2_to_float2(uint16_t w) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(w));
+  return __half22float2(*reinterpret_cast<const __half2*>(&h));
+}
+
+__global__ void k_dequant_bf16(const uint8_t* __restrict__ codes, const float* __restrict__ scales, uint32_t rows,
+                               int heads, int d, int nbt, __nv_bfloat16* __restrict__ out) {
+  const uint32_t cpr = uint32_t(d) >> 3, n8 = rows * cpr;
+  const int nbd = (d + 127) / 128;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const uint32_t r = i / cpr, c8 = i - r * cpr;
+    const uint32_t h = r % uint32_t(heads), t = r / uint32_t(heads);
+    const float sc = __ldg(scales + (int64_t(h) * nbt + (t >> 7)) * nbd + (c8 >> 4));
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(codes) + i);
+    uint4 o;
+    uint32_t* oo = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const __nv_bfloat162 v = __floats2bfloat162_rn(e4m3_to_float(b[2 * j]) * sc, e4m3_to_float(b[2 * j + 1]) * sc);
-      rr[j] = *reinterpret_cast<const uint32_t*>(&v);
+      const uint32_t word = j < 2 ? w.x : w.y;
+      const float2 f = e4m3x2_to_float2(uint16_t(word >> (16 * (j & 1))));
+      const __nv_bfloat162 v = __floats2bfloat162_rn(f.x * sc, f.y * sc);
+      oo[j] = *reinterpret_cast<const uint32_t*>(&v);
     }
-    *reinterpret_cast<uint4*>(out + e) = r;
+    reinterpret_cast<uint4*>(out)[i] = o;
   }
 }
 
@@ -328,8 +334,10 @@ int launch_fp8_dequant_bf16(const uint8_t* codes, const float* scales, int64_t T
                             cudaStream_t st) {
   if (d % 8) return set_error(VLASIM_ECONFIG, "fp8 dequant: head_dim %d not a multiple of 8", d);
   const int64_t n8 = T * heads * d / 8;
-  const int64_t blocks = std::min<int64_t>((n8 + 255) / 256, int64_t(num_sms()) * 8);
-  k_dequant_bf16<<<blocks, 256, 0, st>>>(codes, scales, T, heads, d, static_cast<__nv_bfloat16*>(out));
+  if (n8 >= (int64_t(1) << 31)) return set_error(VLASIM_ECONFIG, "fp8 dequant: tensor too large");
+  const int64_t blocks = std::min<int64_t>((n8 + 255) / 256, int64_t(num_sms()) * 16);
+  k_dequant_bf16<<<blocks, 256, 0, st>>>(codes, scales, uint32_t(T * heads), heads, d, int((T + 127) / 128),
+                                          static_cast<__nv_bfloat16*>(out));
   VLASIM_LAUNCH_CHECK();
   return VLASIM_OK;
 }

@@ -97,8 +97,17 @@ def main():
             fp8.quant_block(q)
             fp8.quant_block(k)
 
+        dq8, dk8, dv8 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        ws8 = attention.BwdWorkspace()
+
+        def b8():
+            fp8.varlen_attn_bwd_fp8qk(do, qc, qs, kc, ks, v, o8, l8, cu, dq=dq8, dk=dk8, dv=dv8, seg_src=seg,
+                                      workspace=ws8)
+
         t8 = timed(f8, a.iters)
         tq = timed(quant, a.iters)
+        out["fp8_bwd_ms"] = timed(b8, a.iters)
+        out["bwd_ms"] = timed(bwd, a.iters)
         out.update({"fp8_fwd_ms": t8, "fp8_fwd_tflops": fl / t8 / 1e9, "quant_qk_ms": tq,
                     "fp8_vs_bf16_max_abs": float((o8.float() - o.float()).abs().max())})
     else:

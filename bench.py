@@ -632,21 +632,33 @@ def main():
         dist.all_reduce(fl_all)
     toks_all = float(np.sum(L_glob))
 
-    # per-phase device times (eager, events between the phases on the launching stream)
+    # per-phase device times: each phase captured as its own CUDA graph (as in the step) and the
+    # three replayed back to back between events on the launching stream (eager launches when the
+    # step itself is not graphed)
     nrep = min(a.steps, 10)
-    ph = []
-    for _ in range(nrep):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        gpu_lead(stream)
-        ev[0].record(stream)
-        pack_phase(0, bufs)
-        ev[1].record(stream)
-        fwd_phase(0, bufs)
-        ev[2].record(stream)
-        bwd_phase(0, bufs)
-        ev[3].record(stream)
-        torch.cuda.synchronize()
-        ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(3)])
+    phase_fns = [lambda: pack_phase(0, bufs), lambda: fwd_phase(0, bufs), lambda: bwd_phase(0, bufs)]
+    phase_run = phase_fns
+    if use_graph:
+        try:
+            pg = [capture(f) for f in phase_fns]
+            phase_run = [g.replay for g in pg]
+        except RuntimeError:
+            torch.cuda.synchronize()
+    def phase_times(run):
+        ph = []
+        for _ in range(nrep):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            gpu_lead(stream)
+            ev[0].record(stream)
+            for q in range(3):
+                run[q]()
+                ev[q + 1].record(stream)
+            torch.cuda.synchronize()
+            ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(3)])
+        return ph
+
+    ph = phase_times(phase_run)
+    ph_eager = phase_times(phase_fns) if phase_run is not phase_fns else ph
     kpack, kfwd, kbwd = (statistics.median(r[i] for r in ph) for i in range(3))
     kf = boundary_ms(lambda: fwd_phase(0, bufs), 3, nrep, stream)
     kb = boundary_ms(lambda: bwd_phase(0, bufs), 5, nrep, stream)
@@ -793,6 +805,8 @@ def main():
                                           "full) vs algorithmic_bytes", peak_src=PEAKS["src"]),
             "step_roofline": rf_step,
             "phase_ms": {"pack_allgather_ffd_lpt": kpack, "fwd": kfwd, "bwd": kbwd},
+            "phase_ms_eager": {k: statistics.median(r[i] for r in ph_eager)
+                               for i, k in enumerate(("pack_allgather_ffd_lpt", "fwd", "bwd"))},
             "kernel_ms": {"fwd_prep": kf[0], "fwd_attention": kf[1], "bwd_pre": kb[0], "bwd_tiles": kb[1],
                           "bwd_dkdv": kb[2], "bwd_dq": kb[3]},
             "clocks": clk.summary(),

@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(kShardThreads) k_shard_bins(ShardIn in, vlasim
 
 // ---- 2: greedy LPT over the sorted keys (staged in shared memory by the warp), one thread with the
 // rank loads in registers
+// W = world (the per-bin chain is one thread's, so its width is compiled for the rank count).
+template <int W>
 __global__ void __launch_bounds__(32, 1) k_shard_lpt(ShardIn in, int world, vlasim_shard_out o,
                                                      const unsigned long long* __restrict__ gkeys) {
   extern __shared__ unsigned long long keys[];
@@ -117,17 +119,53 @@ __global__ void __launch_bounds__(32, 1) k_shard_lpt(ShardIn in, int world, vlas
   // greedy LPT (one thread): rank r's load packed with its index, key_r = load_r · 16 + r, so the
   // least-loaded rank (ties: lowest rank) is the minimum key — 15 independent 64-bit mins per bin
   // (a 4-level tree) after one predicated add; unused ranks hold UINT64_MAX.
-  unsigned long long kr[kMaxWorld];
+  unsigned long long kr[W];
 #pragma unroll
-  for (int r = 0; r < kMaxWorld; ++r) kr[r] = r < world ? static_cast<unsigned long long>(r) : ~0ull;
-  auto argmin = [&]() {
-    unsigned long long m8[8], m4[4];
+  for (int r = 0; r < W; ++r) kr[r] = r < world ? static_cast<unsigned long long>(r) : ~0ull;
+  constexpr int P2 = W <= 1 ? 1 : W <= 2 ? 2 : W <= 4 ? 4 : W <= 8 ? 8 : 16;
+  auto argmin = [&]() {  // a log2-level tree of independent 64-bit mins (padded to a power of two)
+    unsigned long long t[P2];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) m8[j] = min(kr[2 * j], kr[2 * j + 1]);
+    for (int j = 0; j < P2; ++j) t[j] = j < W ? kr[j] : ~0ull;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) m4[j] = min(m8[2 * j], m8[2 * j + 1]);
-    return min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+    for (int w = P2 / 2; w >= 1; w /= 2)
+#pragma unroll
+      for (int j = 0; j < w; ++j) t[j] = min(t[2 * j], t[2 * j + 1]);
+    return t[0];
   };
+  // Narrow path: greedy LPT keeps max − min rank load ≤ the largest bin cost (keys[0], the first
+  // key), so with that cost below 2^27 the keys relative to the current minimum load fit 32 bits.
+  // The W keys are kept SORTED in registers: the least-loaded rank is s[0]; after its load grows it
+  // is re-inserted (W−1 independent compares, two selects per slot) and every key is rebased on
+  // the new minimum — no min tree and no per-rank predicated add on the per-bin chain.
+  if (B > 0 && (keys[0] >> 32) < (1ull << 27)) {
+    uint32_t sk[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) sk[r] = uint32_t(r);  // load 0, rank r: sorted
+    unsigned long long base = 0;  // absolute load (without the ×16) of the relative zero
+    unsigned long long k = keys[0];
+    for (int i = 0; i < B; ++i) {
+      const unsigned long long kn = i + 1 < B ? keys[i + 1] : 0ull;
+      o.bin_rank[int(0xFFFFFFFFull - (k & 0xFFFFFFFFull))] = int(sk[0] & 15);
+      const uint32_t x = sk[0] + (uint32_t(k >> 32) << 4);
+      bool lt[W + 1];  // lt[j]: sk[j] < x (monotone: a true prefix of 1..W−1)
+      lt[0] = true;
+#pragma unroll
+      for (int j = 1; j < W; ++j) lt[j] = sk[j] < x;
+      lt[W] = false;
+      uint32_t ns[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) ns[q] = lt[q + 1] ? sk[q + 1 < W ? q + 1 : q] : (lt[q] ? x : sk[q]);
+      const uint32_t sub = ns[0] & ~15u;  // rebase on the new minimum load
+#pragma unroll
+      for (int q = 0; q < W; ++q) sk[q] = ns[q] - sub;
+      base += sub >> 4;
+      k = kn;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) o.rank_load[sk[q] & 15] = static_cast<long long>(base + (sk[q] >> 4));
+    return;
+  }
   unsigned long long m = argmin();
   unsigned long long k = B > 0 ? keys[0] : 0ull;
   for (int i = 0; i < B; ++i) {
@@ -136,12 +174,12 @@ __global__ void __launch_bounds__(32, 1) k_shard_lpt(ShardIn in, int world, vlas
     o.bin_rank[int(0xFFFFFFFFull - (k & 0xFFFFFFFFull))] = best;
     const unsigned long long add = (k >> 32) << 4;
 #pragma unroll
-    for (int r = 0; r < kMaxWorld; ++r) kr[r] += r == best ? add : 0ull;
+    for (int r = 0; r < W; ++r) kr[r] += r == best ? add : 0ull;
     m = argmin();
     k = kn;
   }
 #pragma unroll
-  for (int r = 0; r < kMaxWorld; ++r)
+  for (int r = 0; r < W; ++r)
     if (r < world) o.rank_load[r] = static_cast<long long>(kr[r] >> 4);
 }
 
@@ -281,8 +319,14 @@ extern "C" int vlasim_shard_lpt_cuda(const int32_t* d_len, const vlasim_pack_out
   const size_t smem = size_t(kMaxShardBins) * 8;
   VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_shard_bins, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   k_shard_bins<<<1, kShardThreads, smem, st>>>(in, *out, cost);
-  VLASIM_CUDA_TRY(cudaFuncSetAttribute(k_shard_lpt, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k_shard_lpt<<<1, 32, smem, st>>>(in, world, *out, cost);
+  using LptKernel = void (*)(ShardIn, int, vlasim_shard_out, const unsigned long long*);
+  static const LptKernel lpts[kMaxWorld] = {k_shard_lpt<1>,  k_shard_lpt<2>,  k_shard_lpt<3>,  k_shard_lpt<4>,
+                                            k_shard_lpt<5>,  k_shard_lpt<6>,  k_shard_lpt<7>,  k_shard_lpt<8>,
+                                            k_shard_lpt<9>,  k_shard_lpt<10>, k_shard_lpt<11>, k_shard_lpt<12>,
+                                            k_shard_lpt<13>, k_shard_lpt<14>, k_shard_lpt<15>, k_shard_lpt<16>};
+  const LptKernel lpt = lpts[world - 1];
+  VLASIM_CUDA_TRY(cudaFuncSetAttribute(lpt, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  lpt<<<1, 32, smem, st>>>(in, world, *out, cost);
   k_shard_binscan<<<1, kShardThreads, 0, st>>>(in, rank, *out, lmo, lto);
   k_shard_scan_reduce<<<nblk, 1024, 0, st>>>(in, n, rank, *out, part);
   k_shard_scan_parts<<<1, 1024, 0, st>>>(part, nblk, out->status);

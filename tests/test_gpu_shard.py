@@ -43,6 +43,24 @@ def test_device_lpt_matches_host(gpu, world):
     assert seen.all()
 
 
+@pytest.mark.parametrize("cap,lo,hi,world", [(65535, 9000, 65535, 5), (65535, 9000, 65535, 16),
+                                             (8192, 16, 8192, 16), (16384, 12000, 16384, 7)])
+def test_device_lpt_wide_and_narrow_keys(gpu, cap, lo, hi, world):
+    """Bin costs past 2^27 (the 64-bit LPT keys) and below (the rebased 32-bit keys), every world
+    width of the argmin tree up to 16: same assignment and loads as the host LPT."""
+    from paper_2603_11101_b200 import dist as vdist, packing, synthetic
+    L = synthetic.gen_lengths(600, synthetic.DIST_UNIFORM, lo, hi, seed=cap + world)
+    plan = packing.pack_ffd(L, cap)
+    nb = plan.num_bins()
+    host = vdist.lpt_assign(plan, L, world)
+    costs = vdist.bin_costs([b.member_ids for b in plan.to_host(L)], L)
+    sp = vdist.shard_lpt(plan, world, 0)
+    br = sp.bin_rank[:nb].cpu().numpy()
+    for r in range(world):
+        assert sorted(np.nonzero(br == r)[0].tolist()) == host[r]
+    assert np.array_equal(sp.rank_load.cpu().numpy()[:world], [int(sum(costs[b] for b in host[q])) for q in range(world)])
+
+
 @pytest.mark.parametrize("world,mask", [(2, 0), (4, 0), (3, 2)])
 def test_union_of_rank_shards_equals_single_rank(gpu, world, mask):
     from paper_2603_11101_b200 import attention, dist as vdist, packing, synthetic

@@ -723,9 +723,34 @@ def main():
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         h2d = sum(x.numel() * x.element_size() for x in hin.values())
         d2h = sum(x.numel() * x.element_size() for x in hout)
+        # the link's own ceiling on this box: pinned H2D and D2H at once on the two copy streams
+        # (same tensors), so the e2e line can be read against PCIe rather than against the kernels
+        src_h, dst_d = hin["q"], sets[1]["q"]
+        src_d, dst_h = sets[0]["o"], hout[0]
+        best = 1e9
+        for _ in range(3):
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            s_in.wait_event(c0)
+            s_out.wait_event(c0)
+            with torch.cuda.stream(s_in):
+                dst_d.copy_(src_h, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                dst_h.copy_(src_d, non_blocking=True)
+            stream.wait_stream(s_in)
+            stream.wait_stream(s_out)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, c0.elapsed_time(c1))
+        link_gbs = src_h.numel() * src_h.element_size() / (best / 1e3) / 1e9  # per direction, concurrent
+        ceil_ms = max(h2d, d2h) / (link_gbs * 1e9) * 1e3
         e2e = {"value": toks_all / (float(ems.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item()),
-               "pipelining": "H2D / compute / D2H on separate streams, double-buffered device sets"}
+               "pipelining": "H2D / compute / D2H on separate streams, double-buffered device sets",
+               "pcie_concurrent_gbs_per_direction": link_gbs,
+               "link_ceiling_tokens_per_s": toks_all / (ceil_ms / 1e3),
+               "frac_of_link_ceiling": (toks_all / (float(ems.item()) / 1e3)) / (toks_all / (ceil_ms / 1e3))}
         del sets, hin, hout
 
     # ---------------------------------------------------------------- DDP gradient all-reduce (N > 1)

@@ -154,25 +154,35 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
   const bool cv = ch * 8 < min(128, d - c0);
   __shared__ float red[8];
   uint4 v[8];
-  __nv_bfloat162 m2 = __floats2bfloat162_rn(0.f, 0.f);
-  int bad = -1;
+  // |x| as bf16 bit patterns orders like the values (non-negative), and every non-finite bf16 has the
+  // exponent all ones (≥ 0x7F80): one unsigned 16-bit-pair max per word gives both the block
+  // maximum and the finiteness test
+  uint32_t mb = 0;
+  const size_t rstride = size_t(16) * heads * d;  // 16 token rows
+  const __nv_bfloat16* xp = x + (int64_t(t0 + r0) * heads + h) * d + c0 + ch * 8;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int t = t0 + r0 + 16 * i;
     v[i] = make_uint4(0, 0, 0, 0);
-    if (cv && t < T)
-      v[i] = __ldcs(reinterpret_cast<const uint4*>(x + (int64_t(t) * heads + h) * d + c0 + ch * 8));
-    if (bf16x2_nonfinite(v[i].x) | bf16x2_nonfinite(v[i].y) | bf16x2_nonfinite(v[i].z) | bf16x2_nonfinite(v[i].w))
-      bad = 8 * i + first_nonfinite(v[i]);
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) m2 = __hmax2(m2, __habs2(b[j]));
+    if (cv && t < T) v[i] = __ldcs(reinterpret_cast<const uint4*>(xp + i * rstride));
+    mb = __vmaxu2(mb, v[i].x & 0x7FFF7FFFu);
+    mb = __vmaxu2(mb, v[i].y & 0x7FFF7FFFu);
+    mb = __vmaxu2(mb, v[i].z & 0x7FFF7FFFu);
+    mb = __vmaxu2(mb, v[i].w & 0x7FFF7FFFu);
   }
-  if (__syncthreads_or(bad >= 0)) {  // non-finite input → error (no codes written)
-    if (bad >= 0) report_nonfinite(status, (int64_t(t0 + r0 + 16 * (bad >> 3)) * heads + h) * d + c0 + ch * 8 + (bad & 7));
+  const uint32_t top = max(mb & 0xFFFFu, mb >> 16);
+  if (__syncthreads_or(top >= 0x7F80u)) {  // non-finite input → error (no codes written)
+    if (top >= 0x7F80u) {
+      int bad = 0;
+#pragma unroll
+      for (int i = 7; i >= 0; --i)
+        if (bf16x2_nonfinite(v[i].x) | bf16x2_nonfinite(v[i].y) | bf16x2_nonfinite(v[i].z) | bf16x2_nonfinite(v[i].w))
+          bad = 8 * i + first_nonfinite(v[i]);
+      report_nonfinite(status, (int64_t(t0 + r0 + 16 * (bad >> 3)) * heads + h) * d + c0 + ch * 8 + (bad & 7));
+    }
     return;
   }
-  float amax = fmaxf(__bfloat162float(m2.x), __bfloat162float(m2.y));
+  float amax = __uint_as_float(top << 16);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
@@ -196,11 +206,10 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
   const float Bs = fast ? amax * p2 : scale, As = fast ? 448.f * p2 : 1.f;
   const float rs = __frcp_rn(Bs);
   const float2 r2 = make_float2(rs, rs), ns2 = make_float2(-Bs, -Bs), a2 = make_float2(As, As);
-  auto quot = [&](float2 f) {  // (the correction turns −0 into +0: the sign is restored)
+  auto quot = [&](float2 f) {  // (the correction turns −0 into +0: the sign bytes are OR-ed in below)
     const float2 fa = f2_mul(f, a2);
     const float2 q0 = f2_mul(fa, r2);
-    const float2 q = f2_fma(f2_fma(q0, ns2, fa), r2, q0);
-    return make_float2(copysignf(q.x, f.x), copysignf(q.y, f.y));
+    return f2_fma(f2_fma(q0, ns2, fa), r2, q0);
   };
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -215,7 +224,9 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
       qv[4 * j] = q0.x, qv[4 * j + 1] = q0.y, qv[4 * j + 2] = q1.x, qv[4 * j + 3] = q1.y;
       const uint32_t lo = cvt_e4m3x2(q0.x, q0.y);
       const uint32_t hi = cvt_e4m3x2(q1.x, q1.y);
-      w[j] = lo | (hi << 16);
+      // the four inputs' sign bits (bf16 high bytes) onto the four codes: −0 keeps its sign
+      const uint32_t wa = j ? v[i].z : v[i].x, wb = j ? v[i].w : v[i].y;
+      w[j] = (lo | (hi << 16)) | (__byte_perm(wa, wb, 0x7531) & 0x80808080u);
     }
     if (!fast && amax != 0.f) {  // degenerate block maximum (block-uniform): fp64 re-decision
 #pragma unroll
@@ -227,7 +238,8 @@ __global__ void __launch_bounds__(256) k_quant_block_v(const __nv_bfloat16* __re
         w[k >> 2] = (w[k >> 2] & ~(0xFFu << sh)) | (f << sh);
       }
     }
-    __stcs(reinterpret_cast<uint2*>(codes + (int64_t(t) * heads + h) * d + c0 + ch * 8), make_uint2(w[0], w[1]));
+    __stcs(reinterpret_cast<uint2*>(codes + (int64_t(t0 + r0) * heads + h) * d + c0 + ch * 8 + i * rstride),
+           make_uint2(w[0], w[1]));
   }
 }
 

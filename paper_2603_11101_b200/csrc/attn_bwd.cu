@@ -218,7 +218,11 @@ struct DkvCfg {
   // single-pass launches (head_dim ≤ 128) write dK / dV through an SW128 staging tile and TMA stores
   // (128 rows × HO bf16, 64-column boxes of 16 KB); the head-dim-256 passes store rows directly
   static constexpr bool kTmaEpi = MODE == 0 && HD <= 128;
-  static constexpr int THREADS = 576;
+  // single-pass launches (d ≤ 128): four dedicated epilogue warps (20-23, one per TMEM lane
+  // quadrant) drain dK / dV, so the softmax groups never stall on an item boundary; registers are
+  // rebalanced with setmaxnreg (softmax 96, the rest 48: 768 threads × 80 at launch)
+  static constexpr bool kEpiWarps = kTmaEpi;
+  static constexpr int THREADS = kEpiWarps ? 768 : 576;
   static constexpr int OFF_STG = kTmaEpi ? (OFF_DSUM + NQ * VEC + 1023) & ~1023 : OFF_DSUM + NQ * VEC;
   static constexpr int STG = kTmaEpi ? 128 * HO * 2 : 0;
   static constexpr int OFF_BAR = OFF_STG + STG;
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
     mbar_init(bar_kv_full, 1);
     mbar_init(bar_kv_empty, 1);
     mbar_init(bar_dkv_full, 1);
-    mbar_init(bar_dkv_empty, 8);
+    mbar_init(bar_dkv_empty, Cfg::kEpiWarps ? 4 : 8);
     mbar_init(bar_epi_done, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
@@ -387,7 +391,98 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 16) {
+  if (warp >= 16) {
+  // warpgroups 4-5 (producer, MMA, epilogue): registers handed to the softmax warpgroups
+  if constexpr (Cfg::kEpiWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 48;\n" ::: "memory");
+  if (Cfg::kEpiWarps && warp >= 18) {
+    // ================================================ dK / dV epilogue warps (20-23; 18, 19 idle)
+    // Per item: wait dkv_full; dV rows (this warp's lane quadrant, all HO columns) → SW128 staging
+    // tile → TMA stores by one elected thread; once their smem reads are done, dK the same way;
+    // TMEM released (dkv_empty, 4 arrivals) after the last dK load.  Partial tiles: 64/32/16/8-row
+    // boxes + direct stores of the last n & 7 rows; the row_map layout stores every row directly.
+    if constexpr (Cfg::kEpiWarps) {
+      if (warp >= 20) {
+        const int q = warp & 3, r = q * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const bool elected = warp == 20 && lane == 0;
+        uint8_t* stg = smem + Cfg::OFF_STG;
+        const int64_t stride = int64_t(p.Hkv) * HD;
+        const int n_items = __ldg(p.ntiles) * p.Hkv;
+        int4 tn = kv_tile(p, sched_item(0) < n_items ? sched_item(0) : 0);
+        for (int k = 0, i = sched_item(0); i < n_items; i = sched_item(++k)) {
+          const int4 t = tn;
+          if (sched_item(k + 1) < n_items) tn = kv_tile(p, sched_item(k + 1));
+          const int kh = i % p.Hkv, k0 = t.x, n = t.y - t.x, row0 = t.x + t.z;
+          const bool tail = r >= (n & ~7) && r < n;
+          const int dst_row = r < n ? (p.row_map ? __ldg(p.row_map + k0 + r) : row0 + r) : -1;
+          mbar_wait(bar_dkv_full, k & 1);
+          tc_fence_after();
+          auto pass = [&](uint32_t col0, float sc, __nv_bfloat16* out, const CUtensorMap* maps, bool last) {
+            // TMEM → bf16 → staging (or direct rows), 32 columns at a time
+#pragma unroll
+            for (int cc = 0; cc < HO; cc += 32) {
+              uint32_t v[32];
+              tmem_ld32(tmem + lane_off + col0 + cc, v);
+              tmem_wait_ld();
+              uint32_t w[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                w[j] = pack_bf16x2(__uint_as_float(v[2 * j]) * sc, __uint_as_float(v[2 * j + 1]) * sc);
+              if (p.row_map) {
+                if (dst_row >= 0) {
+                  uint4* dst = reinterpret_cast<uint4*>(out + int64_t(dst_row) * stride + kh * HD + cc);
+#pragma unroll
+                  for (int t4 = 0; t4 < 4; ++t4) dst[t4] = make_uint4(w[4 * t4], w[4 * t4 + 1], w[4 * t4 + 2], w[4 * t4 + 3]);
+                }
+              } else {
+#pragma unroll
+                for (int t4 = 0; t4 < 4; ++t4) {
+                  const int col = cc + 8 * t4;
+                  *reinterpret_cast<uint4*>(stg + (col >> 6) * 16384 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4)) =
+                      make_uint4(w[4 * t4], w[4 * t4 + 1], w[4 * t4 + 2], w[4 * t4 + 3]);
+                }
+                if (tail) {
+                  uint4* dst = reinterpret_cast<uint4*>(out + int64_t(row0 + r) * stride + kh * HD + cc);
+#pragma unroll
+                  for (int t4 = 0; t4 < 4; ++t4) dst[t4] = make_uint4(w[4 * t4], w[4 * t4 + 1], w[4 * t4 + 2], w[4 * t4 + 3]);
+                }
+              }
+            }
+            if (last) {
+              tc_fence_before();
+              warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV / dK may start
+            }
+            if (p.row_map) return;
+            fence_proxy_async_smem();
+            named_bar_sync(3, 128);  // staged
+            if (elected) {
+              if (n == 128) {
+#pragma unroll
+                for (int b = 0; b < HO / 64; ++b) tma_store_2d(&maps[0], kh * HD + b * 64, row0, stg + b * 16384);
+              } else {
+                int r0 = 0;
+#pragma unroll
+                for (int bi = 1; bi <= 4; ++bi) {
+                  const int bh = 128 >> bi;
+                  if (!(n & bh)) continue;
+#pragma unroll
+                  for (int b = 0; b < HO / 64; ++b)
+                    tma_store_2d(&maps[bi], kh * HD + b * 64, row0 + r0, stg + b * 16384 + r0 * 128);
+                  r0 += bh;
+                }
+              }
+              bulk_commit();
+              bulk_wait_read0();  // the staging tile may take the next pass
+            }
+            named_bar_sync(3, 128);
+          };
+          pass(Cfg::DV_COL, 1.f, p.dv, om.dv, false);
+          pass(Cfg::DK_COL, p.scale, p.dk, om.dk, true);
+        }
+        if (elected) bulk_wait_all();
+      }
+    }
+  } else if (warp == 16) {
     // ================================================ TMA producer
     if (lane == 0) {
       WaitProf<PROF> wp;
@@ -596,7 +691,9 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
       }
       if (lane == 0) wp.flush(p.prof + 8);
     }
+  }
   } else {
+    if constexpr (Cfg::kEpiWarps) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");
     // ================================================ softmax warps 0-15
     const int g = warp >> 3, quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
@@ -724,7 +821,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
         wp.template add_since<5>(tb);
         }  // phase B (dK)
       }
-      if (c.last() && (c.u & 1) == g) {
+      if (!Cfg::kEpiWarps && c.last() && (c.u & 1) == g) {
         // ---- item epilogue, by the group that ran the item's last unit (the other group goes
         //      straight on to the next item's first unit): TMEM → registers → release TMEM →
         //      8-lane chunk transpose → stores of 4 rows × 128 B per warp instruction.  Warp

@@ -593,6 +593,79 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
           umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
                       sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
       };
+      if constexpr (MODE == 0) {
+        // Single-pass launches: one cursor, stages / parities / TMEM buffers derived from the
+        // unit ordinal (NQ = ND, compile-time).  S/dP of unit x are issued in the block of x − 2
+        // when both lie in the same item; an item's first min(2, units) S/dP are issued after the
+        // previous item's last block (item 0: before the loop) — no second cursor, no search.
+        static_assert(NQ == ND, "single-pass stage rings");
+        auto sdp = [&](int x, bool item_first, int k, bool item_last) {  // S and dP of unit x
+          const uint32_t st = uint32_t(x % NQ), sph = uint32_t((x / NQ) & 1), bb = uint32_t(x & 1);
+          if (item_first) wp.template wait<0>(bar_kv_full, k & 1);
+          wp.template wait<1>(&bar_qd_full[st], sph);
+          wp.template wait<1>(&bar_do_full[st], sph);
+          tc_fence_after();
+          if (elect_one()) {
+            mma_S(Cfg::s_col(bb), st * QT16);
+            umma_commit(&bar_s_full[bb]);
+            mma_dP(Cfg::dp_col(bb), st * QT16);
+            umma_commit(&bar_dp_full[bb]);
+            if (item_last) umma_commit(bar_kv_empty);  // the item's last readers of K and V
+          }
+          __syncwarp();
+        };
+        UnitCursor<UQ> cc;
+        bool vc = cc.start(p);
+        if (vc) {
+          sdp(0, true, 0, cc.itm.iters == 1);
+          if (cc.itm.iters >= 2) sdp(1, false, 0, cc.itm.iters == 2);
+        }
+        for (int u = 0; vc; vc = cc.next(p), ++u) {
+          const int it = cc.it, iters = cc.itm.iters;
+          const bool la = it + 2 < iters;  // S/dP(u+2) in this block
+          const uint32_t b = uint32_t(u & 1), cs = uint32_t(u % NQ);
+          const uint32_t ls = uint32_t((u + 2) % NQ), lph = uint32_t(((u + 2) / NQ) & 1);
+          if (la) {
+            wp.template wait<1>(&bar_qd_full[ls], lph);
+            wp.template wait<1>(&bar_do_full[ls], lph);
+          }
+          wp.template wait<5>(&bar_ds_full[b], uint32_t((u >> 1) & 1));
+          if (it == 0 && cc.k > 0) wp.template wait<4>(bar_dkv_empty, (cc.k - 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t acc0 = it > 0 ? 1u : 0u;
+            const uint64_t om = opaque(dOm) + cs * QT16, qm = opaque(dQm) + cs * QT16;
+#pragma unroll
+            for (int j = 0; j < UQ / 16; ++j)  // dV += Pᵀ·dO (A = Pᵀ in TMEM over the S columns)
+              umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(b) + Cfg::a_col(j), sdesc_add(om, j * 2048), id_acc,
+                          j > 0 ? 1u : acc0);
+            if (la) {  // S(u+2) over Pᵀ(u): after dV(u) in issue order
+              mma_S(Cfg::s_col(b), ls * QT16);
+              umma_commit(&bar_s_full[b]);
+            }
+#pragma unroll
+            for (int j = 0; j < UQ / 16; ++j)  // dK += dSᵀ·Q (A = dSᵀ in TMEM over the dP columns)
+              umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(b) + Cfg::a_col(j), sdesc_add(qm, j * 2048), id_acc,
+                          j > 0 ? 1u : acc0);
+            umma_commit(&bar_qd_empty[cs]);
+            umma_commit(&bar_do_empty[cs]);  // dV(u) was dO's last reader
+            if (it + 1 == iters) umma_commit(bar_dkv_full);
+            if (la) {  // dP(u+2) over dSᵀ(u): after dK(u) in issue order
+              mma_dP(Cfg::dp_col(b), ls * QT16);
+              umma_commit(&bar_dp_full[b]);
+              if (it + 3 == iters) umma_commit(bar_kv_empty);
+            }
+          }
+          __syncwarp();
+          if (it + 1 == iters && cc.has_next()) {  // the next item's first units (after its dkv_full)
+            KvItem nx = cc.nxt;
+            kv_item_finish<UQ>(p, nx);
+            sdp(u + 1, true, cc.k + 1, nx.iters == 1);
+            if (nx.iters >= 2) sdp(u + 2, false, cc.k + 1, nx.iters == 2);
+          }
+        }
+        if (lane == 0) wp.flush(p.prof + 8);
+      } else {
       UnitCursor<UQ> ca, cc;
       uint32_t as = 0, aph = 0;    // Q stage / parity of the look-ahead unit ca.u
       uint32_t ads = 0, adph = 0;  // its dO stage / parity
@@ -690,6 +763,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
         ph ^= b ^ 1;  // flips after each pair of units (when b returns to 0)
       }
       if (lane == 0) wp.flush(p.prof + 8);
+      }  // MODE != 0
     }
   }
   } else {

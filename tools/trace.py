@@ -6,7 +6,8 @@ import sys
 NAMES = {36: "S0.item_start", 37: "S1.item_start", 38: "S0.unit_setup", 39: "S1.unit_setup", 1: "P.qload", 2: "P.kvload", 14: "M.bSdP_enter", 15: "M.bSdP_ready", 10: "M.pt_seen", 11: "M.dV+S2", 12: "M.ds_seen", 13: "M.dK+dP2", 
          20: "S0.s_seen", 21: "S1.s_seen", 22: "S0.pt_arr", 23: "S1.pt_arr", 24: "S0.dp_seen", 25: "S1.dp_seen",
          26: "S0.ds_arr", 27: "S1.ds_arr", 30: "E0.enter", 31: "E1.enter", 32: "E0.dkv_seen", 33: "E1.dkv_seen",
-         34: "E0.done", 35: "E1.done", 50: "E.tmem_drained", 51: "E.dV_staged", 52: "E.dV_read"}
+         34: "E0.done", 35: "E1.done", 50: "E.tmem_drained", 51: "E.dV_staged", 52: "E.dV_read",
+         40: "M.ahead_adv", 41: "M.bnd_checked", 42: "M.next_unit", 43: "M.loads_seen"}
 data = open(sys.argv[1], "rb").read()
 off = 0
 runs = []

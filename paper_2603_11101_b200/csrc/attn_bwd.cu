@@ -196,14 +196,17 @@ struct BwdParams {
 template <int HD, int UQ = 64, int MODE = 0>
 struct DkvCfg {
   static constexpr int HO = MODE ? HD : (HD < 128 ? HD : 128);  // dK / dV head-dim columns per launch
-  static constexpr int CW = UQ / 2;               // query columns per softmax warp
+  // MODE 3 (head_dim ≤ 128, one pass): K and V resident in TMEM (A operands of Sᵀ and dPᵀ: no
+  // smem-bound SS MMAs), single Sᵀ / dPᵀ buffers, all 16 softmax warps on every unit (16 queries each)
+  static constexpr bool kTm = MODE == 3;
+  static constexpr int CW = kTm ? 16 : UQ / 2;    // query columns per softmax warp
   static constexpr int QBOX = UQ * 128;           // one 64-column TMA box of a Q / dO stage
   static constexpr int KT = 128 * HD * 2;  // K or V tile (128 keys)
   static constexpr int QT = UQ * HD * 2;   // Q or dO tile (UQ queries)
   // Q / dO stages: 5, except head_dim 256 with K and V resident (3); the dV pass loads no V, and its
   // 64 KB hold two more stages — with S look-ahead of 2 units, 3 stages leave no load in flight
   // head_dim 128 (one pass): 4, so that the dK / dV staging tile of the TMA-store epilogue fits
-  static constexpr int NS = HD == 256 && MODE != 1 ? 3 : (HD == 128 && MODE == 0 ? 4 : 5);
+  static constexpr int NS = HD == 256 && MODE != 1 ? 3 : (HD == 128 && (MODE == 0 || MODE == 3) ? 4 : 5);
   // Q (+ lse2 / D windows) and dO have separate rings: NQ / ND stages.  Where dO is read only by
   // dP (the dK pass) its stage is released right after dP — 4 Q + 2 dO stages in the smem of 3 pairs,
   // so one more unit's loads are in flight; elsewhere dV reads dO at the end of the unit (NQ = ND).
@@ -217,7 +220,7 @@ struct DkvCfg {
   static constexpr int OFF_DSUM = OFF_LSE + NQ * VEC;
   // single-pass launches (head_dim ≤ 128) write dK / dV through an SW128 staging tile and TMA stores
   // (128 rows × HO bf16, 64-column boxes of 16 KB); the head-dim-256 passes store rows directly
-  static constexpr bool kTmaEpi = MODE == 0 && HD <= 128;
+  static constexpr bool kTmaEpi = (MODE == 0 || MODE == 3) && HD <= 128;
   // single-pass launches (d ≤ 128): four dedicated epilogue warps (20-23, one per TMEM lane
   // quadrant) drain dK / dV, so the softmax groups never stall on an item boundary; registers are
   // rebalanced with setmaxnreg (softmax 96, the rest 48: 768 threads × 80 at launch)
@@ -228,16 +231,17 @@ struct DkvCfg {
   static constexpr int OFF_BAR = OFF_STG + STG;
   static constexpr int NUM_BARS = 12 + 2 * NQ + 2 * ND + 1;  // + epi_done
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;  // dynamic smem base is 1 KB aligned
-  static constexpr uint32_t DV_COL = 256, DK_COL = MODE ? 256 : 256 + HO;
+  static constexpr uint32_t DV_COL = 256, DK_COL = (MODE == 1 || MODE == 2) ? 256 : 256 + HO;
   // head_dim-256 passes: the item's K tile lives in TMEM (tcgen05.cp from the TMA-loaded smem tile at
   // the item's first unit), so Sᵀ = K·Qᵀ takes A from TMEM instead of re-reading 64 KB of smem per
   // 32-query unit: 16 K-steps × 8 columns in the columns S / dP leave free
-  static constexpr bool kKTmem = HD == 256 && MODE != 0;
+  static constexpr bool kKTmem = HD == 256 && (MODE == 1 || MODE == 2);
   __host__ __device__ static constexpr uint32_t k_col(int s) {
-    return MODE == 1 ? 128u + 8u * s : (s < 8 ? 64u + 8u * s : 192u + 8u * (s - 8));
+    return kTm ? 128u + 8u * s : MODE == 1 ? 128u + 8u * s : (s < 8 ? 64u + 8u * s : 192u + 8u * (s - 8));
   }
-  __host__ __device__ static constexpr uint32_t s_col(int b) { return b ? uint32_t(UQ) : 0u; }
-  __host__ __device__ static constexpr uint32_t dp_col(int b) { return 128u + (b ? uint32_t(UQ) : 0u); }
+  __host__ __device__ static constexpr uint32_t v_col(int s) { return 128u + uint32_t(HD / 2) + 8u * s; }  // MODE 3
+  __host__ __device__ static constexpr uint32_t s_col(int b) { return kTm ? 0u : (b ? uint32_t(UQ) : 0u); }
+  __host__ __device__ static constexpr uint32_t dp_col(int b) { return kTm ? 64u : 128u + (b ? uint32_t(UQ) : 0u); }
   // TMEM column of K-step j (16 queries) of Pᵀ / dSᵀ: warp chunks of CW queries sit at column
   // offsets part·CW, each packed into CW/2 columns as bf16 pairs
   __host__ __device__ static constexpr uint32_t a_col(int j) { return (j / (CW / 16)) * CW + (j % (CW / 16)) * 8; }
@@ -373,8 +377,10 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_s_full[b], 1);
       mbar_init(&bar_dp_full[b], 1);
-      mbar_init(&bar_ds_full[b], 8);
+      mbar_init(&bar_ds_full[b], Cfg::kTm ? 16 : 8);
     }
+    mbar_init(bars + 8, 16);  // MODE 3: Pᵀ written (16 softmax warps)
+    mbar_init(bars + 9, 4);   // MODE 3: dK drained (bar_dkv_empty then tracks dV alone)
     for (int s = 0; s < NQ; ++s) {
       mbar_init(&bar_qd_full[s], 1);
       mbar_init(&bar_qd_empty[s], 1);
@@ -448,9 +454,9 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
                 }
               }
             }
-            if (last) {
+            if (last || Cfg::kTm) {  // MODE 3: dV and dK accumulators released separately
               tc_fence_before();
-              warp_arrive(bar_dkv_empty);  // TMEM drained: the next item's dV / dK may start
+              warp_arrive(Cfg::kTm && last ? bars + 9 : bar_dkv_empty);  // the next item's dV / dK may start
             }
             if (p.row_map) return;
             fence_proxy_async_smem();
@@ -593,7 +599,102 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
           umma_f16_ss(tmem + col, sdesc_add(a0, (j / 4) * 16384 + (j % 4) * 32),
                       sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32), id_s, j > 0);
       };
-      if constexpr (MODE == 0) {
+      if constexpr (MODE == 3) {
+        // K / V resident in TMEM; single Sᵀ / dPᵀ buffers.  Per unit u of an item:
+        //   wait Pᵀ(u) → dV(u) · Sᵀ(u+1)   (Sᵀ(u+1) over Pᵀ(u), after its reader in issue order)
+        //   wait dSᵀ(u) → dK(u) · dPᵀ(u+1)
+        // At an item's start: wait K/V, copy both tiles to TMEM (after the previous item's last
+        // Sᵀ / dPᵀ in issue order; the smem tiles are released at once), then Sᵀ / dPᵀ of its first unit.
+        uint64_t* bar_p_full = bars + 8;
+        auto mma_St = [&](uint32_t soff) {  // Sᵀ = K·Qᵀ, A = K in TMEM, B = Q (K-major)
+          const uint64_t b0 = opaque(dQk) + soff;
+#pragma unroll
+          for (int j = 0; j < HD / 16; ++j)
+            umma_f16_ts(tmem + Cfg::s_col(0), tmem + Cfg::k_col(j), sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32),
+                        id_s, j > 0 ? 1u : 0u);
+        };
+        auto mma_dPt = [&](uint32_t soff) {  // dPᵀ = V·dOᵀ, A = V in TMEM
+          const uint64_t b0 = opaque(dOk) + soff;
+#pragma unroll
+          for (int j = 0; j < HD / 16; ++j)
+            umma_f16_ts(tmem + Cfg::dp_col(0), tmem + Cfg::v_col(j), sdesc_add(b0, (j / 4) * Cfg::QBOX + (j % 4) * 32),
+                        id_s, j > 0 ? 1u : 0u);
+        };
+        UnitCursor<UQ> c;
+        int u = 0;
+        for (bool v = c.start(p); v;) {
+          const int k = c.k;
+          {  // item start
+            const uint32_t st = uint32_t(u % NQ), sph = uint32_t((u / NQ) & 1);
+            wp.template wait<0>(bar_kv_full, k & 1);
+            wp.template wait<1>(&bar_qd_full[st], sph);
+            wp.template wait<1>(&bar_do_full[st], sph);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t ka = opaque(dK0), va = opaque(dV0);
+#pragma unroll
+              for (int j = 0; j < HD / 16; ++j)
+                tmem_cp_128x256b(tmem + Cfg::k_col(j), sdesc_add(ka, (j / 4) * 16384 + (j % 4) * 32));
+#pragma unroll
+              for (int j = 0; j < HD / 16; ++j)
+                tmem_cp_128x256b(tmem + Cfg::v_col(j), sdesc_add(va, (j / 4) * 16384 + (j % 4) * 32));
+              umma_commit(bar_kv_empty);  // K / V smem tiles free once copied
+              mma_St(st * QT16);
+              umma_commit(&bar_s_full[0]);
+              mma_dPt(st * QT16);
+              umma_commit(&bar_dp_full[0]);
+            }
+            __syncwarp();
+          }
+          for (;;) {
+            const int it = c.it, iters = c.itm.iters;
+            const bool nx = it + 1 < iters;
+            const uint32_t cs = uint32_t(u % NQ), ns = uint32_t((u + 1) % NQ), nph = uint32_t(((u + 1) / NQ) & 1);
+            const uint32_t par = uint32_t(u & 1);
+            wp.template wait<5>(bar_p_full, par);
+            if (it == 0 && k > 0) wp.template wait<4>(bar_dkv_empty, (k - 1) & 1);  // previous item's dV drained
+            if (nx) wp.template wait<1>(&bar_qd_full[ns], nph);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t acc0 = it > 0 ? 1u : 0u;
+              const uint64_t om = opaque(dOm) + cs * QT16;
+#pragma unroll
+              for (int j = 0; j < UQ / 16; ++j)  // dV += Pᵀ·dO
+                umma_f16_ts(tmem + Cfg::DV_COL, tmem + Cfg::s_col(0) + Cfg::a_col(j), sdesc_add(om, j * 2048), id_acc,
+                            j > 0 ? 1u : acc0);
+              umma_commit(&bar_do_empty[cs]);  // dPᵀ(u) and dV(u) have read dO(u)
+              if (nx) {
+                mma_St(ns * QT16);
+                umma_commit(&bar_s_full[0]);
+              }
+            }
+            __syncwarp();
+            wp.template wait<5>(&bar_ds_full[0], par);
+            if (it == 0 && k > 0) wp.template wait<4>(bars + 9, (k - 1) & 1);  // previous item's dK drained
+            if (nx) wp.template wait<1>(&bar_do_full[ns], nph);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t acc0 = it > 0 ? 1u : 0u;
+              const uint64_t qm = opaque(dQm) + cs * QT16;
+#pragma unroll
+              for (int j = 0; j < UQ / 16; ++j)  // dK += dSᵀ·Q
+                umma_f16_ts(tmem + Cfg::DK_COL, tmem + Cfg::dp_col(0) + Cfg::a_col(j), sdesc_add(qm, j * 2048), id_acc,
+                            j > 0 ? 1u : acc0);
+              umma_commit(&bar_qd_empty[cs]);  // Sᵀ(u) and dK(u) have read Q(u)
+              if (!nx) umma_commit(bar_dkv_full);
+              if (nx) {
+                mma_dPt(ns * QT16);
+                umma_commit(&bar_dp_full[0]);
+              }
+            }
+            __syncwarp();
+            ++u;
+            v = c.next(p);
+            if (!v || !nx) break;
+          }
+        }
+        if (lane == 0) wp.flush(p.prof + 8);
+      } else if constexpr (MODE == 0) {
         // Single-pass launches: one cursor, stages / parities / TMEM buffers derived from the
         // unit ordinal (NQ = ND, compile-time).  S/dP of unit x are issued in the block of x − 2
         // when both lie in the same item; an item's first min(2, units) S/dP are issued after the
@@ -768,6 +869,103 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
   }
   } else {
     if constexpr (Cfg::kEpiWarps) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");
+    if constexpr (MODE == 3) {
+    // ================================================ softmax warps 0-15, MODE 3: every warp on every
+    // unit — TMEM lane quadrant w%4 (32 keys) × query slice w/4 (16 of the unit's 64 queries)
+    const int quad = warp & 3, part = warp >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int krow = quad * 32 + lane;
+    const int c0 = part * CW;
+    uint64_t* bar_p_full = bars + 8;
+    WaitProf<PROF, 12> wp;
+    UnitCursor<UQ> c;
+    auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
+    int ss = 0;  // stage of unit c.u
+    int2 ks = make_int2(0, 0), ks_nxt = ks;
+    int u = 0;
+    for (bool v = c.start(p); v; v = c.next(p), ++u) {
+      if (c.it == 0) {  // this item's key spans were prefetched one item ahead (first item: now)
+        ks = c.k == 0 ? span_of(c.itm.k0 + krow) : ks_nxt;
+        if (c.has_next()) ks_nxt = span_of(c.nxt.k0 + krow);
+      }
+      const int s = ss;
+      if (++ss == NQ) ss = 0;
+      const uint32_t par = uint32_t(u & 1);
+      const int qb = c.qb();
+      const int c_lo = ks.x - qb - c0, c_hi = ks.y - qb - c0;  // visible query columns of this slice
+      const bool all_full = __all_sync(0xffffffffu, c_lo <= 0 && c_hi >= CW);
+      const bool none = __all_sync(0xffffffffu, c_hi <= 0 || c_lo >= CW);
+      const int lo = max(c_lo, 0), hi = min(c_hi, CW);
+      const uint32_t vis = hi <= lo ? 0u : ((hi >= 32 ? 0xffffffffu : (1u << hi) - 1u) & ~((1u << lo) - 1u));
+      const float4* lse4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_LSE + s * Cfg::VEC) + c0 / 4;
+      const float4* dsum4 = reinterpret_cast<const float4*>(smem + Cfg::OFF_DSUM + s * Cfg::VEC) + c0 / 4;
+      uint32_t pp[CW / 2];
+      // ---- phase A: Sᵀ → Pᵀ (bf16 over this slice's first CW/2 S columns)
+      wp.template wait<0>(&bar_s_full[0], par);
+      const long long ta = wp.now();
+      tc_fence_after();
+      if (!none) {
+        uint32_t sa[CW];
+        tmem_ld16(tmem + lane_off + Cfg::s_col(0) + c0, sa);
+        tmem_wait_ld();
+        if (!all_full) {
+#pragma unroll
+          for (int q = 0; q < CW; ++q) sa[q] = ((vis >> q) & 1u) ? sa[q] : __float_as_uint(-INFINITY);
+        }
+        const float2 sl2v = make_float2(p.scale_log2, p.scale_log2);
+#pragma unroll
+        for (int j4 = 0; j4 < CW / 4; ++j4) {
+          const float4 l = lse4[j4];
+          const float2 a0 = f2_fma(make_float2(__uint_as_float(sa[4 * j4 + 0]), __uint_as_float(sa[4 * j4 + 1])), sl2v,
+                                   make_float2(-l.x, -l.y));
+          const float2 a1 = f2_fma(make_float2(__uint_as_float(sa[4 * j4 + 2]), __uint_as_float(sa[4 * j4 + 3])), sl2v,
+                                   make_float2(-l.z, -l.w));
+          pp[2 * j4] = pack_bf16x2(ex2_approx(a0.x), ex2_approx(a0.y));
+          pp[2 * j4 + 1] = pack_bf16x2(ex2_approx(a1.x), ex2_approx(a1.y));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CW / 2; ++j) pp[j] = 0u;
+      }
+      tmem_st8(tmem + lane_off + Cfg::s_col(0) + c0, pp);
+      tmem_wait_st();
+      tc_fence_before();
+      warp_arrive(bar_p_full);
+      wp.template add_since<4>(ta);
+      // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over this slice's first CW/2 dP columns
+      wp.template wait<1>(&bar_dp_full[0], par);
+      const long long tb = wp.now();
+      tc_fence_after();
+      uint32_t pk[CW / 2];
+      if (!none) {
+        uint32_t dr[CW];
+        tmem_ld16(tmem + lane_off + Cfg::dp_col(0) + c0, dr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j4 = 0; j4 < CW / 4; ++j4) {
+          const float4 dd = dsum4[j4];
+          const int q = 4 * j4;
+          const float p0 = __uint_as_float(pp[2 * j4] << 16), p1 = __uint_as_float(pp[2 * j4] & 0xFFFF0000u);
+          const float p2 = __uint_as_float(pp[2 * j4 + 1] << 16), p3 = __uint_as_float(pp[2 * j4 + 1] & 0xFFFF0000u);
+          const float2 d0 = f2_mul(make_float2(p0, p1), f2_add(make_float2(__uint_as_float(dr[q]), __uint_as_float(dr[q + 1])),
+                                                               make_float2(-dd.x, -dd.y)));
+          const float2 d1 = f2_mul(make_float2(p2, p3), f2_add(make_float2(__uint_as_float(dr[q + 2]), __uint_as_float(dr[q + 3])),
+                                                               make_float2(-dd.z, -dd.w)));
+          pk[2 * j4] = pack_bf16x2(d0.x, d0.y);
+          pk[2 * j4 + 1] = pack_bf16x2(d1.x, d1.y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CW / 2; ++j) pk[j] = 0u;
+      }
+      tmem_st8(tmem + lane_off + Cfg::dp_col(0) + c0, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      warp_arrive(&bar_ds_full[0]);
+      wp.template add_since<5>(tb);
+    }
+    if (warp == 0 && lane == 0) wp.flush(p.prof + 16);
+    } else {
     // ================================================ softmax warps 0-15
     const int g = warp >> 3, quad = warp & 3, part = warp >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
@@ -1028,6 +1226,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
     }
     bulk_wait_all();  // dK / dV row stores of the last item
     if (warp == 0 && lane == 0) wp.flush(p.prof + 16);  // 12 slots: 16..27
+    }  // MODE != 3
   }
   tc_fence_before();
   __syncthreads();
@@ -1575,18 +1774,25 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   // head_dim 256: a dV pass (MODE 1) and a dK pass (MODE 2) over the full head dim (VLASIM_DKV_HALVES
   // selects the previous two head-dim halves, for comparison); head_dim ≤ 128: one launch (MODE 0)
   const bool halves = HD == 256 && getenv("VLASIM_DKV_HALVES");
+  // head_dim ≤ 128: MODE 3 (K / V resident in TMEM); VLASIM_DKV_MODE0 selects the double-buffered
+  // MODE 0 kernel for comparison
+  static const bool mode0 = getenv("VLASIM_DKV_MODE0") != nullptr;
   const int nlaunch = HD == 256 ? 2 : 1;
   for (int half = 0; half < nlaunch; ++half) {
     const int grid = persistent_grid(max_tiles * Hkv, a->sm_budget);
     p.prof = prof_enabled() ? prof_buffer() : nullptr;
     p.ohalf = halves ? half : 0;
-    auto kern = HD != 256 || halves ? (p.prof ? k_bwd_dkdv<HD, UQ, true, 0> : k_bwd_dkdv<HD, UQ, false, 0>)
-              : half == 0           ? (p.prof ? k_bwd_dkdv<HD, UQ, true, 1> : k_bwd_dkdv<HD, UQ, false, 1>)
-                                    : (p.prof ? k_bwd_dkdv<HD, UQ, true, 2> : k_bwd_dkdv<HD, UQ, false, 2>);
-    const int smem = HD != 256 || halves ? DkvCfg<HD, UQ, 0>::SMEM
+    constexpr int M1 = HD <= 128 ? 3 : 0;  // single-pass mode
+    const bool tm = HD <= 128 && !mode0;
+    auto kern = HD != 256 || halves
+                    ? (tm ? (p.prof ? k_bwd_dkdv<HD, UQ, true, M1> : k_bwd_dkdv<HD, UQ, false, M1>)
+                          : (p.prof ? k_bwd_dkdv<HD, UQ, true, 0> : k_bwd_dkdv<HD, UQ, false, 0>))
+                : half == 0 ? (p.prof ? k_bwd_dkdv<HD, UQ, true, 1> : k_bwd_dkdv<HD, UQ, false, 1>)
+                            : (p.prof ? k_bwd_dkdv<HD, UQ, true, 2> : k_bwd_dkdv<HD, UQ, false, 2>);
+    const int smem = HD != 256 || halves ? (tm ? DkvCfg<HD, UQ, M1>::SMEM : DkvCfg<HD, UQ, 0>::SMEM)
                      : half == 0         ? DkvCfg<HD, UQ, 1>::SMEM
                                          : DkvCfg<HD, UQ, 2>::SMEM;
-    const int threads = HD != 256 || halves ? DkvCfg<HD, UQ, 0>::THREADS
+    const int threads = HD != 256 || halves ? (tm ? DkvCfg<HD, UQ, M1>::THREADS : DkvCfg<HD, UQ, 0>::THREADS)
                         : half == 0         ? DkvCfg<HD, UQ, 1>::THREADS
                                             : DkvCfg<HD, UQ, 2>::THREADS;
     VLASIM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

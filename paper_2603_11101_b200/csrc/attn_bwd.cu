@@ -652,6 +652,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
             const uint32_t cs = uint32_t(u % NQ), ns = uint32_t((u + 1) % NQ), nph = uint32_t(((u + 1) / NQ) & 1);
             const uint32_t par = uint32_t(u & 1);
             wp.template wait<5>(bar_p_full, par);
+            trace(10, u);  // M: Pᵀ seen
             if (it == 0 && k > 0) wp.template wait<4>(bar_dkv_empty, (k - 1) & 1);  // previous item's dV drained
             if (nx) wp.template wait<1>(&bar_qd_full[ns], nph);
             tc_fence_after();
@@ -669,7 +670,9 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
               }
             }
             __syncwarp();
+            trace(11, u);  // M: dV + S issued
             wp.template wait<5>(&bar_ds_full[0], par);
+            trace(12, u);  // M: dSᵀ seen
             if (it == 0 && k > 0) wp.template wait<4>(bars + 9, (k - 1) & 1);  // previous item's dK drained
             if (nx) wp.template wait<1>(&bar_do_full[ns], nph);
             tc_fence_after();
@@ -688,6 +691,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
               }
             }
             __syncwarp();
+            trace(13, u);  // M: dK + dP issued
             ++u;
             v = c.next(p);
             if (!v || !nx) break;
@@ -878,6 +882,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
     const int c0 = part * CW;
     uint64_t* bar_p_full = bars + 8;
     WaitProf<PROF, 12> wp;
+    TraceCtr trace(lane == 0 && warp == 0 && trb ? trb + 2001 * 2 : nullptr);
     UnitCursor<UQ> c;
     auto span_of = [&](int key) { return key < p.T ? __ldg(p.cols_span + key) : make_int2(0, 0); };
     int ss = 0;  // stage of unit c.u
@@ -902,6 +907,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
       uint32_t pp[CW / 2];
       // ---- phase A: Sᵀ → Pᵀ (bf16 over this slice's first CW/2 S columns)
       wp.template wait<0>(&bar_s_full[0], par);
+      trace(20, u);  // S: s_full seen
       const long long ta = wp.now();
       tc_fence_after();
       if (!none) {
@@ -931,9 +937,11 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
       tmem_wait_st();
       tc_fence_before();
       warp_arrive(bar_p_full);
+      trace(22, u);  // S: Pᵀ arrived
       wp.template add_since<4>(ta);
       // ---- phase B: dPᵀ → dSᵀ = Pᵀ ∘ (dPᵀ − D) → bf16 over this slice's first CW/2 dP columns
       wp.template wait<1>(&bar_dp_full[0], par);
+      trace(24, u);  // S: dp_full seen
       const long long tb = wp.now();
       tc_fence_after();
       uint32_t pk[CW / 2];
@@ -962,6 +970,7 @@ __global__ void __launch_bounds__(DkvCfg<HD, UQ, MODE>::THREADS, 1)
       tmem_wait_st();
       tc_fence_before();
       warp_arrive(&bar_ds_full[0]);
+      trace(26, u);  // S: dSᵀ arrived
       wp.template add_since<5>(tb);
     }
     if (warp == 0 && lane == 0) wp.flush(p.prof + 16);

@@ -135,3 +135,40 @@ def test_config2_scale_consistency(gpu):
     # north_star FP8 tolerance, relative to max(1, max|o|) (the bf16 output stands in for the reference)
     err = (o8.float() - o_s.float()).abs().max().item() / max(1.0, o_s.float().abs().max().item())
     assert err < 6e-2, err
+
+
+_MODE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2603_11101_b200 import attention, packing, synthetic
+L = synthetic.gen_lengths(96, 0, 16, 512)
+plan = packing.pack_ffd(L, 4096)
+T, H, d = int(L.sum()), 4, int(sys.argv[3])
+g = torch.Generator(device="cuda").manual_seed(3)
+q, k, v, do = (torch.randn(T, H, d, device="cuda", generator=g).bfloat16() for _ in range(4))
+cu, seg = plan.cu_seqlens, packing.seg_src(plan)
+o, lse = attention.varlen_attn_fwd(q, k, v, cu, seg_src=seg)
+dq, dk, dv = attention.varlen_attn_bwd(do, q, k, v, o, lse, cu, seg_src=seg)
+np.savez(sys.argv[2], dk=dk.float().cpu().numpy(), dv=dv.float().cpu().numpy(), dq=dq.float().cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_dkdv_mode3_matches_mode0(gpu, tmp_path, d):
+    """The default single-pass dK/dV kernel (K / V resident in TMEM, MODE 3) against the
+    double-buffered one (VLASIM_DKV_MODE0): the same gradients (fresh processes: the switch is read
+    once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for tag, env in (("m3", {}), ("m0", {"VLASIM_DKV_MODE0": "1"})):
+        f = tmp_path / f"{tag}.npz"
+        r = subprocess.run([sys.executable, "-c", _MODE_SCRIPT, root, str(f), str(d)],
+                           env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[tag] = np.load(f)
+    for key in ("dk", "dv", "dq"):
+        a, b = outs["m3"][key], outs["m0"][key]
+        assert np.allclose(a, b, rtol=0, atol=2e-2 * max(1.0, float(np.abs(b).max()))), key

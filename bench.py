@@ -800,8 +800,13 @@ def main():
 
     if rank == 0:
         fb, bb = attn_bytes(T, H, HKV, D)
-        rf_bwd = roofline(2.5 * fl_fwd, bb, kbwd, PEAKS["bf16_tflops"], "backward pass: k_bwd_pre + k_bwd_dkdv + k_bwd_dq")
-        rf_step = roofline(fl_total, fb + bb, kfwd + kbwd, PEAKS["bf16_tflops"], "attention fwd + bwd")
+        # kernel time = the sum of the phase's kernels between the C-ABI's kernel-boundary CUDA events
+        # (device time of the kernels themselves; the phase replays beside it also carry the gaps
+        # between launches and vary more from run to run)
+        kb_sum, kf_sum = float(sum(kb)), float(sum(kf))
+        rf_bwd = roofline(2.5 * fl_fwd, bb, kb_sum, PEAKS["bf16_tflops"], "backward pass: k_bwd_pre + k_bwd_dkdv + k_bwd_dq")
+        rf_bwd["time_src"] = "kernel-boundary CUDA events (pre + tiles + dK/dV + dQ)"
+        rf_step = roofline(fl_total, fb + bb, kf_sum + kb_sum, PEAKS["bf16_tflops"], "attention fwd + bwd")
         traffic, tsrc = ncu_traffic()
         bwd_traffic = None
         if traffic:

@@ -5,7 +5,9 @@
 using namespace vlasim_dev;
 
 // mode 0: SS 128x64 K-major   1: SS 128x128 K-major   2: TS 128x128 B MN-major   3: TS 128x64 B MN-major
-// 4: SS 128x256 K-major
+// 4: SS 128x256 K-major   5: TS 128x64 B K-major
+// 6: the dK/dV MODE-3 unit (24 instructions): dV 4× TS 128x128 (B MN-major) · Sᵀ 8× TS 128x64
+//    (B K-major) · dK 4× TS 128x128 · dPᵀ 8× TS 128x64 — reported per instruction (÷ 24 per unit)
 // LDW warps (1..LDW) hammer tcgen05.ld on TMEM columns [0,128) while warp 0 issues MMAs
 // (MMAs write columns [256, 512); TS modes read A from columns [0, 32)).
 template <int MODE, int LDW = 0>
@@ -26,17 +28,36 @@ __global__ void __launch_bounds__(576, 1) k_mma(int iters, unsigned long long* o
     const uint64_t da = make_sdesc_sw128(smem_u32(smem), 16, 1024);
     const uint64_t db = make_sdesc_sw128(smem_u32(smem + 32768), 16, 1024);
     const uint64_t dbm = make_sdesc_sw128(smem_u32(smem + 32768), 8192, 1024);
-    constexpr uint32_t N = MODE == 0 || MODE == 3 ? 64 : (MODE == 4 ? 256 : 128);
+    constexpr uint32_t N = MODE == 0 || MODE == 3 || MODE == 5 ? 64 : (MODE == 4 ? 256 : 128);
     constexpr uint32_t id = make_idesc_bf16(128, N, false, MODE == 2 || MODE == 3);
+    constexpr uint32_t id64k = make_idesc_bf16(128, 64, false, false);   // Sᵀ / dPᵀ: B K-major
+    constexpr uint32_t id128m = make_idesc_bf16(128, 128, false, true);  // dV / dK: B MN-major
     const long long t0 = clock64();
     if (elect_one()) {
       for (int it = 0; it < iters; ++it) {
+        if constexpr (MODE == 6) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (MODE == 0 || MODE == 1 || MODE == 4)
-            umma_f16_ss(tmem + 256 * (MODE == 4 ? 0 : (it & 1)), sdesc_add(da, (j % 4) * 32), sdesc_add(db, (j % 4) * 32), id, 1);
-          else
-            umma_f16_ts(tmem + 256 + 128 * (it & 1), tmem + (j & 3) * 8, sdesc_add(dbm, (j & 3) * 2048), id, 1);
+          for (int j = 0; j < 4; ++j)  // dV
+            umma_f16_ts(tmem + 256, tmem + 64 + j * 8, sdesc_add(dbm, j * 2048), id128m, 1);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)  // Sᵀ (A = K in TMEM cols 128.., B = Q K-major)
+            umma_f16_ts(tmem + 0, tmem + 128 + j * 8, sdesc_add(db, (j % 4) * 32), id64k, j > 0 ? 1u : 0u);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)  // dK
+            umma_f16_ts(tmem + 384, tmem + 64 + j * 8, sdesc_add(dbm, j * 2048), id128m, 1);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)  // dPᵀ (A = V in TMEM cols 192..)
+            umma_f16_ts(tmem + 64, tmem + 192 + j * 8, sdesc_add(db, (j % 4) * 32), id64k, j > 0 ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (MODE == 0 || MODE == 1 || MODE == 4)
+              umma_f16_ss(tmem + 256 * (MODE == 4 ? 0 : (it & 1)), sdesc_add(da, (j % 4) * 32), sdesc_add(db, (j % 4) * 32), id, 1);
+            else if (MODE == 5)
+              umma_f16_ts(tmem + 256 + 128 * (it & 1), tmem + (j & 3) * 8, sdesc_add(db, (j % 4) * 32), id, 1);
+            else
+              umma_f16_ts(tmem + 256 + 128 * (it & 1), tmem + (j & 3) * 8, sdesc_add(dbm, (j & 3) * 2048), id, 1);
+          }
         }
       }
       umma_commit(&bar);
@@ -77,12 +98,19 @@ void run(int blocks, const char* name, double flop_per_instr) {
   double avg = 0;
   for (int i = 0; i < blocks; ++i) avg += h[i];
   avg /= blocks;
-  printf("%-28s ldw=%2d blocks=%3d  %.1f cycles/instr  %.0f flop/clk/SM  (%s)\n", name, LDW, blocks, avg / (iters * 8.0),
-         flop_per_instr * iters * 8 / avg, cudaGetErrorString(e));
+  const double per = MODE == 6 ? 24.0 : 8.0;  // instructions per iteration
+  printf("%-28s ldw=%2d blocks=%3d  %.1f cycles/instr  %.0f cycles/iter  %.0f flop/clk/SM  (%s)\n", name, LDW, blocks,
+         avg / (iters * per), avg / iters, flop_per_instr * iters * per / avg, cudaGetErrorString(e));
   cudaFree(d);
 }
 
 int main() {
+  // the dK/dV MODE-3 unit: 1024 cycles at the per-instruction floor (flop per instr averaged)
+  run<5>(1, "TS 128x64x16 B K-major", 2.0 * 128 * 64 * 16);
+  run<6>(1, "MODE-3 unit (24 instr)", 2.0 * 128 * 128 * 64 * 4 / 24.0);
+  run<6, 16>(1, "MODE-3 unit (24 instr)", 2.0 * 128 * 128 * 64 * 4 / 24.0);
+  run<6>(148, "MODE-3 unit (24 instr)", 2.0 * 128 * 128 * 64 * 4 / 24.0);
+  run<6, 16>(148, "MODE-3 unit (24 instr)", 2.0 * 128 * 128 * 64 * 4 / 24.0);
   run<2, 4>(1, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);
   run<2, 8>(1, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);
   run<2, 16>(1, "TS 128x128x16 B MN-major", 2.0 * 128 * 128 * 16);

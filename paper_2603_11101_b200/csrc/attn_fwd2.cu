@@ -74,17 +74,21 @@ struct Fwd2Cfg {
   static constexpr int OFF_Q = 0;                        // [NQ]
   static constexpr int OFF_K = NQ * Q_BYTES;             // [KS] K ring
   static constexpr int OFF_V = OFF_K + KS * K_BYTES;     // [VS] V ring
-  // FP8: the E4M3 Q buffer is too small to stage the bf16 O tile, so O gets its own staging tile
+  // FP8: the E4M3 Q buffer is too small to stage the bf16 O tile, so O gets its own staging tiles,
+  // two (items alternate): the producer then has to have issued item k-3's store — not k-2's — before
+  // loading item k's Q, so short items' Q / K loads never wait for the previous item's epilogue
+  static constexpr int NOST = FP8 ? 2 : 0;
+  static constexpr int OST_BYTES = BM * HD * 2;
   static constexpr int OFF_OST = OFF_V + VS * KV_BYTES;
   // row-max / row-sum exchange, 512 B per TMEM lane quadrant: bf16 maxima [2 parity][4 quarter][32
   // rows] for the tiles, fp32 sums [4 quarter][32 rows] once per item over the same bytes
-  static constexpr int OFF_XCH = OFF_OST + (FP8 ? BM * HD * 2 : 0);
+  static constexpr int OFF_XCH = OFF_OST + NOST * OST_BYTES;
   // decoded item descriptors, written by the producer one item ahead (the softmax warps hold no
   // next-item state in registers)
   static constexpr int NDESC = 4;
   static constexpr int OFF_DESC = OFF_XCH + 4 * 512;   // int4 [NDESC][2]
   static constexpr int OFF_BAR = OFF_DESC + NDESC * 32;
-  static constexpr int NUM_BARS = 2 * NQ + 2 * KS + 2 * VS + 9 + NQ + 1 + 2 * NDESC;
+  static constexpr int NUM_BARS = 2 * NQ + 2 * KS + 2 * VS + 9 + NQ + 2 + 2 * NDESC;
   // dynamic smem starts 1 KB aligned (no static smem in this kernel): no alignment slack
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, O_COL = 256;
@@ -159,8 +163,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* bar_o_empty = bar_s_full + 6;        // [2] 16 warp arrivals: epilogue drained O[k%2]
   uint64_t* bar_o_ready = bar_s_full + 8;        // one completion per PV
   uint64_t* bar_o_staged = bar_s_full + 9;       // [NQ] 16 warp arrivals: item's O staged in its Q buffer
-  uint64_t* bar_ost_free = bar_o_staged + NQ;    // FP8: the O staging tile has been read by its TMA store
-  uint64_t* bar_desc_full = bar_ost_free + 1;    // [NDESC] producer wrote item m's descriptor
+  uint64_t* bar_ost_free = bar_o_staged + NQ;    // [2] FP8: O staging tile k&1 has been read by its TMA store
+  uint64_t* bar_desc_full = bar_ost_free + 2;    // [NDESC] producer wrote item m's descriptor
   uint64_t* bar_desc_empty = bar_desc_full + Cfg::NDESC;  // [NDESC] 16 warp arrivals: read
   int4* descs = reinterpret_cast<int4*>(smem + Cfg::OFF_DESC);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
@@ -192,7 +196,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bar_o_empty[s], 16);
     }
     mbar_init(bar_o_ready, 1);
-    mbar_init(bar_ost_free, 1);
+    mbar_init(&bar_ost_free[0], 1);
+    mbar_init(&bar_ost_free[1], 1);
     for (int d = 0; d < Cfg::NDESC; ++d) {
       mbar_init(&bar_desc_full[d], 1);
       mbar_init(&bar_desc_empty[d], 16);
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto store_o = [&](int kk) {
         const int b = kk % NQ;
         wp.template wait<0>(&bar_o_staged[b], (kk / NQ) & 1);
-        const uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + b * Cfg::Q_BYTES);
+        const uint8_t* so = smem + (FP8 ? Cfg::OFF_OST + (kk & 1) * Cfg::OST_BYTES : Cfg::OFF_Q + b * Cfg::Q_BYTES);
         if (hn[b] == 128) {
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c) tma_store_2d(&tmO, hh[b] * HD + c * 64, hq0[b], so + c * 16384);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         bulk_commit();
         if constexpr (FP8) {
           bulk_wait_read0();
-          mbar_arrive(bar_ost_free);  // the next item's O may be staged
+          mbar_arrive(&bar_ost_free[kk & 1]);  // item kk+2's O may be staged
         }
       };
       auto try_stores = [&](int upto) {  // O stores of items < upto that are staged already (never blocks)
@@ -290,10 +295,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             bulk_wait_read0();
           }
         }
-        // FP8: one O staging tile released through ost_free, whose parity waits stay exact only while
-        // the stores trail the epilogues by at most one item
-        if (FP8 && k >= 2)
-          while (st <= k - 2) store_o(st++);
+        // FP8: staging tile b is released through ost_free[b] (item e's epilogue waits for item e-2's
+        // store); the store of item e-2 must be issued while item e is in flight — item e's epilogue
+        // runs during item e+1, so the producer issues stores up to k-3 at item k (never a wait on
+        // the previous item's epilogue, which would hold back item k's Q and K loads)
+        if (FP8 && k >= 3)
+          while (st <= k - 3) store_o(st++);
         hq0[qs] = itm.q0 + itm.dl;  // data row of the tile (O stores)
         hh[qs] = itm.h;
         hn[qs] = itm.qe - itm.q0;
@@ -438,8 +445,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float inv_l = (valid && e_l > 0.f) ? 1.f / e_l : 0.f;
       if (valid && qp == 0)
         p.lse[static_cast<int64_t>(e_h) * p.T + e_row] = (e_m + __log2f(e_l)) * 0.69314718055994530942f;
-      // staging tile: bf16 → this item's Q buffer; FP8 → the O tile, once item ek-1's store has read it
-      uint8_t* so = smem + (FP8 ? Cfg::OFF_OST : Cfg::OFF_Q + (ek % NQ) * Cfg::Q_BYTES);
+      // staging tile: bf16 → this item's Q buffer; FP8 → O tile ek&1, once item ek-2's store has read it
+      uint8_t* so = smem + (FP8 ? Cfg::OFF_OST + (ek & 1) * Cfg::OST_BYTES : Cfg::OFF_Q + (ek % NQ) * Cfg::Q_BYTES);
       tmem_wait_ld();
       tc_fence_before();
       warp_arrive(&bar_o_empty[ek & 1]);  // O is in registers: the buffer may take item ek+2
@@ -448,7 +455,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int t = 0; t < OC / 2; ++t)
         pk[t] = pack_bf16x2(__uint_as_float(o[2 * t]) * inv_l, __uint_as_float(o[2 * t + 1]) * inv_l);
       {  // SW128 staging: 64-column box col / 64, 16-B chunk XOR row
-        if (FP8 && ek > 0) wp.template wait<2>(bar_ost_free, (ek - 1) & 1);
+        if (FP8 && ek > 1) wp.template wait<2>(&bar_ost_free[ek & 1], ((ek >> 1) - 1) & 1);
 #pragma unroll
         for (int t = 0; t < OC / 8; ++t) {
           const int col = qp * OC + 8 * t;
@@ -513,21 +520,30 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if constexpr (FP8) sl2 = p.scale_log2 * qs;
       (void)qs;
       float m_run = -INFINITY, l_run = 0.f;
-      // FP8: this quarter's K block scales, one tile ahead in registers (data-row blocks)
+      // FP8: this quarter's K block scales, one tile ahead in registers.  BN = the 128-token scale
+      // block, so tile j of the quarter starts in data-row block kb0 + j at the same offset: the
+      // split column cbq (keys before it take block kb0 + j's scale, the rest kb0 + j + 1's) is fixed
+      // for the item, and each tile loads one new scale (its second block is the next tile's first)
+      static_assert(!FP8 || BN == 128, "FP8 K scales assume 128-key tiles");
       const float* ksc = FP8 ? p.k_scale + int64_t(itm.kh) * p.nbt : nullptr;
-      auto kscale = [&](int jj, float& a, float& b) {
-        const int kb = (itm.kv_lo + jj * BN + c0 + itm.dl) / 128;
-        a = __ldg(ksc + min(kb, p.nbt - 1));
-        b = __ldg(ksc + min(kb + 1, p.nbt - 1));
-      };
+      int kb0 = 0, cbq = 128;
       float k0n = 1.f, k1n = 1.f;
-      if constexpr (FP8) kscale(0, k0n, k1n);
+      if constexpr (FP8) {
+        const int base = itm.kv_lo + c0 + itm.dl;  // data row of the quarter's first key (≥ 0)
+        kb0 = base >> 7;
+        cbq = 128 - (base & 127);
+        k0n = __ldg(ksc + min(kb0, p.nbt - 1));
+        k1n = __ldg(ksc + min(kb0 + 1, p.nbt - 1));
+      }
       for (int j = 0; j < itm.nkv; ++j, ++g) {
         const uint32_t s_tm = tmem + lane_off + Cfg::S_COL + (g & 1) * 128 + c0;
         const int kv0 = itm.kv_lo + j * BN + c0;
         const float k0s = k0n, k1s = k1n;
         if constexpr (FP8)
-          if (j + 1 < itm.nkv) kscale(j + 1, k0n, k1n);
+          if (j + 1 < itm.nkv) {
+            k0n = k1n;
+            k1n = __ldg(ksc + min(kb0 + j + 2, p.nbt - 1));
+          }
         if (j + 1 == itm.nkv && qp >= ((itm.kv_hi - kv0 + c0 + 31) >> 5)) {
           // The item's last key tile covers only ⌈valid/32⌉ quarters (its S MMA ran with N = 32 of
           // them): this quarter has no S, exponentials or P.  It still takes part in the row-max
@@ -579,7 +595,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // work); a quarter straddling two blocks scales its columns (a quarter spans ≤ 2 blocks).
         float ksc = 1.f;
         if constexpr (FP8) {
-          const int cb = ((kv0 + itm.dl) / 128 + 1) * 128 - (kv0 + itm.dl);
+          const int cb = cbq;
           if (cb >= 32) {
             ksc = k0s;
           } else {
@@ -794,5 +810,5 @@ extern "C" int vlasim_varlen_attn_fwd_fp8qk_cuda(const vlasim_attn_args* a, void
   if (a->head_dim != 128) return set_error(VLASIM_ECONFIG, "fp8 Q/K attention: head_dim must be 128");
   const size_t need = fwd_ws_bytes(a);
   if (!ws || ws_bytes < need) return set_error(VLASIM_ECONFIG, "attention fwd: workspace %zu < %zu", ws_bytes, need);
-  return launch_fwd2<128, 3, 3, true>(a, static_cast<int2*>(ws), fwd_ws_tiles(a, ws), as_stream(stream));
+  return launch_fwd2<128, 2, 2, true>(a, static_cast<int2*>(ws), fwd_ws_tiles(a, ws), as_stream(stream));
 }

@@ -407,14 +407,14 @@ __global__ void __launch_bounds__(256) k_tensor_codes(const T* __restrict__ x, i
 }
 
 // Groups whose elements form a 2-D region (nr rows × nc contiguous columns, row pitch ld): PerBlock
-// (≤ 128 × 128) and PerChannel with outer·inner ≤ kFusedMax.  A persistent CTA of 512 threads per
-// SM walks the groups; each group is held in registers (32 elements per thread), so amax, scale and
-// codes come from ONE read of x (5 B/element of HBM traffic for fp32), and the next group's loads
-// are issued before the current group is reduced and encoded (two register sets, A/B), so the
-// encode arithmetic overlaps the HBM stream instead of alternating with it.
-constexpr int kFusedThreads = 512;
-constexpr int kFusedUnits = 8;                                          // 4-element slots per thread
-constexpr int64_t kFusedMax = int64_t(kFusedThreads) * 4 * kFusedUnits;  // 16384 elements per group
+// (≤ 128 × 128) and PerChannel with outer·inner ≤ kFusedMax.  Persistent CTAs of NT threads walk
+// the groups; each group is held in registers (16 elements per thread), so amax, scale and codes
+// come from ONE read of x (5 B/element of HBM traffic for fp32), and the next group's loads are
+// issued before the current group is reduced and encoded (two register sets, A/B), so the encode
+// arithmetic overlaps the HBM stream instead of alternating with it.  NT = 1024 (one CTA per SM) for
+// groups above 8 K elements, else 512 (two per SM): 32 warps per SM either way, ≤ 64 registers.
+constexpr int kFusedUnits = 4;                                          // 4-element slots per thread
+constexpr int64_t kFusedMax = int64_t(1024) * 4 * kFusedUnits;          // 16384 elements per group
 
 struct Region {
   int64_t base, ld;
@@ -423,6 +423,7 @@ struct Region {
 };
 
 // (groups < 2^31 and block-grid extents < 2^31: 32-bit divisions, host-checked)
+template <int NT>
 __device__ __forceinline__ Region group_region(const GroupMap& m, int64_t g64) {
   Region rg;
   const uint32_t g = uint32_t(g64);
@@ -442,7 +443,7 @@ __device__ __forceinline__ Region group_region(const GroupMap& m, int64_t g64) {
   const uint32_t upr = uint32_t(rg.nc) >> 2, t = threadIdx.x;
   if (upr) {
     rg.row0 = int(t / upr), rg.col0 = int(t - uint32_t(rg.row0) * upr);
-    rg.drow = int(uint32_t(kFusedThreads) / upr), rg.dcol = int(uint32_t(kFusedThreads) - uint32_t(rg.drow) * upr);
+    rg.drow = int(uint32_t(NT) / upr), rg.dcol = int(uint32_t(NT) - uint32_t(rg.drow) * upr);
   }
   return rg;
 }
@@ -459,9 +460,9 @@ __device__ __forceinline__ Region group_region(const GroupMap& m, int64_t g64) {
     if (col >= upr_) col -= upr_, ++row; \
   } while (0)
 
-// slot k: one 4-element unit u = tid + 512k (VEC = 4, nc % 4 == 0, host-checked) or the 4 scalar
-// elements (4k + j)·512 + tid (VEC = 1)
-template <typename T, int VEC>
+// slot k: one 4-element unit u = tid + NT·k (VEC = 4, nc % 4 == 0, host-checked) or the 4 scalar
+// elements (4k + j)·NT + tid (VEC = 1)
+template <typename T, int VEC, int NT>
 __device__ __forceinline__ void fused_load(const T* __restrict__ x, const Region& rg, float (&v)[kFusedUnits][4]) {
   const int tid = int(threadIdx.x);
   if constexpr (VEC == 4) {
@@ -478,7 +479,7 @@ __device__ __forceinline__ void fused_load(const T* __restrict__ x, const Region
     {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int e = tid + kFusedThreads * (4 * k + j);
+        const int e = tid + NT * (4 * k + j);
         if (e < rg.nr * rg.nc) {
           const int row = e / rg.nc, col = e - row * rg.nc;
           v[k][j] = load_f(x, rg.base + row * rg.ld + col);
@@ -488,7 +489,7 @@ __device__ __forceinline__ void fused_load(const T* __restrict__ x, const Region
   }
 }
 
-template <int VEC>
+template <int VEC, int NT>
 __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const float (&v)[kFusedUnits][4],
                                              float* s_red, uint8_t* __restrict__ codes, float* __restrict__ scales,
                                              int32_t* __restrict__ status) {
@@ -499,7 +500,7 @@ __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const 
 #pragma unroll
   for (int k = 0; k < kFusedUnits; ++k) {
     if constexpr (VEC == 4) {
-      if (4 * (tid + kFusedThreads * k) < total) {  // whole unit valid (nc % 4 == 0)
+      if (4 * (tid + NT * k) < total) {  // whole unit valid (nc % 4 == 0)
         const float m4 = fmaxf(fmaxf(fabsf(v[k][0]), fabsf(v[k][1])), fmaxf(fabsf(v[k][2]), fabsf(v[k][3])));
         // a non-finite element makes the sum non-finite (an overflowing sum of finite values only
         // sends the unit to the exact per-element test)
@@ -510,7 +511,7 @@ __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const 
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (tid + kFusedThreads * (4 * k + j) < total) {
+        if (tid + NT * (4 * k + j) < total) {
           ok &= isfinite(v[k][j]);
           mx = fmaxf(mx, fabsf(v[k][j]));
         }
@@ -525,7 +526,7 @@ __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const 
       for (int k = 0; k < kFusedUnits; ++k)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int e = VEC == 4 ? 4 * (tid + kFusedThreads * k) + j : tid + kFusedThreads * (4 * k + j);
+          const int e = VEC == 4 ? 4 * (tid + NT * k) + j : tid + NT * (4 * k + j);
           if (e < rg.nr * rg.nc && !isfinite(v[k][j])) {
             const int row = e / rg.nc, col = e - row * rg.nc;
             report_bad(status, rg.base + row * rg.ld + col);
@@ -536,7 +537,7 @@ __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const 
   }
   float a = 0.f;
 #pragma unroll
-  for (int w = 0; w < kFusedThreads / 32; ++w) a = fmaxf(a, s_red[w]);
+  for (int w = 0; w < NT / 32; ++w) a = fmaxf(a, s_red[w]);
   if (tid == 0) scales[g] = a == 0.f ? 1.f : __fdiv_rn(a, 448.f);
   const float r = group_rcp(a);
   if constexpr (VEC == 4) {
@@ -563,7 +564,7 @@ __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const 
     {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int e = tid + kFusedThreads * (4 * k + j);
+        const int e = tid + NT * (4 * k + j);
         if (e < rg.nr * rg.nc) {
           const int row = e / rg.nc, col = e - row * rg.nc;
           codes[rg.base + row * rg.ld + col] = uint8_t(code_of(v[k][j], a, r));
@@ -573,29 +574,29 @@ __device__ __forceinline__ void fused_encode(const Region& rg, int64_t g, const 
   }
 }
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(kFusedThreads, 1) k_group_fused(const T* __restrict__ x, GroupMap m,
-                                                                  uint8_t* __restrict__ codes, float* __restrict__ scales,
-                                                                  int32_t* __restrict__ status) {
-  __shared__ float s_red[2][kFusedThreads / 32];  // by group parity: one barrier per group suffices
+template <typename T, int VEC, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_group_fused(const T* __restrict__ x, GroupMap m,
+                                                               uint8_t* __restrict__ codes, float* __restrict__ scales,
+                                                               int32_t* __restrict__ status) {
+  __shared__ float s_red[2][NT / 32];  // by group parity: one barrier per group suffices
   float va[kFusedUnits][4], vb[kFusedUnits][4];
   int64_t g = blockIdx.x;
   if (g >= m.groups) return;
-  Region ra = group_region(m, g), rb;
-  fused_load<T, VEC>(x, ra, va);
+  Region ra = group_region<NT>(m, g), rb;
+  fused_load<T, VEC, NT>(x, ra, va);
   for (;;) {
     const int64_t g1 = g + gridDim.x, g2 = g1 + gridDim.x;
     if (g1 < m.groups) {
-      rb = group_region(m, g1);
-      fused_load<T, VEC>(x, rb, vb);  // in flight while group g is encoded
+      rb = group_region<NT>(m, g1);
+      fused_load<T, VEC, NT>(x, rb, vb);  // in flight while group g is encoded
     }
-    fused_encode<VEC>(ra, g, va, s_red[0], codes, scales, status);
+    fused_encode<VEC, NT>(ra, g, va, s_red[0], codes, scales, status);
     if (g1 >= m.groups) break;
     if (g2 < m.groups) {
-      ra = group_region(m, g2);
-      fused_load<T, VEC>(x, ra, va);
+      ra = group_region<NT>(m, g2);
+      fused_load<T, VEC, NT>(x, ra, va);
     }
-    fused_encode<VEC>(rb, g1, vb, s_red[1], codes, scales, status);
+    fused_encode<VEC, NT>(rb, g1, vb, s_red[1], codes, scales, status);
     if (g2 >= m.groups) break;
     g = g2;
   }
@@ -885,9 +886,17 @@ extern "C" int vlasim_fp8_quantize_cuda(const void* d_x, int32_t dtype, const in
       const int64_t nc = m.kind == VLASIM_GRAN_BLOCK ? m.cols : m.inner;
       const int64_t ld = m.kind == VLASIM_GRAN_BLOCK ? m.cols : m.ch * m.inner;
       const bool v4 = al4 && nc % 4 == 0 && ld % 4 == 0;
-      const int grid = int(std::min<int64_t>(m.groups, nsm));
-      if (v4) k_group_fused<T, 4><<<grid, kFusedThreads, 0, st>>>(x, m, d_codes, d_scales, d_status);
-      else k_group_fused<T, 1><<<grid, kFusedThreads, 0, st>>>(x, m, d_codes, d_scales, d_status);
+      const int64_t gelems = m.kind == VLASIM_GRAN_BLOCK ? std::min<int64_t>(m.rows, 128) * std::min<int64_t>(m.cols, 128)
+                                                         : outer * m.inner;
+      if (gelems > 8192) {
+        const int grid = int(std::min<int64_t>(m.groups, nsm));
+        if (v4) k_group_fused<T, 4, 1024><<<grid, 1024, 0, st>>>(x, m, d_codes, d_scales, d_status);
+        else k_group_fused<T, 1, 1024><<<grid, 1024, 0, st>>>(x, m, d_codes, d_scales, d_status);
+      } else {
+        const int grid = int(std::min<int64_t>(m.groups, 2 * int64_t(nsm)));
+        if (v4) k_group_fused<T, 4, 512><<<grid, 512, 0, st>>>(x, m, d_codes, d_scales, d_status);
+        else k_group_fused<T, 1, 512><<<grid, 512, 0, st>>>(x, m, d_codes, d_scales, d_status);
+      }
       return VLASIM_OK;
     }
     if (colwise) {

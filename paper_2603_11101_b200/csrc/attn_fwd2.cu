@@ -595,17 +595,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // work); a quarter straddling two blocks scales its columns (a quarter spans ≤ 2 blocks).
         float ksc = 1.f;
         if constexpr (FP8) {
-          const int cb = cbq;
-          if (cb >= 32) {
-            ksc = k0s;
-          } else {
+          ksc = k0s;
+          if (cbq < 32) {  // columns ≥ cbq: block kb0+j+1, rescaled by k1/k0 (one predicated FMUL each)
+            const float rr = __fdividef(k1s, k0s);
+            uint32_t hi;  // opaque to the compiler: bit tests become R2P + predicated FMULs, not 32 compares
+            asm("mov.b32 %0, %1;" : "=r"(hi) : "r"(0xFFFFFFFFu << cbq));
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              const float2 sc = make_float2(c < cb ? k0s : k1s, c + 1 < cb ? k0s : k1s);
-              const float2 y = f2_mul(make_float2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])), sc);
-              x[c] = __float_as_uint(y.x);
-              x[c + 1] = __float_as_uint(y.y);
-            }
+            for (int c = 0; c < 32; ++c)
+              if ((hi >> c) & 1u) x[c] = __float_as_uint(__uint_as_float(x[c]) * rr);
           }
         }
         if (!__all_sync(0xffffffffu, c_lo <= 0 && c_hi >= 32)) {  // some row of the warp is partial

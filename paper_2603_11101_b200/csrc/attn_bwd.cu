@@ -1259,6 +1259,11 @@ struct DqCfg {
   static constexpr int OFF_Q = 0, OFF_DO = TILE;
   static constexpr int OFF_K = 2 * TILE;             // K ring [KS]: released after dQ
   static constexpr int OFF_V = OFF_K + KS * KTILE;   // V ring [VS]: released after dP
+  // VS = 0 (head_dim 256): ONE ring of 3 slots shared by K and V.  K(g) is held until dQ(g), V(g)
+  // only until dP(g), so with K(g) in slot g % 3 and V(g) in slot (g+1) % 3, K(g+1) reuses the slot
+  // V(g) frees at dP(g) and V(g+2) the slot K(g) frees at dQ(g): the S(g+1) load no longer waits
+  // for dQ(g−1) (split 2 K + 1 V rings: the MMA waited for K 28 % of the kernel)
+  static_assert(VS > 0 || KS == 3, "unified K/V ring: 3 slots");
   // decoded item descriptors, written by the producer one item ahead: the softmax warps hold no
   // next-item state in registers (at the 96-register cap it spilled and exposed the loads)
   static constexpr int NDESC = 4;
@@ -1405,8 +1410,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
         for (int j = 0; j < itm.nkv; ++j, ++g) {
           const int kv0 = itm.kv_lo + j * BN + itm.dl;  // data row
-          const int ks = g % KS, vs = g % VS;
-          if (g >= KS) mbar_wait(&bar_k_empty[ks], ((g / KS) - 1) & 1);
+          // ring slots and their use ordinals (unified ring: K(g) → g % 3, V(g) → (g+1) % 3)
+          const int ks = VS ? g % KS : g % 3, vs = VS ? g % VS : (g + 1) % 3;
+          const int ku = VS ? g / KS : g / 3 + (g + 2) / 3, vu = VS ? g / VS : (g + 1) / 3 + g / 3;
+          uint64_t* const vfull = VS ? bar_v_full : bar_k_full;
+          uint64_t* const vempty = VS ? bar_v_empty : bar_k_empty;
+          uint8_t* const vbase = smem + (VS ? Cfg::OFF_V : Cfg::OFF_K);
+          if (ku > 0) mbar_wait(&bar_k_empty[ks], (ku - 1) & 1);
           if (PROF && (p.dbg & 2)) {  // timing experiment: no K/V traffic (the trace lives in the K ring)
             mbar_arrive(&bar_k_full[ks]);
           } else {
@@ -1416,15 +1426,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
               tma_load_2d(smem + Cfg::OFF_K + ks * Cfg::KTILE + c * (BN * 128), &tmK, itm.kh * HD + c * 64, kv0,
                           &bar_k_full[ks]);
           }
-          if (g >= VS) mbar_wait(&bar_v_empty[vs], ((g / VS) - 1) & 1);
+          if (vu > 0) mbar_wait(&vempty[vs], (vu - 1) & 1);
           if (PROF && (p.dbg & 2)) {
-            mbar_arrive(&bar_v_full[vs]);
+            mbar_arrive(&vfull[vs]);
           } else {
-            mbar_expect_tx(&bar_v_full[vs], Cfg::KTILE);
+            mbar_expect_tx(&vfull[vs], Cfg::KTILE);
 #pragma unroll
             for (int c = 0; c < HD / 64; ++c)
-              tma_load_2d(smem + Cfg::OFF_V + vs * Cfg::KTILE + c * (BN * 128), &tmV, itm.kh * HD + c * 64, kv0,
-                          &bar_v_full[vs]);
+              tma_load_2d(vbase + vs * Cfg::KTILE + c * (BN * 128), &tmV, itm.kh * HD + c * 64, kv0, &vfull[vs]);
           }
         }
         ++k;
@@ -1442,7 +1451,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const uint64_t dQk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_Q), 16, 1024);
       const uint64_t dOk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_DO), 16, 1024);
       const uint64_t dKk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), 16, 1024);
-      const uint64_t dVk = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_V), 16, 1024);
+      const uint64_t dVk = make_sdesc_sw128(smem_u32(smem + (VS ? Cfg::OFF_V : Cfg::OFF_K)), 16, 1024);
+      uint64_t* const vfull = VS ? bar_v_full : bar_k_full;
+      uint64_t* const vempty = VS ? bar_v_empty : bar_k_empty;
       const uint64_t dKm = make_sdesc_sw128(smem_u32(smem + Cfg::OFF_K), BN * 128, 1024);  // MN-major view
       int g = 0, k = 0;
       int ks = 0, vs = 0;          // K / V ring stages of tile g
@@ -1486,6 +1497,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           // the item's last key tile: N = W · ⌈valid keys / W⌉ for S and dP, dQ over those keys
           const int na = j + 1 < itm.nkv ? 4 : (itm.kv_hi - itm.kv_lo - j * BN + W - 1) / W;
           const uint32_t id_kk = id_kk0 | (uint32_t(na * W / 8) << 17);
+          if constexpr (VS == 0) {  // unified ring (producer comment): slots and use parities from g
+            ks = g % 3;
+            vs = (g + 1) % 3;
+            kph = uint32_t(g / 3 + (g + 2) / 3) & 1u;
+            vph = uint32_t((g + 1) / 3 + g / 3) & 1u;
+          }
           mbar_wait(&bar_k_full[ks], kph);
           trace(12, g);  // M: K seen
           tc_fence_after();
@@ -1500,7 +1517,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           __syncwarp();
           // dP_g as soon as phase B(g−1) has loaded dP_{g−1} (dS goes over S, not dP), then dQ_{g−1}
           if (g > 0) mbar_wait(bar_dp_free, (g - 1) & 1);
-          mbar_wait(&bar_v_full[vs], vph);
+          mbar_wait(&vfull[vs], vph);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
@@ -1508,7 +1525,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
               umma_f16_ss(tmem + Cfg::DP_COL, sdesc_add(dOk, (s / 4) * 16384 + (s % 4) * 32),
                           sdesc_add(dVk, (s / 4) * (BN * 128) + (s % 4) * 32) + vs * T16, id_kk, s > 0);
             umma_commit(bar_dp_full);
-            umma_commit(&bar_v_empty[vs]);
+            umma_commit(&vempty[vs]);
             if (j == itm.nkv - 1) umma_commit(bar_qdo_empty);
           }
           __syncwarp();
@@ -1521,8 +1538,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           pg = g;
           pk = k;
           pna = na;
-          if (++ks == KS) { ks = 0; kph ^= 1; }
-          if (++vs == VS) { vs = 0; vph ^= 1; }
+          if constexpr (VS > 0) {
+            if (++ks == KS) { ks = 0; kph ^= 1; }
+            if (++vs == VS) { vs = 0; vph ^= 1; }
+          }
         }
         ++k;
       }
@@ -1817,7 +1836,7 @@ int launch_bwd(const vlasim_attn_args* a, const vlasim_attn_grads* g, const BwdW
   mark_boundary(st);
   {
     constexpr int BN = HD == 256 ? 64 : 128;
-    constexpr int KS = HD == 64 ? 5 : (HD == 128 ? 3 : 2), VS = HD == 64 ? 4 : (HD == 128 ? 2 : 1);
+    constexpr int KS = HD == 64 ? 5 : 3, VS = HD == 64 ? 4 : (HD == 128 ? 2 : 0);  // VS 0: unified K/V ring
     using Cfg = DqCfg<HD, BN, KS, VS>;
     auto kern = p.prof ? k_bwd_dq<HD, BN, KS, VS, true> : k_bwd_dq<HD, BN, KS, VS, false>;
     if (p.prof) prof_buffer();  // fresh counters / trace for this launch

@@ -1,3 +1,4 @@
+# A/B/C of three builds (lib_ab/base.so, c1.so, c2.so) on config 4 (bf16 and FP8 forward), alternating
 mkdir -p gpurun_out
 for r in 1 2 3; do
   for v in base c1 c2; do
